@@ -1,0 +1,50 @@
+"""Generator determinism and recipe checks (CPU only)."""
+import numpy as np
+
+import workloads as wl
+
+
+def test_cfg1_recipe():
+    p = wl.cfg1()
+    assert p.vol.shape == (1, 32, 32, 32) and p.vol.dtype == np.float32
+    assert p.fixed.sum() == 40
+    assert p.values[0][p.fixed > 0].sum() == 20
+    q = wl.cfg1()
+    assert np.array_equal(p.vol, q.vol) and np.array_equal(p.fixed, q.fixed)
+
+
+def test_cfg2_brick_recipe_and_determinism():
+    v, f, val = wl.cfg2_brick(7)
+    v2, f2, val2 = wl.cfg2_brick(7)
+    assert np.array_equal(v, v2) and np.array_equal(f, f2) and np.array_equal(val, val2)
+    assert v.dtype == np.uint16 and v.shape == (64, 64, 64)
+    # shell fully fixed with values in [0,1]; 262 interior seeds
+    shell = np.ones((64, 64, 64), bool)
+    shell[1:-1, 1:-1, 1:-1] = False
+    assert np.all(f[shell] == 1)
+    assert (val[shell] >= 0).all() and (val[shell] <= 1).all()
+    inner = f[1:-1, 1:-1, 1:-1]
+    assert inner.sum() == 262
+    iv = val[1:-1, 1:-1, 1:-1][inner > 0]
+    assert set(np.unique(iv).tolist()) <= {0.0, 1.0}
+    assert (iv == 1).sum() >= 1 and (iv == 0).sum() == 131
+
+
+def test_cfg2_subset_matches_full_ids():
+    p = wl.cfg2(bricks=[3, 5], n=16)
+    v, f, val = wl.cfg2_brick(5, 16)
+    assert np.array_equal(p.vol[1], v) and np.array_equal(p.values[0, 1], val)
+
+
+def test_cfg3_cfg4_small():
+    p = wl.cfg3(scale=0.125, seeds_per_region=20)
+    assert p.vol.dtype == np.int16 and p.vol.shape == (1, 32, 64, 64)
+    assert p.values[0][p.fixed > 0].sum() == 20          # liver seeds = 1
+    lp = wl.cfg4(n=32, seeds_per_label=10)
+    assert lp.labels.max() == 4 and (lp.labels > 0).sum() == 40
+
+
+def test_cfg5_slab_decomposition_invariant():
+    a = wl.cfg5_slab(0, 6, scale=1 / 64)
+    b = np.concatenate([wl.cfg5_slab(0, 3, scale=1 / 64), wl.cfg5_slab(3, 6, scale=1 / 64)])
+    assert np.array_equal(a, b) and a.dtype == np.uint16
