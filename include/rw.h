@@ -1,0 +1,189 @@
+/*
+ * rw.h -- C ABI of librw: the B200 (sm_100a) hot path of the hierarchical random walker
+ * of Drees, Eilers & Jiang, arXiv 2103.09564 ("PAPER.md").
+ *
+ * Citations: P:n = PAPER.md line n.  Readings c1..c17 = DESIGN.md section 3.
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ *  - Pointers named "device" are CUDA device pointers owned by the caller (e.g. torch
+ *    tensors).  Host pointers are marked "host".  The library never frees caller memory
+ *    and allocates no device memory inside rw_* compute calls (the only library-owned
+ *    memory is the rw_queue ring, allocated in rw_queue_create).
+ *  - Layout: x fastest, then y, z, then brick, then right-hand side:
+ *        idx = ((r*batch + b)*nz + z)*ny*nx + y*nx + x
+ *    Brick dims are constant over a batch.  nx must be a multiple of 4; every dim >= 1.
+ *    Device pointers must be 16-byte aligned.
+ *  - Work is enqueued on the given stream (cudaStream_t passed as void*; NULL = legacy
+ *    default stream); results are valid once that stream has synchronised.
+ *  - Validation happens before anything is enqueued: on RW_EINVAL nothing ran.
+ *  - On any non-OK status rw_last_error() returns a thread-local description.
+ */
+#ifndef RW_H_
+#define RW_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t rw_status;
+enum {
+  RW_OK = 0,
+  RW_EINVAL = 1,        /* bad argument; nothing enqueued                                 */
+  RW_ECUDA = 2,         /* a CUDA call failed; rw_last_error() carries the CUDA message     */
+  RW_ENOMEM = 3,        /* workspace too small / pinned allocation failed                  */
+  RW_EUNSUPPORTED = 4   /* valid request this build does not implement                     */
+};
+
+typedef int32_t rw_dtype;
+enum { RW_U8 = 0, RW_U16 = 1, RW_I16 = 2, RW_F32 = 3 };
+
+typedef struct { int32_t nx, ny, nz; } rw_dims;
+/* Intensity normalisation g = clamp(v*scale + offset, 0, 1) in fp32 (reading c2):
+ * u8 {1/255, 0}, u16 {1/65535, 0}, i16 HU window {1/2000, 0.5}, f32 {1, 0}.            */
+typedef struct { float scale, offset; } rw_norm;
+
+/* Per-(rhs, brick) exit status written to the optional `status` outputs. */
+enum {
+  RW_ST_CONVERGED = 1,  /* stopping rule met                                               */
+  RW_ST_MAXITER = 2,    /* max_iter reached first (not an error, SURVEY S:208)              */
+  RW_ST_TRIVIAL = 3,    /* no fixed voxel (x = x0) or no unknown voxel: 0 iterations       */
+  RW_ST_ZERO_B = 4,     /* b = 0 with fixed voxels: exact solution x_U = 0, 0 iterations   */
+  RW_ST_BREAKDOWN = 5   /* p.Ap <= 0 or non-finite: brick frozen at its last iterate      */
+};
+
+const char* rw_last_error(void);
+const char* rw_version(void);
+
+/* ------------------------------------------------------------------------------------
+ * rw_brick_weights -- edge weights of the 6-connected brick graph.
+ *   P:75 "a 3D grid of vertices with edges between 6-neighbors"; P:77 Grady weight
+ *   w_pq = exp(-beta (n[p]-n[q])^2), plus eps > 0 (reading c1) so L_UU is SPD.
+ *   vol    device [batch][nz][ny][nx] of `dtype`, normalised with `nm`.
+ *   W      device fp32 [3][batch][nz][ny][nx]:  W[a][v] = w(v, v + e_a), a = x,y,z;
+ *          0 where v + e_a lies outside the brick (no edges leave a brick, reading c4).
+ *   dinv   device fp32 [batch][n] or NULL: 1 / sum of the 6 incident weights (the Jacobi
+ *          preconditioner), 0 where fixed[v] != 0.
+ *   fixed  device u8 [batch][n] or NULL (NULL: no voxel fixed).
+ *   Errors: RW_EINVAL for bad dims/dtype, beta < 0, eps <= 0, NULL vol/W.
+ * ---------------------------------------------------------------------------------- */
+rw_status rw_brick_weights(const void* vol, rw_dtype dtype, rw_norm nm, int32_t batch,
+                           rw_dims d, float beta, float eps, float* W, float* dinv,
+                           const uint8_t* fixed, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * rw_solve_workspace_bytes -- device workspace needed by rw_solve_bricks /
+ * rw_solve_labels for this shape.  weights_given != 0: the caller passes W (the
+ * workspace then holds no weight planes).
+ * ---------------------------------------------------------------------------------- */
+size_t rw_solve_workspace_bytes(int32_t batch, rw_dims d, int32_t nrhs, int32_t weights_given);
+
+/* ------------------------------------------------------------------------------------
+ * rw_solve_bricks -- batched random walker solve (the hot path).
+ *   For every brick b and right-hand side r, with S = {v : fixed[b][v] != 0} (seeds and
+ *   Dirichlet faces) and U its complement, solves the discrete Dirichlet problem of P:77
+ *        L_UU x_U = -B^T x_S,        x_S = values[r][b][S]
+ *   with Jacobi-preconditioned CG, matrix-free: the SpMV is the edge-difference
+ *   stencil q_i = sum_j w_ij (p_i - p_j) (reading c8), fp32 vectors, fp64 dot products.
+ *   All right-hand sides share one operator (W is read once per iteration for all r).
+ *   Stopping (reading c5), checked before every iteration on the recurrence residual:
+ *        tol_mode 0: ||r_k||_2 <= tol * ||b||_2      tol_mode 1: ||r_k||_2 <= tol
+ *   or k == max_iter.  Converged (rhs, brick) pairs drop out of the batch.
+ *
+ *   batch, d     brick count and brick dims (nx % 4 == 0).
+ *   vol, dtype, nm   device intensities (as rw_brick_weights) -- or NULL when W is given.
+ *   W            device fp32 [3][batch][n] precomputed weights, or NULL when vol is given.
+ *                Exactly one of vol / W must be non-NULL.
+ *   fixed        device u8 [batch][n]: 0 = unknown, else Dirichlet.
+ *   values       device fp32 [nrhs][batch][n]: Dirichlet values (read only where fixed).
+ *   nrhs         1 .. 64 right-hand sides.
+ *   beta, eps    weight parameters (used only with vol).  eps > 0.
+ *   tol, max_iter, tol_mode   stopping rule; tol > 0, max_iter >= 1.
+ *   x0           device fp32 [nrhs][batch][n] initial guess or NULL (0.5 on U, reading c6).
+ *   workspace    device, >= rw_solve_workspace_bytes(batch, d, nrhs, W != NULL) bytes,
+ *                256-byte aligned; contents are scratch.
+ *   prob   out   device fp32 [nrhs][batch][n]: x clamped to [0,1] (reading c9), fixed
+ *                voxels hold their values.  Also used as the iterate storage.
+ *   iters  out   device int32 [nrhs][batch]: CG iterations (SpMVs) per pair.
+ *   resid  out   device fp32 [nrhs][batch] or NULL: recurrence residual at exit,
+ *                ||r||/||b|| (mode 0) or ||r|| (mode 1) (reading c16).
+ *   status out   device int32 [nrhs][batch] or NULL: RW_ST_* per pair.
+ *   labels out   device u8 [batch][n] or NULL: prob[0] > 0.5 (0.5 -> 0, c10).
+ *   Not errors: non-convergence (iters = max_iter, status MAXITER); a brick without fixed
+ *   voxels (prob = x0 clamped, iters 0, status TRIVIAL).
+ *   The call blocks the host until the iteration loop has finished (it polls a device
+ *   counter every few iterations); all work is ordered on `stream`.
+ * ---------------------------------------------------------------------------------- */
+rw_status rw_solve_bricks(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype,
+                          rw_norm nm, const float* W, const uint8_t* fixed,
+                          const float* values, int32_t nrhs, float beta, float eps,
+                          float tol, int32_t max_iter, int32_t tol_mode, const float* x0,
+                          void* workspace, size_t ws_bytes, float* prob, int32_t* iters,
+                          float* resid, int32_t* status, uint8_t* labels, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * rw_solve_labels -- multi-class random walker, P:79 / P:107: class k's probability is the
+ *   solution with class-k seeds = 1 and all other seeds = 0; class = argmax.  Classes are
+ *   1..K (K in 2..65); classes 1..K-1 are solved as K-1 right-hand sides sharing one
+ *   operator and class K is derived as 1 - sum (linearity of the Dirichlet problem,
+ *   reading c11).
+ *   seeds    device u8 [batch][n]: 0 = unseeded, k in 1..K = seed of class k.
+ *   prob     out device fp32 [K-1][batch][n] (classes 1..K-1, clamped).
+ *   labels   out device u8 [batch][n]: argmax over the K probabilities (ties -> lowest
+ *            class id), seeds keep their class.
+ *   workspace: rw_solve_labels_workspace_bytes(batch, d, K, W != NULL).
+ *   Other arguments as rw_solve_bricks.
+ * ---------------------------------------------------------------------------------- */
+size_t rw_solve_labels_workspace_bytes(int32_t batch, rw_dims d, int32_t K, int32_t weights_given);
+rw_status rw_solve_labels(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype,
+                          rw_norm nm, const float* W, const uint8_t* seeds, int32_t K,
+                          float beta, float eps, float tol, int32_t max_iter,
+                          int32_t tol_mode, void* workspace, size_t ws_bytes, float* prob,
+                          int32_t* iters, float* resid, uint8_t* labels, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * rw_build_pyramid -- LOD pyramid levels 1..levels of a volume ("applying a 2^3
+ *   mean filter and downsampling"; P:109 border bricks smaller than s^3).  Reading c12:
+ *   level l+1 voxel (X,Y,Z) = mean of the present level-l children (2X..2X+1, ...);
+ *   dims ceil(d/2); integer dtypes: round-half-up floor((sum + floor(cnt/2))/cnt),
+ *   bit-exact; f32: fp32 sum in fixed pairwise order, one IEEE division by cnt.
+ *   vol        device [d.nz][d.ny][d.nx] of dtype (any dims >= 1; nx need not be % 4).
+ *   levels     1..16.
+ *   level_out  host array of `levels` device pointers; level l (1-based) has dims
+ *              ceil(d / 2^l) applied per level and the input dtype.
+ * rw_build_pyramid_slab -- the same over a z-slab [z0, z0+nzs) of a larger volume whose
+ *   full dims are `d` (streamed input, config 5): z0 must be a multiple of 2^levels and
+ *   nzs a multiple of 2^levels unless z0+nzs == d.nz.  Writes only the output planes
+ *   that the slab fully determines; successive slabs produce the same bytes as one call.
+ * ---------------------------------------------------------------------------------- */
+rw_status rw_build_pyramid(const void* vol, rw_dtype dtype, rw_dims d, int32_t levels,
+                           void* const* level_out, void* stream);
+rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int32_t z0,
+                                int32_t nzs, int32_t levels, void* const* level_out,
+                                void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Pinned, double-buffered host->device queue for inputs larger than HBM (north star item
+ * 5; P:105 constant-memory brick-wise loading).  A ring of `depth` (>= 2) slots, each a
+ * pinned host buffer plus a device buffer of slot_bytes, allocated once here (library-
+ * owned).  push: waits until the slot's previous consumer released it, copies host_src
+ * (pageable or pinned, host) into the pinned slot with several host threads, enqueues
+ * the H2D copy on copy_stream and returns the device slot pointer and its id.
+ * wait: makes compute_stream wait for that slot's copy.  release: records on
+ * compute_stream that the slot's consumers are done (slot reusable after that point).
+ * ---------------------------------------------------------------------------------- */
+typedef struct rw_queue rw_queue;
+rw_status rw_queue_create(size_t slot_bytes, int32_t depth, rw_queue** q);
+rw_status rw_queue_push(rw_queue* q, const void* host_src, size_t bytes, void* copy_stream,
+                        void** dev_slot, int32_t* slot_id);
+rw_status rw_queue_wait(rw_queue* q, int32_t slot_id, void* compute_stream);
+rw_status rw_queue_release(rw_queue* q, int32_t slot_id, void* compute_stream);
+void rw_queue_destroy(rw_queue* q);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RW_H_ */

@@ -1,0 +1,11 @@
+"""B200-native (sm_100a) hot path of the hierarchical random walker, arXiv 2103.09564.
+
+The product is the C-ABI library ``librw.so`` (include/rw.h) built from ``csrc/``;
+``api`` is a thin ctypes binding (argument marshalling only).  No CPU fallback exists:
+importing ``api`` works without a GPU, calling a compute function needs the CUDA build.
+"""
+from . import api  # noqa: F401
+from .api import (  # noqa: F401
+    brick_weights, solve_bricks, solve_labels, build_pyramid, build_pyramid_slab, Queue,
+    solve_workspace_bytes, solve_labels_workspace_bytes, level_dims,
+)

@@ -1,0 +1,230 @@
+"""Thin Python binding over librw (include/rw.h) -- marshalling only.
+
+PyTorch provides device memory and streams; every step of the hot path runs in the
+CUDA kernels behind the C ABI.  Function names follow the ABI without the ``rw_`` prefix.
+Tensors are contiguous, [batch, nz, ny, nx] (x fastest); per-RHS tensors add a leading
+[nrhs] axis.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import lib, check, rw_dims, rw_norm
+
+DTYPES = {torch.uint8: 0, torch.uint16: 1, torch.int16: 2, torch.float32: 3}
+DEFAULT_NORM = {torch.uint8: (1 / 255, 0.0), torch.uint16: (1 / 65535, 0.0),
+                torch.int16: (1 / 2000, 0.5), torch.float32: (1.0, 0.0)}
+
+ST_NAMES = {1: "converged", 2: "maxiter", 3: "trivial", 4: "zero_b", 5: "breakdown"}
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None, device=None):
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return C.c_void_p(s.cuda_stream)
+
+
+def _need(t, name, dtype=None):
+    if t is None:
+        return
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def dims_of(t):
+    *_, nz, ny, nx = t.shape
+    return rw_dims(nx, ny, nz)
+
+
+def solve_workspace_bytes(batch, dims, nrhs=1, weights_given=False):
+    nx, ny, nz = dims
+    return lib().rw_solve_workspace_bytes(batch, rw_dims(nx, ny, nz), nrhs, int(weights_given))
+
+
+def solve_labels_workspace_bytes(batch, dims, K, weights_given=False):
+    nx, ny, nz = dims
+    return lib().rw_solve_labels_workspace_bytes(batch, rw_dims(nx, ny, nz), K, int(weights_given))
+
+
+def alloc_workspace(nbytes, device):
+    # 256-byte aligned (torch's caching allocator returns >= 512-byte aligned blocks)
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def brick_weights(vol, beta=100.0, eps=1e-6, fixed=None, norm=None, want_dinv=True, stream=None):
+    """rw_brick_weights: returns (W [3, B, nz, ny, nx] fp32, dinv [B, nz, ny, nx] or None)."""
+    _need(vol, "vol")
+    _need(fixed, "fixed", torch.uint8)
+    if vol.dim() == 3:
+        vol = vol.unsqueeze(0)
+    B = vol.shape[0]
+    sc, of = norm or DEFAULT_NORM[vol.dtype]
+    W = torch.empty((3,) + tuple(vol.shape), dtype=torch.float32, device=vol.device)
+    dinv = torch.empty(tuple(vol.shape), dtype=torch.float32, device=vol.device) if want_dinv else None
+    st = lib().rw_brick_weights(_ptr(vol), DTYPES[vol.dtype], rw_norm(sc, of), B, dims_of(vol),
+                                beta, eps, _ptr(W), _ptr(dinv), _ptr(fixed), _stream(stream, vol.device))
+    check(st, "rw_brick_weights")
+    return W, dinv
+
+
+def solve_bricks(fixed, values, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6,
+                 max_iter=5000, tol_mode=0, x0=None, norm=None, labels=False, workspace=None,
+                 out=None, stream=None):
+    """rw_solve_bricks.  ``values``/``x0``: [nrhs, B, nz, ny, nx] (or [B, ...] for nrhs=1).
+
+    Returns dict(prob [nrhs,B,nz,ny,nx], iters [nrhs,B], resid [nrhs,B], status [nrhs,B],
+    labels [B,nz,ny,nx] u8 or None).  Stream-ordered; the call itself blocks only until the
+    device iteration loop has been fully enqueued/finished (see rw.h).
+    """
+    _need(fixed, "fixed", torch.uint8)
+    if values.dim() == 4:
+        values = values.unsqueeze(0)
+    if x0 is not None and x0.dim() == 4:
+        x0 = x0.unsqueeze(0)
+    _need(values, "values", torch.float32)
+    _need(x0, "x0", torch.float32)
+    _need(vol, "vol")
+    _need(W, "W", torch.float32)
+    R, B = values.shape[0], values.shape[1]
+    d = dims_of(fixed)
+    dev = fixed.device
+    dt = DTYPES[vol.dtype] if vol is not None else 3
+    sc, of = norm or (DEFAULT_NORM[vol.dtype] if vol is not None else (1.0, 0.0))
+    need = lib().rw_solve_workspace_bytes(B, d, R, int(W is not None))
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need, dev)
+    if out is None:
+        out = dict(prob=torch.empty_like(values),
+                   iters=torch.empty((R, B), dtype=torch.int32, device=dev),
+                   resid=torch.empty((R, B), dtype=torch.float32, device=dev),
+                   status=torch.empty((R, B), dtype=torch.int32, device=dev),
+                   labels=torch.empty(tuple(fixed.shape), dtype=torch.uint8, device=dev) if labels else None)
+    st = lib().rw_solve_bricks(B, d, _ptr(vol), dt, rw_norm(sc, of), _ptr(W), _ptr(fixed),
+                               _ptr(values), R, beta, eps, tol, max_iter, tol_mode, _ptr(x0),
+                               _ptr(workspace), workspace.numel(), _ptr(out["prob"]),
+                               _ptr(out["iters"]), _ptr(out["resid"]), _ptr(out["status"]),
+                               _ptr(out["labels"]), _stream(stream, dev))
+    check(st, "rw_solve_bricks")
+    return out
+
+
+def solve_labels(seeds, K, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6, max_iter=5000,
+                 tol_mode=0, norm=None, workspace=None, stream=None):
+    """rw_solve_labels: seeds u8 [B,nz,ny,nx] (0 unseeded, 1..K).  Returns dict(prob
+    [K-1,B,...] for classes 1..K-1, labels [B,...] in 1..K, iters [K-1,B], resid)."""
+    _need(seeds, "seeds", torch.uint8)
+    _need(vol, "vol")
+    _need(W, "W", torch.float32)
+    B = seeds.shape[0]
+    d = dims_of(seeds)
+    dev = seeds.device
+    dt = DTYPES[vol.dtype] if vol is not None else 3
+    sc, of = norm or (DEFAULT_NORM[vol.dtype] if vol is not None else (1.0, 0.0))
+    need = lib().rw_solve_labels_workspace_bytes(B, d, K, int(W is not None))
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need, dev)
+    prob = torch.empty((K - 1,) + tuple(seeds.shape), dtype=torch.float32, device=dev)
+    iters = torch.empty((K - 1, B), dtype=torch.int32, device=dev)
+    resid = torch.empty((K - 1, B), dtype=torch.float32, device=dev)
+    labels = torch.empty(tuple(seeds.shape), dtype=torch.uint8, device=dev)
+    st = lib().rw_solve_labels(B, d, _ptr(vol), dt, rw_norm(sc, of), _ptr(W), _ptr(seeds), K,
+                               beta, eps, tol, max_iter, tol_mode, _ptr(workspace),
+                               workspace.numel(), _ptr(prob), _ptr(iters), _ptr(resid),
+                               _ptr(labels), _stream(stream, dev))
+    check(st, "rw_solve_labels")
+    return dict(prob=prob, labels=labels, iters=iters, resid=resid)
+
+
+def level_dims(dims, levels):
+    nx, ny, nz = dims
+    out = []
+    for _ in range(levels):
+        nx, ny, nz = (nx + 1) // 2, (ny + 1) // 2, (nz + 1) // 2
+        out.append((nx, ny, nz))
+    return out
+
+
+def build_pyramid(vol, levels, outs=None, stream=None):
+    """rw_build_pyramid: vol [nz, ny, nx] -> list of ``levels`` tensors (levels 1..L)."""
+    _need(vol, "vol")
+    nz, ny, nx = vol.shape
+    if outs is None:
+        outs = [torch.empty((z, y, x), dtype=vol.dtype, device=vol.device)
+                for (x, y, z) in level_dims((nx, ny, nz), levels)]
+    arr = (C.c_void_p * levels)(*[o.data_ptr() for o in outs])
+    st = lib().rw_build_pyramid(_ptr(vol), DTYPES[vol.dtype], rw_dims(nx, ny, nz), levels, arr,
+                                _stream(stream, vol.device))
+    check(st, "rw_build_pyramid")
+    return outs
+
+
+def build_pyramid_slab(slab, full_dims, z0, levels, outs, stream=None):
+    """rw_build_pyramid_slab: slab = planes [z0, z0+slab.shape[0]) of a volume of
+    ``full_dims`` = (nx, ny, nz); ``outs`` = preallocated full-size level tensors."""
+    _need(slab, "slab")
+    nx, ny, nz = full_dims
+    arr = (C.c_void_p * levels)(*[o.data_ptr() for o in outs])
+    st = lib().rw_build_pyramid_slab(_ptr(slab), DTYPES[slab.dtype], rw_dims(nx, ny, nz), z0,
+                                     slab.shape[0], levels, arr, _stream(stream, slab.device))
+    check(st, "rw_build_pyramid_slab")
+    return outs
+
+
+class Queue:
+    """rw_queue: pinned double-buffered host->device ring (library-owned buffers)."""
+
+    def __init__(self, slot_bytes, depth=2):
+        h = C.c_void_p()
+        check(lib().rw_queue_create(slot_bytes, depth, C.byref(h)), "rw_queue_create")
+        self._q = h
+        self.slot_bytes = slot_bytes
+
+    def push(self, host_array, copy_stream):
+        """Copy a host numpy array / CPU tensor into the next slot; returns (dev_ptr, slot)."""
+        import numpy as np
+        a = np.ascontiguousarray(host_array)
+        dev = C.c_void_p()
+        sid = C.c_int32()
+        check(lib().rw_queue_push(self._q, C.c_void_p(a.ctypes.data), a.nbytes,
+                                  C.c_void_p(copy_stream.cuda_stream), C.byref(dev), C.byref(sid)),
+              "rw_queue_push")
+        return dev.value, sid.value
+
+    def wait(self, slot, compute_stream):
+        check(lib().rw_queue_wait(self._q, slot, C.c_void_p(compute_stream.cuda_stream)), "rw_queue_wait")
+
+    def release(self, slot, compute_stream):
+        check(lib().rw_queue_release(self._q, slot, C.c_void_p(compute_stream.cuda_stream)), "rw_queue_release")
+
+    def close(self):
+        if self._q:
+            lib().rw_queue_destroy(self._q)
+            self._q = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def device_view(ptr, shape, dtype, device):
+    """Wrap a raw device pointer (e.g. a queue slot) as a torch tensor without copying."""
+    import numpy as np
+    n = int(np.prod(shape))
+    itemsize = torch.tensor([], dtype=dtype).element_size()
+
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": (n * itemsize,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+    t = torch.as_tensor(_Holder(), device=device)
+    return t.view(dtype).view(shape)

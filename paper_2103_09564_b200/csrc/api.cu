@@ -1,0 +1,336 @@
+// api.cu -- the C ABI of include/rw.h: validation, workspace carving, launch orchestration.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/rw.h"
+#include "rw_common.cuh"
+
+namespace rw {
+cudaError_t launch_pyramid_group(const void*, int, int, int, int, int, int, int, const PyrOut&,
+                                 cudaStream_t);
+cudaError_t launch_weights(const void*, int, float, float, int, int, int, int, float, float,
+                           float*, float*, const uint8_t*, int, cudaStream_t);
+cudaError_t launch_dinv(const float*, int, int, int, int, const uint8_t*, float*, int, cudaStream_t);
+cudaError_t launch_setup(const Plan&, const Bufs&, cudaStream_t);
+cudaError_t launch_iteration_A(const Plan&, const Bufs&, const Ctl&, int, cudaStream_t);
+cudaError_t launch_iteration_B(const Plan&, const Bufs&, int, cudaStream_t);
+cudaError_t launch_finalize(const Plan&, const Bufs&, const Ctl&, float*, int*, uint8_t*, cudaStream_t);
+cudaError_t launch_labels_prep(const uint8_t*, long long, int, uint8_t*, float*, int, cudaStream_t);
+cudaError_t launch_argmax(const float*, long long, int, uint8_t*, int, cudaStream_t);
+}  // namespace rw
+
+namespace {
+
+thread_local std::string g_err;
+
+rw_status fail(rw_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define RW_CK(call)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(RW_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),        \
+                  __FILE__, __LINE__);                                                     \
+  } while (0)
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+// Tiling depends only on the brick dims (never on the batch), so a brick's fp64 partial
+// sums -- and therefore its bits -- are identical whether it is solved alone or batched.
+rw::Plan make_plan(int B, rw_dims d, int R) {
+  rw::Plan P;
+  P.nx = d.nx; P.ny = d.ny; P.nz = d.nz;
+  P.n = (long long)d.nx * d.ny * d.nz;
+  P.B = B; P.R = R;
+  P.tpx = d.nx / 4 < 16 ? d.nx / 4 : 16;
+  P.TX = 4 * P.tpx;
+  P.TY = RW_THREADS / P.tpx;
+  P.TXP = P.TX + 8;
+  P.tiles_x = (d.nx + P.TX - 1) / P.TX;
+  P.tiles_y = (d.ny + P.TY - 1) / P.TY;
+  int zc = 64;
+  while (zc > 8 && P.tiles_x * P.tiles_y * ((d.nz + zc - 1) / zc) < 4) zc /= 2;
+  P.ZC = zc;
+  P.tiles_z = (d.nz + zc - 1) / zc;
+  P.U = P.tiles_x * P.tiles_y * P.tiles_z;
+  return P;
+}
+
+struct Layout {
+  size_t W, dinv, r, p0, p1, q, PA, PB, PS, status, ctr, fixed, values, total;
+};
+
+size_t up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Layout layout(const rw::Plan& P, bool weights_given, int label_K) {
+  Layout L{};
+  const size_t BN = (size_t)P.B * P.n, RBN = (size_t)P.R * BN, RB = (size_t)P.R * P.B;
+  size_t o = 0;
+  L.W = o;      o += weights_given ? 0 : up(3 * BN * sizeof(float));
+  L.dinv = o;   o += up(BN * sizeof(float));
+  L.r = o;      o += up(RBN * sizeof(float));
+  L.p0 = o;     o += up(RBN * sizeof(float));
+  L.p1 = o;     o += up(RBN * sizeof(float));
+  L.q = o;      o += up(RBN * sizeof(float));
+  L.PA = o;     o += up(2 * RB * P.U * sizeof(double));
+  L.PB = o;     o += up(2 * RB * P.U * sizeof(double2));
+  L.PS = o;     o += up(RB * P.U * sizeof(double4));
+  L.status = o; o += up(RB * sizeof(int));
+  L.ctr = o;    o += up(2 * sizeof(int));
+  L.fixed = o;  o += label_K ? up(BN) : 0;
+  L.values = o; o += label_K ? up((size_t)(label_K - 1) * BN * sizeof(float)) : 0;
+  L.total = o;
+  return L;
+}
+
+bool dims_ok(rw_dims d) { return d.nx >= 4 && d.ny >= 1 && d.nz >= 1 && d.nx % 4 == 0; }
+
+struct Pinned {
+  int* h = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  ~Pinned() {}
+};
+thread_local Pinned g_pin;
+
+rw_status ensure_pinned() {
+  if (g_pin.h) return RW_OK;
+  RW_CK(cudaHostAlloc((void**)&g_pin.h, 64, cudaHostAllocDefault));
+  RW_CK(cudaEventCreateWithFlags(&g_pin.ev[0], cudaEventDisableTiming));
+  RW_CK(cudaEventCreateWithFlags(&g_pin.ev[1], cudaEventDisableTiming));
+  return RW_OK;
+}
+
+// Core solve with fixed/values already on the device.
+rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, rw_norm nm,
+                     const float* W, const uint8_t* fixed, const float* values, int32_t nrhs,
+                     float beta, float eps, float tol, int32_t max_iter, int32_t tol_mode,
+                     const float* x0, char* ws, const Layout& Lw, const rw::Plan& P,
+                     float* prob, int32_t* iters, float* resid, int32_t* status,
+                     uint8_t* labels, cudaStream_t s) {
+  const int sms = num_sms();
+  rw::Bufs Bf{};
+  float* Wd = W ? const_cast<float*>(W) : reinterpret_cast<float*>(ws + Lw.W);
+  float* dinv = reinterpret_cast<float*>(ws + Lw.dinv);
+  if (vol) {
+    RW_CK(rw::launch_weights(vol, dtype, nm.scale, nm.offset, batch, d.nx, d.ny, d.nz, beta,
+                             eps, Wd, dinv, fixed, sms, s));
+  } else {
+    RW_CK(rw::launch_dinv(W, batch, d.nx, d.ny, d.nz, fixed, dinv, sms, s));
+  }
+  Bf.W = Wd;
+  Bf.dinv = dinv;
+  Bf.fixed = fixed;
+  Bf.values = values;
+  Bf.x0 = x0;
+  Bf.x = prob;
+  Bf.r = reinterpret_cast<float*>(ws + Lw.r);
+  Bf.p0 = reinterpret_cast<float*>(ws + Lw.p0);
+  Bf.p1 = reinterpret_cast<float*>(ws + Lw.p1);
+  Bf.q = reinterpret_cast<float*>(ws + Lw.q);
+  Bf.PA = reinterpret_cast<double*>(ws + Lw.PA);
+  Bf.PB = reinterpret_cast<double2*>(ws + Lw.PB);
+  Bf.PS = reinterpret_cast<double4*>(ws + Lw.PS);
+  Bf.status = reinterpret_cast<int*>(ws + Lw.status);
+  Bf.iters = iters;
+  Bf.ctr = reinterpret_cast<int*>(ws + Lw.ctr);
+  rw::Ctl C{tol, tol_mode, max_iter};
+  RW_CK(cudaMemsetAsync(Bf.status, 0, (size_t)P.R * P.B * sizeof(int), s));
+  RW_CK(rw::launch_setup(P, Bf, s));
+  rw_status st = ensure_pinned();
+  if (st != RW_OK) return st;
+  // Host-polled loop: every CHECK iterations the active-pair count is copied to pinned
+  // memory; the host waits only on the previous checkpoint, so it stays <= 2*CHECK
+  // iterations ahead of the GPU and stops launching once a checkpoint reads 0.
+  const int CHECK = 8;
+  int j = 0;
+  for (int k = 0; k <= max_iter; ++k) {
+    RW_CK(cudaMemsetAsync(Bf.ctr + (k & 1), 0, sizeof(int), s));
+    RW_CK(rw::launch_iteration_A(P, Bf, C, k, s));
+    if (k < max_iter) RW_CK(rw::launch_iteration_B(P, Bf, k, s));
+    if (k % CHECK == CHECK - 1 || k == max_iter) {
+      const int slot = j & 1;
+      RW_CK(cudaMemcpyAsync(g_pin.h + slot, Bf.ctr + (k & 1), sizeof(int),
+                            cudaMemcpyDeviceToHost, s));
+      RW_CK(cudaEventRecord(g_pin.ev[slot], s));
+      if (j >= 1) {
+        RW_CK(cudaEventSynchronize(g_pin.ev[slot ^ 1]));
+        if (g_pin.h[slot ^ 1] == 0) break;
+      }
+      ++j;
+    }
+  }
+  RW_CK(rw::launch_finalize(P, Bf, C, resid, status, labels, s));
+  return RW_OK;
+}
+
+}  // namespace
+
+namespace rw {
+void set_last_error(const char* msg) { g_err = msg; }
+}  // namespace rw
+
+extern "C" {
+
+const char* rw_last_error(void) { return g_err.c_str(); }
+const char* rw_version(void) { return "librw 0.1 (sm_100a)"; }
+
+rw_status rw_brick_weights(const void* vol, rw_dtype dtype, rw_norm nm, int32_t batch,
+                           rw_dims d, float beta, float eps, float* W, float* dinv,
+                           const uint8_t* fixed, void* stream) {
+  if (!vol || !W) return fail(RW_EINVAL, "rw_brick_weights: vol and W must be non-NULL");
+  if (!dims_ok(d) || batch < 1) return fail(RW_EINVAL, "rw_brick_weights: bad dims/batch");
+  if (dtype < RW_U8 || dtype > RW_F32) return fail(RW_EINVAL, "rw_brick_weights: bad dtype");
+  if (!(eps > 0.f) || !(beta >= 0.f)) return fail(RW_EINVAL, "rw_brick_weights: need eps > 0, beta >= 0");
+  if (!aligned16(W) || (dinv && !aligned16(dinv)) || !aligned16(vol))
+    return fail(RW_EINVAL, "rw_brick_weights: pointers must be 16-byte aligned");
+  RW_CK(rw::launch_weights(vol, dtype, nm.scale, nm.offset, batch, d.nx, d.ny, d.nz, beta, eps,
+                           W, dinv, fixed, num_sms(), (cudaStream_t)stream));
+  return RW_OK;
+}
+
+size_t rw_solve_workspace_bytes(int32_t batch, rw_dims d, int32_t nrhs, int32_t weights_given) {
+  if (!dims_ok(d) || batch < 1 || nrhs < 1) return 0;
+  return layout(make_plan(batch, d, nrhs), weights_given != 0, 0).total;
+}
+
+size_t rw_solve_labels_workspace_bytes(int32_t batch, rw_dims d, int32_t K, int32_t weights_given) {
+  if (!dims_ok(d) || batch < 1 || K < 2) return 0;
+  return layout(make_plan(batch, d, K - 1), weights_given != 0, K).total;
+}
+
+static rw_status validate_solve(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype,
+                                const float* W, int32_t nrhs, float eps, float tol,
+                                int32_t max_iter, int32_t tol_mode, void* ws) {
+  if (batch < 1) return fail(RW_EINVAL, "batch must be >= 1");
+  if (!dims_ok(d)) return fail(RW_EINVAL, "dims must be >= 1 with nx >= 4 and nx %% 4 == 0");
+  if ((vol == nullptr) == (W == nullptr)) return fail(RW_EINVAL, "exactly one of vol / W must be given");
+  if (vol && (dtype < RW_U8 || dtype > RW_F32)) return fail(RW_EINVAL, "bad dtype");
+  if (vol && !(eps > 0.f)) return fail(RW_EINVAL, "eps must be > 0");
+  if (nrhs < 1 || nrhs > 64) return fail(RW_EINVAL, "nrhs must be in 1..64");
+  if (!(tol > 0.f)) return fail(RW_EINVAL, "tol must be > 0");
+  if (max_iter < 1) return fail(RW_EINVAL, "max_iter must be >= 1");
+  if (tol_mode != 0 && tol_mode != 1) return fail(RW_EINVAL, "tol_mode must be 0 or 1");
+  if (((uintptr_t)ws & 255u) != 0) return fail(RW_EINVAL, "workspace must be 256-byte aligned");
+  return RW_OK;
+}
+
+rw_status rw_solve_bricks(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype,
+                          rw_norm nm, const float* W, const uint8_t* fixed,
+                          const float* values, int32_t nrhs, float beta, float eps,
+                          float tol, int32_t max_iter, int32_t tol_mode, const float* x0,
+                          void* workspace, size_t ws_bytes, float* prob, int32_t* iters,
+                          float* resid, int32_t* status, uint8_t* labels, void* stream) {
+  rw_status v = validate_solve(batch, d, vol, dtype, W, nrhs, eps, tol, max_iter, tol_mode, workspace);
+  if (v != RW_OK) return v;
+  if (!fixed || !values || !prob || !iters || !workspace)
+    return fail(RW_EINVAL, "fixed, values, prob, iters and workspace must be non-NULL");
+  const void* ptrs[] = {vol, W, fixed, values, x0, prob, labels};
+  for (const void* p : ptrs)
+    if (p && !aligned16(p)) return fail(RW_EINVAL, "device pointers must be 16-byte aligned");
+  const rw::Plan P = make_plan(batch, d, nrhs);
+  const Layout Lw = layout(P, W != nullptr, 0);
+  if (ws_bytes < Lw.total)
+    return fail(RW_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, Lw.total);
+  return solve_core(batch, d, vol, dtype, nm, W, fixed, values, nrhs, beta, eps, tol, max_iter,
+                    tol_mode, x0, (char*)workspace, Lw, P, prob, iters, resid, status, labels,
+                    (cudaStream_t)stream);
+}
+
+rw_status rw_solve_labels(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype,
+                          rw_norm nm, const float* W, const uint8_t* seeds, int32_t K,
+                          float beta, float eps, float tol, int32_t max_iter,
+                          int32_t tol_mode, void* workspace, size_t ws_bytes, float* prob,
+                          int32_t* iters, float* resid, uint8_t* labels, void* stream) {
+  if (K < 2 || K > 65) return fail(RW_EINVAL, "K must be in 2..65");
+  rw_status v = validate_solve(batch, d, vol, dtype, W, K - 1, eps, tol, max_iter, tol_mode, workspace);
+  if (v != RW_OK) return v;
+  if (!seeds || !prob || !iters || !labels || !workspace)
+    return fail(RW_EINVAL, "seeds, prob, iters, labels and workspace must be non-NULL");
+  const void* ptrs[] = {vol, W, seeds, prob, labels};
+  for (const void* p : ptrs)
+    if (p && !aligned16(p)) return fail(RW_EINVAL, "device pointers must be 16-byte aligned");
+  const rw::Plan P = make_plan(batch, d, K - 1);
+  const Layout Lw = layout(P, W != nullptr, K);
+  if (ws_bytes < Lw.total)
+    return fail(RW_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, Lw.total);
+  char* ws = (char*)workspace;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* fixed = reinterpret_cast<uint8_t*>(ws + Lw.fixed);
+  float* values = reinterpret_cast<float*>(ws + Lw.values);
+  const long long BN = (long long)batch * P.n;
+  RW_CK(rw::launch_labels_prep(seeds, BN, K, fixed, values, num_sms(), s));
+  rw_status st = solve_core(batch, d, vol, dtype, nm, W, fixed, values, K - 1, beta, eps, tol,
+                            max_iter, tol_mode, nullptr, ws, Lw, P, prob, iters, resid, nullptr,
+                            nullptr, s);
+  if (st != RW_OK) return st;
+  RW_CK(rw::launch_argmax(prob, BN, K, labels, num_sms(), s));
+  return RW_OK;
+}
+
+static size_t dtype_size(rw_dtype t) { return t == RW_U8 ? 1 : (t == RW_F32 ? 4 : 2); }
+
+rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int32_t z0,
+                                int32_t nzs, int32_t levels, void* const* level_out,
+                                void* stream) {
+  if (!slab || !level_out) return fail(RW_EINVAL, "rw_build_pyramid: NULL pointer");
+  if (d.nx < 1 || d.ny < 1 || d.nz < 1) return fail(RW_EINVAL, "rw_build_pyramid: dims must be >= 1");
+  if (dtype < RW_U8 || dtype > RW_F32) return fail(RW_EINVAL, "rw_build_pyramid: bad dtype");
+  if (levels < 1 || levels > 16) return fail(RW_EINVAL, "rw_build_pyramid: levels must be in 1..16");
+  const long long step = 1LL << levels;
+  if (z0 < 0 || nzs < 1 || z0 + nzs > d.nz || (z0 % step) != 0 ||
+      ((nzs % step) != 0 && z0 + nzs != d.nz))
+    return fail(RW_EINVAL, "rw_build_pyramid_slab: z0 must be a multiple of 2^levels and nzs a "
+                "multiple of 2^levels unless the slab ends the volume");
+  for (int l = 0; l < levels; ++l)
+    if (!level_out[l]) return fail(RW_EINVAL, "rw_build_pyramid: level_out[%d] is NULL", l);
+  cudaStream_t s = (cudaStream_t)stream;
+  // level dims
+  int nx[17], ny[17], nz[17];
+  nx[0] = d.nx; ny[0] = d.ny; nz[0] = d.nz;
+  for (int l = 1; l <= levels; ++l) {
+    nx[l] = (nx[l - 1] + 1) / 2; ny[l] = (ny[l - 1] + 1) / 2; nz[l] = (nz[l - 1] + 1) / 2;
+  }
+  const void* in = slab;
+  int lz0 = z0, lzc = nzs;
+  for (int l0 = 0; l0 < levels; l0 += 5) {
+    const int L = levels - l0 < 5 ? levels - l0 : 5;
+    rw::PyrOut o{};
+    for (int k = 0; k < L; ++k) {
+      o.p[k] = level_out[l0 + k];
+      o.nx[k] = nx[l0 + k + 1]; o.ny[k] = ny[l0 + k + 1]; o.nz[k] = nz[l0 + k + 1];
+    }
+    RW_CK(rw::launch_pyramid_group(in, dtype, nx[l0], ny[l0], nz[l0], lz0, lzc, L, o, s));
+    // next group reads the coarsest level just written, restricted to this slab's planes
+    const int nlz0 = lz0 >> L;
+    const int nlzc = ((lz0 + lzc + (1 << L) - 1) >> L) - nlz0;
+    const size_t plane = (size_t)nx[l0 + L] * ny[l0 + L] * dtype_size(dtype);
+    in = (const char*)level_out[l0 + L - 1] + (size_t)nlz0 * plane;
+    lz0 = nlz0;
+    lzc = nlzc;
+  }
+  return RW_OK;
+}
+
+rw_status rw_build_pyramid(const void* vol, rw_dtype dtype, rw_dims d, int32_t levels,
+                           void* const* level_out, void* stream) {
+  return rw_build_pyramid_slab(vol, dtype, d, 0, d.nz, levels, level_out, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// queue.cu -- SURVEY §8(a) row a9: pinned, double-buffered host->device brick queue.
+//
+// North star item 5 / P:105 ("constant memory", brick-wise loading): inputs larger than
+// HBM stream through a ring of `depth` slots.  Each slot = one pinned host buffer + one
+// device buffer + two events: `ready` (H2D copy done, recorded on the copy stream) and
+// `freed` (its consumers done, recorded on the compute stream).  With depth >= 2 the H2D
+// copy of slot k+1 overlaps the kernels consuming slot k; the host-side staging copy of
+// slot k+2 overlaps both.
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/rw.h"
+
+struct rw_queue {
+  size_t slot_bytes = 0;
+  int depth = 0;
+  int next = 0;
+  std::vector<void*> host, dev;
+  std::vector<cudaEvent_t> ready, freed;
+  std::vector<bool> used;
+};
+
+namespace rw { void set_last_error(const char* msg); }
+
+namespace {
+rw_status qfail(rw_status s, const char* m) { rw::set_last_error(m); return s; }
+
+void parallel_copy(void* dst, const void* src, size_t bytes) {
+  const size_t chunk = 64u << 20;
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt > 16) nt = 16;
+  if (bytes < chunk || nt < 2) { std::memcpy(dst, src, bytes); return; }
+  size_t per = (bytes + nt - 1) / nt;
+  per = (per + 4095) & ~(size_t)4095;
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t) {
+    const size_t o = (size_t)t * per;
+    if (o >= bytes) break;
+    const size_t n = (o + per > bytes) ? bytes - o : per;
+    th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, n); });
+  }
+  for (auto& x : th) x.join();
+}
+}  // namespace
+
+extern "C" rw_status rw_queue_create(size_t slot_bytes, int32_t depth, rw_queue** q) {
+  if (!q || depth < 2 || depth > 64 || slot_bytes == 0)
+    return qfail(RW_EINVAL, "rw_queue_create: need q != NULL, 2 <= depth <= 64, slot_bytes > 0");
+  rw_queue* Q = new rw_queue;
+  Q->slot_bytes = slot_bytes;
+  Q->depth = depth;
+  for (int i = 0; i < depth; ++i) {
+    void *h = nullptr, *d = nullptr;
+    cudaEvent_t a, b;
+    if (cudaHostAlloc(&h, slot_bytes, cudaHostAllocDefault) != cudaSuccess ||
+        cudaMalloc(&d, slot_bytes) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b, cudaEventDisableTiming) != cudaSuccess) {
+      if (h) cudaFreeHost(h);
+      if (d) cudaFree(d);
+      rw_queue_destroy(Q);
+      return qfail(RW_ENOMEM, "rw_queue_create: pinned/device allocation failed");
+    }
+    Q->host.push_back(h);
+    Q->dev.push_back(d);
+    Q->ready.push_back(a);
+    Q->freed.push_back(b);
+    Q->used.push_back(false);
+  }
+  *q = Q;
+  return RW_OK;
+}
+
+extern "C" rw_status rw_queue_push(rw_queue* q, const void* host_src, size_t bytes,
+                                   void* copy_stream, void** dev_slot, int32_t* slot_id) {
+  if (!q || !host_src || !dev_slot || bytes > q->slot_bytes)
+    return qfail(RW_EINVAL, "rw_queue_push: bad arguments or bytes > slot_bytes");
+  const int s = q->next;
+  q->next = (q->next + 1) % q->depth;
+  // the slot's previous H2D copy must be done (host buffer reuse) and its consumers must
+  // have released it (device buffer reuse)
+  if (q->used[s] && (cudaEventSynchronize(q->ready[s]) != cudaSuccess ||
+                     cudaEventSynchronize(q->freed[s]) != cudaSuccess))
+    return qfail(RW_ECUDA, "rw_queue_push: waiting for slot release failed");
+  parallel_copy(q->host[s], host_src, bytes);
+  cudaStream_t cs = (cudaStream_t)copy_stream;
+  if (cudaMemcpyAsync(q->dev[s], q->host[s], bytes, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+      cudaEventRecord(q->ready[s], cs) != cudaSuccess)
+    return qfail(RW_ECUDA, "rw_queue_push: H2D copy enqueue failed");
+  q->used[s] = true;
+  *dev_slot = q->dev[s];
+  if (slot_id) *slot_id = s;
+  return RW_OK;
+}
+
+extern "C" rw_status rw_queue_wait(rw_queue* q, int32_t slot_id, void* compute_stream) {
+  if (!q || slot_id < 0 || slot_id >= q->depth) return qfail(RW_EINVAL, "rw_queue_wait: bad slot");
+  if (cudaStreamWaitEvent((cudaStream_t)compute_stream, q->ready[slot_id], 0) != cudaSuccess)
+    return qfail(RW_ECUDA, "rw_queue_wait: cudaStreamWaitEvent failed");
+  return RW_OK;
+}
+
+extern "C" rw_status rw_queue_release(rw_queue* q, int32_t slot_id, void* compute_stream) {
+  if (!q || slot_id < 0 || slot_id >= q->depth) return qfail(RW_EINVAL, "rw_queue_release: bad slot");
+  if (cudaEventRecord(q->freed[slot_id], (cudaStream_t)compute_stream) != cudaSuccess)
+    return qfail(RW_ECUDA, "rw_queue_release: cudaEventRecord failed");
+  return RW_OK;
+}
+
+extern "C" void rw_queue_destroy(rw_queue* q) {
+  if (!q) return;
+  for (size_t i = 0; i < q->host.size(); ++i) {
+    cudaEventSynchronize(q->freed[i]);
+    cudaFreeHost(q->host[i]);
+    cudaFree(q->dev[i]);
+    cudaEventDestroy(q->ready[i]);
+    cudaEventDestroy(q->freed[i]);
+  }
+  delete q;
+}
