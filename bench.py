@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 random walker hot path (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {b200,reference}]
+
+One step = one ``rw_solve_bricks`` call on the whole config-2 batch (512 independent
+64^3 u16 bricks): weights from intensities (a1/a2), implicit assembly (a3), the fused
+Jacobi-PCG loop until every brick has converged (a4/a5), finalise + labels (a6).  Inputs
+are resident in HBM; the per-iteration working set (7.5 GB) is far larger than L2, so no
+L2 flush is needed between steps.  value = voxel-CG-iterations/s over all ranks
+(sum_b n_b * iters_b / step time), weak scaling (each rank solves its own 512 bricks).
+
+--impl reference times the fp64 oracle (oracle/, numpy+scipy) on the host cores on a
+bounded sample of the same workload -- this tier's reference arm (no reference code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "voxel-CG-iterations/s"
+UNIT = "voxel-CG-iter/s"
+WORKLOAD = "cfg2: 512 x 64^3 u16 bricks, 1-5 blobs, Dirichlet shell, 0.1% seeds, beta=100, tol=1e-6 rel, max_iter=2000"
+BATCH, N = 512, 64
+# algorithmic bytes per active voxel per launch: pass A reads r, p, dinv, x,
+# Wx, Wy, Wz and writes p, x, q (k = 0: no x traffic); pass B reads r, q, dinv, writes r
+BYTES_A, BYTES_A0, BYTES_B = 40, 32, 16
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def make_inputs(rank, workers):
+    import workloads as wl
+    ids = list(range(rank * BATCH, (rank + 1) * BATCH))
+    t = time.time()
+    p = wl.cfg2(bricks=ids, n=N, workers=workers)
+    log(f"[rank {rank}] generated {len(ids)} bricks in {time.time() - t:.1f}s")
+    return p
+
+
+def cpu_oracle_sample(nbricks, seed0=0):
+    """Time the fp64 oracle (as it stands) on ``nbricks`` bricks of the same workload at the
+    same tolerance; returns (voxel-iter/s, seconds, voxel-iterations, threads used)."""
+    import workloads as wl
+    from oracle import rw_oracle as ro
+    from threadpoolctl import threadpool_limits
+    p = wl.cfg2(bricks=list(range(seed0, seed0 + nbricks)), n=N)
+    with threadpool_limits(1):
+        t = time.perf_counter()
+        o = ro.solve_problem(p, tol=p.tol, max_iter=p.max_iter)
+        dt = time.perf_counter() - t
+    vi = float(np.sum(o["iters"])) * N ** 3
+    return vi / dt, dt, vi, 1
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    nb = 3
+    vals, tot_t = [], 0.0
+    for s in range(args.warmup + args.steps):
+        v, dt, vi, cores = cpu_oracle_sample(nb, seed0=(s * nb) % BATCH)
+        if s >= args.warmup:
+            vals.append(v)
+            tot_t += dt
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * tot_t / max(1, args.steps), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": f"{nb} bricks of 64^3 per step (of 512)",
+                   "parallelism": "single host thread"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{nb} cfg2 bricks per step, fp64 CSR Jacobi-PCG to rel 1e-6"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import paper_2103_09564_b200 as rwb
+    from paper_2103_09564_b200 import api
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    p = make_inputs(rank, args.workers)
+    vol = torch.from_numpy(p.vol).to(dev)
+    fixed = torch.from_numpy(p.fixed).to(dev)
+    values = torch.from_numpy(p.values).to(dev)
+    need = rwb.solve_workspace_bytes(BATCH, (N, N, N), 1)
+    ws = api.alloc_workspace(need, dev)
+    out = dict(prob=torch.empty_like(values),
+               iters=torch.empty((1, BATCH), dtype=torch.int32, device=dev),
+               resid=torch.empty((1, BATCH), dtype=torch.float32, device=dev),
+               status=torch.empty((1, BATCH), dtype=torch.int32, device=dev),
+               labels=torch.empty(tuple(fixed.shape), dtype=torch.uint8, device=dev))
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        rwb.solve_bricks(fixed, values, vol=vol, beta=p.beta, eps=p.eps, tol=p.tol,
+                         max_iter=p.max_iter, workspace=ws, out=out, stream=stream)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    iters = out["iters"].cpu().numpy().astype(np.int64)
+    assert (out["status"].cpu().numpy() == 1).all(), "not all bricks converged"
+    vox_iters = float(iters.sum()) * N ** 3
+
+    # ---------------- device-timed region (inputs resident) ----------------
+    clk = Clocks(local_rank)
+    api.profile_enable(True)
+    barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    prof = api.profile_read()
+    api.profile_enable(False)
+    t_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    ms_per_step = t_max / args.steps
+    value = vox_iters * world / (ms_per_step / 1000.0)
+
+    # ---------------- roofline of the dominant kernel ----------------
+    launches = {k: v[0] for k, v in prof.items()}
+    kms = {k: v[1] for k, v in prof.items()}
+    dom = max(("passA", "passB"), key=lambda k: kms[k])
+    nbr = BATCH
+    vox = float(N ** 3)
+    # algorithmic bytes: every active (brick, iteration) pays BYTES per voxel
+    alg_A = args.steps * (BYTES_A * vox_iters - (BYTES_A - BYTES_A0) * vox * nbr)
+    alg_B = args.steps * BYTES_B * vox_iters
+    alg = {"passA": alg_A, "passB": alg_B}
+    peak, peak_kind = measured_peak()
+    achieved = alg[dom] / (kms[dom] / 1000.0) / 1e9
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            with open(tr_path) as f:
+                traffic = json.load(f).get(dom)
+        except Exception:
+            traffic = None
+
+    # ---------------- end to end through the API with host buffers ----------------
+    h_vol = torch.from_numpy(p.vol).pin_memory()
+    h_fixed = torch.from_numpy(p.fixed).pin_memory()
+    h_values = torch.from_numpy(p.values).pin_memory()
+    h_labels = torch.empty(tuple(fixed.shape), dtype=torch.uint8).pin_memory()
+    h_iters = torch.empty((1, BATCH), dtype=torch.int32).pin_memory()
+    d_vol, d_fixed, d_values = torch.empty_like(vol), torch.empty_like(fixed), torch.empty_like(values)
+
+    def e2e_step():
+        d_vol.copy_(h_vol, non_blocking=True)
+        d_fixed.copy_(h_fixed, non_blocking=True)
+        d_values.copy_(h_values, non_blocking=True)
+        rwb.solve_bricks(d_fixed, d_values, vol=d_vol, beta=p.beta, eps=p.eps, tol=p.tol,
+                         max_iter=p.max_iter, workspace=ws, out=out, stream=stream)
+        h_labels.copy_(out["labels"], non_blocking=True)
+        h_iters.copy_(out["iters"], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ems], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e_value = vox_iters * world / (ems / args.steps / 1000.0)
+    h2d = h_vol.numel() * h_vol.element_size() + h_fixed.numel() + h_values.numel() * 4
+    d2h = h_labels.numel() + h_iters.numel() * 4
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, dt, vi, cores = cpu_oracle_sample(args.cpu_bricks)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{args.cpu_bricks} cfg2 bricks (64^3) at rel tol 1e-6, {dt:.1f}s, "
+                         "fp64 numpy/scipy CSR Jacobi-PCG, 1 thread"}
+    gpu_launches = sum(launches.values())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "batch_per_gpu": BATCH, "brick": [N, N, N],
+                   "global_batch": BATCH * world, "parallelism": f"bricks sharded over {world} GPU(s), no collective",
+                   "l2": "inputs larger than L2 (7.5 GB per-iteration working set), no flush",
+                   "iters": {"min": int(iters.min()), "median": float(np.median(iters)),
+                             "max": int(iters.max())}},
+        "bricks_per_s": BATCH * world / (ms_per_step / 1000.0),
+        "full_solve_ms": ms_per_step,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "per_kernel_ms_per_step": {k: v / args.steps for k, v in kms.items() if v > 0},
+                     "alg_bytes_per_voxel_iter": {"passA": BYTES_A, "passB": BYTES_B}},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps},
+        "gpu_launches": int(gpu_launches),
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workers", type=int, default=min(16, os.cpu_count() or 1))
+    ap.add_argument("--cpu-bricks", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

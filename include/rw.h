@@ -183,6 +183,19 @@ rw_status rw_queue_wait(rw_queue* q, int32_t slot_id, void* compute_stream);
 rw_status rw_queue_release(rw_queue* q, int32_t slot_id, void* compute_stream);
 void rw_queue_destroy(rw_queue* q);
 
+/* ------------------------------------------------------------------------------------
+ * Instrumentation.  Every kernel launch made by librw is counted per kernel class
+ * (always on, host-side counter).  With rw_profile_enable(1) each launch is additionally
+ * bracketed by CUDA events recorded on the stream it is launched on; rw_profile_read
+ * synchronises the pending events and returns the summed device time per class.
+ * rw_profile_enable(on) also resets both tallies.  Not thread-safe (one solver thread).
+ *   launches  out host int64[RW_K_COUNT] or NULL;  ms  out host double[RW_K_COUNT] or NULL.
+ * ---------------------------------------------------------------------------------- */
+enum { RW_K_WEIGHTS = 0, RW_K_SETUP = 1, RW_K_PASSA = 2, RW_K_PASSB = 3, RW_K_FINALIZE = 4,
+       RW_K_PYRAMID = 5, RW_K_OTHER = 6, RW_K_COUNT = 7 };
+rw_status rw_profile_enable(int32_t on);
+rw_status rw_profile_read(int64_t* launches, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,7 +40,11 @@ SIGNATURES = {
     "rw_queue_wait": (I32, [P, I32, P]),
     "rw_queue_release": (I32, [P, I32, P]),
     "rw_queue_destroy": (None, [P]),
+    "rw_profile_enable": (I32, [I32]),
+    "rw_profile_read": (I32, [P, P]),
 }
+
+KERNEL_CLASSES = ["weights", "setup", "passA", "passB", "finalize", "pyramid", "other"]
 
 
 def header_symbols(path: str = HEADER):

@@ -228,3 +228,18 @@ def device_view(ptr, shape, dtype, device):
             "shape": (n * itemsize,), "typestr": "|u1", "data": (ptr, False), "version": 3}
     t = torch.as_tensor(_Holder(), device=device)
     return t.view(dtype).view(shape)
+
+
+def profile_enable(on=True):
+    """Reset the library's launch counters; with on=True also time every launch with CUDA
+    events on its stream (include/rw.h rw_profile_enable)."""
+    check(lib().rw_profile_enable(int(on)), "rw_profile_enable")
+
+
+def profile_read():
+    """-> {kernel class: (launches, device ms)} since the last profile_enable()."""
+    from ._lib import KERNEL_CLASSES
+    n = (C.c_int64 * len(KERNEL_CLASSES))()
+    ms = (C.c_double * len(KERNEL_CLASSES))()
+    check(lib().rw_profile_read(C.cast(n, C.c_void_p), C.cast(ms, C.c_void_p)), "rw_profile_read")
+    return {k: (int(n[i]), float(ms[i])) for i, k in enumerate(KERNEL_CLASSES)}

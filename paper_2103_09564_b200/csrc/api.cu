@@ -3,6 +3,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/rw.h"
 #include "rw_common.cuh"
@@ -117,6 +119,56 @@ rw_status ensure_pinned() {
   return RW_OK;
 }
 
+// ------------------------------------------------------------------ instrumentation
+// Launch counts per kernel class (always) and, when enabled, CUDA events bracketing each
+// launch on its own stream; read() synchronises the pending pairs and sums their times.
+struct Prof {
+  bool on = false;
+  long long launches[RW_K_COUNT] = {};
+  double ms[RW_K_COUNT] = {};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t open = nullptr;
+  void begin(cudaStream_t s) {
+    if (!on) return;
+    open = get();
+    cudaEventRecord(open, s);
+  }
+  void end(int kind, cudaStream_t s, int n = 1) {
+    launches[kind] += n;
+    if (!on) return;
+    cudaEvent_t e = get();
+    cudaEventRecord(e, s);
+    pending.push_back({kind, {open, e}});
+    if (pending.size() > 4096) drain();
+  }
+  void drain() {
+    for (auto& p : pending) {
+      cudaEventSynchronize(p.second.second);
+      float t = 0.f;
+      cudaEventElapsedTime(&t, p.second.first, p.second.second);
+      ms[p.first] += t;
+      pool.push_back(p.second.first);
+      pool.push_back(p.second.second);
+    }
+    pending.clear();
+  }
+};
+Prof g_prof;
+
+#define RW_TIMED(kind, s, n, call)   \
+  do {                               \
+    g_prof.begin(s);                 \
+    RW_CK(call);                     \
+    g_prof.end(kind, s, n);          \
+  } while (0)
+
 // Core solve with fixed/values already on the device.
 rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, rw_norm nm,
                      const float* W, const uint8_t* fixed, const float* values, int32_t nrhs,
@@ -129,10 +181,11 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   float* Wd = W ? const_cast<float*>(W) : reinterpret_cast<float*>(ws + Lw.W);
   float* dinv = reinterpret_cast<float*>(ws + Lw.dinv);
   if (vol) {
-    RW_CK(rw::launch_weights(vol, dtype, nm.scale, nm.offset, batch, d.nx, d.ny, d.nz, beta,
-                             eps, Wd, dinv, fixed, sms, s));
+    RW_TIMED(RW_K_WEIGHTS, s, 1,
+             rw::launch_weights(vol, dtype, nm.scale, nm.offset, batch, d.nx, d.ny, d.nz, beta,
+                                eps, Wd, dinv, fixed, sms, s));
   } else {
-    RW_CK(rw::launch_dinv(W, batch, d.nx, d.ny, d.nz, fixed, dinv, sms, s));
+    RW_TIMED(RW_K_WEIGHTS, s, 1, rw::launch_dinv(W, batch, d.nx, d.ny, d.nz, fixed, dinv, sms, s));
   }
   Bf.W = Wd;
   Bf.dinv = dinv;
@@ -152,7 +205,8 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   Bf.ctr = reinterpret_cast<int*>(ws + Lw.ctr);
   rw::Ctl C{tol, tol_mode, max_iter};
   RW_CK(cudaMemsetAsync(Bf.status, 0, (size_t)P.R * P.B * sizeof(int), s));
-  RW_CK(rw::launch_setup(P, Bf, s));
+  RW_TIMED(RW_K_SETUP, s, 1, rw::launch_setup(P, Bf, s));
+  const int nchunks = (P.R + 3) / 4;
   rw_status st = ensure_pinned();
   if (st != RW_OK) return st;
   // Host-polled loop: every CHECK iterations the active-pair count is copied to pinned
@@ -162,8 +216,8 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   int j = 0;
   for (int k = 0; k <= max_iter; ++k) {
     RW_CK(cudaMemsetAsync(Bf.ctr + (k & 1), 0, sizeof(int), s));
-    RW_CK(rw::launch_iteration_A(P, Bf, C, k, s));
-    if (k < max_iter) RW_CK(rw::launch_iteration_B(P, Bf, k, s));
+    RW_TIMED(RW_K_PASSA, s, nchunks, rw::launch_iteration_A(P, Bf, C, k, s));
+    if (k < max_iter) RW_TIMED(RW_K_PASSB, s, nchunks, rw::launch_iteration_B(P, Bf, k, s));
     if (k % CHECK == CHECK - 1 || k == max_iter) {
       const int slot = j & 1;
       RW_CK(cudaMemcpyAsync(g_pin.h + slot, Bf.ctr + (k & 1), sizeof(int),
@@ -176,7 +230,7 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       ++j;
     }
   }
-  RW_CK(rw::launch_finalize(P, Bf, C, resid, status, labels, s));
+  RW_TIMED(RW_K_FINALIZE, s, 1, rw::launch_finalize(P, Bf, C, resid, status, labels, s));
   return RW_OK;
 }
 
@@ -189,6 +243,22 @@ void set_last_error(const char* msg) { g_err = msg; }
 extern "C" {
 
 const char* rw_last_error(void) { return g_err.c_str(); }
+
+rw_status rw_profile_enable(int32_t on) {
+  g_prof.drain();
+  g_prof.on = on != 0;
+  for (int k = 0; k < RW_K_COUNT; ++k) { g_prof.launches[k] = 0; g_prof.ms[k] = 0.0; }
+  return RW_OK;
+}
+
+rw_status rw_profile_read(int64_t* launches, double* ms) {
+  g_prof.drain();
+  for (int k = 0; k < RW_K_COUNT; ++k) {
+    if (launches) launches[k] = g_prof.launches[k];
+    if (ms) ms[k] = g_prof.ms[k];
+  }
+  return RW_OK;
+}
 const char* rw_version(void) { return "librw 0.1 (sm_100a)"; }
 
 rw_status rw_brick_weights(const void* vol, rw_dtype dtype, rw_norm nm, int32_t batch,
@@ -200,8 +270,9 @@ rw_status rw_brick_weights(const void* vol, rw_dtype dtype, rw_norm nm, int32_t 
   if (!(eps > 0.f) || !(beta >= 0.f)) return fail(RW_EINVAL, "rw_brick_weights: need eps > 0, beta >= 0");
   if (!aligned16(W) || (dinv && !aligned16(dinv)) || !aligned16(vol))
     return fail(RW_EINVAL, "rw_brick_weights: pointers must be 16-byte aligned");
-  RW_CK(rw::launch_weights(vol, dtype, nm.scale, nm.offset, batch, d.nx, d.ny, d.nz, beta, eps,
-                           W, dinv, fixed, num_sms(), (cudaStream_t)stream));
+  RW_TIMED(RW_K_WEIGHTS, (cudaStream_t)stream, 1,
+           rw::launch_weights(vol, dtype, nm.scale, nm.offset, batch, d.nx, d.ny, d.nz, beta, eps,
+                              W, dinv, fixed, num_sms(), (cudaStream_t)stream));
   return RW_OK;
 }
 
@@ -275,12 +346,12 @@ rw_status rw_solve_labels(int32_t batch, rw_dims d, const void* vol, rw_dtype dt
   uint8_t* fixed = reinterpret_cast<uint8_t*>(ws + Lw.fixed);
   float* values = reinterpret_cast<float*>(ws + Lw.values);
   const long long BN = (long long)batch * P.n;
-  RW_CK(rw::launch_labels_prep(seeds, BN, K, fixed, values, num_sms(), s));
+  RW_TIMED(RW_K_OTHER, s, 1, rw::launch_labels_prep(seeds, BN, K, fixed, values, num_sms(), s));
   rw_status st = solve_core(batch, d, vol, dtype, nm, W, fixed, values, K - 1, beta, eps, tol,
                             max_iter, tol_mode, nullptr, ws, Lw, P, prob, iters, resid, nullptr,
                             nullptr, s);
   if (st != RW_OK) return st;
-  RW_CK(rw::launch_argmax(prob, BN, K, labels, num_sms(), s));
+  RW_TIMED(RW_K_OTHER, s, 1, rw::launch_argmax(prob, BN, K, labels, num_sms(), s));
   return RW_OK;
 }
 
@@ -316,7 +387,8 @@ rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int
       o.p[k] = level_out[l0 + k];
       o.nx[k] = nx[l0 + k + 1]; o.ny[k] = ny[l0 + k + 1]; o.nz[k] = nz[l0 + k + 1];
     }
-    RW_CK(rw::launch_pyramid_group(in, dtype, nx[l0], ny[l0], nz[l0], lz0, lzc, L, o, s));
+    RW_TIMED(RW_K_PYRAMID, s, 1,
+             rw::launch_pyramid_group(in, dtype, nx[l0], ny[l0], nz[l0], lz0, lzc, L, o, s));
     // next group reads the coarsest level just written, restricted to this slab's planes
     const int nlz0 = lz0 >> L;
     const int nlzc = ((lz0 + lzc + (1 << L) - 1) >> L) - nlz0;
