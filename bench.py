@@ -33,9 +33,10 @@ METRIC = "voxel-CG-iterations/s"
 UNIT = "voxel-CG-iter/s"
 WORKLOAD = "cfg2: 512 x 64^3 u16 bricks, 1-5 blobs, Dirichlet shell, 0.1% seeds, beta=100, tol=1e-6 rel, max_iter=2000"
 BATCH, N = 512, 64
-# algorithmic bytes per active voxel per launch: pass A reads r, p, dinv, x,
-# Wx, Wy, Wz and writes p, x, q (k = 0: no x traffic); pass B reads r, q, dinv, writes r
-BYTES_A, BYTES_A0, BYTES_B = 40, 32, 16
+# algorithmic bytes per active voxel per launch.  Pass A (weights recomputed
+# from the u16 intensities, VM_U16) reads r, p, dinv, x (16 B) + the intensity (2 B) and
+# writes p, x, q (12 B); at k = 0 there is no x traffic.  Pass B reads r, q, dinv, writes r.
+BYTES_A, BYTES_A0, BYTES_B = 30, 22, 16
 
 
 def log(*a):

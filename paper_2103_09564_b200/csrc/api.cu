@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/rw.h"
+#include "passA.cuh"
 #include "rw_common.cuh"
 
 namespace rw {
@@ -15,12 +16,13 @@ cudaError_t launch_pyramid_group(const void*, int, int, int, int, int, int, int,
 cudaError_t launch_weights(const void*, int, float, float, int, int, int, int, float, float,
                            float*, float*, const uint8_t*, int, cudaStream_t);
 cudaError_t launch_dinv(const float*, int, int, int, int, const uint8_t*, float*, int, cudaStream_t);
-cudaError_t launch_setup(const Plan&, const Bufs&, cudaStream_t);
-cudaError_t launch_iteration_A(const Plan&, const Bufs&, const Ctl&, int, cudaStream_t);
+cudaError_t launch_setup(const Plan&, const Bufs&, const Ctl&, cudaStream_t);
+cudaError_t launch_iteration_A(const Plan&, const Bufs&, const Ctl&, int, const Maps&, cudaStream_t);
 cudaError_t launch_iteration_B(const Plan&, const Bufs&, int, cudaStream_t);
 cudaError_t launch_finalize(const Plan&, const Bufs&, const Ctl&, float*, int*, uint8_t*, cudaStream_t);
 cudaError_t launch_labels_prep(const uint8_t*, long long, int, uint8_t*, float*, int, cudaStream_t);
 cudaError_t launch_argmax(const float*, long long, int, uint8_t*, int, cudaStream_t);
+int passA_rc(const Plan&);
 }  // namespace rw
 
 namespace {
@@ -54,16 +56,21 @@ int num_sms() {
   return n;
 }
 
-// Tiling depends only on the brick dims (never on the batch), so a brick's fp64 partial
-// sums -- and therefore its bits -- are identical whether it is solved alone or batched.
+// Tiling depends only on the brick dims and nrhs (never on the batch), so a brick's fp64
+// partial sums -- and therefore its bits -- are identical whether it is solved alone or
+// batched.  CTA: tpx threads along x (4 voxels each) x TY rows; 256 threads for one RHS,
+// 128 when several RHS share the operator (their TMA stages are larger).
 rw::Plan make_plan(int B, rw_dims d, int R) {
   rw::Plan P;
   P.nx = d.nx; P.ny = d.ny; P.nz = d.nz;
   P.n = (long long)d.nx * d.ny * d.nz;
   P.B = B; P.R = R;
+  P.threads = R == 1 ? 256 : 128;
   P.tpx = d.nx / 4 < 16 ? d.nx / 4 : 16;
   P.TX = 4 * P.tpx;
-  P.TY = RW_THREADS / P.tpx;
+  P.TY = P.threads / P.tpx < 128 ? P.threads / P.tpx : 128;
+  P.hx = P.TX < d.nx ? 4 : 0;
+  P.TXh = P.TX + 2 * P.hx;
   P.TXP = P.TX + 8;
   P.tiles_x = (d.nx + P.TX - 1) / P.TX;
   P.tiles_y = (d.ny + P.TY - 1) / P.TY;
@@ -72,11 +79,32 @@ rw::Plan make_plan(int B, rw_dims d, int R) {
   P.ZC = zc;
   P.tiles_z = (d.nz + zc - 1) / zc;
   P.U = P.tiles_x * P.tiles_y * P.tiles_z;
+  P.vm = rw::VM_STORED;
+  P.hxv = P.hx;
+  P.TXhv = P.TXh;
   return P;
 }
 
+// Weights recomputed from the intensities inside pass A when the TMA box of the volume
+// is expressible (row pitch and box width multiples of 16 bytes); else stored planes.
+int choose_vm(const rw::Plan& P, const void* vol, rw_dtype dtype) {
+  if (!vol) return rw::VM_STORED;
+  const int vm = dtype == RW_U8 ? rw::VM_U8 : dtype == RW_U16 ? rw::VM_U16
+               : dtype == RW_I16 ? rw::VM_I16 : rw::VM_F32;
+  const int es = rw::vm_esize(vm);
+  if ((P.nx * es) % 16 != 0) return rw::VM_STORED;
+  return vm;
+}
+
+void set_vm(rw::Plan& P, int vm) {
+  P.vm = vm;
+  const int es = rw::vm_esize(vm);
+  P.hxv = P.TX < P.nx ? 16 / es : 0;
+  P.TXhv = P.TX + 2 * P.hxv;
+}
+
 struct Layout {
-  size_t W, dinv, r, p0, p1, q, PA, PB, PS, status, ctr, fixed, values, total;
+  size_t W, dinv, r, p, q, PA, PB, PS, status, ctr, fixed, values, total;
 };
 
 size_t up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -88,8 +116,7 @@ Layout layout(const rw::Plan& P, bool weights_given, int label_K) {
   L.W = o;      o += weights_given ? 0 : up(3 * BN * sizeof(float));
   L.dinv = o;   o += up(BN * sizeof(float));
   L.r = o;      o += up(RBN * sizeof(float));
-  L.p0 = o;     o += up(RBN * sizeof(float));
-  L.p1 = o;     o += up(RBN * sizeof(float));
+  L.p = o;      o += up(2 * RBN * sizeof(float));
   L.q = o;      o += up(RBN * sizeof(float));
   L.PA = o;     o += up(2 * RB * P.U * sizeof(double));
   L.PB = o;     o += up(2 * RB * P.U * sizeof(double2));
@@ -100,6 +127,58 @@ Layout layout(const rw::Plan& P, bool weights_given, int label_K) {
   L.values = o; o += label_K ? up((size_t)(label_K - 1) * BN * sizeof(float)) : 0;
   L.total = o;
   return L;
+}
+
+// ------------------------------------------------------------------ TMA descriptors
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  }
+  return fn;
+}
+
+// 3-D map (x, y, plane) over `planes` planes of nx x ny elements; box {bx, by, 1}.
+bool tmap(CUtensorMap* m, const void* base, int es, int nx, int ny, long long planes, int bx, int by) {
+  EncodeTiled enc = encoder();
+  if (!enc) return false;
+  const CUtensorMapDataType dt = es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                               : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)nx * es, (cuuint64_t)nx * ny * es};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+  const cuuint32_t el[3] = {1, 1, 1};
+  return enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, el,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+rw_status make_maps(const rw::Plan& P, const rw::Bufs& Bf, rw::Maps* M) {
+  std::memset(M, 0, sizeof(*M));
+  const long long BZ = (long long)P.B * P.nz, RBZ = (long long)P.R * BZ;
+  bool ok = tmap(&M->r, Bf.r, 4, P.nx, P.ny, RBZ, P.TXh, P.TY + 2) &&
+            tmap(&M->p, Bf.p, 4, P.nx, P.ny, 2 * RBZ, P.TXh, P.TY + 2) &&
+            tmap(&M->x, Bf.x, 4, P.nx, P.ny, RBZ, P.TX, P.TY) &&
+            tmap(&M->d, Bf.dinv, 4, P.nx, P.ny, BZ, P.TXh, P.TY + 2);
+  if (ok && P.vm == rw::VM_STORED)
+    ok = tmap(&M->wx, Bf.W, 4, P.nx, P.ny, 3 * BZ, P.TXh, P.TY) &&
+         tmap(&M->wy, Bf.W, 4, P.nx, P.ny, 3 * BZ, P.TX, P.TY + 1) &&
+         tmap(&M->wz, Bf.W, 4, P.nx, P.ny, 3 * BZ, P.TX, P.TY);
+  if (ok && P.vm != rw::VM_STORED)
+    ok = tmap(&M->v, Bf.vol, rw::vm_esize(P.vm), P.nx, P.ny, BZ, P.TXhv, P.TY + 2);
+  if (!ok) return fail(RW_ECUDA, "cuTensorMapEncodeTiled failed (driver entry point %s)",
+                       encoder() ? "found" : "missing");
+  return RW_OK;
 }
 
 bool dims_ok(rw_dims d) { return d.nx >= 4 && d.ny >= 1 && d.nz >= 1 && d.nx % 4 == 0; }
@@ -173,29 +252,33 @@ Prof g_prof;
 rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, rw_norm nm,
                      const float* W, const uint8_t* fixed, const float* values, int32_t nrhs,
                      float beta, float eps, float tol, int32_t max_iter, int32_t tol_mode,
-                     const float* x0, char* ws, const Layout& Lw, const rw::Plan& P,
+                     const float* x0, char* ws, const Layout& Lw, const rw::Plan& P0,
                      float* prob, int32_t* iters, float* resid, int32_t* status,
                      uint8_t* labels, cudaStream_t s) {
   const int sms = num_sms();
+  rw::Plan P = P0;
+  set_vm(P, choose_vm(P, vol, dtype));
   rw::Bufs Bf{};
   float* Wd = W ? const_cast<float*>(W) : reinterpret_cast<float*>(ws + Lw.W);
   float* dinv = reinterpret_cast<float*>(ws + Lw.dinv);
   if (vol) {
+    // on-the-fly modes need dinv only; stored mode also writes the weight planes
+    float* Wout = P.vm == rw::VM_STORED ? Wd : nullptr;
     RW_TIMED(RW_K_WEIGHTS, s, 1,
              rw::launch_weights(vol, dtype, nm.scale, nm.offset, batch, d.nx, d.ny, d.nz, beta,
-                                eps, Wd, dinv, fixed, sms, s));
+                                eps, Wout, dinv, fixed, sms, s));
   } else {
     RW_TIMED(RW_K_WEIGHTS, s, 1, rw::launch_dinv(W, batch, d.nx, d.ny, d.nz, fixed, dinv, sms, s));
   }
-  Bf.W = Wd;
+  Bf.W = P.vm == rw::VM_STORED ? Wd : nullptr;
+  Bf.vol = P.vm == rw::VM_STORED ? nullptr : vol;
   Bf.dinv = dinv;
   Bf.fixed = fixed;
   Bf.values = values;
   Bf.x0 = x0;
   Bf.x = prob;
   Bf.r = reinterpret_cast<float*>(ws + Lw.r);
-  Bf.p0 = reinterpret_cast<float*>(ws + Lw.p0);
-  Bf.p1 = reinterpret_cast<float*>(ws + Lw.p1);
+  Bf.p = reinterpret_cast<float*>(ws + Lw.p);
   Bf.q = reinterpret_cast<float*>(ws + Lw.q);
   Bf.PA = reinterpret_cast<double*>(ws + Lw.PA);
   Bf.PB = reinterpret_cast<double2*>(ws + Lw.PB);
@@ -203,11 +286,15 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   Bf.status = reinterpret_cast<int*>(ws + Lw.status);
   Bf.iters = iters;
   Bf.ctr = reinterpret_cast<int*>(ws + Lw.ctr);
-  rw::Ctl C{tol, tol_mode, max_iter};
+  rw::Ctl C{tol, tol_mode, max_iter, nm.scale, nm.offset, rw::nbl2_of(beta), eps};
+  rw::Maps M;
+  rw_status st = make_maps(P, Bf, &M);
+  if (st != RW_OK) return st;
   RW_CK(cudaMemsetAsync(Bf.status, 0, (size_t)P.R * P.B * sizeof(int), s));
-  RW_TIMED(RW_K_SETUP, s, 1, rw::launch_setup(P, Bf, s));
-  const int nchunks = (P.R + 3) / 4;
-  rw_status st = ensure_pinned();
+  RW_TIMED(RW_K_SETUP, s, 1, rw::launch_setup(P, Bf, C, s));
+  const int nA = (P.R + rw::passA_rc(P) - 1) / rw::passA_rc(P);
+  const int nB = (P.R + 3) / 4;
+  st = ensure_pinned();
   if (st != RW_OK) return st;
   // Host-polled loop: every CHECK iterations the active-pair count is copied to pinned
   // memory; the host waits only on the previous checkpoint, so it stays <= 2*CHECK
@@ -216,8 +303,8 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   int j = 0;
   for (int k = 0; k <= max_iter; ++k) {
     RW_CK(cudaMemsetAsync(Bf.ctr + (k & 1), 0, sizeof(int), s));
-    RW_TIMED(RW_K_PASSA, s, nchunks, rw::launch_iteration_A(P, Bf, C, k, s));
-    if (k < max_iter) RW_TIMED(RW_K_PASSB, s, nchunks, rw::launch_iteration_B(P, Bf, k, s));
+    RW_TIMED(RW_K_PASSA, s, nA, rw::launch_iteration_A(P, Bf, C, k, M, s));
+    if (k < max_iter) RW_TIMED(RW_K_PASSB, s, nB, rw::launch_iteration_B(P, Bf, k, s));
     if (k % CHECK == CHECK - 1 || k == max_iter) {
       const int slot = j & 1;
       RW_CK(cudaMemcpyAsync(g_pin.h + slot, Bf.ctr + (k & 1), sizeof(int),

@@ -1,0 +1,168 @@
+// cg_device.cuh -- device helpers shared by the CG kernels (cg.cu, passA.cu).
+#pragma once
+#include "rw_common.cuh"
+
+namespace rw {
+
+// --------------------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;  // identical in every lane (a+b == b+a in IEEE)
+}
+
+// Sum of a[0..U) (stride `stride`) in a fixed order by one warp; result in all lanes.
+__device__ __forceinline__ double warp_sum_array(const double* a, int U, int stride, int lane) {
+  double s = 0.0;
+  for (int u = lane; u < U; u += 32) s += a[(long long)u * stride];
+  return warp_sum(s);
+}
+
+// Block-wide fixed-order reduction of NV values per thread; result written by thread 0.
+// Callers separate consecutive calls with __syncthreads().
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* out) {
+  __shared__ double red[RW_MAX_THREADS / 32][NV];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) red[warp][j] = v[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += red[w][j];
+      out[j] = s;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------- tiles
+struct Tile {
+  int x0, y0, z0, z1, lx, ly, x, y;
+  bool in;  // this thread's 4 columns exist and are inside the brick
+};
+
+__device__ __forceinline__ Tile make_tile(const Plan& P, int u) {
+  Tile t;
+  const int tx = u % P.tiles_x;
+  const int rest = u / P.tiles_x;
+  const int ty = rest % P.tiles_y;
+  const int tz = rest / P.tiles_y;
+  t.x0 = tx * P.TX;
+  t.y0 = ty * P.TY;
+  t.z0 = tz * P.ZC;
+  t.z1 = min(t.z0 + P.ZC, P.nz);
+  t.lx = threadIdx.x % P.tpx;
+  t.ly = threadIdx.x / P.tpx;
+  t.x = t.x0 + 4 * t.lx;
+  t.y = t.y0 + t.ly;
+  // P.threads % tpx may be != 0: threads past the TY rows own nothing
+  t.in = (t.x < P.nx) && (t.y < P.ny) && (t.ly < P.TY);
+  return t;
+}
+
+// --------------------------------------------------------------------------- float4 math
+// explicit _rn intrinsics everywhere: no contraction freedom for the compiler, so every
+// template instantiation produces the same bits
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
+__device__ __forceinline__ float4 fma4(float a, float4 x, float4 y) {
+  return make_float4(__fmaf_rn(a, x.x, y.x), __fmaf_rn(a, x.y, y.y), __fmaf_rn(a, x.z, y.z),
+                     __fmaf_rn(a, x.w, y.w));
+}
+__device__ __forceinline__ float4 mul4(float4 a, float4 b) {
+  return make_float4(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y), __fmul_rn(a.z, b.z),
+                     __fmul_rn(a.w, b.w));
+}
+// p_new = beta * p_old + dinv * r   (z = dinv r never stored)
+__device__ __forceinline__ float4 pnew4(float be, float4 po, float4 d, float4 r) {
+  return fma4(be, po, mul4(d, r));
+}
+__device__ __forceinline__ float pnew1(float be, float po, float d, float r) {
+  return __fmaf_rn(be, po, __fmul_rn(d, r));
+}
+// fp64 accumulation of a float4 dot product in a fixed order
+__device__ __forceinline__ double dot4_acc(float4 a, float4 b, double acc) {
+  acc = __fma_rn((double)a.x, (double)b.x, acc);
+  acc = __fma_rn((double)a.y, (double)b.y, acc);
+  acc = __fma_rn((double)a.z, (double)b.z, acc);
+  return __fma_rn((double)a.w, (double)b.w, acc);
+}
+__device__ __forceinline__ float comp(const float4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+}
+
+// edge-difference stencil of one voxel (reading c8): q = sum_a w_a (p - p_a), fixed -> 0
+__device__ __forceinline__ float stencil1(float p, float xp, float xm, float yp, float ym,
+                                          float zp, float zm, float wx, float wxm, float wy,
+                                          float wym, float wz, float wzm, float dv) {
+  float q = __fmul_rn(wx, __fsub_rn(p, xp));
+  q = __fmaf_rn(wxm, __fsub_rn(p, xm), q);
+  q = __fmaf_rn(wy, __fsub_rn(p, yp), q);
+  q = __fmaf_rn(wym, __fsub_rn(p, ym), q);
+  q = __fmaf_rn(wz, __fsub_rn(p, zp), q);
+  q = __fmaf_rn(wzm, __fsub_rn(p, zm), q);
+  return dv == 0.f ? 0.f : q;
+}
+
+// --------------------------------------------------------------------------- scalars
+// Decision of pass A(k) for one (rhs, brick), computed redundantly by every CTA of the
+// brick from the same partials in the same order (so every CTA agrees).
+struct Scal {
+  int active;
+  float beta, alpha;
+};
+
+__device__ inline Scal passA_scalars(const Plan& P, const Bufs& Bf, const Ctl& C, int rb, int k,
+                                     int u, int lane) {
+  Scal s = {0, 0.f, 0.f};
+  const int st = Bf.status[rb];
+  if (st != ST_ACTIVE) return s;
+  const long long RBU = (long long)P.R * P.B * P.U;
+  const double* pb = reinterpret_cast<const double*>(Bf.PB);
+  const double rz_k = warp_sum_array(pb + 2 * ((k & 1) * RBU + (long long)rb * P.U), P.U, 2, lane);
+  const double rr_k = warp_sum_array(pb + 2 * ((k & 1) * RBU + (long long)rb * P.U) + 1, P.U, 2, lane);
+  const double* ps = reinterpret_cast<const double*>(Bf.PS) + 4LL * rb * P.U;
+  const double bb = warp_sum_array(ps + 0, P.U, 4, lane);
+  int nst = ST_ACTIVE;
+  double rz_km1 = 0.0, pq_km1 = 0.0;
+  if (k == 0) {
+    const double nf = warp_sum_array(ps + 1, P.U, 4, lane);
+    const double nu = warp_sum_array(ps + 2, P.U, 4, lane);
+    if (nf == 0.0 || nu == 0.0) nst = ST_TRIVIAL;
+    else if (bb == 0.0) nst = ST_ZERO_B;
+  } else {
+    rz_km1 = warp_sum_array(pb + 2 * (((k - 1) & 1) * RBU + (long long)rb * P.U), P.U, 2, lane);
+    pq_km1 = warp_sum_array(Bf.PA + ((k - 1) & 1) * RBU + (long long)rb * P.U, P.U, 1, lane);
+    if (!(pq_km1 > 0.0) || !isfinite(rz_k) || !isfinite(pq_km1)) nst = ST_BREAKDOWN;
+  }
+  if (nst == ST_ACTIVE) {
+    const double t2 = (double)C.tol * (double)C.tol;
+    const bool conv = (C.tol_mode == 0) ? (rr_k <= t2 * bb) : (rr_k <= t2);
+    if (conv) nst = ST_CONVERGED;
+    else if (k >= C.max_iter) nst = ST_MAXITER;
+  }
+  if (nst != ST_ACTIVE) {
+    if (u == 0 && lane == 0) {
+      Bf.status[rb] = nst;
+      Bf.iters[rb] = (nst == ST_TRIVIAL || nst == ST_ZERO_B) ? 0 : k;
+    }
+    return s;
+  }
+  if (u == 0 && lane == 0) atomicAdd(Bf.ctr + (k & 1), 1);
+  s.active = 1;
+  if (k > 0) {
+    s.alpha = (float)(rz_km1 / pq_km1);
+    s.beta = (float)(rz_k / rz_km1);
+  }
+  return s;
+}
+
+}  // namespace rw

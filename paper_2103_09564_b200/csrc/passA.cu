@@ -1,0 +1,381 @@
+// passA.cu -- SURVEY §8(a) row a4: CG pass A, the SpMV pass (dominant kernel).
+//
+// For iteration k and every active (rhs, brick):   (readings c5, c8)
+//   p_k = dinv*r_k + beta_{k-1} p_{k-1}            (z = dinv r never stored)
+//   x_k = x_{k-1} + alpha_{k-1} p_{k-1}            (lagged x update)
+//   q   = L_UU p_k   as  q_i = sum_j w_ij (p_i - p_j),  q = 0 on fixed voxels
+//   partial p_k . q  (fp64, fixed order)
+//
+// B200 design.  A CTA owns a TX x TY column tile of one brick and marches over ZC planes.
+// One elected thread streams each plane's boxes (r, p_{k-1}, x, dinv and either the three
+// weight planes or the raw intensities) into a 3-stage shared-memory ring with TMA
+// (cp.async.bulk.tensor, mbarrier completion), so HBM reads run two planes ahead of the
+// math with no register cost.  The y/x halo of r, p, dinv (needed to form p_k at the
+// tile's neighbours) comes in the same boxes; out-of-brick cells are zero-filled by TMA.
+// p_k of plane z is shared through a padded smem plane for the x/y neighbours; the z
+// neighbours stay in registers (sliding window).  Edge weights are either read (VM_STORED)
+// or recomputed from the intensities (VM_U8..F32: 1-4 B/voxel instead of 12 B), with the
+// same grady() expression every other kernel uses, so the operator is bit-identical.
+#include "cg_device.cuh"
+#include "passA.cuh"
+#include "tma.cuh"
+
+namespace rw {
+
+template <int RC, int VM>
+__global__ void __launch_bounds__(RW_MAX_THREADS, 2)
+k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps M) {
+  using T = typename VolT<VM>::T;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ float s_beta[RC], s_alpha[RC];
+  __shared__ int s_act[RC];
+  const int u = blockIdx.x, b = blockIdx.y;
+  const int rbase = r_first + blockIdx.z * RC;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const ALayout L = a_layout(P, RC, VM);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bars);
+  if (warp < RC) {
+    Scal s = {0, 0.f, 0.f};
+    if (rbase + warp < P.R) s = passA_scalars(P, Bf, C, (rbase + warp) * P.B + b, k, u, lane);
+    if (lane == 0) { s_act[warp] = s.active; s_beta[warp] = s.beta; s_alpha[warp] = s.alpha; }
+  }
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  bool act[RC];
+  float be[RC], al[RC];
+  bool any = false;
+#pragma unroll
+  for (int c = 0; c < RC; ++c) {
+    act[c] = s_act[c] != 0;
+    be[c] = s_beta[c];
+    al[c] = s_alpha[c];
+    any |= act[c];
+  }
+  if (!any) return;
+
+  const Tile t = make_tile(P, u);
+  const int TX = P.TX, TY = P.TY, TXh = P.TXh, hx = P.hx, TXP = P.TXP;
+  const int zs = max(t.z0 - 1, 0), ze = min(t.z1, P.nz - 1);  // planes streamed
+  const int np = ze - zs + 1;
+  const int xb = t.x0 - hx, yb = t.y0 - 1;
+  const int par = k & 1;
+  const long long BN = (long long)P.B * P.n;
+  const long long RBN = (long long)P.R * BN;
+  const long long plane = (long long)P.nx * P.ny;
+  float* Pnew = Bf.p + (long long)((k + 1) & 1) * RBN;
+
+  // ---------------------------------------------------------------- producer (tid 0)
+  auto issue = [&](int j) {
+    if (tid != 0 || j >= np) return;
+    const int zz = zs + j;
+    unsigned char* st = smem + (j % kStages) * L.stage;
+    uint64_t* bj = bar + (j % kStages);
+    uint32_t bytes = L.eRP + (VM == VM_STORED ? L.eWx + L.eWy + L.eWz : L.eV);
+#pragma unroll
+    for (int c = 0; c < RC; ++c)
+      if (act[c]) bytes += 2 * L.eRP + (k > 0 ? L.eX : 0);
+    mbar_arrive_expect_tx(bj, bytes);
+#pragma unroll
+    for (int c = 0; c < RC; ++c) {
+      if (!act[c]) continue;
+      const int pr = ((rbase + c) * P.B + b) * P.nz + zz;
+      const int pp = ((par * P.R + rbase + c) * P.B + b) * P.nz + zz;
+      tma_load_3d(st + L.oR + c * L.bRP, &M.r, bj, xb, yb, pr);
+      tma_load_3d(st + L.oP + c * L.bRP, &M.p, bj, xb, yb, pp);
+      if (k > 0) tma_load_3d(st + L.oX + c * L.bX, &M.x, bj, t.x0, t.y0, pr);
+    }
+    const int pd = b * P.nz + zz;
+    tma_load_3d(st + L.oD, &M.d, bj, xb, yb, pd);
+    if (VM == VM_STORED) {
+      tma_load_3d(st + L.oW, &M.wx, bj, xb, t.y0, pd);
+      tma_load_3d(st + L.oW + L.bWx, &M.wy, bj, t.x0, yb, (P.B + b) * P.nz + zz);
+      tma_load_3d(st + L.oW + L.bWx + L.bWy, &M.wz, bj, t.x0, t.y0, (2 * P.B + b) * P.nz + zz);
+    } else {
+      tma_load_3d(st + L.oW, &M.v, bj, t.x0 - P.hxv, yb, pd);
+    }
+  };
+  auto wait = [&](int j) { mbar_wait(bar + (j % kStages), (uint32_t)((j / kStages) & 1)); };
+  auto stg = [&](int j) -> const unsigned char* { return smem + (j % kStages) * L.stage; };
+  auto sRP = [&](int j, int off) { return reinterpret_cast<const float*>(stg(j) + off); };
+
+  if (tid == 0) {
+    prefetch_tmap(&M.r);
+    prefetch_tmap(&M.p);
+    prefetch_tmap(&M.d);
+    prefetch_tmap(VM == VM_STORED ? &M.wx : &M.v);
+  }
+  for (int j = 0; j < kStages; ++j) issue(j);
+
+  const int cc = hx + 4 * t.lx;              // column of this thread's voxels in a halo box
+  const int crow = (t.ly + 1) * TXh + cc;    // its element offset in a (TY+2) x TXh box
+  // the intensity box has its own halo offset hxv = 16 B / element size: TMA box starts
+  // must stay 16-byte aligned in x
+  const int vrow = (t.ly + 1) * P.TXhv + P.hxv + 4 * t.lx;
+  auto centre_pnew = [&](const unsigned char* st, int c) -> float4 {
+    const float* R = reinterpret_cast<const float*>(st + L.oR + c * L.bRP);
+    const float* Pp = reinterpret_cast<const float*>(st + L.oP + c * L.bRP);
+    const float* D = reinterpret_cast<const float*>(st + L.oD);
+    return pnew4(be[c], ld4(Pp + crow), ld4(D + crow), ld4(R + crow));
+  };
+  // normalised intensities of 4 consecutive box elements (vector smem load)
+  auto gvol4 = [&](const unsigned char* st, int off, float g[4]) {
+    const T* v = reinterpret_cast<const T*>(st + L.oW) + off;
+    if (sizeof(T) == 4) {
+      const float4 a = *reinterpret_cast<const float4*>(v);
+      g[0] = a.x; g[1] = a.y; g[2] = a.z; g[3] = a.w;
+    } else if (sizeof(T) == 2) {
+      const uint2 a = *reinterpret_cast<const uint2*>(v);
+      const T* e = reinterpret_cast<const T*>(&a);
+      g[0] = (float)e[0]; g[1] = (float)e[1]; g[2] = (float)e[2]; g[3] = (float)e[3];
+    } else {
+      const uint32_t a = *reinterpret_cast<const uint32_t*>(v);
+      const T* e = reinterpret_cast<const T*>(&a);
+      g[0] = (float)e[0]; g[1] = (float)e[1]; g[2] = (float)e[2]; g[3] = (float)e[3];
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) g[e] = normv(g[e], C.scale, C.offset);
+  };
+  auto gvol1 = [&](const unsigned char* st, int off) -> float {
+    return normv((float)reinterpret_cast<const T*>(st + L.oW)[off], C.scale, C.offset);
+  };
+  float* Wys = reinterpret_cast<float*>(smem + L.wys);   // +y weights of this plane's rows
+
+  float4 pm[RC], pc[RC], pn[RC];
+  float4 wzm = f4(0.f);
+  float gcur[4] = {0.f, 0.f, 0.f, 0.f};     // VM modes: normalised intensities of plane z
+#pragma unroll
+  for (int c = 0; c < RC; ++c) pm[c] = pc[c] = pn[c] = f4(0.f);
+  const int jz0 = t.z0 - zs;
+  if (t.z0 > 0) {                            // plane z0-1 = stage 0: z-neighbour + Wz(z0-1)
+    wait(0);
+    if (t.in) {
+#pragma unroll
+      for (int c = 0; c < RC; ++c)
+        if (act[c]) pm[c] = centre_pnew(stg(0), c);
+      if (VM == VM_STORED) wzm = ld4(sRP(0, L.oW + L.bWx + L.bWy) + t.ly * TX + 4 * t.lx);
+    }
+  }
+  wait(jz0);
+  if (t.in) {
+#pragma unroll
+    for (int c = 0; c < RC; ++c)
+      if (act[c]) pc[c] = centre_pnew(stg(jz0), c);
+    if (VM != VM_STORED) {
+      gvol4(stg(jz0), vrow, gcur);
+      if (t.z0 > 0) {
+        float gm[4];
+        gvol4(stg(0), vrow, gm);
+        wzm = make_float4(grady(__fsub_rn(gcur[0], gm[0]), C.nbl2, C.eps),
+                          grady(__fsub_rn(gcur[1], gm[1]), C.nbl2, C.eps),
+                          grady(__fsub_rn(gcur[2], gm[2]), C.nbl2, C.eps),
+                          grady(__fsub_rn(gcur[3], gm[3]), C.nbl2, C.eps));
+      }
+    }
+  }
+
+  double acc[RC];
+#pragma unroll
+  for (int c = 0; c < RC; ++c) acc[c] = 0.0;
+  const int spc = (TY + 2) * TXP;            // floats per p_new plane (one rhs)
+  const int nhx = 2 * P.tpx;
+  const int nhalo = nhx + 2 * TY;
+
+  for (int z = t.z0; z < t.z1; ++z) {
+    const int jz = z - zs;
+    __syncthreads();                         // plane z-1's stage and p_new plane are free
+    if (jz >= 1) issue(jz - 1 + kStages);
+    const bool hasn = z + 1 <= ze;
+    const unsigned char* s0 = stg(jz);
+    const unsigned char* s1 = stg(jz + 1);
+    if (hasn) wait(jz + 1);
+    if (t.in) {
+#pragma unroll
+      for (int c = 0; c < RC; ++c) pn[c] = (hasn && act[c]) ? centre_pnew(s1, c) : f4(0.f);
+    }
+    // p_k of plane z (centre + x/y halo) into the shared plane
+    float* spz0 = reinterpret_cast<float*>(smem + L.sp) + (z & 1) * RC * spc;
+    if (t.ly < TY) {
+#pragma unroll
+      for (int c = 0; c < RC; ++c)
+        st4(spz0 + c * spc + (t.ly + 1) * TXP + 4 + 4 * t.lx, (t.in && act[c]) ? pc[c] : f4(0.f));
+    }
+    for (int h = tid; h < nhalo; h += blockDim.x) {
+      if (h < nhx) {                         // rows y0-1 / y0+TY (zero-filled if outside)
+        const int side = h / P.tpx, g = h % P.tpx;
+        const int brow = side ? TY + 1 : 0;
+        const int off = brow * TXh + hx + 4 * g;
+#pragma unroll
+        for (int c = 0; c < RC; ++c) {
+          float4 v = f4(0.f);
+          if (act[c])
+            v = pnew4(be[c], ld4(sRP(jz, L.oP + c * L.bRP) + off), ld4(sRP(jz, L.oD) + off),
+                      ld4(sRP(jz, L.oR + c * L.bRP) + off));
+          st4(spz0 + c * spc + brow * TXP + 4 + 4 * g, v);
+        }
+      } else {                               // columns x0-1 / x0+TX
+        const int hh = h - nhx;
+        const int side = hh / TY, ry = hh % TY;
+        const int scol = side ? TX + 4 : 3;
+        const int off = (ry + 1) * TXh + (side ? hx + TX : hx - 1);
+#pragma unroll
+        for (int c = 0; c < RC; ++c) {
+          float v = 0.f;
+          if (hx && act[c])
+            v = pnew1(be[c], sRP(jz, L.oP + c * L.bRP)[off], sRP(jz, L.oD)[off],
+                      sRP(jz, L.oR + c * L.bRP)[off]);
+          spz0[c * spc + (ry + 1) * TXP + scol] = v;
+        }
+      }
+    }
+    // ---- edge weights of this thread's 4 voxels
+    float4 wx = f4(0.f), wxm = f4(0.f), wy = f4(0.f), wym = f4(0.f), wz = f4(0.f);
+    float gz[4] = {0.f, 0.f, 0.f, 0.f};
+    if (t.in) {
+      if (VM == VM_STORED) {
+        const float* Wxb = sRP(jz, L.oW);
+        const float* Wyb = sRP(jz, L.oW + L.bWx);
+        const float* Wzb = sRP(jz, L.oW + L.bWx + L.bWy);
+        wx = ld4(Wxb + t.ly * TXh + cc);
+        const float wl = (t.x > 0) ? Wxb[t.ly * TXh + cc - 1] : 0.f;
+        wxm = make_float4(wl, wx.x, wx.y, wx.z);
+        wy = ld4(Wyb + (t.ly + 1) * TX + 4 * t.lx);
+        wym = ld4(Wyb + t.ly * TX + 4 * t.lx);
+        wz = ld4(Wzb + t.ly * TX + 4 * t.lx);
+      } else {
+        // forward weights of the own voxels; -x of voxels 1..3 is +x of voxels 0..2, -y comes
+        // from the row above through shared memory, -z from the previous plane (registers)
+        float gu[4];
+        if (hasn) gvol4(s1, vrow, gz);
+        gvol4(s0, vrow + P.TXhv, gu);
+        const float gl = (t.x > 0) ? gvol1(s0, vrow - 1) : 0.f;
+        const float gr = (t.x + 4 < P.nx) ? gvol1(s0, vrow + 4) : 0.f;
+        float a[4], yy[4], zz[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float nx_ = e < 3 ? gcur[e + 1] : gr;
+          a[e] = (t.x + e + 1 < P.nx) ? grady(__fsub_rn(nx_, gcur[e]), C.nbl2, C.eps) : 0.f;
+          yy[e] = (t.y + 1 < P.ny) ? grady(__fsub_rn(gu[e], gcur[e]), C.nbl2, C.eps) : 0.f;
+          zz[e] = (z + 1 < P.nz) ? grady(__fsub_rn(gz[e], gcur[e]), C.nbl2, C.eps) : 0.f;
+        }
+        const float am0 = (t.x > 0) ? grady(__fsub_rn(gcur[0], gl), C.nbl2, C.eps) : 0.f;
+        wx = make_float4(a[0], a[1], a[2], a[3]);
+        wxm = make_float4(am0, a[0], a[1], a[2]);
+        wy = make_float4(yy[0], yy[1], yy[2], yy[3]);
+        wz = make_float4(zz[0], zz[1], zz[2], zz[3]);
+        st4(Wys + t.ly * TX + 4 * t.lx, wy);
+        if (t.ly == 0 && t.y > 0) {          // first tile row: -y weights from the halo row
+          float gd[4];
+          gvol4(s0, vrow - P.TXhv, gd);
+          wym = make_float4(grady(__fsub_rn(gcur[0], gd[0]), C.nbl2, C.eps),
+                            grady(__fsub_rn(gcur[1], gd[1]), C.nbl2, C.eps),
+                            grady(__fsub_rn(gcur[2], gd[2]), C.nbl2, C.eps),
+                            grady(__fsub_rn(gcur[3], gd[3]), C.nbl2, C.eps));
+        }
+      }
+    }
+    __syncthreads();
+    if (t.in) {
+      if (VM != VM_STORED && t.ly > 0) wym = ld4(Wys + (t.ly - 1) * TX + 4 * t.lx);
+      const float4 dvc = ld4(sRP(jz, L.oD) + crow);
+      const long long o = (long long)b * P.n + (long long)z * plane + (long long)t.y * P.nx + t.x;
+#pragma unroll
+      for (int c = 0; c < RC; ++c) {
+        if (!act[c]) continue;
+        const float* s = spz0 + c * spc;
+        const int sc = 4 + 4 * t.lx;
+        const float4 yp = ld4(s + (t.ly + 2) * TXP + sc);
+        const float4 ym = ld4(s + t.ly * TXP + sc);
+        const float xl = s[(t.ly + 1) * TXP + sc - 1];
+        const float xr = s[(t.ly + 1) * TXP + sc + 4];
+        const float4 p = pc[c];
+        float4 q;
+        q.x = stencil1(p.x, p.y, xl, yp.x, ym.x, pn[c].x, pm[c].x, wx.x, wxm.x, wy.x, wym.x, wz.x, wzm.x, dvc.x);
+        q.y = stencil1(p.y, p.z, p.x, yp.y, ym.y, pn[c].y, pm[c].y, wx.y, wxm.y, wy.y, wym.y, wz.y, wzm.y, dvc.y);
+        q.z = stencil1(p.z, p.w, p.y, yp.z, ym.z, pn[c].z, pm[c].z, wx.z, wxm.z, wy.z, wym.z, wz.z, wzm.z, dvc.z);
+        q.w = stencil1(p.w, xr, p.z, yp.w, ym.w, pn[c].w, pm[c].w, wx.w, wxm.w, wy.w, wym.w, wz.w, wzm.w, dvc.w);
+        const long long ov = (long long)(rbase + c) * BN + o;
+        if (k > 0) {
+          const float4 po = ld4(sRP(jz, L.oP + c * L.bRP) + crow);
+          const float4 xo = ld4(sRP(jz, L.oX + c * L.bX) + t.ly * TX + 4 * t.lx);
+          st4(Bf.x + ov, fma4(al[c], po, xo));
+        }
+        st4(Pnew + ov, p);
+        st4(Bf.q + ov, q);
+        acc[c] = dot4_acc(p, q, acc[c]);
+      }
+      wzm = wz;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) gcur[e] = gz[e];
+    }
+#pragma unroll
+    for (int c = 0; c < RC; ++c) { pm[c] = pc[c]; pc[c] = pn[c]; }
+  }
+  // per-rhs CTA partial of p.q
+  const long long RBU = (long long)P.R * P.B * P.U;
+#pragma unroll
+  for (int c = 0; c < RC; ++c) {
+    double v[1] = {acc[c]};
+    __syncthreads();
+    if (act[c]) block_sum<1>(v, Bf.PA + (k & 1) * RBU + (long long)((rbase + c) * P.B + b) * P.U + u);
+  }
+}
+
+// ------------------------------------------------------------------------- launcher
+template <int RC, int VM>
+static cudaError_t launch_rc(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0,
+                             const Maps& M, cudaStream_t s) {
+  static int attr = 48 * 1024;   // largest dynamic smem opted in so far for this instance
+  const ALayout L = a_layout(P, RC, VM);
+  if (L.total > attr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_passA<RC, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+    if (e != cudaSuccess) return e;
+    attr = L.total;
+  }
+  k_passA<RC, VM><<<dim3(P.U, P.B, 1), P.threads, L.total, s>>>(P, Bf, C, k, r0, M);
+  return cudaGetLastError();
+}
+
+template <int VM>
+static cudaError_t launch_vm(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0, int rc,
+                             const Maps& M, cudaStream_t s) {
+  switch (rc) {
+    case 1: return launch_rc<1, VM>(P, Bf, C, k, r0, M, s);
+    case 2: return launch_rc<2, VM>(P, Bf, C, k, r0, M, s);
+    case 3: return launch_rc<3, VM>(P, Bf, C, k, r0, M, s);
+    default: return launch_rc<4, VM>(P, Bf, C, k, r0, M, s);
+  }
+}
+
+// right-hand sides per CTA: up to 4 sharing one operator load, fewer if smem is short
+int passA_rc(const Plan& P) {
+  int rc = P.R < 4 ? P.R : 4;
+  while (rc > 1 && a_layout(P, rc, P.vm).total > 220 * 1024) --rc;
+  return rc;
+}
+
+size_t passA_smem(const Plan& P, int rc) { return (size_t)a_layout(P, rc, P.vm).total; }
+
+cudaError_t launch_iteration_A(const Plan& P, const Bufs& Bf, const Ctl& C, int k,
+                               const Maps& M, cudaStream_t s) {
+  const int rcmax = passA_rc(P);
+  for (int r0 = 0; r0 < P.R; r0 += rcmax) {
+    const int rc = P.R - r0 < rcmax ? P.R - r0 : rcmax;
+    cudaError_t e;
+    switch (P.vm) {
+      case VM_U8: e = launch_vm<VM_U8>(P, Bf, C, k, r0, rc, M, s); break;
+      case VM_U16: e = launch_vm<VM_U16>(P, Bf, C, k, r0, rc, M, s); break;
+      case VM_I16: e = launch_vm<VM_I16>(P, Bf, C, k, r0, rc, M, s); break;
+      case VM_F32: e = launch_vm<VM_F32>(P, Bf, C, k, r0, rc, M, s); break;
+      default: e = launch_vm<VM_STORED>(P, Bf, C, k, r0, rc, M, s); break;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace rw

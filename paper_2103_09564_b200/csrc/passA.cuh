@@ -1,0 +1,63 @@
+// passA.cuh -- TMA descriptors and shared-memory layout of the CG pass-A kernel.
+#pragma once
+#include <cuda.h>
+
+#include "rw_common.cuh"
+
+namespace rw {
+
+// 3-D tiled tensor maps (x, y, plane) over the arrays pass A streams.  Arrays indexed
+// [q][b][z] collapse (q, b, z) into one plane coordinate (q*B + b)*nz + z.
+struct Maps {
+  CUtensorMap r;    // r      [R][B] planes, box {TXh, TY+2, 1}
+  CUtensorMap p;    // P      [2][R][B],    box {TXh, TY+2, 1}
+  CUtensorMap x;    // x      [R][B],       box {TX, TY, 1}
+  CUtensorMap d;    // dinv   [B],          box {TXh, TY+2, 1}
+  CUtensorMap wx;   // W      [3][B],       box {TXh, TY, 1}     (VM_STORED)
+  CUtensorMap wy;   //                      box {TX, TY+1, 1}    (VM_STORED)
+  CUtensorMap wz;   //                      box {TX, TY, 1}      (VM_STORED)
+  CUtensorMap v;    // vol    [B],          box {TXhv, TY+2, 1}  (VM_U8..VM_F32)
+};
+
+constexpr int kStages = 3;  // TMA ring depth (prefetch distance 2 planes)
+
+__host__ __device__ inline int rup128(int b) { return (b + 127) & ~127; }
+__host__ __device__ inline int vm_esize(int vm) {
+  return vm == VM_U8 ? 1 : ((vm == VM_U16 || vm == VM_I16) ? 2 : 4);
+}
+
+struct ALayout {
+  int eRP, eX, eWx, eWy, eWz, eV;   // exact box bytes (mbarrier transaction counts)
+  int bRP, bX, bWx, bWy, bWz, bV;   // 128-byte rounded smem footprints
+  int oR, oP, oX, oD, oW;           // offsets inside a stage (rhs c adds c * b..)
+  int stage, sp, wys, bars, total;  // stage size; p_new planes; +y weights; mbarriers; total
+};
+
+__host__ __device__ inline ALayout a_layout(const Plan& P, int RC, int vm) {
+  ALayout L;
+  L.eRP = P.TXh * (P.TY + 2) * 4;
+  L.eX = P.TX * P.TY * 4;
+  L.eWx = P.TXh * P.TY * 4;
+  L.eWy = P.TX * (P.TY + 1) * 4;
+  L.eWz = L.eX;
+  L.eV = P.TXhv * (P.TY + 2) * vm_esize(vm);
+  L.bRP = rup128(L.eRP);
+  L.bX = rup128(L.eX);
+  L.bWx = rup128(L.eWx);
+  L.bWy = rup128(L.eWy);
+  L.bWz = rup128(L.eWz);
+  L.bV = rup128(L.eV);
+  L.oR = 0;
+  L.oP = RC * L.bRP;
+  L.oX = 2 * RC * L.bRP;
+  L.oD = L.oX + RC * L.bX;
+  L.oW = L.oD + L.bRP;
+  L.stage = L.oW + (vm == VM_STORED ? L.bWx + L.bWy + L.bWz : L.bV);
+  L.sp = kStages * L.stage;
+  L.wys = L.sp + rup128(2 * RC * (P.TY + 2) * P.TXP * 4);
+  L.bars = L.wys + (vm == VM_STORED ? 0 : rup128(P.TY * P.TX * 4));
+  L.total = L.bars + kStages * 8;
+  return L;
+}
+
+}  // namespace rw

@@ -58,7 +58,7 @@ __device__ __forceinline__ T mean8(G get) {
 // in: input level, plane zb (global) at in[0]; level dims nx,ny,nz; process planes
 // [zb, zb+zc) (zb multiple of 2^L, zc multiple of 2^L unless zb+zc == nz).
 template <typename T>
-__global__ void __launch_bounds__(RW_THREADS)
+__global__ void __launch_bounds__(256)
 k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int L, PyrOut o) {
   using A = typename std::conditional<std::is_same<T, float>::value, float, int>::type;
   __shared__ A s1[16 * 16 * 16];
@@ -72,7 +72,7 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
     const int X0 = blockIdx.x * 16, Y0 = blockIdx.y * 16, Z0 = (zb >> 1) + blockIdx.z * 16;
     T* out = (T*)o.p[0];
     const long long po = (long long)o.nx[0] * o.ny[0];
-    for (int idx = threadIdx.x; idx < 4096; idx += RW_THREADS) {
+    for (int idx = threadIdx.x; idx < 4096; idx += 256) {
       const int lx = idx & 15, ly = (idx >> 4) & 15, lz = idx >> 8;
       const int X = X0 + lx, Y = Y0 + ly, Z = Z0 + lz;
       A v = 0;
@@ -99,7 +99,7 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
     T* out = (T*)o.p[l];
     const long long po = (long long)o.nx[l] * o.ny[l];
     const int pe = 2 * e;                 // child box extent
-    for (int idx = threadIdx.x; idx < e * e * e; idx += RW_THREADS) {
+    for (int idx = threadIdx.x; idx < e * e * e; idx += 256) {
       const int lx = idx % e, ly = (idx / e) % e, lz = idx / (e * e);
       const int X = X0 + lx, Y = Y0 + ly, Z = Z0 + lz;
       A v = 0;
@@ -122,10 +122,10 @@ cudaError_t launch_pyramid_group(const void* in, int dtype, int nx, int ny, int 
                                  int zc, int L, const PyrOut& o, cudaStream_t s) {
   const dim3 g((nx + 31) / 32, (ny + 31) / 32, (zc + 31) / 32);
   switch (dtype) {
-    case 0: k_pyramid<uint8_t><<<g, RW_THREADS, 0, s>>>((const uint8_t*)in, nx, ny, nz, zb, zc, L, o); break;
-    case 1: k_pyramid<uint16_t><<<g, RW_THREADS, 0, s>>>((const uint16_t*)in, nx, ny, nz, zb, zc, L, o); break;
-    case 2: k_pyramid<int16_t><<<g, RW_THREADS, 0, s>>>((const int16_t*)in, nx, ny, nz, zb, zc, L, o); break;
-    default: k_pyramid<float><<<g, RW_THREADS, 0, s>>>((const float*)in, nx, ny, nz, zb, zc, L, o); break;
+    case 0: k_pyramid<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)in, nx, ny, nz, zb, zc, L, o); break;
+    case 1: k_pyramid<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)in, nx, ny, nz, zb, zc, L, o); break;
+    case 2: k_pyramid<int16_t><<<g, 256, 0, s>>>((const int16_t*)in, nx, ny, nz, zb, zc, L, o); break;
+    default: k_pyramid<float><<<g, 256, 0, s>>>((const float*)in, nx, ny, nz, zb, zc, L, o); break;
   }
   return cudaGetLastError();
 }

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+python tools/dbg_cases.py
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -5
+echo "tests rc=${PIPESTATUS[0]}"
+timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_pass -s 60 -c 2 -o gpurun_out/pass2 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu2.log 2>&1; echo "ncu2 rc=$?"
