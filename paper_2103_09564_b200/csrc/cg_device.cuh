@@ -95,6 +95,13 @@ __device__ __forceinline__ double dot4_acc(float4 a, float4 b, double acc) {
   acc = __fma_rn((double)a.z, (double)b.z, acc);
   return __fma_rn((double)a.w, (double)b.w, acc);
 }
+// fp32 dot of a float4 pair in a fixed order (explicit fma chain)
+__device__ __forceinline__ float dot4f(float4 a, float4 b) {
+  float s = __fmul_rn(a.x, b.x);
+  s = __fmaf_rn(a.y, b.y, s);
+  s = __fmaf_rn(a.z, b.z, s);
+  return __fmaf_rn(a.w, b.w, s);
+}
 __device__ __forceinline__ float comp(const float4& v, int c) {
   return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }

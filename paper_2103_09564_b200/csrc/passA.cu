@@ -56,21 +56,37 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
     any |= act[c];
   }
   if (!any) return;
+#pragma unroll
+  for (int c = 0; c < RC; ++c) act[c] = act[c] || RC == 1;   // RC == 1: active if we got here
 
+  // ---------------------------------------------------------------- hoisted geometry
   const Tile t = make_tile(P, u);
-  const int TX = P.TX, TY = P.TY, TXh = P.TXh, hx = P.hx, TXP = P.TXP;
-  const int zs = max(t.z0 - 1, 0), ze = min(t.z1, P.nz - 1);  // planes streamed
+  const int nz = P.nz, TX = P.TX, TY = P.TY, TXh = P.TXh, TXP = P.TXP, tpx = P.tpx;
+  const int hx = P.hx, TXhv = P.TXhv;
+  const int zs = max(t.z0 - 1, 0), ze = min(t.z1, nz - 1);  // planes streamed
   const int np = ze - zs + 1;
-  const int xb = t.x0 - hx, yb = t.y0 - 1;
-  const int par = k & 1;
+  const float nbl2 = C.nbl2, eps = C.eps, gsc = C.scale, gof = C.offset;
   const long long BN = (long long)P.B * P.n;
-  const long long RBN = (long long)P.R * BN;
   const long long plane = (long long)P.nx * P.ny;
-  float* Pnew = Bf.p + (long long)((k + 1) & 1) * RBN;
+  const long long RBN = (long long)P.R * BN;
+  const bool in = t.in;
+  // boundary predicates of this thread's 4 voxels (nx % 4 == 0: only the outer ones vary)
+  const bool hasl = t.x > 0, hasr = t.x + 4 < P.nx, hasu = t.y + 1 < P.ny, hasd = t.y > 0;
+  const int crow = (t.ly + 1) * TXh + hx + 4 * t.lx;   // centre in (TY+2) x TXh boxes
+  const int xrow = t.ly * TX + 4 * t.lx;               // centre in TY x TX boxes
+  const int vrow = (t.ly + 1) * TXhv + P.hxv + 4 * t.lx;  // centre in the intensity box
+  const int spo = (t.ly + 1) * TXP + 4 + 4 * t.lx;     // centre in a p_new plane
+  const int spc = (TY + 2) * TXP;                      // floats per p_new plane (one rhs)
+  float* const sp = reinterpret_cast<float*>(smem + L.sp);
+  float* const Wys = reinterpret_cast<float*>(smem + L.wys);   // [2][TY][TX] +y weights
+  const long long ocol = (long long)b * P.n + (long long)t.y * P.nx + t.x;
+  float* const Pnew = Bf.p + (long long)((k + 1) & 1) * RBN;
+  const int par = k & 1;
 
   // ---------------------------------------------------------------- producer (tid 0)
+  // plane j (z = zs + j) -> ring slot j % kStages; its n-th use completes phase n & 1
   auto issue = [&](int j) {
-    if (tid != 0 || j >= np) return;
+    if (j >= np) return;
     const int zz = zs + j;
     unsigned char* st = smem + (j % kStages) * L.stage;
     uint64_t* bj = bar + (j % kStages);
@@ -79,49 +95,34 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
     for (int c = 0; c < RC; ++c)
       if (act[c]) bytes += 2 * L.eRP + (k > 0 ? L.eX : 0);
     mbar_arrive_expect_tx(bj, bytes);
+    const int xb = t.x0 - hx, yb = t.y0 - 1;
 #pragma unroll
     for (int c = 0; c < RC; ++c) {
       if (!act[c]) continue;
-      const int pr = ((rbase + c) * P.B + b) * P.nz + zz;
-      const int pp = ((par * P.R + rbase + c) * P.B + b) * P.nz + zz;
+      const int pr = ((rbase + c) * P.B + b) * nz + zz;
+      const int pp = ((par * P.R + rbase + c) * P.B + b) * nz + zz;
       tma_load_3d(st + L.oR + c * L.bRP, &M.r, bj, xb, yb, pr);
       tma_load_3d(st + L.oP + c * L.bRP, &M.p, bj, xb, yb, pp);
       if (k > 0) tma_load_3d(st + L.oX + c * L.bX, &M.x, bj, t.x0, t.y0, pr);
     }
-    const int pd = b * P.nz + zz;
+    const int pd = b * nz + zz;
     tma_load_3d(st + L.oD, &M.d, bj, xb, yb, pd);
     if (VM == VM_STORED) {
       tma_load_3d(st + L.oW, &M.wx, bj, xb, t.y0, pd);
-      tma_load_3d(st + L.oW + L.bWx, &M.wy, bj, t.x0, yb, (P.B + b) * P.nz + zz);
-      tma_load_3d(st + L.oW + L.bWx + L.bWy, &M.wz, bj, t.x0, t.y0, (2 * P.B + b) * P.nz + zz);
+      tma_load_3d(st + L.oW + L.bWx, &M.wy, bj, t.x0, yb, (P.B + b) * nz + zz);
+      tma_load_3d(st + L.oW + L.bWx + L.bWy, &M.wz, bj, t.x0, t.y0, (2 * P.B + b) * nz + zz);
     } else {
       tma_load_3d(st + L.oW, &M.v, bj, t.x0 - P.hxv, yb, pd);
     }
   };
   auto wait = [&](int j) { mbar_wait(bar + (j % kStages), (uint32_t)((j / kStages) & 1)); };
   auto stg = [&](int j) -> const unsigned char* { return smem + (j % kStages) * L.stage; };
-  auto sRP = [&](int j, int off) { return reinterpret_cast<const float*>(stg(j) + off); };
-
-  if (tid == 0) {
-    prefetch_tmap(&M.r);
-    prefetch_tmap(&M.p);
-    prefetch_tmap(&M.d);
-    prefetch_tmap(VM == VM_STORED ? &M.wx : &M.v);
-  }
-  for (int j = 0; j < kStages; ++j) issue(j);
-
-  const int cc = hx + 4 * t.lx;              // column of this thread's voxels in a halo box
-  const int crow = (t.ly + 1) * TXh + cc;    // its element offset in a (TY+2) x TXh box
-  // the intensity box has its own halo offset hxv = 16 B / element size: TMA box starts
-  // must stay 16-byte aligned in x
-  const int vrow = (t.ly + 1) * P.TXhv + P.hxv + 4 * t.lx;
+  auto F = [](const unsigned char* st, int off) { return reinterpret_cast<const float*>(st + off); };
   auto centre_pnew = [&](const unsigned char* st, int c) -> float4 {
-    const float* R = reinterpret_cast<const float*>(st + L.oR + c * L.bRP);
-    const float* Pp = reinterpret_cast<const float*>(st + L.oP + c * L.bRP);
-    const float* D = reinterpret_cast<const float*>(st + L.oD);
-    return pnew4(be[c], ld4(Pp + crow), ld4(D + crow), ld4(R + crow));
+    return pnew4(be[c], ld4(F(st, L.oP + c * L.bRP) + crow), ld4(F(st, L.oD) + crow),
+                 ld4(F(st, L.oR + c * L.bRP) + crow));
   };
-  // normalised intensities of 4 consecutive box elements (vector smem load)
+  // normalised intensities of 4 consecutive intensity-box elements (one vector smem load)
   auto gvol4 = [&](const unsigned char* st, int off, float g[4]) {
     const T* v = reinterpret_cast<const T*>(st + L.oW) + off;
     if (sizeof(T) == 4) {
@@ -137,12 +138,27 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       g[0] = (float)e[0]; g[1] = (float)e[1]; g[2] = (float)e[2]; g[3] = (float)e[3];
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) g[e] = normv(g[e], C.scale, C.offset);
+    for (int e = 0; e < 4; ++e) g[e] = normv(g[e], gsc, gof);
   };
   auto gvol1 = [&](const unsigned char* st, int off) -> float {
-    return normv((float)reinterpret_cast<const T*>(st + L.oW)[off], C.scale, C.offset);
+    return normv((float)reinterpret_cast<const T*>(st + L.oW)[off], gsc, gof);
   };
-  float* Wys = reinterpret_cast<float*>(smem + L.wys);   // +y weights of this plane's rows
+
+  if (tid == 0) {
+    prefetch_tmap(&M.r);
+    prefetch_tmap(&M.p);
+    prefetch_tmap(&M.d);
+    prefetch_tmap(VM == VM_STORED ? &M.wx : &M.v);
+    // planes 0 .. jz0 + kStages - 2 now; step z issues plane (z - zs) + kStages - 1
+    for (int j = 0; j <= (t.z0 - zs) + kStages - 2; ++j) issue(j);
+  }
+  // out-of-tile halo columns of the p_new planes stay zero when the tile spans the brick
+  if (hx == 0) {
+    for (int h = tid; h < 2 * 2 * RC * TY; h += blockDim.x) {
+      const int side = h & 1, ry = (h >> 1) % TY, pc_ = (h >> 1) / TY;   // pc_ = buf*RC + c
+      sp[pc_ * spc + (ry + 1) * TXP + (side ? TX + 4 : 3)] = 0.f;
+    }
+  }
 
   float4 pm[RC], pc[RC], pn[RC];
   float4 wzm = f4(0.f);
@@ -152,15 +168,15 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   const int jz0 = t.z0 - zs;
   if (t.z0 > 0) {                            // plane z0-1 = stage 0: z-neighbour + Wz(z0-1)
     wait(0);
-    if (t.in) {
+    if (in) {
 #pragma unroll
       for (int c = 0; c < RC; ++c)
         if (act[c]) pm[c] = centre_pnew(stg(0), c);
-      if (VM == VM_STORED) wzm = ld4(sRP(0, L.oW + L.bWx + L.bWy) + t.ly * TX + 4 * t.lx);
+      if (VM == VM_STORED) wzm = ld4(F(stg(0), L.oW + L.bWx + L.bWy) + xrow);
     }
   }
   wait(jz0);
-  if (t.in) {
+  if (in) {
 #pragma unroll
     for (int c = 0; c < RC; ++c)
       if (act[c]) pc[c] = centre_pnew(stg(jz0), c);
@@ -169,10 +185,10 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       if (t.z0 > 0) {
         float gm[4];
         gvol4(stg(0), vrow, gm);
-        wzm = make_float4(grady(__fsub_rn(gcur[0], gm[0]), C.nbl2, C.eps),
-                          grady(__fsub_rn(gcur[1], gm[1]), C.nbl2, C.eps),
-                          grady(__fsub_rn(gcur[2], gm[2]), C.nbl2, C.eps),
-                          grady(__fsub_rn(gcur[3], gm[3]), C.nbl2, C.eps));
+        wzm = make_float4(grady(__fsub_rn(gcur[0], gm[0]), nbl2, eps),
+                          grady(__fsub_rn(gcur[1], gm[1]), nbl2, eps),
+                          grady(__fsub_rn(gcur[2], gm[2]), nbl2, eps),
+                          grady(__fsub_rn(gcur[3], gm[3]), nbl2, eps));
       }
     }
   }
@@ -180,117 +196,117 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   double acc[RC];
 #pragma unroll
   for (int c = 0; c < RC; ++c) acc[c] = 0.0;
-  const int spc = (TY + 2) * TXP;            // floats per p_new plane (one rhs)
-  const int nhx = 2 * P.tpx;
-  const int nhalo = nhx + 2 * TY;
+  const int nrow = 2 * tpx;                   // row-halo float4 items per rhs
+  const int nhalo = nrow + (hx ? 2 * TY : 0); // + column-halo scalar items
 
   for (int z = t.z0; z < t.z1; ++z) {
     const int jz = z - zs;
-    __syncthreads();                         // plane z-1's stage and p_new plane are free
-    if (jz >= 1) issue(jz - 1 + kStages);
     const bool hasn = z + 1 <= ze;
     const unsigned char* s0 = stg(jz);
     const unsigned char* s1 = stg(jz + 1);
+    const int buf = z & 1;
     if (hasn) wait(jz + 1);
-    if (t.in) {
+    if (in) {
 #pragma unroll
       for (int c = 0; c < RC; ++c) pn[c] = (hasn && act[c]) ? centre_pnew(s1, c) : f4(0.f);
     }
-    // p_k of plane z (centre + x/y halo) into the shared plane
-    float* spz0 = reinterpret_cast<float*>(smem + L.sp) + (z & 1) * RC * spc;
+    // p_k of plane z (centre + x/y halo) into shared plane `buf`
+    float* spz = sp + buf * RC * spc;
     if (t.ly < TY) {
 #pragma unroll
-      for (int c = 0; c < RC; ++c)
-        st4(spz0 + c * spc + (t.ly + 1) * TXP + 4 + 4 * t.lx, (t.in && act[c]) ? pc[c] : f4(0.f));
+      for (int c = 0; c < RC; ++c) st4(spz + c * spc + spo, (in && act[c]) ? pc[c] : f4(0.f));
     }
     for (int h = tid; h < nhalo; h += blockDim.x) {
-      if (h < nhx) {                         // rows y0-1 / y0+TY (zero-filled if outside)
-        const int side = h / P.tpx, g = h % P.tpx;
+      if (h < nrow) {                        // rows y0-1 / y0+TY (zero-filled if outside)
+        const int side = h >= tpx, g = side ? h - tpx : h;
         const int brow = side ? TY + 1 : 0;
         const int off = brow * TXh + hx + 4 * g;
 #pragma unroll
         for (int c = 0; c < RC; ++c) {
           float4 v = f4(0.f);
           if (act[c])
-            v = pnew4(be[c], ld4(sRP(jz, L.oP + c * L.bRP) + off), ld4(sRP(jz, L.oD) + off),
-                      ld4(sRP(jz, L.oR + c * L.bRP) + off));
-          st4(spz0 + c * spc + brow * TXP + 4 + 4 * g, v);
+            v = pnew4(be[c], ld4(F(s0, L.oP + c * L.bRP) + off), ld4(F(s0, L.oD) + off),
+                      ld4(F(s0, L.oR + c * L.bRP) + off));
+          st4(spz + c * spc + brow * TXP + 4 + 4 * g, v);
         }
-      } else {                               // columns x0-1 / x0+TX
-        const int hh = h - nhx;
-        const int side = hh / TY, ry = hh % TY;
-        const int scol = side ? TX + 4 : 3;
+      } else {                               // columns x0-1 / x0+TX (tile narrower than brick)
+        const int hh = h - nrow;
+        const int side = hh >= TY, ry = side ? hh - TY : hh;
         const int off = (ry + 1) * TXh + (side ? hx + TX : hx - 1);
 #pragma unroll
         for (int c = 0; c < RC; ++c) {
           float v = 0.f;
-          if (hx && act[c])
-            v = pnew1(be[c], sRP(jz, L.oP + c * L.bRP)[off], sRP(jz, L.oD)[off],
-                      sRP(jz, L.oR + c * L.bRP)[off]);
-          spz0[c * spc + (ry + 1) * TXP + scol] = v;
+          if (act[c])
+            v = pnew1(be[c], F(s0, L.oP + c * L.bRP)[off], F(s0, L.oD)[off],
+                      F(s0, L.oR + c * L.bRP)[off]);
+          spz[c * spc + (ry + 1) * TXP + (side ? TX + 4 : 3)] = v;
         }
       }
     }
     // ---- edge weights of this thread's 4 voxels
-    float4 wx = f4(0.f), wxm = f4(0.f), wy = f4(0.f), wym = f4(0.f), wz = f4(0.f);
+    float4 wx, wxm, wy, wym, wz;
     float gz[4] = {0.f, 0.f, 0.f, 0.f};
-    if (t.in) {
-      if (VM == VM_STORED) {
-        const float* Wxb = sRP(jz, L.oW);
-        const float* Wyb = sRP(jz, L.oW + L.bWx);
-        const float* Wzb = sRP(jz, L.oW + L.bWx + L.bWy);
-        wx = ld4(Wxb + t.ly * TXh + cc);
-        const float wl = (t.x > 0) ? Wxb[t.ly * TXh + cc - 1] : 0.f;
-        wxm = make_float4(wl, wx.x, wx.y, wx.z);
-        wy = ld4(Wyb + (t.ly + 1) * TX + 4 * t.lx);
-        wym = ld4(Wyb + t.ly * TX + 4 * t.lx);
-        wz = ld4(Wzb + t.ly * TX + 4 * t.lx);
-      } else {
-        // forward weights of the own voxels; -x of voxels 1..3 is +x of voxels 0..2, -y comes
-        // from the row above through shared memory, -z from the previous plane (registers)
-        float gu[4];
-        if (hasn) gvol4(s1, vrow, gz);
-        gvol4(s0, vrow + P.TXhv, gu);
-        const float gl = (t.x > 0) ? gvol1(s0, vrow - 1) : 0.f;
-        const float gr = (t.x + 4 < P.nx) ? gvol1(s0, vrow + 4) : 0.f;
-        float a[4], yy[4], zz[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float nx_ = e < 3 ? gcur[e + 1] : gr;
-          a[e] = (t.x + e + 1 < P.nx) ? grady(__fsub_rn(nx_, gcur[e]), C.nbl2, C.eps) : 0.f;
-          yy[e] = (t.y + 1 < P.ny) ? grady(__fsub_rn(gu[e], gcur[e]), C.nbl2, C.eps) : 0.f;
-          zz[e] = (z + 1 < P.nz) ? grady(__fsub_rn(gz[e], gcur[e]), C.nbl2, C.eps) : 0.f;
-        }
-        const float am0 = (t.x > 0) ? grady(__fsub_rn(gcur[0], gl), C.nbl2, C.eps) : 0.f;
-        wx = make_float4(a[0], a[1], a[2], a[3]);
-        wxm = make_float4(am0, a[0], a[1], a[2]);
-        wy = make_float4(yy[0], yy[1], yy[2], yy[3]);
-        wz = make_float4(zz[0], zz[1], zz[2], zz[3]);
-        st4(Wys + t.ly * TX + 4 * t.lx, wy);
-        if (t.ly == 0 && t.y > 0) {          // first tile row: -y weights from the halo row
-          float gd[4];
-          gvol4(s0, vrow - P.TXhv, gd);
-          wym = make_float4(grady(__fsub_rn(gcur[0], gd[0]), C.nbl2, C.eps),
-                            grady(__fsub_rn(gcur[1], gd[1]), C.nbl2, C.eps),
-                            grady(__fsub_rn(gcur[2], gd[2]), C.nbl2, C.eps),
-                            grady(__fsub_rn(gcur[3], gd[3]), C.nbl2, C.eps));
-        }
+    if (VM != VM_STORED && in) {
+      // forward weights of the own voxels; -x of voxels 1..3 is +x of voxels 0..2, -y comes
+      // from the row above through shared memory, -z from the previous plane (registers)
+      float gu[4];
+      if (hasn) gvol4(s1, vrow, gz);
+      gvol4(s0, vrow + TXhv, gu);
+      const float gl = hasl ? gvol1(s0, vrow - 1) : 0.f;
+      const float gr = hasr ? gvol1(s0, vrow + 4) : 0.f;
+      const bool hz = z + 1 < nz;
+      const float a0 = grady(__fsub_rn(gcur[1], gcur[0]), nbl2, eps);
+      const float a1 = grady(__fsub_rn(gcur[2], gcur[1]), nbl2, eps);
+      const float a2 = grady(__fsub_rn(gcur[3], gcur[2]), nbl2, eps);
+      const float a3 = hasr ? grady(__fsub_rn(gr, gcur[3]), nbl2, eps) : 0.f;
+      const float am0 = hasl ? grady(__fsub_rn(gcur[0], gl), nbl2, eps) : 0.f;
+      wx = make_float4(a0, a1, a2, a3);
+      wxm = make_float4(am0, a0, a1, a2);
+      wy = hasu ? make_float4(grady(__fsub_rn(gu[0], gcur[0]), nbl2, eps),
+                              grady(__fsub_rn(gu[1], gcur[1]), nbl2, eps),
+                              grady(__fsub_rn(gu[2], gcur[2]), nbl2, eps),
+                              grady(__fsub_rn(gu[3], gcur[3]), nbl2, eps))
+                : f4(0.f);
+      wz = hz ? make_float4(grady(__fsub_rn(gz[0], gcur[0]), nbl2, eps),
+                            grady(__fsub_rn(gz[1], gcur[1]), nbl2, eps),
+                            grady(__fsub_rn(gz[2], gcur[2]), nbl2, eps),
+                            grady(__fsub_rn(gz[3], gcur[3]), nbl2, eps))
+              : f4(0.f);
+      st4(Wys + buf * TY * TX + xrow, wy);
+      wym = f4(0.f);
+      if (t.ly == 0 && hasd) {               // first tile row: -y weights from the halo row
+        float gd[4];
+        gvol4(s0, vrow - TXhv, gd);
+        wym = make_float4(grady(__fsub_rn(gcur[0], gd[0]), nbl2, eps),
+                          grady(__fsub_rn(gcur[1], gd[1]), nbl2, eps),
+                          grady(__fsub_rn(gcur[2], gd[2]), nbl2, eps),
+                          grady(__fsub_rn(gcur[3], gd[3]), nbl2, eps));
       }
     }
-    __syncthreads();
-    if (t.in) {
-      if (VM != VM_STORED && t.ly > 0) wym = ld4(Wys + (t.ly - 1) * TX + 4 * t.lx);
-      const float4 dvc = ld4(sRP(jz, L.oD) + crow);
-      const long long o = (long long)b * P.n + (long long)z * plane + (long long)t.y * P.nx + t.x;
+    __syncthreads();                          // p_new plane + Wys of plane z complete
+    if (tid == 0) issue(jz + kStages - 1);    // refill the slot of plane z-1 (all done with it)
+    if (in) {
+      if (VM == VM_STORED) {
+        const float* Wxb = F(s0, L.oW);
+        wx = ld4(Wxb + t.ly * TXh + hx + 4 * t.lx);
+        const float wl = hasl ? Wxb[t.ly * TXh + hx + 4 * t.lx - 1] : 0.f;
+        wxm = make_float4(wl, wx.x, wx.y, wx.z);
+        wy = ld4(F(s0, L.oW + L.bWx) + xrow + TX);
+        wym = ld4(F(s0, L.oW + L.bWx) + xrow);
+        wz = ld4(F(s0, L.oW + L.bWx + L.bWy) + xrow);
+      } else if (t.ly > 0) {
+        wym = ld4(Wys + buf * TY * TX + xrow - TX);
+      }
+      const float4 dvc = ld4(F(s0, L.oD) + crow);
+      const long long o = ocol + (long long)z * plane;
 #pragma unroll
       for (int c = 0; c < RC; ++c) {
         if (!act[c]) continue;
-        const float* s = spz0 + c * spc;
-        const int sc = 4 + 4 * t.lx;
-        const float4 yp = ld4(s + (t.ly + 2) * TXP + sc);
-        const float4 ym = ld4(s + t.ly * TXP + sc);
-        const float xl = s[(t.ly + 1) * TXP + sc - 1];
-        const float xr = s[(t.ly + 1) * TXP + sc + 4];
+        const float* s = spz + c * spc;
+        const float4 yp = ld4(s + spo + TXP);
+        const float4 ym = ld4(s + spo - TXP);
+        const float xl = s[spo - 1];
+        const float xr = s[spo + 4];
         const float4 p = pc[c];
         float4 q;
         q.x = stencil1(p.x, p.y, xl, yp.x, ym.x, pn[c].x, pm[c].x, wx.x, wxm.x, wy.x, wym.x, wz.x, wzm.x, dvc.x);
@@ -299,13 +315,13 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
         q.w = stencil1(p.w, xr, p.z, yp.w, ym.w, pn[c].w, pm[c].w, wx.w, wxm.w, wy.w, wym.w, wz.w, wzm.w, dvc.w);
         const long long ov = (long long)(rbase + c) * BN + o;
         if (k > 0) {
-          const float4 po = ld4(sRP(jz, L.oP + c * L.bRP) + crow);
-          const float4 xo = ld4(sRP(jz, L.oX + c * L.bX) + t.ly * TX + 4 * t.lx);
+          const float4 po = ld4(F(s0, L.oP + c * L.bRP) + crow);
+          const float4 xo = ld4(F(s0, L.oX + c * L.bX) + xrow);
           st4(Bf.x + ov, fma4(al[c], po, xo));
         }
         st4(Pnew + ov, p);
         st4(Bf.q + ov, q);
-        acc[c] = dot4_acc(p, q, acc[c]);
+        acc[c] += (double)dot4f(p, q);
       }
       wzm = wz;
 #pragma unroll

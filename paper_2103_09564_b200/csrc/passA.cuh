@@ -19,7 +19,7 @@ struct Maps {
   CUtensorMap v;    // vol    [B],          box {TXhv, TY+2, 1}  (VM_U8..VM_F32)
 };
 
-constexpr int kStages = 3;  // TMA ring depth (prefetch distance 2 planes)
+constexpr int kStages = 4;  // TMA ring depth (planes issued ~2 steps before use)
 
 __host__ __device__ inline int rup128(int b) { return (b + 127) & ~127; }
 __host__ __device__ inline int vm_esize(int vm) {
@@ -55,7 +55,7 @@ __host__ __device__ inline ALayout a_layout(const Plan& P, int RC, int vm) {
   L.stage = L.oW + (vm == VM_STORED ? L.bWx + L.bWy + L.bWz : L.bV);
   L.sp = kStages * L.stage;
   L.wys = L.sp + rup128(2 * RC * (P.TY + 2) * P.TXP * 4);
-  L.bars = L.wys + (vm == VM_STORED ? 0 : rup128(P.TY * P.TX * 4));
+  L.bars = L.wys + (vm == VM_STORED ? 0 : rup128(2 * P.TY * P.TX * 4));
   L.total = L.bars + kStages * 8;
   return L;
 }
