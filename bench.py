@@ -98,9 +98,10 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
-def make_inputs(rank, workers):
+def make_inputs(rank, world, workers):
     import workloads as wl
-    ids = list(range(rank * BATCH, (rank + 1) * BATCH))
+    from paper_2103_09564_b200.dist import shard_bricks
+    ids = shard_bricks(rank, world, BATCH)
     t = time.time()
     p = wl.cfg2(bricks=ids, n=N, workers=workers)
     log(f"[rank {rank}] generated {len(ids)} bricks in {time.time() - t:.1f}s")
@@ -151,13 +152,14 @@ def run_b200(args, rank, world, local_rank):
     import torch
     import paper_2103_09564_b200 as rwb
     from paper_2103_09564_b200 import api
+    from paper_2103_09564_b200.dist import reduce_metric
 
     dist = None
     if world > 1:
         import torch.distributed as dist
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    p = make_inputs(rank, args.workers)
+    p = make_inputs(rank, world, args.workers)
     vol = torch.from_numpy(p.vol).to(dev)
     fixed = torch.from_numpy(p.fixed).to(dev)
     values = torch.from_numpy(p.values).to(dev)
@@ -202,13 +204,10 @@ def run_b200(args, rank, world, local_rank):
     ms = e0.elapsed_time(e1)
     prof = api.profile_read()
     api.profile_enable(False)
-    t_max = ms
-    if dist is not None:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
+    # max device time over ranks, total work over ranks (paper_2103_09564_b200.dist)
+    t_max, work_all = reduce_metric(ms, vox_iters, dev)
     ms_per_step = t_max / args.steps
-    value = vox_iters * world / (ms_per_step / 1000.0)
+    value = work_all / (ms_per_step / 1000.0)
 
     # ---------------- roofline of the dominant kernel ----------------
     launches = {k: v[0] for k, v in prof.items()}
@@ -256,12 +255,8 @@ def run_b200(args, rank, world, local_rank):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    ems = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ems], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t.item())
-    e2e_value = vox_iters * world / (ems / args.steps / 1000.0)
+    ems, _ = reduce_metric(e0.elapsed_time(e1), vox_iters, dev)
+    e2e_value = work_all / (ems / args.steps / 1000.0)
     h2d = h_vol.numel() * h_vol.element_size() + h_fixed.numel() + h_values.numel() * 4
     d2h = h_labels.numel() + h_iters.numel() * 4
 

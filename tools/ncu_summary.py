@@ -15,7 +15,8 @@ import json
 import os
 import subprocess
 
-UNITS = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+UNITS = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
 BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
