@@ -12,7 +12,7 @@
 
 namespace rw {
 cudaError_t launch_pyramid_group(const void*, int, int, int, int, int, int, int, const PyrOut&,
-                                 cudaStream_t);
+                                 const CUtensorMap*, cudaStream_t);
 cudaError_t launch_weights(const void*, int, float, float, int, int, int, int, float, float,
                            float*, float*, const uint8_t*, int, cudaStream_t);
 cudaError_t launch_dinv(const float*, int, int, int, int, const uint8_t*, float*, int, cudaStream_t);
@@ -148,7 +148,8 @@ EncodeTiled encoder() {
 }
 
 // 3-D map (x, y, plane) over `planes` planes of nx x ny elements; box {bx, by, 1}.
-bool tmap(CUtensorMap* m, const void* base, int es, int nx, int ny, long long planes, int bx, int by) {
+bool tmap(CUtensorMap* m, const void* base, int es, int nx, int ny, long long planes, int bx, int by,
+          int bz = 1) {
   EncodeTiled enc = encoder();
   if (!enc) return false;
   const CUtensorMapDataType dt = es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
@@ -156,7 +157,7 @@ bool tmap(CUtensorMap* m, const void* base, int es, int nx, int ny, long long pl
                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)planes};
   const cuuint64_t strides[2] = {(cuuint64_t)nx * es, (cuuint64_t)nx * ny * es};
-  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
   const cuuint32_t el[3] = {1, 1, 1};
   return enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, el,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -474,8 +475,14 @@ rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int
       o.p[k] = level_out[l0 + k];
       o.nx[k] = nx[l0 + k + 1]; o.ny[k] = ny[l0 + k + 1]; o.nz[k] = nz[l0 + k + 1];
     }
+    // stage each CTA's 32^3 input box with one TMA load when the row pitch allows it
+    CUtensorMap map;
+    const int es = (int)dtype_size(dtype);
+    const bool use_tma = ((size_t)nx[l0] * es) % 16 == 0 && ((uintptr_t)in & 15u) == 0 &&
+                         tmap(&map, in, es == 4 ? 4 : es, nx[l0], ny[l0], lzc, 32, 32, 32);
     RW_TIMED(RW_K_PYRAMID, s, 1,
-             rw::launch_pyramid_group(in, dtype, nx[l0], ny[l0], nz[l0], lz0, lzc, L, o, s));
+             rw::launch_pyramid_group(in, dtype, nx[l0], ny[l0], nz[l0], lz0, lzc, L, o,
+                                      use_tma ? &map : nullptr, s));
     // next group reads the coarsest level just written, restricted to this slab's planes
     const int nlz0 = lz0 >> L;
     const int nlzc = ((lz0 + lzc + (1 << L) - 1) >> L) - nlz0;

@@ -11,6 +11,7 @@
 #include <type_traits>
 
 #include "rw_common.cuh"
+#include "tma.cuh"
 
 namespace rw {
 
@@ -55,17 +56,37 @@ __device__ __forceinline__ T mean8(G get) {
   return finish<T, A>(tadd(s01, s23));
 }
 
+__device__ __forceinline__ int pe3(int l) { const int e = 16 >> l; return (2 * e) * (2 * e) * (2 * e); }
+
 // in: input level, plane zb (global) at in[0]; level dims nx,ny,nz; process planes
 // [zb, zb+zc) (zb multiple of 2^L, zc multiple of 2^L unless zb+zc == nz).
-template <typename T>
+// USE_TMA: the CTA's 32^3 input box is staged in shared memory by one TMA load
+// (cp.async.bulk.tensor, zero-filled outside the volume) instead of scattered 1-4 byte
+// global loads; requires nx * sizeof(T) % 16 == 0 (tensor-map row pitch).
+template <typename T, bool USE_TMA>
 __global__ void __launch_bounds__(256)
-k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int L, PyrOut o) {
+k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int L, PyrOut o,
+          const __grid_constant__ CUtensorMap map) {
   using A = typename std::conditional<std::is_same<T, float>::value, float, int>::type;
-  __shared__ A s1[16 * 16 * 16];
-  __shared__ A s2[8 * 8 * 8];
-  __shared__ A s3[4 * 4 * 4];
-  __shared__ A s4[2 * 2 * 2];
-  A* sl[4] = {s1, s2, s3, s4};
+  extern __shared__ __align__(128) unsigned char dsm[];
+  const T* box = reinterpret_cast<const T*>(dsm);
+  if (USE_TMA) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(dsm + 32 * 32 * 32 * sizeof(T));
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(bar, 32 * 32 * 32 * sizeof(T));
+      tma_load_3d(dsm, &map, bar, blockIdx.x * 32, blockIdx.y * 32, blockIdx.z * 32);
+    }
+    mbar_wait(bar, 0);
+  }
+  // level buffers 1..4 (16^3, 8^3, 4^3, 2^3) in one array; offsets computed, not indexed
+  // through a pointer table (which would live in local memory)
+  __shared__ A lv[4096 + 512 + 64 + 8];
+  A* s1 = lv;
   const long long pin = (long long)nx * ny;
   // level 1 from global
   {
@@ -76,11 +97,27 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
       const int lx = idx & 15, ly = (idx >> 4) & 15, lz = idx >> 8;
       const int X = X0 + lx, Y = Y0 + ly, Z = Z0 + lz;
       A v = 0;
-      if (X < o.nx[0] && Y < o.ny[0] && Z < o.nz[0] && 2 * Z < zb + zc) {
+      if (USE_TMA && 2 * X + 1 < nx && 2 * Y + 1 < ny && 2 * Z + 1 < nz && 2 * Z + 1 < zb + zc) {
+        // interior fast path: all 8 children present -> same rule, no count bookkeeping
+        const T* c = box + ((2 * lz) * 32 + 2 * ly) * 32 + 2 * lx;
+        T r;
+        if (std::is_same<T, float>::value) {
+          const float s01 = ((float)c[0] + (float)c[1]) + ((float)c[32] + (float)c[33]);
+          const float s23 = ((float)c[1024] + (float)c[1025]) + ((float)c[1056] + (float)c[1057]);
+          r = (T)((s01 + s23) / 8.0f);
+        } else {
+          const int s = ((int)c[0] + (int)c[1]) + ((int)c[32] + (int)c[33]) +
+                        ((int)c[1024] + (int)c[1025]) + ((int)c[1056] + (int)c[1057]);
+          r = (T)((s + 4) >> 3);                // floor((s + 4) / 8), arithmetic shift
+        }
+        out[(long long)Z * po + (long long)Y * o.nx[0] + X] = r;
+        v = (A)r;
+      } else if (X < o.nx[0] && Y < o.ny[0] && Z < o.nz[0] && 2 * Z < zb + zc) {
         const T r = mean8<T, A>([&](int dx, int dy, int dz, A& val) {
           const int x = 2 * X + dx, y = 2 * Y + dy, z = 2 * Z + dz;
           if (x >= nx || y >= ny || z >= nz) return false;
-          val = (A)in[(long long)(z - zb) * pin + (long long)y * nx + x];
+          val = USE_TMA ? (A)box[((2 * lz + dz) * 32 + (2 * ly + dy)) * 32 + (2 * lx + dx)]
+                        : (A)in[(long long)(z - zb) * pin + (long long)y * nx + x];
           return true;
         });
         out[(long long)Z * po + (long long)Y * o.nx[0] + X] = r;
@@ -90,12 +127,15 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
     }
   }
   // levels 2..L from shared memory
-  for (int l = 1; l < L; ++l) {
+#pragma unroll
+  for (int l = 1; l < 5; ++l) {
+    if (l >= L) break;
     __syncthreads();
     const int e = 16 >> l;                // box extent at this level
     const int X0 = blockIdx.x * e, Y0 = blockIdx.y * e, Z0 = (zb >> (l + 1)) + blockIdx.z * e;
-    const A* src = sl[l - 1];
-    A* dst = (l < 4) ? sl[l] : nullptr;
+    const int off_src = l == 1 ? 0 : (l == 2 ? 4096 : (l == 3 ? 4608 : 4672));
+    const A* src = lv + off_src;
+    A* dst = (l < 4) ? lv + off_src + pe3(l) : nullptr;
     T* out = (T*)o.p[l];
     const long long po = (long long)o.nx[l] * o.ny[l];
     const int pe = 2 * e;                 // child box extent
@@ -103,7 +143,24 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
       const int lx = idx % e, ly = (idx / e) % e, lz = idx / (e * e);
       const int X = X0 + lx, Y = Y0 + ly, Z = Z0 + lz;
       A v = 0;
-      if (X < o.nx[l] && Y < o.ny[l] && Z < o.nz[l] && 2 * Z < ((zb + zc + (1 << l) - 1) >> l)) {
+      const int zend = (zb + zc + (1 << l) - 1) >> l;   // slab end at the child level
+      if (2 * X + 1 < o.nx[l - 1] && 2 * Y + 1 < o.ny[l - 1] && 2 * Z + 1 < o.nz[l - 1] &&
+          2 * Z + 1 < zend) {                           // interior: 8 children present
+        const A* c = src + ((2 * lz) * pe + 2 * ly) * pe + 2 * lx;
+        const int pp = pe * pe;
+        T r;
+        if (std::is_same<T, float>::value) {
+          const float s01 = ((float)c[0] + (float)c[1]) + ((float)c[pe] + (float)c[pe + 1]);
+          const float s23 = ((float)c[pp] + (float)c[pp + 1]) + ((float)c[pp + pe] + (float)c[pp + pe + 1]);
+          r = (T)((s01 + s23) / 8.0f);
+        } else {
+          const int s = ((int)c[0] + (int)c[1]) + ((int)c[pe] + (int)c[pe + 1]) +
+                        ((int)c[pp] + (int)c[pp + 1]) + ((int)c[pp + pe] + (int)c[pp + pe + 1]);
+          r = (T)((s + 4) >> 3);
+        }
+        out[(long long)Z * po + (long long)Y * o.nx[l] + X] = r;
+        v = (A)r;
+      } else if (X < o.nx[l] && Y < o.ny[l] && Z < o.nz[l] && 2 * Z < zend) {
         const T r = mean8<T, A>([&](int dx, int dy, int dz, A& val) {
           const int x = 2 * X + dx, y = 2 * Y + dy, z = 2 * Z + dz;
           if (x >= o.nx[l - 1] || y >= o.ny[l - 1] || z >= o.nz[l - 1]) return false;
@@ -118,16 +175,36 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
   }
 }
 
-cudaError_t launch_pyramid_group(const void* in, int dtype, int nx, int ny, int nz, int zb,
-                                 int zc, int L, const PyrOut& o, cudaStream_t s) {
+template <typename T>
+static cudaError_t launch_t(const void* in, int nx, int ny, int nz, int zb, int zc, int L,
+                           const PyrOut& o, const CUtensorMap* map, cudaStream_t s) {
   const dim3 g((nx + 31) / 32, (ny + 31) / 32, (zc + 31) / 32);
-  switch (dtype) {
-    case 0: k_pyramid<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)in, nx, ny, nz, zb, zc, L, o); break;
-    case 1: k_pyramid<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)in, nx, ny, nz, zb, zc, L, o); break;
-    case 2: k_pyramid<int16_t><<<g, 256, 0, s>>>((const int16_t*)in, nx, ny, nz, zb, zc, L, o); break;
-    default: k_pyramid<float><<<g, 256, 0, s>>>((const float*)in, nx, ny, nz, zb, zc, L, o); break;
+  if (map) {
+    const int smem = 32 * 32 * 32 * sizeof(T) + 8;
+    static int attr = 0;
+    if (attr < smem) {
+      const cudaError_t e = cudaFuncSetAttribute(k_pyramid<T, true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      attr = smem;
+    }
+    k_pyramid<T, true><<<g, 256, smem, s>>>((const T*)in, nx, ny, nz, zb, zc, L, o, *map);
+  } else {
+    CUtensorMap dummy{};
+    k_pyramid<T, false><<<g, 256, 0, s>>>((const T*)in, nx, ny, nz, zb, zc, L, o, dummy);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_pyramid_group(const void* in, int dtype, int nx, int ny, int nz, int zb,
+                                 int zc, int L, const PyrOut& o, const CUtensorMap* map,
+                                 cudaStream_t s) {
+  switch (dtype) {
+    case 0: return launch_t<uint8_t>(in, nx, ny, nz, zb, zc, L, o, map, s);
+    case 1: return launch_t<uint16_t>(in, nx, ny, nz, zb, zc, L, o, map, s);
+    case 2: return launch_t<int16_t>(in, nx, ny, nz, zb, zc, L, o, map, s);
+    default: return launch_t<float>(in, nx, ny, nz, zb, zc, L, o, map, s);
+  }
 }
 
 }  // namespace rw
