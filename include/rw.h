@@ -166,6 +166,27 @@ rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int
                                 void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * Solver selection.  rw_solve_bricks / rw_solve_labels run one of two implementations of
+ * the same Jacobi-PCG with the same stopping rule, status codes and outputs:
+ *   streaming  -- CG state in HBM, two fused passes per iteration (any brick shape, any
+ *                 nrhs);
+ *   resident   -- one thread-block cluster per brick keeps the whole CG state on chip
+ *                 (shared + tensor memory, registers) for all iterations (SURVEY 8(f)
+ *                 f2/f4); bricks of 64x64x64 or 32x32x32, nrhs == 1, device permitting.
+ * RW_OPT_SOLVER: RW_SOLVER_AUTO (default: resident when available, else streaming),
+ * RW_SOLVER_STREAMING, RW_SOLVER_RESIDENT (a solve it cannot serve returns
+ * RW_EUNSUPPORTED).  Process-wide setting; not thread-safe against concurrent solves.
+ * rw_resident_available(d, nrhs): 1 if the resident solver can serve this shape on the
+ * current device, else 0.  Results of the two solvers agree to the solver tolerance, not
+ * bitwise (different fp64 reduction trees); each is deterministic and batch-invariant.
+ * ---------------------------------------------------------------------------------- */
+enum { RW_OPT_SOLVER = 0 };
+enum { RW_SOLVER_AUTO = 0, RW_SOLVER_STREAMING = 1, RW_SOLVER_RESIDENT = 2 };
+rw_status rw_set_option(int32_t key, int64_t value);
+int64_t rw_get_option(int32_t key);
+int32_t rw_resident_available(rw_dims d, int32_t nrhs);
+
+/* ------------------------------------------------------------------------------------
  * Pinned, double-buffered host->device queue for inputs larger than HBM (north star item
  * 5; P:105 constant-memory brick-wise loading).  A ring of `depth` (>= 2) slots, each a
  * pinned host buffer plus a device buffer of slot_bytes, allocated once here (library-
@@ -192,7 +213,7 @@ void rw_queue_destroy(rw_queue* q);
  *   launches  out host int64[RW_K_COUNT] or NULL;  ms  out host double[RW_K_COUNT] or NULL.
  * ---------------------------------------------------------------------------------- */
 enum { RW_K_WEIGHTS = 0, RW_K_SETUP = 1, RW_K_PASSA = 2, RW_K_PASSB = 3, RW_K_FINALIZE = 4,
-       RW_K_PYRAMID = 5, RW_K_OTHER = 6, RW_K_COUNT = 7 };
+       RW_K_PYRAMID = 5, RW_K_OTHER = 6, RW_K_RESIDENT = 7, RW_K_COUNT = 8 };
 rw_status rw_profile_enable(int32_t on);
 rw_status rw_profile_read(int64_t* launches, double* ms);
 

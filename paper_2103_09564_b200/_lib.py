@@ -42,9 +42,13 @@ SIGNATURES = {
     "rw_queue_destroy": (None, [P]),
     "rw_profile_enable": (I32, [I32]),
     "rw_profile_read": (I32, [P, P]),
+    "rw_set_option": (I32, [I32, C.c_int64]),
+    "rw_get_option": (C.c_int64, [I32]),
+    "rw_resident_available": (I32, [rw_dims, I32]),
 }
 
-KERNEL_CLASSES = ["weights", "setup", "passA", "passB", "finalize", "pyramid", "other"]
+KERNEL_CLASSES = ["weights", "setup", "passA", "passB", "finalize", "pyramid", "other",
+                  "resident"]
 
 
 def header_symbols(path: str = HEADER):

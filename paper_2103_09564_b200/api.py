@@ -7,6 +7,7 @@ Tensors are contiguous, [batch, nz, ny, nx] (x fastest); per-RHS tensors add a l
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 
 import torch
@@ -43,6 +44,36 @@ def _need(t, name, dtype=None):
 def dims_of(t):
     *_, nz, ny, nx = t.shape
     return rw_dims(nx, ny, nz)
+
+
+SOLVERS = {"auto": 0, "streaming": 1, "resident": 2}
+
+
+def set_solver(name):
+    """rw_set_option(RW_OPT_SOLVER): "auto" | "streaming" | "resident" (include/rw.h)."""
+    check(lib().rw_set_option(0, SOLVERS[name]), "rw_set_option")
+
+
+def get_solver():
+    v = lib().rw_get_option(0)
+    return {v_: k for k, v_ in SOLVERS.items()}[v]
+
+
+@contextlib.contextmanager
+def solver(name):
+    """Run the enclosed solves with the given solver, restoring the previous setting."""
+    old = get_solver()
+    set_solver(name)
+    try:
+        yield
+    finally:
+        set_solver(old)
+
+
+def resident_available(dims, nrhs=1):
+    """rw_resident_available: can the brick-resident (on-chip) solver serve this shape?"""
+    nx, ny, nz = dims
+    return bool(lib().rw_resident_available(rw_dims(nx, ny, nz), nrhs))
 
 
 def solve_workspace_bytes(batch, dims, nrhs=1, weights_given=False):

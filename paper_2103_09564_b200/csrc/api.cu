@@ -9,6 +9,7 @@
 #include "../../include/rw.h"
 #include "passA.cuh"
 #include "rw_common.cuh"
+#include "resident.cuh"
 
 namespace rw {
 cudaError_t launch_pyramid_group(const void*, int, int, int, int, int, int, int, const PyrOut&,
@@ -28,6 +29,7 @@ int passA_rc(const Plan&);
 namespace {
 
 thread_local std::string g_err;
+int g_solver = RW_SOLVER_AUTO;
 
 rw_status fail(rw_status st, const char* fmt, ...) {
   char buf[512];
@@ -122,7 +124,7 @@ Layout layout(const rw::Plan& P, bool weights_given, int label_K) {
   L.PB = o;     o += up(2 * RB * P.U * sizeof(double2));
   L.PS = o;     o += up(RB * P.U * sizeof(double4));
   L.status = o; o += up(RB * sizeof(int));
-  L.ctr = o;    o += up(2 * sizeof(int));
+  L.ctr = o;    o += up(4 * sizeof(int));   // [0..1] active counts, [2] resident brick counter
   L.fixed = o;  o += label_K ? up(BN) : 0;
   L.values = o; o += label_K ? up((size_t)(label_K - 1) * BN * sizeof(float)) : 0;
   L.total = o;
@@ -258,7 +260,12 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
                      uint8_t* labels, cudaStream_t s) {
   const int sms = num_sms();
   rw::Plan P = P0;
-  set_vm(P, choose_vm(P, vol, dtype));
+  const bool res_ok = g_solver != RW_SOLVER_STREAMING && rw::resident_supported(d.nx, d.ny, d.nz, nrhs);
+  if (g_solver == RW_SOLVER_RESIDENT && !res_ok)
+    return fail(RW_EUNSUPPORTED, "resident solver unavailable for %dx%dx%d, nrhs %d on this device",
+                d.nx, d.ny, d.nz, nrhs);
+  // the resident solver reads stored weight planes once per brick
+  set_vm(P, res_ok ? rw::VM_STORED : choose_vm(P, vol, dtype));
   rw::Bufs Bf{};
   float* Wd = W ? const_cast<float*>(W) : reinterpret_cast<float*>(ws + Lw.W);
   float* dinv = reinterpret_cast<float*>(ws + Lw.dinv);
@@ -293,6 +300,26 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   if (st != RW_OK) return st;
   RW_CK(cudaMemsetAsync(Bf.status, 0, (size_t)P.R * P.B * sizeof(int), s));
   RW_TIMED(RW_K_SETUP, s, 1, rw::launch_setup(P, Bf, C, s));
+  if (res_ok) {
+    rw::ResArgs A{};
+    A.W = Wd;
+    A.dinv = dinv;
+    A.r0 = Bf.r;
+    A.x = prob;
+    A.PB = Bf.PB;
+    A.PS = Bf.PS;
+    A.B = P.B;
+    A.U = P.U;
+    A.next = Bf.ctr + 2;
+    A.iters = iters;
+    A.status = status ? status : Bf.status;
+    A.resid = resid;
+    A.labels = labels;
+    A.C = C;
+    RW_CK(cudaMemsetAsync(A.next, 0, sizeof(int), s));
+    RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, s));
+    return RW_OK;
+  }
   const int nA = (P.R + rw::passA_rc(P) - 1) / rw::passA_rc(P);
   const int nB = (P.R + 3) / 4;
   st = ensure_pinned();
@@ -347,7 +374,21 @@ rw_status rw_profile_read(int64_t* launches, double* ms) {
   }
   return RW_OK;
 }
-const char* rw_version(void) { return "librw 0.1 (sm_100a)"; }
+const char* rw_version(void) { return "librw 0.2 (sm_100a)"; }
+
+rw_status rw_set_option(int32_t key, int64_t value) {
+  if (key != RW_OPT_SOLVER) return fail(RW_EINVAL, "rw_set_option: unknown key %d", key);
+  if (value < RW_SOLVER_AUTO || value > RW_SOLVER_RESIDENT)
+    return fail(RW_EINVAL, "rw_set_option: bad solver %lld", (long long)value);
+  g_solver = (int)value;
+  return RW_OK;
+}
+
+int64_t rw_get_option(int32_t key) { return key == RW_OPT_SOLVER ? g_solver : -1; }
+
+int32_t rw_resident_available(rw_dims d, int32_t nrhs) {
+  return rw::resident_supported(d.nx, d.ny, d.nz, nrhs) ? 1 : 0;
+}
 
 rw_status rw_brick_weights(const void* vol, rw_dtype dtype, rw_norm nm, int32_t batch,
                            rw_dims d, float beta, float eps, float* W, float* dinv,

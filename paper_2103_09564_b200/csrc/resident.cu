@@ -1,0 +1,457 @@
+// resident.cu -- SURVEY §8(f) f2/f4: the brick-resident CG solver.
+//
+// Same method as the streaming passes (cg.cu / passA.cu): Jacobi-preconditioned CG
+// (P:197, P:33 fn 2) on L_UU x_U = -B^T x_S, edge-difference SpMV (reading c8),
+// fp64 fixed-order reductions, the same stopping rule and status codes (reading c5).
+// What changes is where the state lives.  The streaming path re-reads the whole CG state
+// from HBM every iteration (two passes, ~46 B per voxel-iteration).  Here one
+// thread-block cluster owns one brick for its whole solve (bricks are independent,
+// P:167): the brick is split into CL z-slabs of ZS = 4 planes, one CTA (one SM) per slab,
+// and every iteration runs on chip:
+//
+//   shared memory : p (own planes + one halo plane on each side), x, the -y / -z weights
+//                   this thread does not own                          (208 KB at 64^3)
+//   tensor memory : dinv and the three forward edge weights of the thread's 32 voxels
+//                   (tcgen05.st once per brick, tcgen05.ld every iteration; 128 columns)
+//   registers     : r and q of the thread's 32 voxels
+//
+// Halo planes of p travel to the neighbouring CTAs through distributed shared memory
+// (st.shared::cluster); the two dot products per iteration are reduced over the cluster
+// by writing each CTA's fp64 partial into every CTA's slot array and summing the CL slots
+// in rank order after a cluster barrier, so every CTA takes the same alpha/beta/stop
+// decision.  The cluster grabs the next brick from a global counter when it is done
+// (persistent, load-balanced over bricks with different iteration counts).  HBM traffic
+// per brick is one read of W/dinv/x/r and one write of the result; per iteration none.
+//
+// Thread map (N = brick x/y extent, QX = N/4 quads per row, T = QX * N/2 threads):
+// thread t owns the x-quad qx = t % QX of rows y = 2j, 2j+1 (j = t / QX) in all ZS planes
+// of its slab: 2*ZS "items" of 4 voxels.  The x-neighbours of a quad come by warp shuffle,
+// the y-neighbours and z-neighbours from the shared p planes.
+#include "cg_device.cuh"
+#include "resident.cuh"
+
+namespace rw {
+
+namespace res {
+
+template <int N, int CL>
+struct Cfg {
+  static constexpr int ZS = 4;              // planes per CTA
+  static constexpr int NZ = ZS * CL;        // brick z extent
+  static constexpr int QX = N / 4;          // quads per row
+  static constexpr int T = QX * (N / 2);    // threads per CTA
+  static constexpr int NI = 2 * ZS;         // items (quads) per thread
+  static constexpr int PL = N * N;          // floats per plane
+  static constexpr int oP = 0;                          // p   [ZS+2][N][N]  (0, ZS+1 = halo)
+  static constexpr int oX = oP + (ZS + 2) * PL;         // x   [ZS][N][N]
+  static constexpr int oWYM = oX + ZS * PL;             // -y weight of rows 2j [ZS][N/2][N]
+  static constexpr int oWZM = oWYM + ZS * (N / 2) * N;  // -z weight of plane 0 [N][N]
+  static constexpr int nF = oWZM + PL;
+  static constexpr int SMEM = nF * 4;
+  static constexpr int NW = T / 32;
+  static constexpr int TCOLS = T >= 512 ? 512 : 128;    // 128 columns per thread
+  static_assert(T % 128 == 0, "thread count must be a multiple of 4 warps");
+};
+
+__device__ __forceinline__ uint32_t sptr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cl4(uint32_t a, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};"
+               :: "r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ void st_cl_f64(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" :: "r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cl_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cl_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ int cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return (int)r;
+}
+
+// TMEM: one x4 load (32-bit lanes x 4 columns) completed before the registers are used:
+// the wait sits in the same asm statement, so no use of the outputs can be hoisted above it.
+__device__ __forceinline__ float4 tm_ld4(uint32_t ta) {
+  uint32_t a, b, c, d;
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(ta));
+  return make_float4(__uint_as_float(a), __uint_as_float(b), __uint_as_float(c), __uint_as_float(d));
+}
+// three x4 loads, one wait
+__device__ __forceinline__ void tm_ld4x3(uint32_t t0, uint32_t t1, uint32_t t2, float4& u,
+                                         float4& v, float4& w) {
+  uint32_t a[12];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%12];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%13];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8, %9, %10, %11}, [%14];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+        "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11])
+      : "r"(t0), "r"(t1), "r"(t2));
+  u = make_float4(__uint_as_float(a[0]), __uint_as_float(a[1]), __uint_as_float(a[2]), __uint_as_float(a[3]));
+  v = make_float4(__uint_as_float(a[4]), __uint_as_float(a[5]), __uint_as_float(a[6]), __uint_as_float(a[7]));
+  w = make_float4(__uint_as_float(a[8]), __uint_as_float(a[9]), __uint_as_float(a[10]), __uint_as_float(a[11]));
+}
+__device__ __forceinline__ void tm_st4(uint32_t ta, float4 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
+               :: "r"(ta), "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)),
+                  "r"(__float_as_uint(v.z)), "r"(__float_as_uint(v.w)) : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+}  // namespace res
+
+
+template <int N, int CL>
+__global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
+  using G = res::Cfg<N, CL>;
+  using namespace res;
+  constexpr int ZS = G::ZS, QX = G::QX, PL = G::PL, NI = G::NI, NW = G::NW;
+  extern __shared__ __align__(16) float sm[];
+  __shared__ double s_red[2][CL][2];   // cluster slots: [0] p.q, [1] (r.z, r.r)
+  __shared__ double s_bred[NW][2];
+  __shared__ int s_brick;
+  __shared__ uint32_t s_taddr;
+  const int t = threadIdx.x, warp = t >> 5;
+  const int rank = cl_rank();
+  const int qx = t % QX, j = t / QX;
+  float* const P = sm + G::oP;
+  float* const X = sm + G::oX;
+  float* const WYM = sm + G::oWYM;
+  float* const WZM = sm + G::oWZM;
+
+  // ---- tensor memory: 128 columns per thread (lane = 32*(warp%4) + lane id)
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(sptr(&s_taddr)), "n"(G::TCOLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // halo planes start at 0 (the outer ones of ranks 0 and CL-1 are never written)
+  for (int i = t; i < PL; i += G::T) {
+    P[i] = 0.f;
+    P[(ZS + 1) * PL + i] = 0.f;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tb = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2);
+  // column map: dinv(it) = 4it, wx(it) = 32+4it, wy(it) = 64+4it, wz(it) = 96+4it
+  auto cD = [&](int it) { return tb + 4u * it; };
+  auto cX = [&](int it) { return tb + 32u + 4u * it; };
+  auto cY = [&](int it) { return tb + 64u + 4u * it; };
+  auto cZ = [&](int it) { return tb + 96u + 4u * it; };
+
+  const int z0 = rank * ZS;
+  const long long n = (long long)PL * G::NZ;
+  const long long BN = (long long)A.B * n;
+  // DSMEM: my plane 0 -> rank-1's upper halo, my plane ZS-1 -> rank+1's lower halo
+  const uint32_t own_off = (uint32_t)(j * 2 * N + 4 * qx) * 4u;   // row 2j, quad qx (bytes)
+  const uint32_t up_halo = rank > 0 ? mapa(sptr(P + (ZS + 1) * PL), rank - 1) : 0u;
+  const uint32_t dn_halo = rank < CL - 1 ? mapa(sptr(P), rank + 1) : 0u;
+  const uint32_t red0 = sptr(&s_red[0][rank][0]);
+  const uint32_t red1 = sptr(&s_red[1][rank][0]);
+  const uint32_t brk = sptr(&s_brick);
+
+  // fp64 cluster-wide sum of NV values per thread, identical in every thread of every CTA
+  auto cluster_sum = [&](double* v, int nv, int slot) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      if (i < nv) v[i] = warp_sum(v[i]);
+    if ((t & 31) == 0)
+      for (int i = 0; i < nv; ++i) s_bred[warp][i] = v[i];
+    __syncthreads();
+    if (t == 0) {
+      double tot[2] = {0.0, 0.0};
+      for (int w = 0; w < NW; ++w)
+        for (int i = 0; i < nv; ++i) tot[i] += s_bred[w][i];
+      const uint32_t base = slot ? red1 : red0;
+      for (int c = 0; c < CL; ++c) {
+        const uint32_t ra = mapa(base, c);
+        for (int i = 0; i < nv; ++i) st_cl_f64(ra + 8u * i, tot[i]);
+      }
+    }
+    cl_arrive();
+    cl_wait();
+    for (int i = 0; i < nv; ++i) {
+      double s = 0.0;
+      for (int c = 0; c < CL; ++c) s += s_red[slot][c][i];
+      v[i] = s;
+    }
+  };
+
+  float4 r[NI], q[NI];
+  while (true) {
+    // ---- next brick (rank 0 draws it, DSMEM broadcast, cluster barrier)
+    if (rank == 0 && t == 0) {
+      const int nb = atomicAdd(A.next, 1);
+      for (int c = 0; c < CL; ++c) st_cl_u32(mapa(brk, c), (uint32_t)nb);
+    }
+    cl_arrive();
+    cl_wait();
+    const int b = s_brick;
+    if (b >= A.B) break;
+
+    // ---- load the slab: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
+    uint32_t fixm = 0;   // bit 4*it+e: voxel is fixed (dinv == 0)
+#pragma unroll
+    for (int it = 0; it < NI; ++it) {
+      const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+      const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
+      const float4 dv = ld4(A.dinv + g);
+      tm_st4(cD(it), dv);
+      tm_st4(cX(it), ld4(A.W + g));
+      tm_st4(cY(it), ld4(A.W + BN + g));
+      tm_st4(cZ(it), ld4(A.W + 2 * BN + g));
+      fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
+      fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
+      fixm |= (dv.z == 0.f ? 4u : 0u) << (4 * it);
+      fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
+      r[it] = ld4(A.r0 + g);
+      const int so = y * N + 4 * qx;
+      st4(X + zl * PL + so, ld4(A.x + g));
+      st4(P + (zl + 1) * PL + so, f4(0.f));
+      if (rr == 0) st4(WYM + (zl * (N / 2) + j) * N + 4 * qx, y > 0 ? ld4(A.W + BN + g - N) : f4(0.f));
+      if (zl == 0) st4(WZM + so, z0 > 0 ? ld4(A.W + 2 * BN + g - PL) : f4(0.f));
+    }
+    res::tm_wait_st();
+    // ---- initial scalars from the setup partials (fixed order; same in every thread)
+    double rz = 0.0, rrn = 0.0, bb = 0.0, nf = 0.0, nu = 0.0;
+    for (int u = 0; u < A.U; ++u) {
+      const double2 pb = A.PB[(long long)b * A.U + u];
+      const double4 ps = A.PS[(long long)b * A.U + u];
+      rz += pb.x; rrn += pb.y; bb += ps.x; nf += ps.y; nu += ps.z;
+    }
+    __syncthreads();
+
+    int st = ST_ACTIVE, k = 0;
+    double rz_prev = 0.0, pq_prev = 0.0;
+    float al = 0.f;   // alpha_{k-1}
+    const double t2 = (double)A.C.tol * (double)A.C.tol;
+    while (true) {
+      // ---- decision of iteration k (as passA_scalars)
+      if (k == 0) {
+        if (nf == 0.0 || nu == 0.0) st = ST_TRIVIAL;
+        else if (bb == 0.0) st = ST_ZERO_B;
+      } else if (!(pq_prev > 0.0) || !isfinite(rz) || !isfinite(pq_prev)) {
+        st = ST_BREAKDOWN;
+      }
+      if (st == ST_ACTIVE) {
+        const bool conv = (A.C.tol_mode == 0) ? (rrn <= t2 * bb) : (rrn <= t2);
+        if (conv) st = ST_CONVERGED;
+        else if (k >= A.C.max_iter) st = ST_MAXITER;
+      }
+      if (st != ST_ACTIVE) break;
+      const float be = k > 0 ? (float)(rz / rz_prev) : 0.f;
+
+      // ---- step 1: x += alpha_{k-1} p_{k-1} (lagged);  p_k = dinv r + beta p_{k-1}
+#pragma unroll
+      for (int it = 0; it < NI; ++it) {
+        const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+        const int so = y * N + 4 * qx;
+        const float4 dv = tm_ld4(cD(it));
+        const float4 po = ld4(P + (zl + 1) * PL + so);
+        if (k > 0) st4(X + zl * PL + so, fma4(al, po, ld4(X + zl * PL + so)));
+        const float4 pn = pnew4(be, po, dv, r[it]);
+        st4(P + (zl + 1) * PL + so, pn);
+        if (zl == 0 && rank > 0) st_cl4(up_halo + own_off + rr * N * 4, pn);
+        if (zl == ZS - 1 && rank < CL - 1) st_cl4(dn_halo + own_off + rr * N * 4, pn);
+      }
+      __syncthreads();
+      cl_arrive();   // halo planes published; waited for before the boundary planes
+
+      // ---- step 2: q = L_UU p (edge-difference stencil), partial p.q
+      double apq = 0.0;
+      auto spmv = [&](int zl) {
+        const float* Pz = P + (zl + 1) * PL;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int it = 2 * zl + rr, y = 2 * j + rr;
+          const int so = y * N + 4 * qx;
+          const float4 pc = ld4(Pz + so);
+          const float4 pzm = ld4(Pz - PL + so);
+          const float4 pzp = ld4(Pz + PL + so);
+          const float4 pym = y > 0 ? ld4(Pz + so - N) : f4(0.f);
+          const float4 pyp = y < N - 1 ? ld4(Pz + so + N) : f4(0.f);
+          const float xl = __shfl_up_sync(0xffffffffu, pc.w, 1, QX);
+          const float xr = __shfl_down_sync(0xffffffffu, pc.x, 1, QX);
+          float4 wx, wy, wz;
+          tm_ld4x3(cX(it), cY(it), cZ(it), wx, wy, wz);
+          const float wl = __shfl_up_sync(0xffffffffu, wx.w, 1, QX);
+          const float4 wxm = make_float4(qx > 0 ? wl : 0.f, wx.x, wx.y, wx.z);
+          const float4 wym = rr == 0 ? ld4(WYM + (zl * (N / 2) + j) * N + 4 * qx) : tm_ld4(cY(it - 1));
+          const float4 wzm = zl == 0 ? ld4(WZM + so) : tm_ld4(cZ(it - 2));
+          const float dummy = 1.f;
+          float4 qq;
+          qq.x = stencil1(pc.x, pc.y, xl, pyp.x, pym.x, pzp.x, pzm.x, wx.x, wxm.x, wy.x, wym.x, wz.x, wzm.x, dummy);
+          qq.y = stencil1(pc.y, pc.z, pc.x, pyp.y, pym.y, pzp.y, pzm.y, wx.y, wxm.y, wy.y, wym.y, wz.y, wzm.y, dummy);
+          qq.z = stencil1(pc.z, pc.w, pc.y, pyp.z, pym.z, pzp.z, pzm.z, wx.z, wxm.z, wy.z, wym.z, wz.z, wzm.z, dummy);
+          qq.w = stencil1(pc.w, xr, pc.z, pyp.w, pym.w, pzp.w, pzm.w, wx.w, wxm.w, wy.w, wym.w, wz.w, wzm.w, dummy);
+          const uint32_t fm = fixm >> (4 * it);
+          if (fm & 1u) qq.x = 0.f;
+          if (fm & 2u) qq.y = 0.f;
+          if (fm & 4u) qq.z = 0.f;
+          if (fm & 8u) qq.w = 0.f;
+          q[it] = qq;
+          apq += (double)dot4f(pc, qq);
+        }
+      };
+#pragma unroll
+      for (int zl = 1; zl < ZS - 1; ++zl) spmv(zl);
+      cl_wait();
+      spmv(0);
+      spmv(ZS - 1);
+      double v1[2] = {apq, 0.0};
+      cluster_sum(v1, 1, 0);
+      const double pq = v1[0];
+      al = (pq > 0.0 && isfinite(pq)) ? (float)(rz / pq) : 0.f;
+
+      // ---- step 3: r -= alpha q;  partials r.(dinv r), r.r
+      double arz = 0.0, arr = 0.0;
+#pragma unroll
+      for (int it = 0; it < NI; ++it) {
+        const float4 dv = tm_ld4(cD(it));
+        const float4 rn = fma4(-al, q[it], r[it]);
+        r[it] = rn;
+        arz = dot4_acc(rn, mul4(dv, rn), arz);
+        arr = dot4_acc(rn, rn, arr);
+      }
+      double v2[2] = {arz, arr};
+      cluster_sum(v2, 2, 1);
+      rz_prev = rz;
+      pq_prev = pq;
+      rz = v2[0];
+      rrn = v2[1];
+      ++k;
+    }
+
+    // ---- finalise (row a6): last lagged x update, clamp, fixed values kept, labels
+    const bool upd = (st == ST_CONVERGED || st == ST_MAXITER) && k >= 1;
+#pragma unroll
+    for (int it = 0; it < NI; ++it) {
+      const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+      const int so = y * N + 4 * qx;
+      float4 xv = ld4(X + zl * PL + so);
+      if (upd && al != 0.f) xv = fma4(al, ld4(P + (zl + 1) * PL + so), xv);
+      const uint32_t fm = fixm >> (4 * it);
+      float o[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (fm & (1u << e)) continue;            // fixed: x holds the Dirichlet value
+        o[e] = st == ST_ZERO_B ? 0.f : fminf(fmaxf(o[e], 0.f), 1.f);
+      }
+      const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
+      st4(A.x + g, make_float4(o[0], o[1], o[2], o[3]));
+      if (A.labels)
+        *reinterpret_cast<uchar4*>(A.labels + g) =
+            make_uchar4(o[0] > 0.5f, o[1] > 0.5f, o[2] > 0.5f, o[3] > 0.5f);
+    }
+    if (rank == 0 && t == 0) {
+      A.status[b] = st;
+      A.iters[b] = (st == ST_TRIVIAL || st == ST_ZERO_B) ? 0 : k;
+      if (A.resid) {
+        double res = 0.0;
+        if (st == ST_CONVERGED || st == ST_MAXITER || st == ST_BREAKDOWN) {
+          res = sqrt(rrn);
+          if (A.C.tol_mode == 0) res = bb > 0.0 ? res / sqrt(bb) : 0.0;
+        }
+        A.resid[b] = (float)res;
+      }
+    }
+  }
+  // ---- release tensor memory
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                 :: "r"(s_taddr), "n"(G::TCOLS) : "memory");
+}
+
+// ------------------------------------------------------------------------- launcher
+// Supported shapes: N x N x 4*CL bricks with (N, CL) in {(64, 16), (32, 8)}.
+template <int N, int CL>
+static int resident_clusters() {
+  static int cached = -1;
+  if (cached >= 0) return cached;
+  using G = res::Cfg<N, CL>;
+  int nc = 0;
+  if (cudaFuncSetAttribute(k_resident<N, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           G::SMEM) != cudaSuccess ||
+      (CL > 8 && cudaFuncSetAttribute(k_resident<N, CL>,
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+    cudaGetLastError();
+    cached = 0;
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(G::T);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cudaOccupancyMaxActiveClusters(&nc, k_resident<N, CL>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    nc = 0;
+  }
+  cached = nc;
+  return nc;
+}
+
+template <int N, int CL>
+static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
+  using G = res::Cfg<N, CL>;
+  const int nc = resident_clusters<N, CL>();
+  if (nc < 1) return cudaErrorNotSupported;
+  const int ncl = nc < A.B ? nc : A.B;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncl * CL);
+  cfg.blockDim = dim3(G::T);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_resident<N, CL>, A);
+}
+
+// Is the resident solver available for this brick shape (and device)?
+bool resident_supported(int nx, int ny, int nz, int R) {
+  if (R != 1) return false;
+  if (nx == 64 && ny == 64 && nz == 64) return resident_clusters<64, 16>() > 0;
+  if (nx == 32 && ny == 32 && nz == 32) return resident_clusters<32, 8>() > 0;
+  return false;
+}
+
+cudaError_t launch_resident(int nx, const ResArgs& A, cudaStream_t s) {
+  if (nx == 64) return launch_res<64, 16>(A, s);
+  return launch_res<32, 8>(A, s);
+}
+
+}  // namespace rw

@@ -1,0 +1,118 @@
+"""GPU parity of the brick-resident solver (one thread-block cluster per brick, CG state on
+chip; include/rw.h "Solver selection") against the fp64 oracle, and its
+agreement with the streaming solver.  Same bars as test_gpu_parity.py (BASELINE.json
+north_star): |dp| <= 1e-4, labels exact outside the 1e-3 band.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2103_09564_b200 as rwb
+import workloads as wl
+from oracle import rw_oracle as ro
+from paper_2103_09564_b200._lib import RWError
+from gpu_helpers import gpu_solve, assert_prob_parity, assert_label_parity
+
+pytestmark = pytest.mark.gpu
+
+
+def resident(p, **kw):
+    with rwb.solver("resident"):
+        return gpu_solve(p, **kw)
+
+
+def streaming(p, **kw):
+    with rwb.solver("streaming"):
+        return gpu_solve(p, **kw)
+
+
+def test_resident_available_shapes():
+    assert rwb.resident_available((64, 64, 64))
+    assert rwb.resident_available((32, 32, 32))
+    assert not rwb.resident_available((64, 64, 64), nrhs=2)
+    assert not rwb.resident_available((48, 48, 48))
+    p = wl.random_brick(48, 8, 8, seed=1, nseed=10)
+    with rwb.solver("resident"), pytest.raises(RWError, match="RW_EUNSUPPORTED"):
+        gpu_solve(p)
+
+
+def test_cfg1_resident_parity():
+    p = wl.cfg1()
+    o = resident(p)
+    ref = ro.solve_problem(p, tol=1e-10)
+    assert_prob_parity(o["prob"], ref["prob"])
+    assert_label_parity(o["labels"], ref["prob"][0])
+    assert o["status"][0, 0] == 1 and o["resid"][0, 0] <= 1e-6
+    it_o = ro.solve_problem(p, tol=1e-6)["iters"][0, 0]
+    assert abs(int(o["iters"][0, 0]) - int(it_o)) <= 5, (o["iters"], it_o)
+
+
+def test_cfg2_resident_parity_batch_invariance_and_streaming_agreement():
+    ids = [0, 37, 101, 150, 199, 255, 300, 333, 377, 400, 421, 450, 470, 490, 500, 511]
+    p = wl.cfg2(bricks=ids)
+    o = resident(p)
+    for j in (0, 5, 15):
+        ref = ro.solve_problem(p, tol=1e-10, bricks=[j])
+        assert_prob_parity(o["prob"][:, j:j + 1], ref["prob"])
+        assert_label_parity(o["labels"][j], ref["prob"][0, 0])
+    # a brick's bits do not depend on the batch or on which cluster solved it
+    alone = resident(p.subset([5]))
+    assert np.array_equal(alone["prob"][0, 0], o["prob"][0, 5])
+    assert alone["iters"][0, 0] == o["iters"][0, 5]
+    assert (o["status"] == 1).all() and (o["iters"] > 100).all()
+    s = streaming(p)
+    assert np.abs(s["prob"] - o["prob"]).max() <= 2e-5
+    assert np.abs(s["iters"].astype(int) - o["iters"].astype(int)).max() <= 3
+    np.testing.assert_allclose(s["resid"], o["resid"], rtol=0.05)
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_resident_random_bricks_many_per_cluster(n):
+    """More bricks than co-resident clusters (each cluster solves several), random seeds with
+    continuous values, Dirichlet shell on odd bricks; u16 intensities."""
+    batch = 40 if n == 32 else 10
+    p = wl.random_brick(n, n, n, seed=100 + n, batch=batch, nseed=n ** 3 // 60,
+                        continuous=True, dtype="u16")
+    o = resident(p, tol=1e-7, max_iter=20000)
+    s = streaming(p, tol=1e-7, max_iter=20000)
+    assert (o["status"] == 1).all()
+    assert np.abs(s["prob"] - o["prob"]).max() <= 2e-5
+    for j in (0, batch - 1):
+        ref = ro.solve_problem(p, tol=1e-11, bricks=[j])
+        assert_prob_parity(o["prob"][:, j:j + 1], ref["prob"])
+
+
+def test_resident_degenerate_bricks():
+    """As test_degenerate_bricks on 32^3: no fixed voxel -> TRIVIAL 0.5; all fixed ->
+    TRIVIAL values; all fixed values 0 -> ZERO_B; a normal brick vs the oracle."""
+    p = wl.random_brick(32, 32, 32, seed=9, batch=4, nseed=300)
+    p.fixed[0] = 0
+    p.fixed[1] = 1
+    p.values[0, 1] = np.random.default_rng(0).uniform(0, 1, p.values[0, 1].shape)
+    p.values[0, 2] = 0.0
+    o = resident(p, tol=1e-7)
+    assert o["status"][0].tolist()[:3] == [3, 3, 4]
+    assert o["iters"][0].tolist()[:3] == [0, 0, 0]
+    assert np.all(o["prob"][0, 0] == 0.5)
+    np.testing.assert_array_equal(o["prob"][0, 1], p.values[0, 1])
+    assert np.all(o["prob"][0, 2] == 0.0)
+    ref = ro.solve_problem(p.subset([3]), tol=1e-11)
+    assert_prob_parity(o["prob"][:, 3:4], ref["prob"])
+    s = streaming(p, tol=1e-7)
+    assert np.array_equal(s["status"], o["status"])
+
+
+def test_resident_max_iter_abs_mode_warm_start_and_W():
+    p = wl.random_brick(32, 32, 32, seed=11, nseed=200)
+    o = resident(p, tol=1e-12, max_iter=3)
+    assert o["iters"][0, 0] == 3 and o["status"][0, 0] == 2
+    s = streaming(p, tol=1e-12, max_iter=3)
+    assert np.abs(s["prob"] - o["prob"]).max() <= 1e-6
+    ref = ro.solve_problem(p, tol=1e-11)
+    a = resident(p, tol=1e-3, tol_mode=1)
+    assert a["status"][0, 0] == 1 and a["resid"][0, 0] <= 1e-3
+    w = resident(p, tol=1e-6, x0=ref["x"].astype(np.float32))
+    assert w["iters"][0, 0] <= 3
+    v = resident(p)
+    u = resident(p, use_W=True)
+    assert np.array_equal(v["prob"], u["prob"]) and np.array_equal(v["iters"], u["iters"])
