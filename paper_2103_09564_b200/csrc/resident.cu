@@ -29,6 +29,7 @@
 // the y-neighbours and z-neighbours from the shared p planes.
 #include "cg_device.cuh"
 #include "resident.cuh"
+#include "tma.cuh"
 
 namespace rw {
 
@@ -117,6 +118,110 @@ __device__ __forceinline__ void tm_st4(uint32_t ta, float4 v) {
 __device__ __forceinline__ void tm_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+// 32 consecutive columns (8 float4) in one load
+__device__ __forceinline__ void tm_ld32(uint32_t ta, float4 (&v)[8]) {
+  uint32_t a[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+        "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]),
+        "=r"(a[14]), "=r"(a[15]), "=r"(a[16]), "=r"(a[17]), "=r"(a[18]), "=r"(a[19]),
+        "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23]), "=r"(a[24]), "=r"(a[25]),
+        "=r"(a[26]), "=r"(a[27]), "=r"(a[28]), "=r"(a[29]), "=r"(a[30]), "=r"(a[31])
+      : "r"(ta));
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    v[i] = make_float4(__uint_as_float(a[4 * i]), __uint_as_float(a[4 * i + 1]),
+                       __uint_as_float(a[4 * i + 2]), __uint_as_float(a[4 * i + 3]));
+}
+// 8 columns (2 float4)
+__device__ __forceinline__ void tm_ld8(uint32_t ta, float4& u, float4& v) {
+  uint32_t a[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+        "=r"(a[7])
+      : "r"(ta));
+  u = make_float4(__uint_as_float(a[0]), __uint_as_float(a[1]), __uint_as_float(a[2]), __uint_as_float(a[3]));
+  v = make_float4(__uint_as_float(a[4]), __uint_as_float(a[5]), __uint_as_float(a[6]), __uint_as_float(a[7]));
+}
+// three 8-column loads, one wait
+__device__ __forceinline__ void tm_ld8x3(uint32_t t0, uint32_t t1, uint32_t t2, float4& a0,
+                                         float4& a1, float4& b0, float4& b1, float4& c0,
+                                         float4& c1) {
+  uint32_t a[24];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%24];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8, %9, %10, %11, %12, %13, %14, %15}, [%25];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16, %17, %18, %19, %20, %21, %22, %23}, [%26];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+        "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]),
+        "=r"(a[14]), "=r"(a[15]), "=r"(a[16]), "=r"(a[17]), "=r"(a[18]), "=r"(a[19]),
+        "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23])
+      : "r"(t0), "r"(t1), "r"(t2));
+  auto F = [&](int i) {
+    return make_float4(__uint_as_float(a[i]), __uint_as_float(a[i + 1]), __uint_as_float(a[i + 2]),
+                       __uint_as_float(a[i + 3]));
+  };
+  a0 = F(0); a1 = F(4); b0 = F(8); b1 = F(12); c0 = F(16); c1 = F(20);
+}
+// DSMEM stores that complete (in bytes) on the receiving CTA's mbarrier
+__device__ __forceinline__ void st_async4(uint32_t a, float4 v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+               :: "r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_async_f64(uint32_t a, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+               :: "r"(a), "l"(__double_as_longlong(v)), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_async_f64x2(uint32_t a, double u, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+               :: "r"(a), "l"(__double_as_longlong(u)), "l"(__double_as_longlong(v)), "r"(bar)
+               : "memory");
+}
+// edge-difference stencil (reading c8) of one quad: voxel e has x-neighbours (e-1, e+1)
+// inside the quad or xl / xr across it; same term order as stencil1
+__device__ __forceinline__ float4 stencil4(float4 p, float xl, float xr, float4 yp, float4 ym,
+                                           float4 zp, float4 zm, float4 wx, float4 wxm,
+                                           float4 wy, float4 wym, float4 wz, float4 wzm) {
+  float4 q;
+  q.x = stencil1(p.x, p.y, xl, yp.x, ym.x, zp.x, zm.x, wx.x, wxm.x, wy.x, wym.x, wz.x, wzm.x, 1.f);
+  q.y = stencil1(p.y, p.z, p.x, yp.y, ym.y, zp.y, zm.y, wx.y, wxm.y, wy.y, wym.y, wz.y, wzm.y, 1.f);
+  q.z = stencil1(p.z, p.w, p.y, yp.z, ym.z, zp.z, zm.z, wx.z, wxm.z, wy.z, wym.z, wz.z, wzm.z, 1.f);
+  q.w = stencil1(p.w, xr, p.z, yp.w, ym.w, zp.w, zm.w, wx.w, wxm.w, wy.w, wym.w, wz.w, wzm.w, 1.f);
+  return q;
+}
+// edge-difference stencil (reading c8) split by axis, same term order as stencil1:
+// q = wx (p - p[+x]);  q += wxm (p - p[-x]);  then +y, -y, +z, -z the same way
+__device__ __forceinline__ float4 xterms(float4 p, float xl, float xr, float4 wx, float wl) {
+  float4 q;
+  q.x = __fmaf_rn(wl, __fsub_rn(p.x, xl), __fmul_rn(wx.x, __fsub_rn(p.x, p.y)));
+  q.y = __fmaf_rn(wx.x, __fsub_rn(p.y, p.x), __fmul_rn(wx.y, __fsub_rn(p.y, p.z)));
+  q.z = __fmaf_rn(wx.y, __fsub_rn(p.z, p.y), __fmul_rn(wx.z, __fsub_rn(p.z, p.w)));
+  q.w = __fmaf_rn(wx.z, __fsub_rn(p.w, p.z), __fmul_rn(wx.w, __fsub_rn(p.w, xr)));
+  return q;
+}
+__device__ __forceinline__ float4 terms2(float4 q, float4 p, float4 pp, float4 pm, float4 wp,
+                                         float4 wm) {
+  q.x = __fmaf_rn(wm.x, __fsub_rn(p.x, pm.x), __fmaf_rn(wp.x, __fsub_rn(p.x, pp.x), q.x));
+  q.y = __fmaf_rn(wm.y, __fsub_rn(p.y, pm.y), __fmaf_rn(wp.y, __fsub_rn(p.y, pp.y), q.y));
+  q.z = __fmaf_rn(wm.z, __fsub_rn(p.z, pm.z), __fmaf_rn(wp.z, __fsub_rn(p.z, pp.z), q.z));
+  q.w = __fmaf_rn(wm.w, __fsub_rn(p.w, pm.w), __fmaf_rn(wp.w, __fsub_rn(p.w, pp.w), q.w));
+  return q;
+}
+// q = 0 on fixed voxels (bit e of fm)
+__device__ __forceinline__ float4 mask4(float4 q, uint32_t fm) {
+  if (fm & 1u) q.x = 0.f;
+  if (fm & 2u) q.y = 0.f;
+  if (fm & 4u) q.z = 0.f;
+  if (fm & 8u) q.w = 0.f;
+  return q;
+}
 
 }  // namespace res
 
@@ -127,7 +232,10 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   using namespace res;
   constexpr int ZS = G::ZS, QX = G::QX, PL = G::PL, NI = G::NI, NW = G::NW;
   extern __shared__ __align__(16) float sm[];
-  __shared__ double s_red[2][CL][2];   // cluster slots: [0] p.q, [1] (r.z, r.r)
+  // mbarriers: [0] halo planes in, [1] p.q partials in, [2] (r.z, r.r) partials in
+  __shared__ __align__(8) uint64_t s_bar[3];
+  __shared__ __align__(16) double s_pq[CL];      // p.q partial of every CTA (rank order)
+  __shared__ __align__(16) double2 s_rz[CL];     // (r.z, r.r) partial of every CTA
   __shared__ double s_bred[NW][2];
   __shared__ int s_brick;
   __shared__ uint32_t s_taddr;
@@ -145,6 +253,10 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
                  :: "r"(sptr(&s_taddr)), "n"(G::TCOLS) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  if (t == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&s_bar[i], 1);
+    fence_mbar_init();
+  }
   // halo planes start at 0 (the outer ones of ranks 0 and CL-1 are never written)
   for (int i = t; i < PL; i += G::T) {
     P[i] = 0.f;
@@ -154,25 +266,27 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2);
-  // column map: dinv(it) = 4it, wx(it) = 32+4it, wy(it) = 64+4it, wz(it) = 96+4it
-  auto cD = [&](int it) { return tb + 4u * it; };
-  auto cX = [&](int it) { return tb + 32u + 4u * it; };
-  auto cY = [&](int it) { return tb + 64u + 4u * it; };
-  auto cZ = [&](int it) { return tb + 96u + 4u * it; };
+  // column map: dinv(it) = 4it, wx(it) = 32+4it, wy(it) = 64+4it, wz(it) = 96+4it;
+  // the two items of plane zl (it = 2zl, 2zl+1) are 8 adjacent columns of each weight
+  const uint32_t cD = tb, cX = tb + 32u, cY = tb + 64u, cZ = tb + 96u;
 
   const int z0 = rank * ZS;
   const long long n = (long long)PL * G::NZ;
   const long long BN = (long long)A.B * n;
-  // DSMEM: my plane 0 -> rank-1's upper halo, my plane ZS-1 -> rank+1's lower halo
+  // DSMEM: my plane 0 -> rank-1's upper halo, my plane ZS-1 -> rank+1's lower halo, each
+  // with st.async completing (in bytes) on the receiver's halo mbarrier
   const uint32_t own_off = (uint32_t)(j * 2 * N + 4 * qx) * 4u;   // row 2j, quad qx (bytes)
   const uint32_t up_halo = rank > 0 ? mapa(sptr(P + (ZS + 1) * PL), rank - 1) : 0u;
+  const uint32_t up_bar = rank > 0 ? mapa(sptr(&s_bar[0]), rank - 1) : 0u;
   const uint32_t dn_halo = rank < CL - 1 ? mapa(sptr(P), rank + 1) : 0u;
-  const uint32_t red0 = sptr(&s_red[0][rank][0]);
-  const uint32_t red1 = sptr(&s_red[1][rank][0]);
+  const uint32_t dn_bar = rank < CL - 1 ? mapa(sptr(&s_bar[0]), rank + 1) : 0u;
+  const uint32_t halo_bytes = (uint32_t)((rank > 0) + (rank < CL - 1)) * PL * 4u;
   const uint32_t brk = sptr(&s_brick);
+  uint32_t ph0 = 0, ph1 = 0, ph2 = 0;   // mbarrier phase parities
 
-  // fp64 cluster-wide sum of NV values per thread, identical in every thread of every CTA
-  auto cluster_sum = [&](double* v, int nv, int slot) {
+  // CTA sum of v[0..NV) -> thread 0, then st.async into slot `rank` of every CTA of the
+  // cluster; every thread waits for all CL partials and sums them in rank order.
+  auto block_to_t0 = [&](double* v, int nv) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
       if (i < nv) v[i] = warp_sum(v[i]);
@@ -180,21 +294,9 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       for (int i = 0; i < nv; ++i) s_bred[warp][i] = v[i];
     __syncthreads();
     if (t == 0) {
-      double tot[2] = {0.0, 0.0};
+      v[0] = v[1] = 0.0;
       for (int w = 0; w < NW; ++w)
-        for (int i = 0; i < nv; ++i) tot[i] += s_bred[w][i];
-      const uint32_t base = slot ? red1 : red0;
-      for (int c = 0; c < CL; ++c) {
-        const uint32_t ra = mapa(base, c);
-        for (int i = 0; i < nv; ++i) st_cl_f64(ra + 8u * i, tot[i]);
-      }
-    }
-    cl_arrive();
-    cl_wait();
-    for (int i = 0; i < nv; ++i) {
-      double s = 0.0;
-      for (int c = 0; c < CL; ++c) s += s_red[slot][c][i];
-      v[i] = s;
+        for (int i = 0; i < nv; ++i) v[i] += s_bred[w][i];
     }
   };
 
@@ -217,10 +319,10 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
       const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
       const float4 dv = ld4(A.dinv + g);
-      tm_st4(cD(it), dv);
-      tm_st4(cX(it), ld4(A.W + g));
-      tm_st4(cY(it), ld4(A.W + BN + g));
-      tm_st4(cZ(it), ld4(A.W + 2 * BN + g));
+      tm_st4(cD + 4u * it, dv);
+      tm_st4(cX + 4u * it, ld4(A.W + g));
+      tm_st4(cY + 4u * it, ld4(A.W + BN + g));
+      tm_st4(cZ + 4u * it, ld4(A.W + 2 * BN + g));
       fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
       fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
       fixm |= (dv.z == 0.f ? 4u : 0u) << (4 * it);
@@ -263,83 +365,126 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       const float be = k > 0 ? (float)(rz / rz_prev) : 0.f;
 
       // ---- step 1: x += alpha_{k-1} p_{k-1} (lagged);  p_k = dinv r + beta p_{k-1}
+      if (t == 0) mbar_arrive_expect_tx(&s_bar[0], halo_bytes);
+      {
+        float4 dv[NI];
+        tm_ld32(cD, dv);
 #pragma unroll
-      for (int it = 0; it < NI; ++it) {
-        const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
-        const int so = y * N + 4 * qx;
-        const float4 dv = tm_ld4(cD(it));
-        const float4 po = ld4(P + (zl + 1) * PL + so);
-        if (k > 0) st4(X + zl * PL + so, fma4(al, po, ld4(X + zl * PL + so)));
-        const float4 pn = pnew4(be, po, dv, r[it]);
-        st4(P + (zl + 1) * PL + so, pn);
-        if (zl == 0 && rank > 0) st_cl4(up_halo + own_off + rr * N * 4, pn);
-        if (zl == ZS - 1 && rank < CL - 1) st_cl4(dn_halo + own_off + rr * N * 4, pn);
+        for (int it = 0; it < NI; ++it) {
+          const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+          const int so = y * N + 4 * qx;
+          const float4 po = ld4(P + (zl + 1) * PL + so);
+          if (k > 0) st4(X + zl * PL + so, fma4(al, po, ld4(X + zl * PL + so)));
+          const float4 pn = pnew4(be, po, dv[it], r[it]);
+          st4(P + (zl + 1) * PL + so, pn);
+          if (zl == 0 && rank > 0) st_async4(up_halo + own_off + rr * N * 4, pn, up_bar);
+          if (zl == ZS - 1 && rank < CL - 1) st_async4(dn_halo + own_off + rr * N * 4, pn, dn_bar);
+        }
       }
       __syncthreads();
-      cl_arrive();   // halo planes published; waited for before the boundary planes
 
-      // ---- step 2: q = L_UU p (edge-difference stencil), partial p.q
+      // ---- step 2: q = L_UU p (edge-difference stencil), partial p.q; one row pair
+      // (items 2zl, 2zl+1) at a time
       double apq = 0.0;
       auto spmv = [&](int zl) {
         const float* Pz = P + (zl + 1) * PL;
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int it = 2 * zl + rr, y = 2 * j + rr;
-          const int so = y * N + 4 * qx;
-          const float4 pc = ld4(Pz + so);
-          const float4 pzm = ld4(Pz - PL + so);
-          const float4 pzp = ld4(Pz + PL + so);
-          const float4 pym = y > 0 ? ld4(Pz + so - N) : f4(0.f);
-          const float4 pyp = y < N - 1 ? ld4(Pz + so + N) : f4(0.f);
-          const float xl = __shfl_up_sync(0xffffffffu, pc.w, 1, QX);
-          const float xr = __shfl_down_sync(0xffffffffu, pc.x, 1, QX);
-          float4 wx, wy, wz;
-          tm_ld4x3(cX(it), cY(it), cZ(it), wx, wy, wz);
-          const float wl = __shfl_up_sync(0xffffffffu, wx.w, 1, QX);
-          const float4 wxm = make_float4(qx > 0 ? wl : 0.f, wx.x, wx.y, wx.z);
-          const float4 wym = rr == 0 ? ld4(WYM + (zl * (N / 2) + j) * N + 4 * qx) : tm_ld4(cY(it - 1));
-          const float4 wzm = zl == 0 ? ld4(WZM + so) : tm_ld4(cZ(it - 2));
-          const float dummy = 1.f;
-          float4 qq;
-          qq.x = stencil1(pc.x, pc.y, xl, pyp.x, pym.x, pzp.x, pzm.x, wx.x, wxm.x, wy.x, wym.x, wz.x, wzm.x, dummy);
-          qq.y = stencil1(pc.y, pc.z, pc.x, pyp.y, pym.y, pzp.y, pzm.y, wx.y, wxm.y, wy.y, wym.y, wz.y, wzm.y, dummy);
-          qq.z = stencil1(pc.z, pc.w, pc.y, pyp.z, pym.z, pzp.z, pzm.z, wx.z, wxm.z, wy.z, wym.z, wz.z, wzm.z, dummy);
-          qq.w = stencil1(pc.w, xr, pc.z, pyp.w, pym.w, pzp.w, pzm.w, wx.w, wxm.w, wy.w, wym.w, wz.w, wzm.w, dummy);
-          const uint32_t fm = fixm >> (4 * it);
-          if (fm & 1u) qq.x = 0.f;
-          if (fm & 2u) qq.y = 0.f;
-          if (fm & 4u) qq.z = 0.f;
-          if (fm & 8u) qq.w = 0.f;
-          q[it] = qq;
-          apq += (double)dot4f(pc, qq);
+        const int so = 2 * j * N + 4 * qx;
+        const float4 p0 = ld4(Pz + so), p1 = ld4(Pz + so + N);
+        float4 q0, q1;
+        {  // x terms (same term order as stencil1: +x, -x, +y, -y, +z, -z)
+          float4 wx0, wx1;
+          tm_ld8(cX + 8u * zl, wx0, wx1);
+          const float xl0 = __shfl_up_sync(0xffffffffu, p0.w, 1, QX);
+          const float xr0 = __shfl_down_sync(0xffffffffu, p0.x, 1, QX);
+          const float xl1 = __shfl_up_sync(0xffffffffu, p1.w, 1, QX);
+          const float xr1 = __shfl_down_sync(0xffffffffu, p1.x, 1, QX);
+          const float wl0 = __shfl_up_sync(0xffffffffu, wx0.w, 1, QX);
+          const float wl1 = __shfl_up_sync(0xffffffffu, wx1.w, 1, QX);
+          q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
+          q1 = xterms(p1, xl1, xr1, wx1, qx > 0 ? wl1 : 0.f);
         }
+        {  // y terms: row 2j+1 is +y of row 2j (and row 2j is -y of row 2j+1)
+          float4 wy0, wy1;
+          tm_ld8(cY + 8u * zl, wy0, wy1);
+          const float4 pym = j > 0 ? ld4(Pz + so - N) : f4(0.f);
+          const float4 pyp = j < N / 2 - 1 ? ld4(Pz + so + 2 * N) : f4(0.f);
+          const float4 wym0 = ld4(WYM + (zl * (N / 2) + j) * N + 4 * qx);
+          q0 = terms2(q0, p0, p1, pym, wy0, wym0);
+          q1 = terms2(q1, p1, pyp, p0, wy1, wy0);
+        }
+        {  // z terms
+          float4 wz0, wz1, wzm0, wzm1;
+          tm_ld8(cZ + 8u * zl, wz0, wz1);
+          if (zl == 0) {
+            wzm0 = ld4(WZM + so);
+            wzm1 = ld4(WZM + so + N);
+          } else {
+            tm_ld8(cZ + 8u * (zl - 1), wzm0, wzm1);
+          }
+          q0 = terms2(q0, p0, ld4(Pz + PL + so), ld4(Pz - PL + so), wz0, wzm0);
+          q1 = terms2(q1, p1, ld4(Pz + PL + so + N), ld4(Pz - PL + so + N), wz1, wzm1);
+        }
+        const uint32_t fm = fixm >> (8 * zl);
+        q0 = mask4(q0, fm);
+        q1 = mask4(q1, fm >> 4);
+        q[2 * zl] = q0;
+        q[2 * zl + 1] = q1;
+        apq += (double)dot4f(p0, q0);
+        apq += (double)dot4f(p1, q1);
       };
 #pragma unroll
       for (int zl = 1; zl < ZS - 1; ++zl) spmv(zl);
-      cl_wait();
+      mbar_wait(&s_bar[0], ph0);   // halo planes of the neighbours have landed
+      ph0 ^= 1u;
       spmv(0);
       spmv(ZS - 1);
       double v1[2] = {apq, 0.0};
-      cluster_sum(v1, 1, 0);
-      const double pq = v1[0];
+      block_to_t0(v1, 1);
+      if (t == 0) {
+        mbar_arrive_expect_tx(&s_bar[1], CL * 8u);
+        const uint32_t slot = sptr(&s_pq[rank]), bar = sptr(&s_bar[1]);
+        for (int c = 0; c < CL; ++c) st_async_f64(mapa(slot, c), v1[0], mapa(bar, c));
+      }
+      mbar_wait(&s_bar[1], ph1);
+      ph1 ^= 1u;
+      double pq = 0.0;
+#pragma unroll
+      for (int c = 0; c < CL; ++c) pq += s_pq[c];
       al = (pq > 0.0 && isfinite(pq)) ? (float)(rz / pq) : 0.f;
 
       // ---- step 3: r -= alpha q;  partials r.(dinv r), r.r
       double arz = 0.0, arr = 0.0;
+      {
+        float4 dv[NI];
+        tm_ld32(cD, dv);
 #pragma unroll
-      for (int it = 0; it < NI; ++it) {
-        const float4 dv = tm_ld4(cD(it));
-        const float4 rn = fma4(-al, q[it], r[it]);
-        r[it] = rn;
-        arz = dot4_acc(rn, mul4(dv, rn), arz);
-        arr = dot4_acc(rn, rn, arr);
+        for (int it = 0; it < NI; ++it) {
+          const float4 rn = fma4(-al, q[it], r[it]);
+          r[it] = rn;
+          arz += (double)dot4f(rn, mul4(dv[it], rn));
+          arr += (double)dot4f(rn, rn);
+        }
       }
       double v2[2] = {arz, arr};
-      cluster_sum(v2, 2, 1);
+      block_to_t0(v2, 2);
+      if (t == 0) {
+        mbar_arrive_expect_tx(&s_bar[2], CL * 16u);
+        const uint32_t slot = sptr(&s_rz[rank]), bar = sptr(&s_bar[2]);
+        for (int c = 0; c < CL; ++c) st_async_f64x2(mapa(slot, c), v2[0], v2[1], mapa(bar, c));
+      }
+      mbar_wait(&s_bar[2], ph2);
+      ph2 ^= 1u;
+      double srz = 0.0, srr = 0.0;
+#pragma unroll
+      for (int c = 0; c < CL; ++c) {
+        const double2 e = s_rz[c];
+        srz += e.x;
+        srr += e.y;
+      }
       rz_prev = rz;
       pq_prev = pq;
-      rz = v2[0];
-      rrn = v2[1];
+      rz = srz;
+      rrn = srr;
       ++k;
     }
 
