@@ -49,6 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    if os.environ.get("RW_RES_TIMING"):      # debug: phase timers in the resident kernel
+        cmd.insert(1, "-DRW_RES_TIMING")
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)

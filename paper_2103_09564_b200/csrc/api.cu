@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of include/rw.h: validation, workspace carving, launch orchestration.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -317,7 +318,24 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
     A.labels = labels;
     A.C = C;
     RW_CK(cudaMemsetAsync(A.next, 0, sizeof(int), s));
+    static long long* dbg = nullptr;
+    if (getenv("RW_DEBUG_RES_TIMING")) {   // debug: phase cycle sums of the resident kernel
+      if (!dbg) RW_CK(cudaMalloc(&dbg, 16 * 8 * sizeof(long long)));
+      RW_CK(cudaMemsetAsync(dbg, 0, 16 * 8 * sizeof(long long), s));
+      A.dbg = dbg;
+    }
     RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, s));
+    if (A.dbg) {
+      long long h[128];
+      RW_CK(cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s));
+      RW_CK(cudaStreamSynchronize(s));
+      const char* names[7] = {"step1+sync", "spmv-int", "halo-wait", "spmv-bnd", "red-pq", "step3", "red-rz"};
+      for (int r = 0; r < 16; r += 5) {
+        fprintf(stderr, "[res-timing rank %2d]", r);
+        for (int i = 0; i < 7; ++i) fprintf(stderr, " %s=%lld", names[i], h[r * 8 + i]);
+        fprintf(stderr, "\n");
+      }
+    }
     return RW_OK;
   }
   const int nA = (P.R + rw::passA_rc(P) - 1) / rw::passA_rc(P);

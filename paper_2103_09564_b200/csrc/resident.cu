@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   __shared__ __align__(16) double s_pq[CL];      // p.q partial of every CTA (rank order)
   __shared__ __align__(16) double2 s_rz[CL];     // (r.z, r.r) partial of every CTA
   __shared__ double s_bred[NW][2];
+  __shared__ double2 s_res;
   __shared__ int s_brick;
   __shared__ uint32_t s_taddr;
   const int t = threadIdx.x, warp = t >> 5;
@@ -284,9 +285,13 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   const uint32_t brk = sptr(&s_brick);
   uint32_t ph0 = 0, ph1 = 0, ph2 = 0;   // mbarrier phase parities
 
-  // CTA sum of v[0..NV) -> thread 0, then st.async into slot `rank` of every CTA of the
-  // cluster; every thread waits for all CL partials and sums them in rank order.
-  auto block_to_t0 = [&](double* v, int nv) {
+  // Cluster-wide fp64 sum of nv (1 or 2) values per thread, identical in every thread of
+  // every CTA: warp xor-shuffle tree -> per-warp partials -> thread 0 adds them in warp order
+  // and st.async's the CTA partial into slot `rank` of every CTA (one 8/16-byte message per
+  // CTA pair, completing on that CTA's mbarrier `bi`; many small messages cost far more,
+  // tools/micro/mb_red.cu); warp 0 waits for the CL partials, thread 0 adds them in rank
+  // order, and a CTA barrier hands the result to every thread.
+  auto cluster_sum = [&](double* v, int nv, int bi, auto* slots, uint32_t& ph) -> double2 {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
       if (i < nv) v[i] = warp_sum(v[i]);
@@ -294,10 +299,37 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       for (int i = 0; i < nv; ++i) s_bred[warp][i] = v[i];
     __syncthreads();
     if (t == 0) {
-      v[0] = v[1] = 0.0;
-      for (int w = 0; w < NW; ++w)
-        for (int i = 0; i < nv; ++i) v[i] += s_bred[w][i];
+      double a0 = 0.0, a1 = 0.0;
+      for (int w = 0; w < NW; ++w) {
+        a0 += s_bred[w][0];
+        if (nv > 1) a1 += s_bred[w][1];
+      }
+      mbar_arrive_expect_tx(&s_bar[bi], CL * 8u * nv);
+      const uint32_t slot = sptr(&slots[rank]), bar = sptr(&s_bar[bi]);
+      for (int c = 0; c < CL; ++c) {
+        if (nv == 1) st_async_f64(mapa(slot, c), a0, mapa(bar, c));
+        else st_async_f64x2(mapa(slot, c), a0, a1, mapa(bar, c));
+      }
     }
+    if (warp == 0) {
+      mbar_wait(&s_bar[bi], ph);
+      if (t == 0) {
+        double a0 = 0.0, a1 = 0.0;
+        for (int c = 0; c < CL; ++c) {
+          if (nv == 1) {
+            a0 += reinterpret_cast<const double*>(slots)[c];
+          } else {
+            const double2 e = reinterpret_cast<const double2*>(slots)[c];
+            a0 += e.x;
+            a1 += e.y;
+          }
+        }
+        s_res = make_double2(a0, a1);
+      }
+    }
+    ph ^= 1u;
+    __syncthreads();
+    return s_res;
   };
 
   float4 r[NI], q[NI];
@@ -364,6 +396,20 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       if (st != ST_ACTIVE) break;
       const float be = k > 0 ? (float)(rz / rz_prev) : 0.f;
 
+#ifdef RW_RES_TIMING
+      // debug phase timer (build with -DRW_RES_TIMING, run with RW_DEBUG_RES_TIMING=1):
+      // cycles per phase summed over cluster 0's iterations, per rank
+      long long tp0 = A.dbg ? clock64() : 0;
+      auto TP = [&](int i) {
+        if (A.dbg && t == 0 && blockIdx.x < CL) {
+          const long long now = clock64();
+          A.dbg[rank * 8 + i] += now - tp0;
+          tp0 = now;
+        }
+      };
+#else
+      auto TP = [](int) {};
+#endif
       // ---- step 1: x += alpha_{k-1} p_{k-1} (lagged);  p_k = dinv r + beta p_{k-1}
       if (t == 0) mbar_arrive_expect_tx(&s_bar[0], halo_bytes);
       {
@@ -382,10 +428,11 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         }
       }
       __syncthreads();
+      TP(0);
 
       // ---- step 2: q = L_UU p (edge-difference stencil), partial p.q; one row pair
       // (items 2zl, 2zl+1) at a time
-      double apq = 0.0;
+      float apq = 0.f;   // this thread's p.q (fp32 over its 32 voxels; fp64 beyond)
       auto spmv = [&](int zl) {
         const float* Pz = P + (zl + 1) * PL;
         const int so = 2 * j * N + 4 * qx;
@@ -429,31 +476,24 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         q1 = mask4(q1, fm >> 4);
         q[2 * zl] = q0;
         q[2 * zl + 1] = q1;
-        apq += (double)dot4f(p0, q0);
-        apq += (double)dot4f(p1, q1);
+        apq = __fadd_rn(apq, __fadd_rn(dot4f(p0, q0), dot4f(p1, q1)));
       };
 #pragma unroll
       for (int zl = 1; zl < ZS - 1; ++zl) spmv(zl);
+      TP(1);
       mbar_wait(&s_bar[0], ph0);   // halo planes of the neighbours have landed
+      TP(2);
       ph0 ^= 1u;
       spmv(0);
       spmv(ZS - 1);
-      double v1[2] = {apq, 0.0};
-      block_to_t0(v1, 1);
-      if (t == 0) {
-        mbar_arrive_expect_tx(&s_bar[1], CL * 8u);
-        const uint32_t slot = sptr(&s_pq[rank]), bar = sptr(&s_bar[1]);
-        for (int c = 0; c < CL; ++c) st_async_f64(mapa(slot, c), v1[0], mapa(bar, c));
-      }
-      mbar_wait(&s_bar[1], ph1);
-      ph1 ^= 1u;
-      double pq = 0.0;
-#pragma unroll
-      for (int c = 0; c < CL; ++c) pq += s_pq[c];
+      TP(3);
+      double v1[2] = {(double)apq, 0.0};
+      const double pq = cluster_sum(v1, 1, 1, s_pq, ph1).x;
       al = (pq > 0.0 && isfinite(pq)) ? (float)(rz / pq) : 0.f;
+      TP(4);
 
       // ---- step 3: r -= alpha q;  partials r.(dinv r), r.r
-      double arz = 0.0, arr = 0.0;
+      float arz = 0.f, arr = 0.f;
       {
         float4 dv[NI];
         tm_ld32(cD, dv);
@@ -461,30 +501,19 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         for (int it = 0; it < NI; ++it) {
           const float4 rn = fma4(-al, q[it], r[it]);
           r[it] = rn;
-          arz += (double)dot4f(rn, mul4(dv[it], rn));
-          arr += (double)dot4f(rn, rn);
+          arz = __fadd_rn(arz, dot4f(rn, mul4(dv[it], rn)));
+          arr = __fadd_rn(arr, dot4f(rn, rn));
         }
       }
-      double v2[2] = {arz, arr};
-      block_to_t0(v2, 2);
-      if (t == 0) {
-        mbar_arrive_expect_tx(&s_bar[2], CL * 16u);
-        const uint32_t slot = sptr(&s_rz[rank]), bar = sptr(&s_bar[2]);
-        for (int c = 0; c < CL; ++c) st_async_f64x2(mapa(slot, c), v2[0], v2[1], mapa(bar, c));
-      }
-      mbar_wait(&s_bar[2], ph2);
-      ph2 ^= 1u;
-      double srz = 0.0, srr = 0.0;
-#pragma unroll
-      for (int c = 0; c < CL; ++c) {
-        const double2 e = s_rz[c];
-        srz += e.x;
-        srr += e.y;
-      }
+      TP(5);
+      double v2[2] = {(double)arz, (double)arr};
+      const double2 srr = cluster_sum(v2, 2, 2, s_rz, ph2);
+      const double srz = srr.x;
+      TP(6);
       rz_prev = rz;
       pq_prev = pq;
       rz = srz;
-      rrn = srr;
+      rrn = srr.y;
       ++k;
     }
 

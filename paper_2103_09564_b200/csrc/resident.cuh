@@ -18,6 +18,7 @@ struct ResArgs {
   float* resid;        // [B] or null
   uint8_t* labels;     // [B][n] or null
   Ctl C;
+  long long* dbg;      // debug: per-(rank, phase) clock64 sums, or null (RW_DEBUG_RES_TIMING)
 };
 
 bool resident_supported(int nx, int ny, int nz, int R);
