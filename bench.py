@@ -4,11 +4,16 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {b200,reference}]
 
 One step = one ``rw_solve_bricks`` call on the whole config-2 batch (512 independent
-64^3 u16 bricks): weights from intensities (a1/a2), implicit assembly (a3), the fused
+64^3 u16 bricks): weights from intensities (a1/a2), implicit assembly (a3), the
 Jacobi-PCG loop until every brick has converged (a4/a5), finalise + labels (a6).  Inputs
-are resident in HBM; the per-iteration working set (7.5 GB) is far larger than L2, so no
-L2 flush is needed between steps.  value = voxel-CG-iterations/s over all ranks
+are resident in HBM (7.5 GB of CG state + inputs, far larger than L2, so no L2 flush is
+needed between steps).  value = voxel-CG-iterations/s over all ranks
 (sum_b n_b * iters_b / step time), weak scaling (each rank solves its own 512 bricks).
+
+--solver auto (default) lets the library pick: the brick-resident solver (one 16-CTA
+cluster per 64^3 brick, CG state on chip) for this shape; --solver streaming forces the
+HBM-streaming passes.  When the resident solver is the headline, the streaming solver is
+also timed on the same inputs and reported under "streaming" with its HBM roofline.
 
 --impl reference times the fp64 oracle (oracle/, numpy+scipy) on the host cores on a
 bounded sample of the same workload -- this tier's reference arm (no reference code).
@@ -37,6 +42,11 @@ BATCH, N = 512, 64
 # from the u16 intensities, VM_U16) reads r, p, dinv, x (16 B) + the intensity (2 B) and
 # writes p, x, q (12 B); at k = 0 there is no x traffic.  Pass B reads r, q, dinv, writes r.
 BYTES_A, BYTES_A0, BYTES_B = 30, 22, 16
+# fp32 flops per voxel-iteration of the resident kernel: edge-difference
+# SpMV 6 sub + 6 mul/fma (18), p = dinv r + beta p (3), x += alpha p (2), r -= alpha q (2),
+# dots p.q (2), r.(dinv r) (3), r.r (2)
+FLOPS_RES = 32
+FP32_LANES_PER_SM, SMS = 128, 148
 
 
 def log(*a):
@@ -148,6 +158,41 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def streaming_roofline(kms, vox_iters, steps, nbr):
+    """HBM roofline of the streaming passes from the profile of `steps` solves."""
+    vox = float(N ** 3)
+    alg_A = steps * (BYTES_A * vox_iters - (BYTES_A - BYTES_A0) * vox * nbr)
+    alg_B = steps * BYTES_B * vox_iters
+    alg = {"passA": alg_A, "passB": alg_B}
+    dom = max(("passA", "passB"), key=lambda k: kms.get(k, 0.0))
+    peak, peak_kind = measured_peak()
+    achieved = alg[dom] / (kms[dom] / 1000.0) / 1e9
+    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(dom),
+            "per_kernel_ms_per_step": {k: v / steps for k, v in kms.items() if v > 0},
+            "alg_bytes_per_voxel_iter": {"passA": BYTES_A, "passB": BYTES_B}}
+
+
+def ncu_traffic(kernel):
+    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(tr_path) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+def fp32_peak_tflops():
+    """fp32 FMA peak from the unit counts and the measured max SM clock."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz, kind = float(json.load(f)["sm_max_mhz"]), "derived: 148 SMs x 128 fp32 lanes x 2 x measured sm_max_mhz"
+    except Exception:
+        mhz, kind = 1965.0, "derived: 148 SMs x 128 fp32 lanes x 2 x 1965 MHz (guide)"
+    return SMS * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12, kind
+
+
 def run_b200(args, rank, world, local_rank):
     import torch
     import paper_2103_09564_b200 as rwb
@@ -171,6 +216,8 @@ def run_b200(args, rank, world, local_rank):
                status=torch.empty((1, BATCH), dtype=torch.int32, device=dev),
                labels=torch.empty(tuple(fixed.shape), dtype=torch.uint8, device=dev))
     stream = torch.cuda.current_stream(dev)
+
+    rwb.set_solver(args.solver)
 
     def step():
         rwb.solve_bricks(fixed, values, vol=vol, beta=p.beta, eps=p.eps, tol=p.tol,
@@ -212,23 +259,46 @@ def run_b200(args, rank, world, local_rank):
     # ---------------- roofline of the dominant kernel ----------------
     launches = {k: v[0] for k, v in prof.items()}
     kms = {k: v[1] for k, v in prof.items()}
-    dom = max(("passA", "passB"), key=lambda k: kms[k])
-    nbr = BATCH
-    vox = float(N ** 3)
-    # algorithmic bytes: every active (brick, iteration) pays BYTES per voxel
-    alg_A = args.steps * (BYTES_A * vox_iters - (BYTES_A - BYTES_A0) * vox * nbr)
-    alg_B = args.steps * BYTES_B * vox_iters
-    alg = {"passA": alg_A, "passB": alg_B}
-    peak, peak_kind = measured_peak()
-    achieved = alg[dom] / (kms[dom] / 1000.0) / 1e9
-    traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tr_path):
-        try:
-            with open(tr_path) as f:
-                traffic = json.load(f).get(dom)
-        except Exception:
-            traffic = None
+    solver_used = "resident" if kms.get("resident", 0.0) > 0 else "streaming"
+    if solver_used == "resident":
+        peak, peak_kind = fp32_peak_tflops()
+        achieved = FLOPS_RES * vox_iters * args.steps / (kms["resident"] / 1000.0) / 1e12
+        roofline = {"bound": "alu", "kernel": "resident", "achieved": achieved, "peak": peak,
+                    "peak_kind": peak_kind, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": ncu_traffic("resident"),
+                    "per_kernel_ms_per_step": {k: v / args.steps for k, v in kms.items() if v > 0},
+                    "alg_flops_per_voxel_iter": FLOPS_RES,
+                    "note": "CG state on chip for all iterations (no per-iteration HBM traffic); "
+                            "bound by on-chip latency: two cluster-wide reductions and a DSMEM "
+                            "halo exchange per iteration (DESIGN.md 5)"}
+    else:
+        roofline = streaming_roofline(kms, vox_iters, args.steps, BATCH)
+
+    streaming = None
+    if solver_used == "resident" and not args.no_streaming:
+        # the HBM-streaming solver on the same inputs (secondary line: % of HBM peak)
+        with rwb.solver("streaming"):
+            step()
+            torch.cuda.synchronize()
+            api.profile_enable(True)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            sms_ = e0.elapsed_time(e1)
+            sprof = api.profile_read()
+            api.profile_enable(False)
+        s_iters = out["iters"].cpu().numpy().astype(np.int64)
+        s_vi = float(s_iters.sum()) * N ** 3
+        st_max, s_work = reduce_metric(sms_, s_vi, dev)
+        streaming = {"value": s_work / (st_max / args.steps / 1000.0), "unit": UNIT,
+                     "ms_per_step": st_max / args.steps,
+                     "roofline": streaming_roofline({k: v[1] for k, v in sprof.items()}, s_vi,
+                                                    args.steps, BATCH),
+                     "gpu_launches": int(sum(v[0] for v in sprof.values()))}
 
     # ---------------- end to end through the API with host buffers ----------------
     h_vol = torch.from_numpy(p.vol).pin_memory()
@@ -276,16 +346,14 @@ def run_b200(args, rank, world, local_rank):
         "data": "synthetic",
         "config": {"workload": WORKLOAD, "batch_per_gpu": BATCH, "brick": [N, N, N],
                    "global_batch": BATCH * world, "parallelism": f"bricks sharded over {world} GPU(s), no collective",
-                   "l2": "inputs larger than L2 (7.5 GB per-iteration working set), no flush",
+                   "l2": "inputs larger than L2 (u16 volume, mask, values, weight planes, CG state: > 2 GB), no flush",
                    "iters": {"min": int(iters.min()), "median": float(np.median(iters)),
                              "max": int(iters.max())}},
         "bricks_per_s": BATCH * world / (ms_per_step / 1000.0),
         "full_solve_ms": ms_per_step,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic,
-                     "per_kernel_ms_per_step": {k: v / args.steps for k, v in kms.items() if v > 0},
-                     "alg_bytes_per_voxel_iter": {"passA": BYTES_A, "passB": BYTES_B}},
+        "solver": solver_used,
+        "roofline": roofline,
+        "streaming": streaming,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps},
@@ -304,6 +372,9 @@ def main():
     ap.add_argument("--workers", type=int, default=min(16, os.cpu_count() or 1))
     ap.add_argument("--cpu-bricks", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solver", default="auto", choices=["auto", "streaming", "resident"])
+    ap.add_argument("--no-streaming", action="store_true",
+                    help="skip the secondary streaming-solver timing")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

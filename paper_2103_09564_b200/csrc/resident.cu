@@ -16,10 +16,11 @@
 //   registers     : r and q of the thread's 32 voxels
 //
 // Halo planes of p travel to the neighbouring CTAs through distributed shared memory
-// (st.shared::cluster); the two dot products per iteration are reduced over the cluster
-// by writing each CTA's fp64 partial into every CTA's slot array and summing the CL slots
-// in rank order after a cluster barrier, so every CTA takes the same alpha/beta/stop
-// decision.  The cluster grabs the next brick from a global counter when it is done
+// (st.async.shared::cluster, completing in bytes on the receiver's mbarrier); the two dot
+// products per iteration are reduced over the cluster by st.async'ing each CTA's fp64
+// partial into every CTA's slot array and summing the CL slots in rank order once that
+// CTA's mbarrier phase completes, so every CTA takes the same alpha/beta/stop decision
+// and no cluster barrier is needed inside the iteration loop.  The cluster grabs the next brick from a global counter when it is done
 // (persistent, load-balanced over bricks with different iteration counts).  HBM traffic
 // per brick is one read of W/dinv/x/r and one write of the result; per iteration none.
 //

@@ -110,7 +110,8 @@ def main():
         tp = os.path.join(os.path.dirname(a.out), "ncu_traffic.json")
         T = json.load(open(tp)) if os.path.exists(tp) else {}
         for d in R:
-            key = {"k_passA": "passA", "k_passB": "passB"}.get(d["kernel"].split("<")[0], d["kernel"])
+            key = {"k_passA": "passA", "k_passB": "passB", "k_resident": "resident"}.get(
+                d["kernel"].split("<")[0], d["kernel"])
             if "dram_bytes" in d:
                 T[key] = d["dram_bytes"]
         T["_source"] = os.path.basename(a.out)
