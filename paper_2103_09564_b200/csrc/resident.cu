@@ -55,8 +55,8 @@ struct Cfg {
   static constexpr int FZ = BY * N;         // floats of a z face
   static constexpr int FY = BZ * N;         // floats of a y face
   static constexpr int oP = 0;                          // p   [BZ+2][BY+2][N] (halo faces)
-  static constexpr int oX = oP + (BZ + 2) * PP;         // x   [BZ][BY][N]
-  static constexpr int oWYM = oX + BZ * BY * N;         // -y weight of rows 2j [BZ][NJ][N]
+  static constexpr int oWX = oP + (BZ + 2) * PP;        // +x weights [BZ][BY][N]
+  static constexpr int oWYM = oWX + BZ * BY * N;        // -y weight of rows 2j [BZ][NJ][N]
   static constexpr int oWZM = oWYM + BZ * NJ * N;       // -z weight of plane 4g [NG][BY][N]
   static constexpr int oZH = oWZM + NG * BY * N;        // z = dinv r of the cells across the
                                                         // 4 faces: -z, +z [BY][N], -y, +y [BZ][N]
@@ -255,18 +255,21 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   extern __shared__ __align__(16) float sm[];
   // mbarriers: [0] halo z values in, [1] p.q partials in, [2] (r.z, r.r) partials in
   __shared__ __align__(8) uint64_t s_bar[3];
-  __shared__ __align__(16) double s_pq[CL];      // p.q partial of every CTA (rank order)
-  __shared__ __align__(16) double2 s_rz[CL];     // (r.z, r.r) partial of every CTA
+  __shared__ __align__(16) double s_pq_slots[CL];  // p.q partial of every CTA (rank order)
+  __shared__ __align__(16) double2 s_rz_slots[CL];  // (r.z, r.r) partial of every CTA
   __shared__ float2 s_bredf[NW];
-  __shared__ double2 s_res;
   __shared__ int s_brick;
+  // CG scalars, updated by thread 0 only (fp64 state kept out of the per-thread registers)
+  __shared__ double s_rz, s_rrn, s_bb, s_pq, s_thr;
+  __shared__ int s_st, s_k;
+  __shared__ float s_be, s_al;
   __shared__ uint32_t s_taddr;
   const int t = threadIdx.x, warp = t >> 5;
   const int rank = cl_rank();
   const int gy = rank % GY, gz = rank / GY;
   const int qx = t % QX, j = (t / QX) % G::NJ, g = t / (QX * G::NJ);
   float* const P = sm + G::oP;
-  float* const X = sm + G::oX;
+  float* const WX = sm + G::oWX;
   float* const WYM = sm + G::oWYM;
   float* const WZM = sm + G::oWZM;
   float* const ZH = sm + G::oZH;
@@ -284,33 +287,37 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     fence_mbar_init();
   }
   // p starts at 0 everywhere, halo faces included (faces on the brick boundary stay 0)
-  for (int i = t; i < G::oX; i += G::T) P[i] = 0.f;
+  for (int i = t; i < G::oWX; i += G::T) P[i] = 0.f;
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2);
-  // column map: dinv(it) = 4it, wx(it) = 32+4it, wy(it) = 64+4it, wz(it) = 96+4it with
-  // it = 2i + rr (i = plane within the thread's group of 4, rr = row of the pair)
+  // column map: dinv(it) = 4it, x(it) = 32+4it, wy(it) = 64+4it, wz(it) = 96+4it with
+  // it = 2i + rr (i = plane within the thread's group of 4, rr = row of the pair); the +x
+  // weights live in shared memory (tensor memory is full)
   const uint32_t cD = tb, cX = tb + 32u, cY = tb + 64u, cZ = tb + 96u;
 
   const int y0 = gy * BY, z0 = gz * BZ;
   const long long n = (long long)N * N * G::NZ;
   const long long PL = (long long)N * N;
   const long long BN = (long long)A.B * n;
-  // neighbours across the 4 faces (-z, +z, -y, +y) and where my boundary z values go
-  const bool hasf[4] = {gz > 0, gz < GZ - 1, gy > 0, gy < GY - 1};
-  const int nbr[4] = {rank - GY, rank + GY, rank - 1, rank + 1};
-  const int foff[4] = {0, FZ, 2 * FZ, 2 * FZ + FY};
-  uint32_t halo_bytes = 0;
-  for (int f = 0; f < 4; ++f)
-    if (hasf[f]) halo_bytes += (f < 2 ? FZ : FY) * 4u;
-  // my plane 0 feeds the -z neighbour's +z face (face 1), my last plane the +z neighbour's
-  // -z face (0), my row 0 the -y neighbour's +y face (3), my last row the +y neighbour's -y
-  // face (2)
+  // neighbours across the 4 faces f = -z, +z, -y, +y (bit f of hmask) and where my boundary
+  // z values go: my plane 0 feeds the -z neighbour's +z face, my last plane the +z
+  // neighbour's -z face, my row 0 the -y neighbour's +y face, my last row the +y
+  // neighbour's -y face.  (Scalars and constant-index arrays only: no local memory.)
+  const uint32_t hmask = (gz > 0 ? 1u : 0u) | (gz < GZ - 1 ? 2u : 0u) | (gy > 0 ? 4u : 0u) |
+                         (gy < GY - 1 ? 8u : 0u);
+  auto foff = [](int f) { return f < 2 ? f * FZ : 2 * FZ + (f - 2) * FY; };
+  auto face_of = [](int e) { return e < FZ ? 0 : e < 2 * FZ ? 1 : e < 2 * FZ + FY ? 2 : 3; };
+  const uint32_t halo_bytes = ((hmask & 1u) ? FZ * 4u : 0u) + ((hmask & 2u) ? FZ * 4u : 0u) +
+                              ((hmask & 4u) ? FY * 4u : 0u) + ((hmask & 8u) ? FY * 4u : 0u);
   uint32_t rface[4], rbar[4];
+#pragma unroll
   for (int f = 0; f < 4; ++f) {
-    rface[f] = hasf[f] ? mapa(sptr(ZH + foff[f ^ 1]), nbr[f]) : 0u;
-    rbar[f] = hasf[f] ? mapa(sptr(&s_bar[0]), nbr[f]) : 0u;
+    const int nb = f == 0 ? rank - GY : f == 1 ? rank + GY : f == 2 ? rank - 1 : rank + 1;
+    const bool h = (hmask >> f) & 1u;
+    rface[f] = h ? mapa(sptr(ZH + foff(f ^ 1)), nb) : 0u;
+    rbar[f] = h ? mapa(sptr(&s_bar[0]), nb) : 0u;
   }
   const uint32_t brk = sptr(&s_brick);
   uint32_t ph0 = 0, ph1 = 0, ph2 = 0;   // mbarrier phase parities
@@ -321,7 +328,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   // 8/16-byte message per CTA pair, completing on that CTA's mbarrier `bi`; many small
   // messages cost far more, tools/micro/mb_red.cu); warp 0 waits for the CL partials,
   // thread 0 adds them in rank order, and a CTA barrier hands the result to every thread.
-  auto cluster_sum = [&](float f0, float f1, int nv, int bi, auto* slots, uint32_t& ph) -> double2 {
+  auto cluster_sum = [&](float f0, float f1, int nv, int bi, auto* slots, uint32_t& ph,
+                         auto&& shadow, auto&& epilogue) {
     f0 = warp_sum_f(f0);
     if (nv > 1) f1 = warp_sum_f(f1);
     if ((t & 31) == 0) s_bredf[warp] = make_float2(f0, f1);
@@ -340,6 +348,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         else st_async_f64x2(mapa(slot, c), a0, a1, mapa(bar, c));
       }
     }
+    shadow();   // independent work while the partials travel
     if (warp == 0) {
       mbar_wait(&s_bar[bi], ph);
       if (t == 0) {
@@ -353,12 +362,11 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
             a1 += e.y;
           }
         }
-        s_res = make_double2(a0, a1);
+        epilogue(make_double2(a0, a1));   // thread 0 updates the CG scalars
       }
     }
     ph ^= 1u;
     __syncthreads();
-    return s_res;
   };
 
   float4 r[NI], q[NI];
@@ -382,7 +390,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       const long long gi = gb + (long long)(z0 + zl) * PL + (y0 + y) * N + 4 * qx;
       const float4 dv = ld4(A.dinv + gi);
       tm_st4(cD + 4u * it, dv);
-      tm_st4(cX + 4u * it, ld4(A.W + gi));
+      tm_st4(cX + 4u * it, ld4(A.x + gi));
       tm_st4(cY + 4u * it, ld4(A.W + BN + gi));
       tm_st4(cZ + 4u * it, ld4(A.W + 2 * BN + gi));
       fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
@@ -390,7 +398,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       fixm |= (dv.z == 0.f ? 4u : 0u) << (4 * it);
       fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
       r[it] = ld4(A.r0 + gi);
-      st4(X + (zl * BY + y) * N + 4 * qx, ld4(A.x + gi));
+      st4(WX + (zl * BY + y) * N + 4 * qx, ld4(A.W + gi));
       st4(P + pidx(zl, y) + 4 * qx, f4(0.f));
       if (rr == 0)
         st4(WYM + (zl * G::NJ + j) * N + 4 * qx, y0 + y > 0 ? ld4(A.W + BN + gi - N) : f4(0.f));
@@ -400,10 +408,10 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     // z0 = dinv r0 of the cells across my faces (the neighbours send the later ones)
     for (int u = t; u < (2 * FZ + 2 * FY) / 4; u += G::T) {
       const int e = 4 * u;
-      const int f = e < FZ ? 0 : e < 2 * FZ ? 1 : e < 2 * FZ + FY ? 2 : 3;
-      const int c = e - foff[f], a = c / N, x = c % N;   // a = row (z faces) / plane (y faces)
+      const int f = face_of(e);
+      const int c = e - foff(f), a = c / N, x = c % N;   // a = row (z faces) / plane (y faces)
       float4 zv = f4(0.f);
-      if (hasf[f]) {
+      if ((hmask >> f) & 1u) {
         const int gz_ = f == 0 ? z0 - 1 : f == 1 ? z0 + BZ : z0 + a;
         const int gy_ = f == 2 ? y0 - 1 : f == 3 ? y0 + BY : y0 + a;
         const long long gi = gb + (long long)gz_ * PL + gy_ * N + x;
@@ -412,40 +420,42 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       st4(ZH + e, zv);
     }
     res::tm_wait_st();
-    // ---- initial scalars from the setup partials (fixed order; same in every thread)
-    double rz = 0.0, rrn = 0.0, bb = 0.0, nf = 0.0, nu = 0.0;
-    for (int u = 0; u < A.U; ++u) {
-      const double2 pb = A.PB[(long long)b * A.U + u];
-      const double4 ps = A.PS[(long long)b * A.U + u];
-      rz += pb.x; rrn += pb.y; bb += ps.x; nf += ps.y; nu += ps.z;
+    // ---- initial scalars from the setup partials (fixed order), decision of iteration 0
+    // (as passA_scalars): thread 0 owns the CG scalars from here on
+    if (t == 0) {
+      double rz = 0.0, rrn = 0.0, bb = 0.0, nf = 0.0, nu = 0.0;
+      for (int u = 0; u < A.U; ++u) {
+        const double2 pb = A.PB[(long long)b * A.U + u];
+        const double4 ps = A.PS[(long long)b * A.U + u];
+        rz += pb.x; rrn += pb.y; bb += ps.x; nf += ps.y; nu += ps.z;
+      }
+      const double t2 = (double)A.C.tol * (double)A.C.tol;
+      s_thr = A.C.tol_mode == 0 ? t2 * bb : t2;
+      int st = ST_ACTIVE;
+      if (nf == 0.0 || nu == 0.0) st = ST_TRIVIAL;
+      else if (bb == 0.0) st = ST_ZERO_B;
+      else if (rrn <= s_thr) st = ST_CONVERGED;
+      else if (A.C.max_iter <= 0) st = ST_MAXITER;
+      s_st = st;
+      s_k = 0;
+      s_rz = rz;
+      s_rrn = rrn;
+      s_bb = bb;
+      s_be = 0.f;
     }
     __syncthreads();
 
-    int st = ST_ACTIVE, k = 0;
-    double rz_prev = 0.0, pq_prev = 0.0;
-    float al = 0.f;   // alpha_{k-1}
-    const double t2 = (double)A.C.tol * (double)A.C.tol;
+    int k = 0;
+    float al = 0.f;   // alpha_k
     while (true) {
-      // ---- decision of iteration k (as passA_scalars)
-      if (k == 0) {
-        if (nf == 0.0 || nu == 0.0) st = ST_TRIVIAL;
-        else if (bb == 0.0) st = ST_ZERO_B;
-      } else if (!(pq_prev > 0.0) || !isfinite(rz) || !isfinite(pq_prev)) {
-        st = ST_BREAKDOWN;
-      }
-      if (st == ST_ACTIVE) {
-        const bool conv = (A.C.tol_mode == 0) ? (rrn <= t2 * bb) : (rrn <= t2);
-        if (conv) st = ST_CONVERGED;
-        else if (k >= A.C.max_iter) st = ST_MAXITER;
-      }
-      if (st != ST_ACTIVE) {
+      if (s_st != ST_ACTIVE) {
         if (k > 0) {   // consume the halo phase iteration k-1 sent (keeps phases in step)
           mbar_wait(&s_bar[0], ph0);
           ph0 ^= 1u;
         }
         break;
       }
-      const float be = k > 0 ? (float)(rz / rz_prev) : 0.f;
+      const float be = s_be;
 #ifdef RW_RES_TIMING
       long long tp0 = A.dbg ? clock64() : 0;
       auto TP = [&](int i) {   // debug phase timer: cluster 0, per rank
@@ -459,9 +469,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       auto TP = [](int) {};
 #endif
 
-      // ---- step 1: x_k = x_{k-1} + alpha_{k-1} p_{k-1} (lagged);  p_k = z_k + beta p_{k-1}
-      // on the own cells (z = dinv r) and on the halo faces (z of the cells across the faces
-      // arrived during the previous reduction)
+      // ---- step 1: p_k = z_k + beta p_{k-1} on the own cells (z = dinv r) and on the halo
+      // faces (z of the cells across the faces arrived during the previous reduction)
       {
         float4 dv[NI];
         tm_ld32(cD, dv);
@@ -469,12 +478,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         for (int it = 0; it < NI; ++it) {
           const int i = it >> 1, rr = it & 1, zl = 4 * g + i, y = 2 * j + rr;
           const int so = pidx(zl, y) + 4 * qx;
-          const float4 po = ld4(P + so);
-          st4(P + so, pnew4(be, po, dv[it], r[it]));
-          if (k > 0) {
-            float* xp = X + (zl * BY + y) * N + 4 * qx;
-            st4(xp, fma4(al, po, ld4(xp)));
-          }
+          st4(P + so, pnew4(be, ld4(P + so), dv[it], r[it]));
         }
       }
       TP(0);
@@ -485,9 +489,9 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       TP(1);
       for (int u = t; u < (2 * FZ + 2 * FY) / 4; u += G::T) {
         const int e = 4 * u;
-        const int f = e < FZ ? 0 : e < 2 * FZ ? 1 : e < 2 * FZ + FY ? 2 : 3;
-        if (!hasf[f]) continue;
-        const int c = e - foff[f], a = c / N, x = c % N;
+        const int f = face_of(e);
+        if (!((hmask >> f) & 1u)) continue;
+        const int c = e - foff(f), a = c / N, x = c % N;
         const int po = (f == 0 ? pidx(-1, a) : f == 1 ? pidx(BZ, a)
                         : f == 2 ? pidx(a, -1) : pidx(a, BY)) + x;
         st4(P + po, fma4(be, ld4(P + po), ld4(ZH + e)));
@@ -498,53 +502,64 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       // ---- step 2: q = L_UU p (edge-difference stencil), partial p.q; one row pair
       // (items 2i, 2i+1) at a time.  Halo faces are part of the padded p planes.
       float apq = 0.f;   // this thread's p.q (fp32 over its 32 voxels; fp64 beyond)
+      {
+        // sliding window over the thread's 4 planes: rows 2j, 2j+1 of planes zl-1, zl, zl+1
+        const int sb = pidx(4 * g, 2 * j) + 4 * qx;
+        float4 pm0 = ld4(P + sb - PP), pm1 = ld4(P + sb - PP + N);
+        float4 p0 = ld4(P + sb), p1 = ld4(P + sb + N);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int zl = 4 * g + i;
-        const int so = pidx(zl, 2 * j) + 4 * qx;
-        const float4 p0 = ld4(P + so), p1 = ld4(P + so + N);
-        float4 q0, q1;
-        {  // x terms (same term order as stencil1: +x, -x, +y, -y, +z, -z)
-          float4 wx0, wx1;
-          tm_ld8(cX + 8u * i, wx0, wx1);
-          const float xl0 = __shfl_up_sync(0xffffffffu, p0.w, 1, QX);
-          const float xr0 = __shfl_down_sync(0xffffffffu, p0.x, 1, QX);
-          const float xl1 = __shfl_up_sync(0xffffffffu, p1.w, 1, QX);
-          const float xr1 = __shfl_down_sync(0xffffffffu, p1.x, 1, QX);
-          const float wl0 = __shfl_up_sync(0xffffffffu, wx0.w, 1, QX);
-          const float wl1 = __shfl_up_sync(0xffffffffu, wx1.w, 1, QX);
-          q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
-          q1 = xterms(p1, xl1, xr1, wx1, qx > 0 ? wl1 : 0.f);
-        }
-        {  // y terms: row 2j+1 is +y of row 2j (and row 2j is -y of row 2j+1)
-          float4 wy0, wy1;
-          tm_ld8(cY + 8u * i, wy0, wy1);
-          const float4 wym0 = ld4(WYM + (zl * G::NJ + j) * N + 4 * qx);
-          q0 = terms2(q0, p0, p1, ld4(P + so - N), wy0, wym0);
-          q1 = terms2(q1, p1, ld4(P + so + 2 * N), p0, wy1, wy0);
-        }
-        {  // z terms
-          float4 wz0, wz1, wzm0, wzm1;
-          tm_ld8(cZ + 8u * i, wz0, wz1);
-          if (i == 0) {
-            wzm0 = ld4(WZM + (g * BY + 2 * j) * N + 4 * qx);
-            wzm1 = ld4(WZM + (g * BY + 2 * j + 1) * N + 4 * qx);
-          } else {
-            tm_ld8(cZ + 8u * (i - 1), wzm0, wzm1);
+        for (int i = 0; i < 4; ++i) {
+          const int zl = 4 * g + i;
+          const int so = sb + i * PP;
+          const float4 pn0 = ld4(P + so + PP), pn1 = ld4(P + so + PP + N);
+          float4 q0, q1;
+          {  // x terms (same term order as stencil1: +x, -x, +y, -y, +z, -z)
+            const float* wxp = WX + (zl * BY + 2 * j) * N + 4 * qx;
+            const float4 wx0 = ld4(wxp), wx1 = ld4(wxp + N);
+            const float xl0 = __shfl_up_sync(0xffffffffu, p0.w, 1, QX);
+            const float xr0 = __shfl_down_sync(0xffffffffu, p0.x, 1, QX);
+            const float xl1 = __shfl_up_sync(0xffffffffu, p1.w, 1, QX);
+            const float xr1 = __shfl_down_sync(0xffffffffu, p1.x, 1, QX);
+            const float wl0 = __shfl_up_sync(0xffffffffu, wx0.w, 1, QX);
+            const float wl1 = __shfl_up_sync(0xffffffffu, wx1.w, 1, QX);
+            q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
+            q1 = xterms(p1, xl1, xr1, wx1, qx > 0 ? wl1 : 0.f);
           }
-          q0 = terms2(q0, p0, ld4(P + so + PP), ld4(P + so - PP), wz0, wzm0);
-          q1 = terms2(q1, p1, ld4(P + so + N + PP), ld4(P + so + N - PP), wz1, wzm1);
+          {  // y terms: row 2j+1 is +y of row 2j (and row 2j is -y of row 2j+1)
+            float4 wy0, wy1;
+            tm_ld8(cY + 8u * i, wy0, wy1);
+            const float4 wym0 = ld4(WYM + (zl * G::NJ + j) * N + 4 * qx);
+            q0 = terms2(q0, p0, p1, ld4(P + so - N), wy0, wym0);
+            q1 = terms2(q1, p1, ld4(P + so + 2 * N), p0, wy1, wy0);
+          }
+          {  // z terms
+            float4 wz0, wz1, wzm0, wzm1;
+            tm_ld8(cZ + 8u * i, wz0, wz1);
+            if (i == 0) {
+              wzm0 = ld4(WZM + (g * BY + 2 * j) * N + 4 * qx);
+              wzm1 = ld4(WZM + (g * BY + 2 * j + 1) * N + 4 * qx);
+            } else {
+              tm_ld8(cZ + 8u * (i - 1), wzm0, wzm1);
+            }
+            q0 = terms2(q0, p0, pn0, pm0, wz0, wzm0);
+            q1 = terms2(q1, p1, pn1, pm1, wz1, wzm1);
+          }
+          const uint32_t fm = fixm >> (8 * i);
+          q0 = mask4(q0, fm);
+          q1 = mask4(q1, fm >> 4);
+          q[2 * i] = q0;
+          q[2 * i + 1] = q1;
+          apq = __fadd_rn(apq, __fadd_rn(dot4f(p0, q0), dot4f(p1, q1)));
+          pm0 = p0; pm1 = p1; p0 = pn0; p1 = pn1;
         }
-        const uint32_t fm = fixm >> (8 * i);
-        q0 = mask4(q0, fm);
-        q1 = mask4(q1, fm >> 4);
-        q[2 * i] = q0;
-        q[2 * i + 1] = q1;
-        apq = __fadd_rn(apq, __fadd_rn(dot4f(p0, q0), dot4f(p1, q1)));
       }
       TP(3);
-      const double pq = cluster_sum(apq, 0.f, 1, 1, s_pq, ph1).x;
-      al = (pq > 0.0 && isfinite(pq)) ? (float)(rz / pq) : 0.f;
+      cluster_sum(apq, 0.f, 1, 1, s_pq_slots, ph1, [] {}, [&](double2 v) {
+        const double pq = v.x;
+        s_pq = pq;
+        s_al = (pq > 0.0 && isfinite(pq)) ? (float)(s_rz / pq) : 0.f;
+      });
+      al = s_al;
       TP(4);
 
       // ---- step 3: r -= alpha q;  z = dinv r;  boundary z to the neighbours' face buffers
@@ -560,31 +575,50 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
           const float4 rn = fma4(-al, q[it], r[it]);
           r[it] = rn;
           const float4 zn = mul4(dv[it], rn);
-          if (zl == 0 && hasf[0]) st_async4(rface[0] + (uint32_t)(y * N + 4 * qx) * 4u, zn, rbar[0]);
-          if (zl == BZ - 1 && hasf[1]) st_async4(rface[1] + (uint32_t)(y * N + 4 * qx) * 4u, zn, rbar[1]);
-          if (y == 0 && hasf[2]) st_async4(rface[2] + (uint32_t)(zl * N + 4 * qx) * 4u, zn, rbar[2]);
-          if (y == BY - 1 && hasf[3]) st_async4(rface[3] + (uint32_t)(zl * N + 4 * qx) * 4u, zn, rbar[3]);
+          if (zl == 0 && (hmask & 1u)) st_async4(rface[0] + (uint32_t)(y * N + 4 * qx) * 4u, zn, rbar[0]);
+          if (zl == BZ - 1 && (hmask & 2u)) st_async4(rface[1] + (uint32_t)(y * N + 4 * qx) * 4u, zn, rbar[1]);
+          if (y == 0 && (hmask & 4u)) st_async4(rface[2] + (uint32_t)(zl * N + 4 * qx) * 4u, zn, rbar[2]);
+          if (y == BY - 1 && (hmask & 8u)) st_async4(rface[3] + (uint32_t)(zl * N + 4 * qx) * 4u, zn, rbar[3]);
           arz = __fadd_rn(arz, dot4f(rn, zn));
           arr = __fadd_rn(arr, dot4f(rn, rn));
         }
       }
       TP(5);
-      const double2 srr = cluster_sum(arz, arr, 2, 2, s_rz, ph2);
+      // x_{k+1} = x_k + alpha_k p_k (own cells, x in tensor memory) in the reduction's shadow
+      cluster_sum(arz, arr, 2, 2, s_rz_slots, ph2, [&] {
+        float4 xv[NI];
+        tm_ld32(cX, xv);
+#pragma unroll
+        for (int it = 0; it < NI; ++it) {
+          const int zl = 4 * g + (it >> 1), y = 2 * j + (it & 1);
+          tm_st4(cX + 4u * it, fma4(al, ld4(P + pidx(zl, y) + 4 * qx), xv[it]));
+        }
+        res::tm_wait_st();
+      }, [&](double2 v) {   // thread 0: decision of iteration k+1 (as passA_scalars), beta_k
+        const double rz_new = v.x, pq = s_pq;
+        int st = ST_ACTIVE;
+        if (!(pq > 0.0) || !isfinite(rz_new) || !isfinite(pq)) st = ST_BREAKDOWN;
+        else if (v.y <= s_thr) st = ST_CONVERGED;
+        else if (s_k + 1 >= A.C.max_iter) st = ST_MAXITER;
+        s_st = st;
+        s_be = (float)(rz_new / s_rz);
+        s_rz = rz_new;
+        s_rrn = v.y;
+        s_k = s_k + 1;
+      });
       TP(6);
-      rz_prev = rz;
-      pq_prev = pq;
-      rz = srr.x;
-      rrn = srr.y;
       ++k;
     }
 
-    // ---- finalise (row a6): last lagged x update, clamp, fixed values kept, labels
-    const bool upd = (st == ST_CONVERGED || st == ST_MAXITER) && k >= 1;
+    // ---- finalise (row a6): clamp, fixed values kept, labels.  x already holds x_k (the
+    // update of iteration k-1 ran in the shadow of its last reduction).
+    const int st = s_st;
+    float4 xfin[NI];
+    tm_ld32(cX, xfin);
 #pragma unroll
     for (int it = 0; it < NI; ++it) {
       const int i = it >> 1, rr = it & 1, zl = 4 * g + i, y = 2 * j + rr;
-      float4 xv = ld4(X + (zl * BY + y) * N + 4 * qx);
-      if (upd && al != 0.f) xv = fma4(al, ld4(P + pidx(zl, y) + 4 * qx), xv);
+      const float4 xv = xfin[it];
       const uint32_t fm = fixm >> (4 * it);
       float o[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
@@ -604,8 +638,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       if (A.resid) {
         double res = 0.0;
         if (st == ST_CONVERGED || st == ST_MAXITER || st == ST_BREAKDOWN) {
-          res = sqrt(rrn);
-          if (A.C.tol_mode == 0) res = bb > 0.0 ? res / sqrt(bb) : 0.0;
+          res = sqrt(s_rrn);
+          if (A.C.tol_mode == 0) res = s_bb > 0.0 ? res / sqrt(s_bb) : 0.0;
         }
         A.resid[b] = (float)res;
       }
