@@ -329,7 +329,7 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       long long h[128];
       RW_CK(cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s));
       RW_CK(cudaStreamSynchronize(s));
-      const char* names[7] = {"step1", "halo-wait", "faces+sync", "spmv", "red-pq", "step3+send", "red-rz"};
+      const char* names[7] = {"step1+sync", "spmv-int", "halo-wait", "spmv-bnd", "red-pq", "step3", "red-rz"};
       for (int r = 0; r < 16; r += 5) {
         fprintf(stderr, "[res-timing rank %2d]", r);
         for (int i = 0; i < 7; ++i) fprintf(stderr, " %s=%lld", names[i], h[r * 8 + i]);

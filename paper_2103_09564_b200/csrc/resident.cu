@@ -38,35 +38,21 @@ namespace res {
 
 template <int N, int CL>
 struct Cfg {
-  // CTA grid over the brick: GY slabs along y x GZ along z (2-D split: half the halo of a
-  // z-only split for the same voxels per CTA)
-  static constexpr int GY = CL >= 16 ? 4 : 2;
-  static constexpr int GZ = CL / GY;
-  static constexpr int NZ = N;              // cubic bricks
-  static constexpr int BY = N / GY;         // rows per CTA
-  static constexpr int BZ = NZ / GZ;        // planes per CTA
+  static constexpr int ZS = 4;              // planes per CTA
+  static constexpr int NZ = ZS * CL;        // brick z extent
   static constexpr int QX = N / 4;          // quads per row
-  static constexpr int NJ = BY / 2;         // row pairs per CTA
-  static constexpr int NG = BZ / 4;         // groups of 4 planes per CTA
-  static constexpr int T = QX * NJ * NG;    // threads per CTA: one per (quad, row pair, group)
-  static constexpr int NI = 8;              // items (quads) per thread: 2 rows x 4 planes
-  static constexpr int PR = BY + 2;         // rows of a padded p plane (halo rows -1, BY)
-  static constexpr int PP = PR * N;         // floats per padded p plane
-  static constexpr int FZ = BY * N;         // floats of a z face
-  static constexpr int FY = BZ * N;         // floats of a y face
-  static constexpr int oP = 0;                          // p   [BZ+2][BY+2][N] (halo faces)
-  static constexpr int oWX = oP + (BZ + 2) * PP;        // +x weights [BZ][BY][N]
-  static constexpr int oWYM = oWX + BZ * BY * N;        // -y weight of rows 2j [BZ][NJ][N]
-  static constexpr int oWZM = oWYM + BZ * NJ * N;       // -z weight of plane 4g [NG][BY][N]
-  static constexpr int oZH = oWZM + NG * BY * N;        // z = dinv r of the cells across the
-                                                        // 4 faces: -z, +z [BY][N], -y, +y [BZ][N]
-  static constexpr int nF = oZH + 2 * FZ + 2 * FY;
+  static constexpr int T = QX * (N / 2);    // threads per CTA
+  static constexpr int NI = 2 * ZS;         // items (quads) per thread
+  static constexpr int PL = N * N;          // floats per plane
+  static constexpr int oP = 0;                          // p   [ZS+2][N][N]  (0, ZS+1 = halo)
+  static constexpr int oX = oP + (ZS + 2) * PL;         // x   [ZS][N][N]
+  static constexpr int oWYM = oX + ZS * PL;             // -y weight of rows 2j [ZS][N/2][N]
+  static constexpr int oWZM = oWYM + ZS * (N / 2) * N;  // -z weight of plane 0 [N][N]
+  static constexpr int nF = oWZM + PL;
   static constexpr int SMEM = nF * 4;
   static constexpr int NW = T / 32;
   static constexpr int TCOLS = T >= 512 ? 512 : 128;    // 128 columns per thread
   static_assert(T % 128 == 0, "thread count must be a multiple of 4 warps");
-  static_assert(BZ % 4 == 0 && BY % 2 == 0, "block must hold whole groups / row pairs");
-  static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
 __device__ __forceinline__ uint32_t sptr(const void* p) {
@@ -229,11 +215,6 @@ __device__ __forceinline__ float4 terms2(float4 q, float4 p, float4 pp, float4 p
   q.w = __fmaf_rn(wm.w, __fsub_rn(p.w, pm.w), __fmaf_rn(wp.w, __fsub_rn(p.w, pp.w), q.w));
   return q;
 }
-__device__ __forceinline__ float warp_sum_f(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;   // identical in every lane
-}
 // q = 0 on fixed voxels (bit e of fm)
 __device__ __forceinline__ float4 mask4(float4 q, uint32_t fm) {
   if (fm & 1u) q.x = 0.f;
@@ -250,31 +231,23 @@ template <int N, int CL>
 __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   using G = res::Cfg<N, CL>;
   using namespace res;
-  constexpr int QX = G::QX, NI = G::NI, NW = G::NW, BY = G::BY, BZ = G::BZ, PP = G::PP;
-  constexpr int GY = G::GY, GZ = G::GZ, FZ = G::FZ, FY = G::FY;
+  constexpr int ZS = G::ZS, QX = G::QX, PL = G::PL, NI = G::NI, NW = G::NW;
   extern __shared__ __align__(16) float sm[];
-  // mbarriers: [0] halo z values in, [1] p.q partials in, [2] (r.z, r.r) partials in
+  // mbarriers: [0] halo planes in, [1] p.q partials in, [2] (r.z, r.r) partials in
   __shared__ __align__(8) uint64_t s_bar[3];
-  __shared__ __align__(16) double s_pq_slots[CL];  // p.q partial of every CTA (rank order)
-  __shared__ __align__(16) double2 s_rz_slots[CL];  // (r.z, r.r) partial of every CTA
-  __shared__ float2 s_bredf[NW];
+  __shared__ __align__(16) double s_pq[CL];      // p.q partial of every CTA (rank order)
+  __shared__ __align__(16) double2 s_rz[CL];     // (r.z, r.r) partial of every CTA
+  __shared__ double s_bred[NW][2];
+  __shared__ double2 s_res;
   __shared__ int s_brick;
-  // CG scalars, updated by thread 0 only (fp64 state kept out of the per-thread registers)
-  __shared__ double s_rz, s_rrn, s_bb, s_pq, s_thr;
-  __shared__ int s_st, s_k;
-  __shared__ float s_be, s_al;
   __shared__ uint32_t s_taddr;
   const int t = threadIdx.x, warp = t >> 5;
   const int rank = cl_rank();
-  const int gy = rank % GY, gz = rank / GY;
-  const int qx = t % QX, j = (t / QX) % G::NJ, g = t / (QX * G::NJ);
+  const int qx = t % QX, j = t / QX;
   float* const P = sm + G::oP;
-  float* const WX = sm + G::oWX;
+  float* const X = sm + G::oX;
   float* const WYM = sm + G::oWYM;
   float* const WZM = sm + G::oWZM;
-  float* const ZH = sm + G::oZH;
-  // padded p index of (local plane zl in -1..BZ, local row y in -1..BY), x = 0
-  auto pidx = [&](int zl, int y) { return ((zl + 1) * G::PR + (y + 1)) * N; };
 
   // ---- tensor memory: 128 columns per thread (lane = 32*(warp%4) + lane id)
   if (warp == 0) {
@@ -286,60 +259,51 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     for (int i = 0; i < 3; ++i) mbar_init(&s_bar[i], 1);
     fence_mbar_init();
   }
-  // p starts at 0 everywhere, halo faces included (faces on the brick boundary stay 0)
-  for (int i = t; i < G::oWX; i += G::T) P[i] = 0.f;
+  // halo planes start at 0 (the outer ones of ranks 0 and CL-1 are never written)
+  for (int i = t; i < PL; i += G::T) {
+    P[i] = 0.f;
+    P[(ZS + 1) * PL + i] = 0.f;
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2);
-  // column map: dinv(it) = 4it, x(it) = 32+4it, wy(it) = 64+4it, wz(it) = 96+4it with
-  // it = 2i + rr (i = plane within the thread's group of 4, rr = row of the pair); the +x
-  // weights live in shared memory (tensor memory is full)
+  // column map: dinv(it) = 4it, wx(it) = 32+4it, wy(it) = 64+4it, wz(it) = 96+4it;
+  // the two items of plane zl (it = 2zl, 2zl+1) are 8 adjacent columns of each weight
   const uint32_t cD = tb, cX = tb + 32u, cY = tb + 64u, cZ = tb + 96u;
 
-  const int y0 = gy * BY, z0 = gz * BZ;
-  const long long n = (long long)N * N * G::NZ;
-  const long long PL = (long long)N * N;
+  const int z0 = rank * ZS;
+  const long long n = (long long)PL * G::NZ;
   const long long BN = (long long)A.B * n;
-  // neighbours across the 4 faces f = -z, +z, -y, +y (bit f of hmask) and where my boundary
-  // z values go: my plane 0 feeds the -z neighbour's +z face, my last plane the +z
-  // neighbour's -z face, my row 0 the -y neighbour's +y face, my last row the +y
-  // neighbour's -y face.  (Scalars and constant-index arrays only: no local memory.)
-  const uint32_t hmask = (gz > 0 ? 1u : 0u) | (gz < GZ - 1 ? 2u : 0u) | (gy > 0 ? 4u : 0u) |
-                         (gy < GY - 1 ? 8u : 0u);
-  auto foff = [](int f) { return f < 2 ? f * FZ : 2 * FZ + (f - 2) * FY; };
-  auto face_of = [](int e) { return e < FZ ? 0 : e < 2 * FZ ? 1 : e < 2 * FZ + FY ? 2 : 3; };
-  const uint32_t halo_bytes = ((hmask & 1u) ? FZ * 4u : 0u) + ((hmask & 2u) ? FZ * 4u : 0u) +
-                              ((hmask & 4u) ? FY * 4u : 0u) + ((hmask & 8u) ? FY * 4u : 0u);
-  uint32_t rface[4], rbar[4];
-#pragma unroll
-  for (int f = 0; f < 4; ++f) {
-    const int nb = f == 0 ? rank - GY : f == 1 ? rank + GY : f == 2 ? rank - 1 : rank + 1;
-    const bool h = (hmask >> f) & 1u;
-    rface[f] = h ? mapa(sptr(ZH + foff(f ^ 1)), nb) : 0u;
-    rbar[f] = h ? mapa(sptr(&s_bar[0]), nb) : 0u;
-  }
+  // DSMEM: my plane 0 -> rank-1's upper halo, my plane ZS-1 -> rank+1's lower halo, each
+  // with st.async completing (in bytes) on the receiver's halo mbarrier
+  const uint32_t own_off = (uint32_t)(j * 2 * N + 4 * qx) * 4u;   // row 2j, quad qx (bytes)
+  const uint32_t up_halo = rank > 0 ? mapa(sptr(P + (ZS + 1) * PL), rank - 1) : 0u;
+  const uint32_t up_bar = rank > 0 ? mapa(sptr(&s_bar[0]), rank - 1) : 0u;
+  const uint32_t dn_halo = rank < CL - 1 ? mapa(sptr(P), rank + 1) : 0u;
+  const uint32_t dn_bar = rank < CL - 1 ? mapa(sptr(&s_bar[0]), rank + 1) : 0u;
+  const uint32_t halo_bytes = (uint32_t)((rank > 0) + (rank < CL - 1)) * PL * 4u;
   const uint32_t brk = sptr(&s_brick);
   uint32_t ph0 = 0, ph1 = 0, ph2 = 0;   // mbarrier phase parities
 
-  // Cluster-wide fp64 sum of nv (1 or 2) per-thread fp32 partials, identical in every
-  // thread of every CTA: warp xor-shuffle tree -> per-warp partials -> thread 0 adds them
-  // in warp order (fp64) and st.async's the CTA partial into slot `rank` of every CTA (one
-  // 8/16-byte message per CTA pair, completing on that CTA's mbarrier `bi`; many small
-  // messages cost far more, tools/micro/mb_red.cu); warp 0 waits for the CL partials,
-  // thread 0 adds them in rank order, and a CTA barrier hands the result to every thread.
-  auto cluster_sum = [&](float f0, float f1, int nv, int bi, auto* slots, uint32_t& ph,
-                         auto&& shadow, auto&& epilogue) {
-    f0 = warp_sum_f(f0);
-    if (nv > 1) f1 = warp_sum_f(f1);
-    if ((t & 31) == 0) s_bredf[warp] = make_float2(f0, f1);
+  // Cluster-wide fp64 sum of nv (1 or 2) values per thread, identical in every thread of
+  // every CTA: warp xor-shuffle tree -> per-warp partials -> thread 0 adds them in warp order
+  // and st.async's the CTA partial into slot `rank` of every CTA (one 8/16-byte message per
+  // CTA pair, completing on that CTA's mbarrier `bi`; many small messages cost far more,
+  // tools/micro/mb_red.cu); warp 0 waits for the CL partials, thread 0 adds them in rank
+  // order, and a CTA barrier hands the result to every thread.
+  auto cluster_sum = [&](double* v, int nv, int bi, auto* slots, uint32_t& ph) -> double2 {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      if (i < nv) v[i] = warp_sum(v[i]);
+    if ((t & 31) == 0)
+      for (int i = 0; i < nv; ++i) s_bred[warp][i] = v[i];
     __syncthreads();
     if (t == 0) {
       double a0 = 0.0, a1 = 0.0;
       for (int w = 0; w < NW; ++w) {
-        const float2 e = s_bredf[w];
-        a0 += (double)e.x;
-        a1 += (double)e.y;
+        a0 += s_bred[w][0];
+        if (nv > 1) a1 += s_bred[w][1];
       }
       mbar_arrive_expect_tx(&s_bar[bi], CL * 8u * nv);
       const uint32_t slot = sptr(&slots[rank]), bar = sptr(&s_bar[bi]);
@@ -348,7 +312,6 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         else st_async_f64x2(mapa(slot, c), a0, a1, mapa(bar, c));
       }
     }
-    shadow();   // independent work while the partials travel
     if (warp == 0) {
       mbar_wait(&s_bar[bi], ph);
       if (t == 0) {
@@ -362,11 +325,12 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
             a1 += e.y;
           }
         }
-        epilogue(make_double2(a0, a1));   // thread 0 updates the CG scalars
+        s_res = make_double2(a0, a1);
       }
     }
     ph ^= 1u;
     __syncthreads();
+    return s_res;
   };
 
   float4 r[NI], q[NI];
@@ -380,85 +344,64 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     cl_wait();
     const int b = s_brick;
     if (b >= A.B) break;
-    const long long gb = (long long)b * n;
 
-    // ---- load the block: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
+    // ---- load the slab: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
     uint32_t fixm = 0;   // bit 4*it+e: voxel is fixed (dinv == 0)
 #pragma unroll
     for (int it = 0; it < NI; ++it) {
-      const int i = it >> 1, rr = it & 1, zl = 4 * g + i, y = 2 * j + rr;
-      const long long gi = gb + (long long)(z0 + zl) * PL + (y0 + y) * N + 4 * qx;
-      const float4 dv = ld4(A.dinv + gi);
+      const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+      const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
+      const float4 dv = ld4(A.dinv + g);
       tm_st4(cD + 4u * it, dv);
-      tm_st4(cX + 4u * it, ld4(A.x + gi));
-      tm_st4(cY + 4u * it, ld4(A.W + BN + gi));
-      tm_st4(cZ + 4u * it, ld4(A.W + 2 * BN + gi));
+      tm_st4(cX + 4u * it, ld4(A.W + g));
+      tm_st4(cY + 4u * it, ld4(A.W + BN + g));
+      tm_st4(cZ + 4u * it, ld4(A.W + 2 * BN + g));
       fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
       fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
       fixm |= (dv.z == 0.f ? 4u : 0u) << (4 * it);
       fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
-      r[it] = ld4(A.r0 + gi);
-      st4(WX + (zl * BY + y) * N + 4 * qx, ld4(A.W + gi));
-      st4(P + pidx(zl, y) + 4 * qx, f4(0.f));
-      if (rr == 0)
-        st4(WYM + (zl * G::NJ + j) * N + 4 * qx, y0 + y > 0 ? ld4(A.W + BN + gi - N) : f4(0.f));
-      if (i == 0)
-        st4(WZM + (g * BY + y) * N + 4 * qx, z0 + zl > 0 ? ld4(A.W + 2 * BN + gi - PL) : f4(0.f));
-    }
-    // z0 = dinv r0 of the cells across my faces (the neighbours send the later ones)
-    for (int u = t; u < (2 * FZ + 2 * FY) / 4; u += G::T) {
-      const int e = 4 * u;
-      const int f = face_of(e);
-      const int c = e - foff(f), a = c / N, x = c % N;   // a = row (z faces) / plane (y faces)
-      float4 zv = f4(0.f);
-      if ((hmask >> f) & 1u) {
-        const int gz_ = f == 0 ? z0 - 1 : f == 1 ? z0 + BZ : z0 + a;
-        const int gy_ = f == 2 ? y0 - 1 : f == 3 ? y0 + BY : y0 + a;
-        const long long gi = gb + (long long)gz_ * PL + gy_ * N + x;
-        zv = mul4(ld4(A.dinv + gi), ld4(A.r0 + gi));
-      }
-      st4(ZH + e, zv);
+      r[it] = ld4(A.r0 + g);
+      const int so = y * N + 4 * qx;
+      st4(X + zl * PL + so, ld4(A.x + g));
+      st4(P + (zl + 1) * PL + so, f4(0.f));
+      if (rr == 0) st4(WYM + (zl * (N / 2) + j) * N + 4 * qx, y > 0 ? ld4(A.W + BN + g - N) : f4(0.f));
+      if (zl == 0) st4(WZM + so, z0 > 0 ? ld4(A.W + 2 * BN + g - PL) : f4(0.f));
     }
     res::tm_wait_st();
-    // ---- initial scalars from the setup partials (fixed order), decision of iteration 0
-    // (as passA_scalars): thread 0 owns the CG scalars from here on
-    if (t == 0) {
-      double rz = 0.0, rrn = 0.0, bb = 0.0, nf = 0.0, nu = 0.0;
-      for (int u = 0; u < A.U; ++u) {
-        const double2 pb = A.PB[(long long)b * A.U + u];
-        const double4 ps = A.PS[(long long)b * A.U + u];
-        rz += pb.x; rrn += pb.y; bb += ps.x; nf += ps.y; nu += ps.z;
-      }
-      const double t2 = (double)A.C.tol * (double)A.C.tol;
-      s_thr = A.C.tol_mode == 0 ? t2 * bb : t2;
-      int st = ST_ACTIVE;
-      if (nf == 0.0 || nu == 0.0) st = ST_TRIVIAL;
-      else if (bb == 0.0) st = ST_ZERO_B;
-      else if (rrn <= s_thr) st = ST_CONVERGED;
-      else if (A.C.max_iter <= 0) st = ST_MAXITER;
-      s_st = st;
-      s_k = 0;
-      s_rz = rz;
-      s_rrn = rrn;
-      s_bb = bb;
-      s_be = 0.f;
+    // ---- initial scalars from the setup partials (fixed order; same in every thread)
+    double rz = 0.0, rrn = 0.0, bb = 0.0, nf = 0.0, nu = 0.0;
+    for (int u = 0; u < A.U; ++u) {
+      const double2 pb = A.PB[(long long)b * A.U + u];
+      const double4 ps = A.PS[(long long)b * A.U + u];
+      rz += pb.x; rrn += pb.y; bb += ps.x; nf += ps.y; nu += ps.z;
     }
     __syncthreads();
 
-    int k = 0;
-    float al = 0.f;   // alpha_k
+    int st = ST_ACTIVE, k = 0;
+    double rz_prev = 0.0, pq_prev = 0.0;
+    float al = 0.f;   // alpha_{k-1}
+    const double t2 = (double)A.C.tol * (double)A.C.tol;
     while (true) {
-      if (s_st != ST_ACTIVE) {
-        if (k > 0) {   // consume the halo phase iteration k-1 sent (keeps phases in step)
-          mbar_wait(&s_bar[0], ph0);
-          ph0 ^= 1u;
-        }
-        break;
+      // ---- decision of iteration k (as passA_scalars)
+      if (k == 0) {
+        if (nf == 0.0 || nu == 0.0) st = ST_TRIVIAL;
+        else if (bb == 0.0) st = ST_ZERO_B;
+      } else if (!(pq_prev > 0.0) || !isfinite(rz) || !isfinite(pq_prev)) {
+        st = ST_BREAKDOWN;
       }
-      const float be = s_be;
+      if (st == ST_ACTIVE) {
+        const bool conv = (A.C.tol_mode == 0) ? (rrn <= t2 * bb) : (rrn <= t2);
+        if (conv) st = ST_CONVERGED;
+        else if (k >= A.C.max_iter) st = ST_MAXITER;
+      }
+      if (st != ST_ACTIVE) break;
+      const float be = k > 0 ? (float)(rz / rz_prev) : 0.f;
+
 #ifdef RW_RES_TIMING
+      // debug phase timer (build with -DRW_RES_TIMING, run with RW_DEBUG_RES_TIMING=1):
+      // cycles per phase summed over cluster 0's iterations, per rank
       long long tp0 = A.dbg ? clock64() : 0;
-      auto TP = [&](int i) {   // debug phase timer: cluster 0, per rank
+      auto TP = [&](int i) {
         if (A.dbg && t == 0 && blockIdx.x < CL) {
           const long long now = clock64();
           A.dbg[rank * 8 + i] += now - tp0;
@@ -468,157 +411,121 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 #else
       auto TP = [](int) {};
 #endif
-
-      // ---- step 1: p_k = z_k + beta p_{k-1} on the own cells (z = dinv r) and on the halo
-      // faces (z of the cells across the faces arrived during the previous reduction)
+      // ---- step 1: x += alpha_{k-1} p_{k-1} (lagged);  p_k = dinv r + beta p_{k-1}
+      if (t == 0) mbar_arrive_expect_tx(&s_bar[0], halo_bytes);
       {
         float4 dv[NI];
         tm_ld32(cD, dv);
 #pragma unroll
         for (int it = 0; it < NI; ++it) {
-          const int i = it >> 1, rr = it & 1, zl = 4 * g + i, y = 2 * j + rr;
-          const int so = pidx(zl, y) + 4 * qx;
-          st4(P + so, pnew4(be, ld4(P + so), dv[it], r[it]));
+          const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+          const int so = y * N + 4 * qx;
+          const float4 po = ld4(P + (zl + 1) * PL + so);
+          if (k > 0) st4(X + zl * PL + so, fma4(al, po, ld4(X + zl * PL + so)));
+          const float4 pn = pnew4(be, po, dv[it], r[it]);
+          st4(P + (zl + 1) * PL + so, pn);
+          if (zl == 0 && rank > 0) st_async4(up_halo + own_off + rr * N * 4, pn, up_bar);
+          if (zl == ZS - 1 && rank < CL - 1) st_async4(dn_halo + own_off + rr * N * 4, pn, dn_bar);
         }
-      }
-      TP(0);
-      if (k > 0) {
-        mbar_wait(&s_bar[0], ph0);
-        ph0 ^= 1u;
-      }
-      TP(1);
-      for (int u = t; u < (2 * FZ + 2 * FY) / 4; u += G::T) {
-        const int e = 4 * u;
-        const int f = face_of(e);
-        if (!((hmask >> f) & 1u)) continue;
-        const int c = e - foff(f), a = c / N, x = c % N;
-        const int po = (f == 0 ? pidx(-1, a) : f == 1 ? pidx(BZ, a)
-                        : f == 2 ? pidx(a, -1) : pidx(a, BY)) + x;
-        st4(P + po, fma4(be, ld4(P + po), ld4(ZH + e)));
       }
       __syncthreads();
-      TP(2);
+      TP(0);
 
       // ---- step 2: q = L_UU p (edge-difference stencil), partial p.q; one row pair
-      // (items 2i, 2i+1) at a time.  Halo faces are part of the padded p planes.
+      // (items 2zl, 2zl+1) at a time
       float apq = 0.f;   // this thread's p.q (fp32 over its 32 voxels; fp64 beyond)
-      {
-        // sliding window over the thread's 4 planes: rows 2j, 2j+1 of planes zl-1, zl, zl+1
-        const int sb = pidx(4 * g, 2 * j) + 4 * qx;
-        float4 pm0 = ld4(P + sb - PP), pm1 = ld4(P + sb - PP + N);
-        float4 p0 = ld4(P + sb), p1 = ld4(P + sb + N);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int zl = 4 * g + i;
-          const int so = sb + i * PP;
-          const float4 pn0 = ld4(P + so + PP), pn1 = ld4(P + so + PP + N);
-          float4 q0, q1;
-          {  // x terms (same term order as stencil1: +x, -x, +y, -y, +z, -z)
-            const float* wxp = WX + (zl * BY + 2 * j) * N + 4 * qx;
-            const float4 wx0 = ld4(wxp), wx1 = ld4(wxp + N);
-            const float xl0 = __shfl_up_sync(0xffffffffu, p0.w, 1, QX);
-            const float xr0 = __shfl_down_sync(0xffffffffu, p0.x, 1, QX);
-            const float xl1 = __shfl_up_sync(0xffffffffu, p1.w, 1, QX);
-            const float xr1 = __shfl_down_sync(0xffffffffu, p1.x, 1, QX);
-            const float wl0 = __shfl_up_sync(0xffffffffu, wx0.w, 1, QX);
-            const float wl1 = __shfl_up_sync(0xffffffffu, wx1.w, 1, QX);
-            q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
-            q1 = xterms(p1, xl1, xr1, wx1, qx > 0 ? wl1 : 0.f);
-          }
-          {  // y terms: row 2j+1 is +y of row 2j (and row 2j is -y of row 2j+1)
-            float4 wy0, wy1;
-            tm_ld8(cY + 8u * i, wy0, wy1);
-            const float4 wym0 = ld4(WYM + (zl * G::NJ + j) * N + 4 * qx);
-            q0 = terms2(q0, p0, p1, ld4(P + so - N), wy0, wym0);
-            q1 = terms2(q1, p1, ld4(P + so + 2 * N), p0, wy1, wy0);
-          }
-          {  // z terms
-            float4 wz0, wz1, wzm0, wzm1;
-            tm_ld8(cZ + 8u * i, wz0, wz1);
-            if (i == 0) {
-              wzm0 = ld4(WZM + (g * BY + 2 * j) * N + 4 * qx);
-              wzm1 = ld4(WZM + (g * BY + 2 * j + 1) * N + 4 * qx);
-            } else {
-              tm_ld8(cZ + 8u * (i - 1), wzm0, wzm1);
-            }
-            q0 = terms2(q0, p0, pn0, pm0, wz0, wzm0);
-            q1 = terms2(q1, p1, pn1, pm1, wz1, wzm1);
-          }
-          const uint32_t fm = fixm >> (8 * i);
-          q0 = mask4(q0, fm);
-          q1 = mask4(q1, fm >> 4);
-          q[2 * i] = q0;
-          q[2 * i + 1] = q1;
-          apq = __fadd_rn(apq, __fadd_rn(dot4f(p0, q0), dot4f(p1, q1)));
-          pm0 = p0; pm1 = p1; p0 = pn0; p1 = pn1;
+      auto spmv = [&](int zl) {
+        const float* Pz = P + (zl + 1) * PL;
+        const int so = 2 * j * N + 4 * qx;
+        const float4 p0 = ld4(Pz + so), p1 = ld4(Pz + so + N);
+        float4 q0, q1;
+        {  // x terms (same term order as stencil1: +x, -x, +y, -y, +z, -z)
+          float4 wx0, wx1;
+          tm_ld8(cX + 8u * zl, wx0, wx1);
+          const float xl0 = __shfl_up_sync(0xffffffffu, p0.w, 1, QX);
+          const float xr0 = __shfl_down_sync(0xffffffffu, p0.x, 1, QX);
+          const float xl1 = __shfl_up_sync(0xffffffffu, p1.w, 1, QX);
+          const float xr1 = __shfl_down_sync(0xffffffffu, p1.x, 1, QX);
+          const float wl0 = __shfl_up_sync(0xffffffffu, wx0.w, 1, QX);
+          const float wl1 = __shfl_up_sync(0xffffffffu, wx1.w, 1, QX);
+          q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
+          q1 = xterms(p1, xl1, xr1, wx1, qx > 0 ? wl1 : 0.f);
         }
-      }
+        {  // y terms: row 2j+1 is +y of row 2j (and row 2j is -y of row 2j+1)
+          float4 wy0, wy1;
+          tm_ld8(cY + 8u * zl, wy0, wy1);
+          const float4 pym = j > 0 ? ld4(Pz + so - N) : f4(0.f);
+          const float4 pyp = j < N / 2 - 1 ? ld4(Pz + so + 2 * N) : f4(0.f);
+          const float4 wym0 = ld4(WYM + (zl * (N / 2) + j) * N + 4 * qx);
+          q0 = terms2(q0, p0, p1, pym, wy0, wym0);
+          q1 = terms2(q1, p1, pyp, p0, wy1, wy0);
+        }
+        {  // z terms
+          float4 wz0, wz1, wzm0, wzm1;
+          tm_ld8(cZ + 8u * zl, wz0, wz1);
+          if (zl == 0) {
+            wzm0 = ld4(WZM + so);
+            wzm1 = ld4(WZM + so + N);
+          } else {
+            tm_ld8(cZ + 8u * (zl - 1), wzm0, wzm1);
+          }
+          q0 = terms2(q0, p0, ld4(Pz + PL + so), ld4(Pz - PL + so), wz0, wzm0);
+          q1 = terms2(q1, p1, ld4(Pz + PL + so + N), ld4(Pz - PL + so + N), wz1, wzm1);
+        }
+        const uint32_t fm = fixm >> (8 * zl);
+        q0 = mask4(q0, fm);
+        q1 = mask4(q1, fm >> 4);
+        q[2 * zl] = q0;
+        q[2 * zl + 1] = q1;
+        apq = __fadd_rn(apq, __fadd_rn(dot4f(p0, q0), dot4f(p1, q1)));
+      };
+#pragma unroll
+      for (int zl = 1; zl < ZS - 1; ++zl) spmv(zl);
+      TP(1);
+      mbar_wait(&s_bar[0], ph0);   // halo planes of the neighbours have landed
+      TP(2);
+      ph0 ^= 1u;
+      spmv(0);
+      spmv(ZS - 1);
       TP(3);
-      cluster_sum(apq, 0.f, 1, 1, s_pq_slots, ph1, [] {}, [&](double2 v) {
-        const double pq = v.x;
-        s_pq = pq;
-        s_al = (pq > 0.0 && isfinite(pq)) ? (float)(s_rz / pq) : 0.f;
-      });
-      al = s_al;
+      double v1[2] = {(double)apq, 0.0};
+      const double pq = cluster_sum(v1, 1, 1, s_pq, ph1).x;
+      al = (pq > 0.0 && isfinite(pq)) ? (float)(rz / pq) : 0.f;
       TP(4);
 
-      // ---- step 3: r -= alpha q;  z = dinv r;  boundary z to the neighbours' face buffers
-      // (st.async, landing while the reduction below runs);  partials r.z, r.r
-      if (t == 0 && halo_bytes) mbar_arrive_expect_tx(&s_bar[0], halo_bytes);
+      // ---- step 3: r -= alpha q;  partials r.(dinv r), r.r
       float arz = 0.f, arr = 0.f;
       {
         float4 dv[NI];
         tm_ld32(cD, dv);
 #pragma unroll
         for (int it = 0; it < NI; ++it) {
-          const int i = it >> 1, rr = it & 1, zl = 4 * g + i, y = 2 * j + rr;
           const float4 rn = fma4(-al, q[it], r[it]);
           r[it] = rn;
-          const float4 zn = mul4(dv[it], rn);
-          if (zl == 0 && (hmask & 1u)) st_async4(rface[0] + (uint32_t)(y * N + 4 * qx) * 4u, zn, rbar[0]);
-          if (zl == BZ - 1 && (hmask & 2u)) st_async4(rface[1] + (uint32_t)(y * N + 4 * qx) * 4u, zn, rbar[1]);
-          if (y == 0 && (hmask & 4u)) st_async4(rface[2] + (uint32_t)(zl * N + 4 * qx) * 4u, zn, rbar[2]);
-          if (y == BY - 1 && (hmask & 8u)) st_async4(rface[3] + (uint32_t)(zl * N + 4 * qx) * 4u, zn, rbar[3]);
-          arz = __fadd_rn(arz, dot4f(rn, zn));
+          arz = __fadd_rn(arz, dot4f(rn, mul4(dv[it], rn)));
           arr = __fadd_rn(arr, dot4f(rn, rn));
         }
       }
       TP(5);
-      // x_{k+1} = x_k + alpha_k p_k (own cells, x in tensor memory) in the reduction's shadow
-      cluster_sum(arz, arr, 2, 2, s_rz_slots, ph2, [&] {
-        float4 xv[NI];
-        tm_ld32(cX, xv);
-#pragma unroll
-        for (int it = 0; it < NI; ++it) {
-          const int zl = 4 * g + (it >> 1), y = 2 * j + (it & 1);
-          tm_st4(cX + 4u * it, fma4(al, ld4(P + pidx(zl, y) + 4 * qx), xv[it]));
-        }
-        res::tm_wait_st();
-      }, [&](double2 v) {   // thread 0: decision of iteration k+1 (as passA_scalars), beta_k
-        const double rz_new = v.x, pq = s_pq;
-        int st = ST_ACTIVE;
-        if (!(pq > 0.0) || !isfinite(rz_new) || !isfinite(pq)) st = ST_BREAKDOWN;
-        else if (v.y <= s_thr) st = ST_CONVERGED;
-        else if (s_k + 1 >= A.C.max_iter) st = ST_MAXITER;
-        s_st = st;
-        s_be = (float)(rz_new / s_rz);
-        s_rz = rz_new;
-        s_rrn = v.y;
-        s_k = s_k + 1;
-      });
+      double v2[2] = {(double)arz, (double)arr};
+      const double2 srr = cluster_sum(v2, 2, 2, s_rz, ph2);
+      const double srz = srr.x;
       TP(6);
+      rz_prev = rz;
+      pq_prev = pq;
+      rz = srz;
+      rrn = srr.y;
       ++k;
     }
 
-    // ---- finalise (row a6): clamp, fixed values kept, labels.  x already holds x_k (the
-    // update of iteration k-1 ran in the shadow of its last reduction).
-    const int st = s_st;
-    float4 xfin[NI];
-    tm_ld32(cX, xfin);
+    // ---- finalise (row a6): last lagged x update, clamp, fixed values kept, labels
+    const bool upd = (st == ST_CONVERGED || st == ST_MAXITER) && k >= 1;
 #pragma unroll
     for (int it = 0; it < NI; ++it) {
-      const int i = it >> 1, rr = it & 1, zl = 4 * g + i, y = 2 * j + rr;
-      const float4 xv = xfin[it];
+      const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+      const int so = y * N + 4 * qx;
+      float4 xv = ld4(X + zl * PL + so);
+      if (upd && al != 0.f) xv = fma4(al, ld4(P + (zl + 1) * PL + so), xv);
       const uint32_t fm = fixm >> (4 * it);
       float o[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
@@ -626,10 +533,10 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         if (fm & (1u << e)) continue;            // fixed: x holds the Dirichlet value
         o[e] = st == ST_ZERO_B ? 0.f : fminf(fmaxf(o[e], 0.f), 1.f);
       }
-      const long long gi = gb + (long long)(z0 + zl) * PL + (y0 + y) * N + 4 * qx;
-      st4(A.x + gi, make_float4(o[0], o[1], o[2], o[3]));
+      const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
+      st4(A.x + g, make_float4(o[0], o[1], o[2], o[3]));
       if (A.labels)
-        *reinterpret_cast<uchar4*>(A.labels + gi) =
+        *reinterpret_cast<uchar4*>(A.labels + g) =
             make_uchar4(o[0] > 0.5f, o[1] > 0.5f, o[2] > 0.5f, o[3] > 0.5f);
     }
     if (rank == 0 && t == 0) {
@@ -638,8 +545,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       if (A.resid) {
         double res = 0.0;
         if (st == ST_CONVERGED || st == ST_MAXITER || st == ST_BREAKDOWN) {
-          res = sqrt(s_rrn);
-          if (A.C.tol_mode == 0) res = s_bb > 0.0 ? res / sqrt(s_bb) : 0.0;
+          res = sqrt(rrn);
+          if (A.C.tol_mode == 0) res = bb > 0.0 ? res / sqrt(bb) : 0.0;
         }
         A.resid[b] = (float)res;
       }
