@@ -111,7 +111,8 @@ def test_ttest_flat_and_shift_invariance():
     step += rng.normal(0, 0.01, step.shape)
     Ws = wo.ttest_planes(step, EPS, 1)
     row = Ws[0, 2, 2, :-1]
-    assert np.argmin(row) == 3 and row[3] < 0.05 < row[0]   # the step edge is the weakest
+    # every edge whose 3^3 neighbourhoods straddle the step (x = 2..4) is weak, the others not
+    assert row[2:5].max() < 0.05 < row[[0, 1, 5, 6]].min()
 
 
 def test_planes_to_edges_roundtrip_and_solve():
