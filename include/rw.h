@@ -75,6 +75,38 @@ rw_status rw_brick_weights(const void* vol, rw_dtype dtype, rw_norm nm, int32_t 
                            const uint8_t* fixed, void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * rw_brick_weights_ex -- the paper's alternative edge-weight functions,
+ *   same output layout and eps floor as rw_brick_weights; pass W to rw_solve_bricks /
+ *   rw_solve_labels to solve with them.  Readings R19-R21:
+ *   RW_W_GRADY    P:77   w = exp(-beta (g_p - g_q)^2) + eps   (== rw_brick_weights)
+ *   RW_W_POISSON  P:133  w = exp(-1/2 (sqrt(n_p) - sqrt(n_q))^2) + eps, n = raw value *
+ *                        count_scale clipped at 0 (the normalisation nm is not applied)
+ *   RW_W_GAUSSIAN P:127  sigma^2 = mean of (g_p - g_q)^2 over the brick's edges (floored
+ *                        1e-8); w = exp(-(g_p - g_q)^2 / (2 sigma^2)) + eps
+ *   RW_W_TTEST    P:123-125  Welch t of the (2 radius + 1)^3 neighbourhoods of p and q
+ *                        (clipped at the brick border; unbiased variances floored 1e-8);
+ *                        w = erfc(|t| / sqrt 2) + eps (two-tailed normal P-value)
+ *   workspace  device, >= rw_weights_workspace_bytes(batch, d, spec) bytes (0 for GRADY /
+ *              POISSON; batch doubles for GAUSSIAN; 2 fp32 per voxel for TTEST); may be
+ *              NULL when that is 0.  Other arguments as rw_brick_weights.
+ *   Errors: RW_EINVAL for bad kind, eps <= 0, radius < 1 (TTEST), count_scale <= 0
+ *   (POISSON), beta < 0 (GRADY), NULL vol/W, short workspace.
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t kind;        /* RW_W_*                                                         */
+  float beta;          /* GRADY                                                          */
+  float eps;           /* additive floor, all kinds (reading c1)                          */
+  float count_scale;   /* POISSON: counts per raw intensity unit                          */
+  int32_t radius;      /* TTEST: neighbourhood radius (1 = 3^3)                           */
+} rw_weight_spec;
+enum { RW_W_GRADY = 0, RW_W_POISSON = 1, RW_W_GAUSSIAN = 2, RW_W_TTEST = 3 };
+size_t rw_weights_workspace_bytes(int32_t batch, rw_dims d, rw_weight_spec spec);
+rw_status rw_brick_weights_ex(const void* vol, rw_dtype dtype, rw_norm nm, int32_t batch,
+                              rw_dims d, rw_weight_spec spec, float* W, float* dinv,
+                              const uint8_t* fixed, void* workspace, size_t ws_bytes,
+                              void* stream);
+
+/* ------------------------------------------------------------------------------------
  * rw_solve_workspace_bytes -- device workspace needed by rw_solve_bricks /
  * rw_solve_labels for this shape.  weights_given != 0: the caller passes W (the
  * workspace then holds no weight planes).

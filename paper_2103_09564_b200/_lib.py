@@ -21,6 +21,11 @@ class rw_norm(C.Structure):
     _fields_ = [("scale", C.c_float), ("offset", C.c_float)]
 
 
+class rw_weight_spec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("beta", C.c_float), ("eps", C.c_float),
+                ("count_scale", C.c_float), ("radius", C.c_int32)]
+
+
 P, I32, F32, SZ = C.c_void_p, C.c_int32, C.c_float, C.c_size_t
 
 SIGNATURES = {
@@ -28,6 +33,8 @@ SIGNATURES = {
     "rw_version": (C.c_char_p, []),
     "rw_brick_weights": (I32, [P, I32, rw_norm, I32, rw_dims, F32, F32, P, P, P, P]),
     "rw_solve_workspace_bytes": (SZ, [I32, rw_dims, I32, I32]),
+    "rw_weights_workspace_bytes": (SZ, [I32, rw_dims, rw_weight_spec]),
+    "rw_brick_weights_ex": (I32, [P, I32, rw_norm, I32, rw_dims, rw_weight_spec, P, P, P, P, SZ, P]),
     "rw_solve_bricks": (I32, [I32, rw_dims, P, I32, rw_norm, P, P, P, I32, F32, F32, F32, I32,
                               I32, P, P, SZ, P, P, P, P, P, P]),
     "rw_solve_labels_workspace_bytes": (SZ, [I32, rw_dims, I32, I32]),

@@ -12,7 +12,7 @@ import ctypes as C
 
 import torch
 
-from ._lib import lib, check, rw_dims, rw_norm
+from ._lib import lib, check, rw_dims, rw_norm, rw_weight_spec
 
 DTYPES = {torch.uint8: 0, torch.uint16: 1, torch.int16: 2, torch.float32: 3}
 DEFAULT_NORM = {torch.uint8: (1 / 255, 0.0), torch.uint16: (1 / 65535, 0.0),
@@ -104,6 +104,32 @@ def brick_weights(vol, beta=100.0, eps=1e-6, fixed=None, norm=None, want_dinv=Tr
     st = lib().rw_brick_weights(_ptr(vol), DTYPES[vol.dtype], rw_norm(sc, of), B, dims_of(vol),
                                 beta, eps, _ptr(W), _ptr(dinv), _ptr(fixed), _stream(stream, vol.device))
     check(st, "rw_brick_weights")
+    return W, dinv
+
+
+WEIGHT_KINDS = {"grady": 0, "poisson": 1, "gaussian": 2, "ttest": 3}
+
+
+def brick_weights_ex(vol, kind="ttest", beta=100.0, eps=1e-6, count_scale=1.0, radius=1,
+                     fixed=None, norm=None, want_dinv=True, stream=None):
+    """rw_brick_weights_ex: the paper's alternative weights; returns (W, dinv)
+    in the rw_brick_weights layout.  Pass W to solve_bricks(..., W=W)."""
+    _need(vol, "vol")
+    _need(fixed, "fixed", torch.uint8)
+    if vol.dim() == 3:
+        vol = vol.unsqueeze(0)
+    B = vol.shape[0]
+    sc, of = norm or DEFAULT_NORM[vol.dtype]
+    spec = rw_weight_spec(WEIGHT_KINDS[kind], beta, eps, count_scale, radius)
+    d = dims_of(vol)
+    W = torch.empty((3,) + tuple(vol.shape), dtype=torch.float32, device=vol.device)
+    dinv = torch.empty(tuple(vol.shape), dtype=torch.float32, device=vol.device) if want_dinv else None
+    need = lib().rw_weights_workspace_bytes(B, d, spec)
+    ws = alloc_workspace(need, vol.device) if need else None
+    st = lib().rw_brick_weights_ex(_ptr(vol), DTYPES[vol.dtype], rw_norm(sc, of), B, d, spec,
+                                   _ptr(W), _ptr(dinv), _ptr(fixed), _ptr(ws),
+                                   0 if ws is None else ws.numel(), _stream(stream, vol.device))
+    check(st, "rw_brick_weights_ex")
     return W, dinv
 
 

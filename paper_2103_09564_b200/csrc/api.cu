@@ -25,6 +25,9 @@ cudaError_t launch_finalize(const Plan&, const Bufs&, const Ctl&, float*, int*, 
 cudaError_t launch_labels_prep(const uint8_t*, long long, int, uint8_t*, float*, int, cudaStream_t);
 cudaError_t launch_argmax(const float*, long long, int, uint8_t*, int, cudaStream_t);
 int passA_rc(const Plan&);
+size_t weights_ex_workspace(int kind, int B, long long n);
+cudaError_t launch_weights_ex(const void*, int, float, float, int, int, int, int, int, float,
+                              float, int, float*, void*, int, cudaStream_t);
 }  // namespace rw
 
 namespace {
@@ -420,6 +423,42 @@ rw_status rw_brick_weights(const void* vol, rw_dtype dtype, rw_norm nm, int32_t 
   RW_TIMED(RW_K_WEIGHTS, (cudaStream_t)stream, 1,
            rw::launch_weights(vol, dtype, nm.scale, nm.offset, batch, d.nx, d.ny, d.nz, beta, eps,
                               W, dinv, fixed, num_sms(), (cudaStream_t)stream));
+  return RW_OK;
+}
+
+size_t rw_weights_workspace_bytes(int32_t batch, rw_dims d, rw_weight_spec spec) {
+  if (!dims_ok(d) || batch < 1) return 0;
+  return rw::weights_ex_workspace(spec.kind, batch, (long long)d.nx * d.ny * d.nz);
+}
+
+rw_status rw_brick_weights_ex(const void* vol, rw_dtype dtype, rw_norm nm, int32_t batch,
+                              rw_dims d, rw_weight_spec spec, float* W, float* dinv,
+                              const uint8_t* fixed, void* workspace, size_t ws_bytes,
+                              void* stream) {
+  if (spec.kind < RW_W_GRADY || spec.kind > RW_W_TTEST)
+    return fail(RW_EINVAL, "rw_brick_weights_ex: unknown weight kind %d", spec.kind);
+  if (spec.kind == RW_W_GRADY)
+    return rw_brick_weights(vol, dtype, nm, batch, d, spec.beta, spec.eps, W, dinv, fixed, stream);
+  if (!vol || !W) return fail(RW_EINVAL, "rw_brick_weights_ex: vol and W must be non-NULL");
+  if (!dims_ok(d) || batch < 1) return fail(RW_EINVAL, "rw_brick_weights_ex: bad dims/batch");
+  if (dtype < RW_U8 || dtype > RW_F32) return fail(RW_EINVAL, "rw_brick_weights_ex: bad dtype");
+  if (!(spec.eps > 0.f)) return fail(RW_EINVAL, "rw_brick_weights_ex: need eps > 0");
+  if (spec.kind == RW_W_TTEST && spec.radius < 1)
+    return fail(RW_EINVAL, "rw_brick_weights_ex: t-test radius must be >= 1");
+  if (spec.kind == RW_W_POISSON && !(spec.count_scale > 0.f))
+    return fail(RW_EINVAL, "rw_brick_weights_ex: count_scale must be > 0");
+  const size_t need = rw::weights_ex_workspace(spec.kind, batch, (long long)d.nx * d.ny * d.nz);
+  if (need > 0 && (!workspace || ws_bytes < need))
+    return fail(RW_ENOMEM, "rw_brick_weights_ex: workspace too small: %zu < %zu bytes", ws_bytes, need);
+  if (!aligned16(W) || (dinv && !aligned16(dinv)) || (workspace && !aligned16(workspace)))
+    return fail(RW_EINVAL, "rw_brick_weights_ex: pointers must be 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int sms = num_sms();
+  RW_TIMED(RW_K_WEIGHTS, s, 1,
+           rw::launch_weights_ex(vol, dtype, nm.scale, nm.offset, batch, d.nx, d.ny, d.nz,
+                                 spec.kind, spec.eps, spec.count_scale, spec.radius, W,
+                                 workspace, sms, s));
+  if (dinv) RW_TIMED(RW_K_WEIGHTS, s, 1, rw::launch_dinv(W, batch, d.nx, d.ny, d.nz, fixed, dinv, sms, s));
   return RW_OK;
 }
 
