@@ -1,0 +1,215 @@
+"""fp64 oracle of the hierarchical random walker driver (TEST INFRASTRUCTURE; see
+oracle/__init__.py).  SURVEY.md §8(f) row f1.
+
+Citations: P:n = /root/reference/PAPER.md line n (§IV); S:n = SPEC.md line n
+(readings only); readings R22-R28 are restated in DESIGN.md §3.
+
+The procedure, level by level from the root (coarsest LOD level) down to the full
+resolution, written in the paper's order:
+
+  levels    volume D^3 with D = s 2^k: level l has D/2^l voxels per axis, l = k is the root
+            (one brick); intensities per level = the integer 2^3-mean pyramid (P:71,
+            pyramid_oracle).
+  seeds     full-resolution label volume: 0 unseeded, 1 foreground, 2 background (the
+            rasterised T_n(l), reading R22).  At level l a voxel carries the labels of
+            the full-resolution voxels it covers; foreground and background together is a
+            conflict cfl: the voxel is left unseeded.
+  root      Eq. 1: x = rw(n_0, T(l)) on the whole root level, x0 = 0.5.
+  level l   for every active brick n (s^3 at level l): the expanded window N(n) of side
+            s_e = floor(e s) (Eq. 3) with margin ceil((s_e - s)/2) on the low side,
+            shifted inward to stay inside the level (reading R23); seeds L(N(n), l) = the
+            user seeds in the window  U  continuous seeds on the window's faces that are
+            interior to the volume, sampled from the parent level's probability field
+            (sample_border; reading R24; user seeds win); initial guess = the
+            parent field sampled at every window voxel (reading R25); solve; contract
+            N^-1: the central s^3 goes to the level's probability field.
+  parent    field sampling = trilinear interpolation at the child voxel centre (i + 0.5)/2 - 0.5
+            in parent voxel units, clamped at the level border (reading R25).
+  pruning   P:139-161: prunable(n) = (hom(n) or dt(n)) and not cfl(n) with hom = max - min <
+            t_hom, dt = min - 0.5 > t_bin or 0.5 - max > t_bin over the brick's s^3
+            probabilities, cfl = a conflict voxel inside the brick at its level.  Children of
+            prunable bricks are not solved; every level's field starts as the trilinear
+            upsample of the parent field and solved bricks overwrite their s^3, so sampling
+            a pruned region falls back to the nearest solved ancestor (reading R26).
+Solves use rw_oracle.solve_brick (fp64 Jacobi-PCG); the output is the level-0 field.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import pyramid_oracle
+from . import rw_oracle as ro
+
+
+def seed_bits(seeds):
+    """Full-resolution labels -> bits (1 = foreground, 2 = background)."""
+    s = np.asarray(seeds)
+    return ((s == 1).astype(np.uint8) | ((s == 2).astype(np.uint8) << 1))
+
+
+def seed_bit_pyramid(seeds, levels):
+    """Level l bits = OR of the 2^3 children bits of level l-1 (reading R22); level 0 first."""
+    out = [seed_bits(seeds)]
+    for _ in range(levels - 1):
+        b = out[-1]
+        nz, ny, nx = b.shape
+        c = b.reshape(nz // 2, 2, ny // 2, 2, nx // 2, 2)
+        out.append(np.bitwise_or.reduce(np.bitwise_or.reduce(np.bitwise_or.reduce(c, 5), 3), 1))
+    return out
+
+
+def seeds_from_bits(bits):
+    """(fixed, value): a voxel is seeded iff exactly one of fg / bg is present."""
+    fg = (bits & 1) > 0
+    bg = (bits & 2) > 0
+    fixed = fg ^ bg
+    return fixed, np.where(fg & ~bg, 1.0, 0.0)
+
+
+def parent_coord(i):
+    """Parent-voxel coordinate of child voxel centre i (reading R25)."""
+    return (np.asarray(i, np.float64) + 0.5) / 2.0 - 0.5
+
+
+def sample_parent(P, zs, ys, xs):
+    """Trilinear sample of the parent field P at the parent coordinates of child voxel
+    indices (zs, ys, xs) (1-D index arrays per axis, outer product), clamped at the border."""
+    out = np.zeros((len(zs), len(ys), len(xs)))
+    idx, wts = [], []
+    for n, c in zip(P.shape, (zs, ys, xs)):
+        u = np.clip(parent_coord(c), 0.0, n - 1)
+        i0 = np.floor(u).astype(int)
+        i1 = np.minimum(i0 + 1, n - 1)
+        f = u - i0
+        idx.append((i0, i1))
+        wts.append((1.0 - f, f))
+    for a in range(2):
+        for b in range(2):
+            for c in range(2):
+                w = (wts[0][a][:, None, None] * wts[1][b][None, :, None] * wts[2][c][None, None, :])
+                out += w * P[np.ix_(idx[0][a], idx[1][b], idx[2][c])]
+    return out
+
+
+def upsample(P, shape):
+    """Dense trilinear upsample of the parent field onto a level of `shape`."""
+    return sample_parent(P, np.arange(shape[0]), np.arange(shape[1]), np.arange(shape[2]))
+
+
+def window_origin(brick, s, se, D):
+    """Reading R23: low margin ceil((se - s)/2), shifted inward to fit [0, D)."""
+    o = brick * s - int(math.ceil((se - s) / 2))
+    return int(min(max(o, 0), D - se))
+
+
+def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, eps=1e-6,
+                 tol=1e-10, max_iter=100000, scale=1.0 / 65535, offset=0.0, prune=True):
+    """Oracle of rw_hier_segment.  vol/seeds [D, D, D] (z, y, x), D = s 2^k.
+
+    Returns dict(prob [D,D,D] fp64 in [0,1], stats per level: solved / pruned_hom /
+    pruned_dt / conflict counts, fields [level] (level 0 first)).
+    """
+    vol = np.asarray(vol)
+    D = vol.shape[0]
+    assert vol.shape == (D, D, D) and D % s == 0
+    k = int(round(math.log2(D // s)))
+    assert s * 2 ** k == D, "volume side must be s * 2^k"
+    levels = k + 1
+    se = int(math.floor(e * s))
+    vols = [vol] + (pyramid_oracle.pyramid(vol, k) if k > 0 else [])
+    bits = seed_bit_pyramid(seeds, levels)
+    stats = [dict(active=0, solved=0, pruned_hom=0, pruned_dt=0, conflict=0, iters=0)
+             for _ in range(levels)]
+    fields = [None] * levels
+
+    # ---- root (Eq. 1)
+    g = ro.normalise(vols[k], scale, offset)
+    fixed, val = seeds_from_bits(bits[k])
+    o = ro.solve_brick(g, fixed, val, beta, eps, tol, max_iter)
+    fields[k] = np.where(fixed, val, np.clip(o["x"], 0.0, 1.0))
+    stats[k].update(active=1, solved=1, iters=o["iters"])
+    active = {(0, 0, 0)}
+    prunable = {}
+    st = _prune_state((0, 0, 0), fields[k], bits[k], s, t_hom, t_bin, prune)
+    prunable[(0, 0, 0)] = st
+    _count(stats[k], st)
+
+    # ---- levels k-1 .. 0 (Eq. 3 with H_p)
+    for l in range(k - 1, -1, -1):
+        Dl = D >> l
+        nb = Dl // s
+        children = set()
+        for (bz, by, bx) in active:
+            if prunable[(bz, by, bx)] in (None, "cfl"):
+                for cz in range(2):
+                    for cy in range(2):
+                        for cx in range(2):
+                            children.add((2 * bz + cz, 2 * by + cy, 2 * bx + cx))
+        P_par = fields[l + 1]
+        F = upsample(P_par, (Dl, Dl, Dl))
+        gl = ro.normalise(vols[l], scale, offset)
+        fx_l, val_l = seeds_from_bits(bits[l])
+        stats[l]["active"] = len(children)
+        new_prunable = {}
+        for (bz, by, bx) in sorted(children):
+            w0 = [window_origin(c, s, se, Dl) for c in (bz, by, bx)]
+            sl = tuple(slice(a, a + se) for a in w0)
+            zs, ys, xs = (np.arange(a, a + se) for a in w0)
+            samp = sample_parent(P_par, zs, ys, xs)
+            fixed = fx_l[sl].copy()
+            values = np.where(fixed, val_l[sl], 0.0)
+            # continuous border seeds on window faces interior to the volume (user seeds win)
+            shell = np.zeros((se, se, se), bool)
+            for ax in range(3):
+                lo = [slice(None)] * 3
+                hi = [slice(None)] * 3
+                lo[ax] = 0
+                hi[ax] = se - 1
+                if w0[ax] > 0:
+                    shell[tuple(lo)] = True
+                if w0[ax] + se < Dl:
+                    shell[tuple(hi)] = True
+            border = shell & ~fixed
+            values = np.where(border, samp, values)
+            fixed = fixed | border
+            o = ro.solve_brick(gl[sl], fixed, values, beta, eps, tol, max_iter, x0=samp)
+            xw = np.where(fixed, values, np.clip(o["x"], 0.0, 1.0))
+            # contract: the brick's own s^3
+            bo = [bz * s - w0[0], by * s - w0[1], bx * s - w0[2]]
+            xb = xw[bo[0]:bo[0] + s, bo[1]:bo[1] + s, bo[2]:bo[2] + s]
+            F[bz * s:(bz + 1) * s, by * s:(by + 1) * s, bx * s:(bx + 1) * s] = xb
+            stats[l]["solved"] += 1
+            stats[l]["iters"] += o["iters"]
+            stt = _prune_state((bz, by, bx), xb, bits[l], s, t_hom, t_bin, prune)
+            new_prunable[(bz, by, bx)] = stt
+            _count(stats[l], stt)
+        fields[l] = F
+        active = children
+        prunable = new_prunable
+    return dict(prob=fields[0], stats=stats, fields=fields)
+
+
+def _prune_state(b, xb, bits_l, s, t_hom, t_bin, prune):
+    """None (keep refining: children are solved) or 'hom' / 'dt'; a seed
+    conflict inside the brick at its level vetoes pruning ('cfl')."""
+    bz, by, bx = b
+    cb = bits_l[bz * s:(bz + 1) * s, by * s:(by + 1) * s, bx * s:(bx + 1) * s]
+    if not prune or np.any(cb == 3):
+        return "cfl" if np.any(cb == 3) else None
+    mn, mx = float(xb.min()), float(xb.max())
+    if t_hom >= 0 and mx - mn < t_hom:
+        return "hom"
+    if t_bin >= 0 and (mn - 0.5 > t_bin or 0.5 - mx > t_bin):
+        return "dt"
+    return None
+
+
+def _count(stat, st):
+    if st == "hom":
+        stat["pruned_hom"] += 1
+    elif st == "dt":
+        stat["pruned_dt"] += 1
+    elif st == "cfl":
+        stat["conflict"] += 1

@@ -1,0 +1,117 @@
+"""Pins of oracle/hier_oracle.py (the hierarchical driver of P:83-161)
+against closed forms, brute force and the plain random walker it must reduce to."""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import hier_oracle as ho
+from oracle import rw_oracle as ro
+import workloads as wl
+
+
+def small_volume(D, seed, nblob=2):
+    """Seeded u16 volume with blobs + noise and a label volume (1 fg inside the first blob,
+    2 bg near the corners)."""
+    rng = np.random.default_rng([21, seed])
+    z, y, x = np.meshgrid(*(np.arange(D),) * 3, indexing="ij")
+    g = np.full((D, D, D), 0.2)
+    cs = []
+    for _ in range(nblob):
+        c = rng.uniform(0.3, 0.7, 3) * D
+        r = rng.uniform(0.15, 0.25) * D
+        g[(z - c[0]) ** 2 + (y - c[1]) ** 2 + (x - c[2]) ** 2 < r * r] = 0.8
+        cs.append(c)
+    g = np.clip(g + rng.normal(0, 0.03, g.shape), 0, 1)
+    vol = np.rint(g * 65535).astype(np.uint16)
+    seeds = np.zeros((D, D, D), np.uint8)
+    c = np.round(cs[0]).astype(int)
+    seeds[c[0], c[1], c[2]] = 1
+    seeds[c[0], c[1], min(c[2] + 1, D - 1)] = 1
+    seeds[1, 1, 1] = seeds[D - 2, D - 2, D - 2] = seeds[1, D - 2, 1] = 2
+    return vol, seeds
+
+
+def test_single_level_is_the_plain_random_walker():
+    """Eq. 1: D = s -> the root solve of the whole volume."""
+    vol, seeds = small_volume(16, 0)
+    o = ho.hier_segment(vol, seeds, s=16, e=1.25, beta=50.0)
+    g = ro.normalise(vol, 1 / 65535, 0.0)
+    fixed, val = ho.seeds_from_bits(ho.seed_bits(seeds))
+    ref = ro.solve_brick(g, fixed, val, 50.0, 1e-6)
+    np.testing.assert_allclose(o["prob"], np.where(fixed, val, np.clip(ref["x"], 0, 1)), atol=1e-12)
+
+
+def test_whole_level_window_reduces_to_plain_solve():
+    """e = 2, D = 2s: the level-0 window is the whole level (no interior faces, so no border
+    seeds) -> the unique plain random walker solution, whatever the initial guess."""
+    vol, seeds = small_volume(16, 1)
+    o = ho.hier_segment(vol, seeds, s=8, e=2.0, beta=50.0, prune=False)
+    g = ro.normalise(vol, 1 / 65535, 0.0)
+    fixed, val = ho.seeds_from_bits(ho.seed_bits(seeds))
+    ref = ro.solve_brick(g, fixed, val, 50.0, 1e-6)
+    np.testing.assert_allclose(o["prob"], np.where(fixed, val, np.clip(ref["x"], 0, 1)), atol=1e-8)
+
+
+def test_trilinear_sampling_closed_forms():
+    """constant -> constant; linear ramp -> the same ramp at interior child
+    voxel centres; 2^3 one-hot parent -> hand-evaluated weights."""
+    P = np.full((4, 4, 4), 0.9)
+    assert np.allclose(ho.upsample(P, (8, 8, 8)), 0.9)
+    px = np.arange(4, dtype=float)
+    R = np.broadcast_to(0.1 * px, (4, 4, 4))
+    U = ho.upsample(R, (8, 8, 8))
+    for i in range(1, 7):                      # interior: child centre (i+0.5)/2 - 0.5
+        assert U[3, 3, i] == pytest.approx(0.1 * ((i + 0.5) / 2 - 0.5))
+    C = np.zeros((2, 2, 2))
+    C[0, 0, 0] = 1.0
+    U = ho.upsample(C, (4, 4, 4))
+    f = {0: 1.0, 1: 0.75, 2: 0.25, 3: 0.0}     # weight of parent 0 at child i (clamped)
+    for z, y, x in itertools.product(range(4), repeat=3):
+        assert U[z, y, x] == pytest.approx(f[z] * f[y] * f[x])
+
+
+def test_seed_pyramid_conflicts_brute_force():
+    rng = np.random.default_rng(3)
+    seeds = rng.choice([0, 0, 0, 1, 2], size=(8, 8, 8)).astype(np.uint8)
+    pyr = ho.seed_bit_pyramid(seeds, 3)
+    for l, b in enumerate(pyr):
+        n = 8 >> l
+        for z, y, x in itertools.product(range(n), repeat=3):
+            blk = seeds[z << l:(z + 1) << l, y << l:(y + 1) << l, x << l:(x + 1) << l]
+            want = (1 if (blk == 1).any() else 0) | (2 if (blk == 2).any() else 0)
+            assert b[z, y, x] == want
+    fixed, val = ho.seeds_from_bits(np.array([0, 1, 2, 3], np.uint8))
+    assert fixed.tolist() == [False, True, True, False] and val.tolist() == [0, 1, 0, 0]
+
+
+def test_window_origin():
+    """Reading R23: margin ceil((se-s)/2) low side, shifted inside, always covering the brick."""
+    s, se = 32, 40
+    assert ho.window_origin(3, s, se, 256) == 3 * 32 - 4
+    assert ho.window_origin(0, s, se, 256) == 0
+    assert ho.window_origin(7, s, se, 256) == 256 - 40
+    for D in (64, 128):
+        for b in range(D // s):
+            o = ho.window_origin(b, s, se, D)
+            assert 0 <= o <= b * s and b * s + s <= o + se <= D
+
+
+def test_constant_parent_gives_constant_children():
+    """All seeds foreground -> the root field is 1 and every border seed and solution is 1."""
+    vol, seeds = small_volume(32, 2)
+    seeds[seeds > 0] = 1
+    o = ho.hier_segment(vol, seeds, s=8, e=1.25, beta=50.0, prune=False)
+    assert np.allclose(o["prob"], 1.0, atol=1e-8)
+
+
+def test_pruning_soundness_against_unpruned():
+    """P:139-161 / S:321: pruned_dt regions threshold like the unpruned run, pruned_hom
+    regions stay within t_hom (+ interpolation slack) of it; pruning solves fewer bricks."""
+    vol, seeds = small_volume(32, 4)
+    full = ho.hier_segment(vol, seeds, s=8, e=1.25, beta=50.0, tol=1e-8, prune=False)
+    pr = ho.hier_segment(vol, seeds, s=8, e=1.25, beta=50.0, tol=1e-8, prune=True)
+    assert sum(st["solved"] for st in pr["stats"]) < sum(st["solved"] for st in full["stats"])
+    assert np.abs(pr["prob"] - full["prob"]).max() < 0.3 + 0.05
+    agree = ((pr["prob"] > 0.5) == (full["prob"] > 0.5)).mean()
+    assert agree > 0.99
