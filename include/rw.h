@@ -198,6 +198,48 @@ rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int
                                 void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * rw_hier_segment -- the hierarchical random walker (Eq. 1-4,
+ *   H_p pruning).  Readings R22-R26.  Input: a cubic volume of side
+ *   D = s 2^k ("we assume a cubical volume size that is a power of two and a
+ *   multiple of s") and rasterised labels at full resolution (0 unseeded, 1 foreground,
+ *   2 background).  The LOD pyramid (rw_build_pyramid) gives levels 0..k (k = root, one
+ *   brick).  The root is solved whole (Eq. 1); then, level by level, every brick whose
+ *   parent was not prunable is expanded to a window of side s_e = floor(e s) (Eq. 3),
+ *   seeded with its user seeds plus continuous seeds sampled (trilinear) from the parent
+ *   level's probability field on window faces interior to the volume (Eq. 2), initialised
+ *   from that field, and all such windows of a level are solved as one batch with
+ *   rw_solve_bricks (resident solver when s_e is 32 or 64).  The brick's s^3 of each
+ *   window solution goes into the level's field; prunable = (hom: max-min < t_hom or
+ *   dt: min-0.5 > t_bin or 0.5-max > t_bin) and no seed conflict in the brick;
+ *   children of prunable bricks keep the upsampled parent field.
+ *   vol      device [D][D][D] of dtype;  seeds  device u8 [D][D][D].
+ *   prob     out device fp32 [D][D][D]: the full-resolution foreground probability.
+ *   stats    out host (nullable): per level (index = level, 0 = full resolution)
+ *            active / solved / pruned_hom / pruned_dt / conflict brick counts, CG iterations.
+ *   workspace  device, >= rw_hier_workspace_bytes(d, dtype, cfg).
+ *   The call blocks the host (brick lists are built on the host between levels).
+ *   Errors: RW_EINVAL for a non-cubic volume, D != s 2^k, s % 4 != 0, s_e % 4 != 0,
+ *   e not in (1, 2], other bad arguments as rw_solve_bricks.
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t s;            /* brick side, level voxels (P:105 suggests 32)                   */
+  float e;              /* expansion factor in (1, 2] (P:119 suggests 1.25)               */
+  float t_hom, t_bin;   /* pruning thresholds (P:143 0.3, P:149 0.01); < 0 disables one  */
+  int32_t prune;        /* 0: solve every brick (plain H), 1: H_p                         */
+  float beta, eps, tol; /* Grady weight and solver settings (as rw_solve_bricks)          */
+  int32_t max_iter, tol_mode;
+  int32_t max_batch;    /* windows per rw_solve_bricks call (workspace size)             */
+} rw_hier_config;
+typedef struct {
+  int32_t levels;
+  int64_t active[16], solved[16], pruned_hom[16], pruned_dt[16], conflict[16], iters[16];
+} rw_hier_stats;
+size_t rw_hier_workspace_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg);
+rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d,
+                          const uint8_t* seeds, rw_hier_config cfg, void* workspace,
+                          size_t ws_bytes, float* prob, rw_hier_stats* stats, void* stream);
+
+/* ------------------------------------------------------------------------------------
  * Solver selection.  rw_solve_bricks / rw_solve_labels run one of two implementations of
  * the same Jacobi-PCG with the same stopping rule, status codes and outputs:
  *   streaming  -- CG state in HBM, two fused passes per iteration (any brick shape, any
@@ -245,7 +287,7 @@ void rw_queue_destroy(rw_queue* q);
  *   launches  out host int64[RW_K_COUNT] or NULL;  ms  out host double[RW_K_COUNT] or NULL.
  * ---------------------------------------------------------------------------------- */
 enum { RW_K_WEIGHTS = 0, RW_K_SETUP = 1, RW_K_PASSA = 2, RW_K_PASSB = 3, RW_K_FINALIZE = 4,
-       RW_K_PYRAMID = 5, RW_K_OTHER = 6, RW_K_RESIDENT = 7, RW_K_COUNT = 8 };
+       RW_K_PYRAMID = 5, RW_K_OTHER = 6, RW_K_RESIDENT = 7, RW_K_HIER = 8, RW_K_COUNT = 9 };
 rw_status rw_profile_enable(int32_t on);
 rw_status rw_profile_read(int64_t* launches, double* ms);
 

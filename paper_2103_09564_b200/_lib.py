@@ -26,6 +26,18 @@ class rw_weight_spec(C.Structure):
                 ("count_scale", C.c_float), ("radius", C.c_int32)]
 
 
+class rw_hier_config(C.Structure):
+    _fields_ = [("s", C.c_int32), ("e", C.c_float), ("t_hom", C.c_float), ("t_bin", C.c_float),
+                ("prune", C.c_int32), ("beta", C.c_float), ("eps", C.c_float), ("tol", C.c_float),
+                ("max_iter", C.c_int32), ("tol_mode", C.c_int32), ("max_batch", C.c_int32)]
+
+
+class rw_hier_stats(C.Structure):
+    _fields_ = [("levels", C.c_int32)] + [(f, C.c_int64 * 16) for f in
+                                          ("active", "solved", "pruned_hom", "pruned_dt",
+                                           "conflict", "iters")]
+
+
 P, I32, F32, SZ = C.c_void_p, C.c_int32, C.c_float, C.c_size_t
 
 SIGNATURES = {
@@ -50,12 +62,15 @@ SIGNATURES = {
     "rw_profile_enable": (I32, [I32]),
     "rw_profile_read": (I32, [P, P]),
     "rw_set_option": (I32, [I32, C.c_int64]),
+    "rw_hier_workspace_bytes": (SZ, [rw_dims, I32, rw_hier_config]),
+    "rw_hier_segment": (I32, [P, I32, rw_norm, rw_dims, P, rw_hier_config, P, SZ, P,
+                              C.POINTER(rw_hier_stats), P]),
     "rw_get_option": (C.c_int64, [I32]),
     "rw_resident_available": (I32, [rw_dims, I32]),
 }
 
 KERNEL_CLASSES = ["weights", "setup", "passA", "passB", "finalize", "pyramid", "other",
-                  "resident"]
+                  "resident", "hier"]
 
 
 def header_symbols(path: str = HEADER):

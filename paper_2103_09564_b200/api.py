@@ -12,7 +12,7 @@ import ctypes as C
 
 import torch
 
-from ._lib import lib, check, rw_dims, rw_norm, rw_weight_spec
+from ._lib import lib, check, rw_dims, rw_norm, rw_weight_spec, rw_hier_config, rw_hier_stats
 
 DTYPES = {torch.uint8: 0, torch.uint16: 1, torch.int16: 2, torch.float32: 3}
 DEFAULT_NORM = {torch.uint8: (1 / 255, 0.0), torch.uint16: (1 / 65535, 0.0),
@@ -143,15 +143,28 @@ def solve_bricks(fixed, values, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6
     device iteration loop has been fully enqueued/finished (see rw.h).
     """
     _need(fixed, "fixed", torch.uint8)
-    if values.dim() == 4:
+    if fixed.dim() == 3:                       # a single brick
+        fixed = fixed.unsqueeze(0)
+    if vol is not None and vol.dim() == 3:
+        vol = vol.unsqueeze(0)
+    while values.dim() < 5:
         values = values.unsqueeze(0)
-    if x0 is not None and x0.dim() == 4:
+    while x0 is not None and x0.dim() < 5:
         x0 = x0.unsqueeze(0)
     _need(values, "values", torch.float32)
     _need(x0, "x0", torch.float32)
     _need(vol, "vol")
     _need(W, "W", torch.float32)
     R, B = values.shape[0], values.shape[1]
+    if fixed.dim() != 4 or tuple(values.shape[1:]) != tuple(fixed.shape):
+        raise ValueError(f"fixed {tuple(fixed.shape)} must be [B,nz,ny,nx] and values "
+                         f"{tuple(values.shape)} [nrhs,B,nz,ny,nx]")
+    if vol is not None and tuple(vol.shape) != tuple(fixed.shape):
+        raise ValueError(f"vol {tuple(vol.shape)} must match fixed {tuple(fixed.shape)}")
+    if W is not None and tuple(W.shape) != (3,) + tuple(fixed.shape):
+        raise ValueError(f"W {tuple(W.shape)} must be [3,B,nz,ny,nx]")
+    if x0 is not None and tuple(x0.shape) != tuple(values.shape):
+        raise ValueError(f"x0 {tuple(x0.shape)} must match values {tuple(values.shape)}")
     d = dims_of(fixed)
     dev = fixed.device
     dt = DTYPES[vol.dtype] if vol is not None else 3
@@ -199,6 +212,35 @@ def solve_labels(seeds, K, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6, max
                                _ptr(labels), _stream(stream, dev))
     check(st, "rw_solve_labels")
     return dict(prob=prob, labels=labels, iters=iters, resid=resid)
+
+
+def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True, beta=100.0,
+                 eps=1e-6, tol=1e-6, max_iter=5000, tol_mode=0, norm=None, max_batch=1024,
+                 workspace=None, stream=None):
+    """rw_hier_segment: vol [D,D,D], seeds u8 [D,D,D] (0 / 1 fg / 2 bg), D = s 2^k.
+    Returns (prob fp32 [D,D,D], stats dict of per-level lists, level 0 = full resolution)."""
+    _need(vol, "vol")
+    _need(seeds, "seeds", torch.uint8)
+    nz, ny, nx = vol.shape
+    d = rw_dims(nx, ny, nz)
+    sc, of = norm or DEFAULT_NORM[vol.dtype]
+    cfg = rw_hier_config(s, e, t_hom, t_bin, int(prune), beta, eps, tol, max_iter, tol_mode, max_batch)
+    need = lib().rw_hier_workspace_bytes(d, DTYPES[vol.dtype], cfg)
+    if need == 0:
+        raise ValueError("hier_segment: need a cubic volume of side s*2^k, s % 4 == 0, "
+                         "e in (1, 2] with floor(e*s) % 4 == 0")
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need, vol.device)
+    prob = torch.empty(tuple(vol.shape), dtype=torch.float32, device=vol.device)
+    st = rw_hier_stats()
+    check(lib().rw_hier_segment(_ptr(vol), DTYPES[vol.dtype], rw_norm(sc, of), d, _ptr(seeds), cfg,
+                                _ptr(workspace), workspace.numel(), _ptr(prob), C.byref(st),
+                                _stream(stream, vol.device)), "rw_hier_segment")
+    L = st.levels
+    stats = {f: [int(getattr(st, f)[l]) for l in range(L)]
+             for f in ("active", "solved", "pruned_hom", "pruned_dt", "conflict", "iters")}
+    stats["levels"] = L
+    return prob, stats
 
 
 def level_dims(dims, levels):

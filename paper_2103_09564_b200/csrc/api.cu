@@ -1,7 +1,9 @@
 // api.cu -- the C ABI of include/rw.h: validation, workspace carving, launch orchestration.
 #include <cstdarg>
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -26,6 +28,14 @@ cudaError_t launch_labels_prep(const uint8_t*, long long, int, uint8_t*, float*,
 cudaError_t launch_argmax(const float*, long long, int, uint8_t*, int, cudaStream_t);
 int passA_rc(const Plan&);
 size_t weights_ex_workspace(int kind, int B, long long n);
+cudaError_t launch_seed_bits(const uint8_t*, long long, uint8_t*, int, cudaStream_t);
+cudaError_t launch_seed_or(const uint8_t*, int, uint8_t*, int, cudaStream_t);
+cudaError_t launch_upsample(const float*, int, float*, int, int, cudaStream_t);
+cudaError_t launch_gather(const void*, int, const uint8_t*, const float*, int, int, const int4*,
+                          int, void*, uint8_t*, float*, float*, int, cudaStream_t);
+cudaError_t launch_contract(const float*, int, const int4*, const int4*, int, int, int,
+                            const uint8_t*, float*, float, float, int, int*, float2*,
+                            cudaStream_t);
 cudaError_t launch_weights_ex(const void*, int, float, float, int, int, int, int, int, float,
                               float, int, float*, void*, int, cudaStream_t);
 }  // namespace rw
@@ -542,6 +552,211 @@ rw_status rw_solve_labels(int32_t batch, rw_dims d, const void* vol, rw_dtype dt
 }
 
 static size_t dtype_size(rw_dtype t) { return t == RW_U8 ? 1 : (t == RW_F32 ? 4 : 2); }
+
+// ------------------------------------------------------------------ hierarchical driver
+namespace {
+
+struct HierGeo {
+  int D, s, se, k, Bc;
+  size_t es;
+};
+
+bool hier_geo(rw_dims d, rw_dtype dt, const rw_hier_config& c, HierGeo* g) {
+  if (d.nx != d.ny || d.ny != d.nz || d.nx < 4) return false;
+  if (c.s < 4 || c.s % 4 != 0 || d.nx % c.s != 0) return false;
+  int q = d.nx / c.s, k = 0;
+  while (q > 1 && q % 2 == 0) { q /= 2; ++k; }
+  if (q != 1 || k > 15) return false;
+  if (!(c.e > 1.f && c.e <= 2.f)) return false;
+  const int se = (int)std::floor((double)c.e * c.s);
+  if (se % 4 != 0 || se <= c.s) return false;
+  g->D = d.nx; g->s = c.s; g->se = se; g->k = k;
+  g->Bc = c.max_batch > 0 ? c.max_batch : 1024;
+  g->es = dtype_size(dt);
+  return true;
+}
+
+struct HierLayout {
+  size_t volp[16], bits[17], probp[16], org, brick, state, range, iters, status, wvol, wfixed,
+      wval, wx0, wprob, solve, total;
+};
+
+HierLayout hier_layout(const HierGeo& g) {
+  HierLayout L{};
+  size_t o = 0;
+  for (int l = 1; l <= g.k; ++l) {
+    const size_t n = (size_t)(g.D >> l) * (g.D >> l) * (g.D >> l);
+    L.volp[l] = o; o += up(n * g.es);
+  }
+  for (int l = 0; l <= g.k; ++l) {
+    const size_t n = (size_t)(g.D >> l) * (g.D >> l) * (g.D >> l);
+    L.bits[l] = o; o += up(n);
+  }
+  for (int l = 1; l <= g.k; ++l) {
+    const size_t n = (size_t)(g.D >> l) * (g.D >> l) * (g.D >> l);
+    L.probp[l] = o; o += up(n * 4);
+  }
+  const size_t B = (size_t)g.Bc, nw = (size_t)g.se * g.se * g.se;
+  const size_t nmax = std::max(nw, (size_t)g.s * g.s * g.s);
+  L.org = o; o += up(B * 16);
+  L.brick = o; o += up(B * 16);
+  L.state = o; o += up(B * 4);
+  L.range = o; o += up(B * 8);
+  L.iters = o; o += up(B * 4);
+  L.status = o; o += up(B * 4);
+  L.wvol = o; o += up(B * nmax * g.es);
+  L.wfixed = o; o += up(B * nmax);
+  L.wval = o; o += up(B * nmax * 4);
+  L.wx0 = o; o += up(B * nmax * 4);
+  L.wprob = o; o += up(B * nmax * 4);
+  const rw_dims dw{g.se, g.se, g.se}, dr{g.s, g.s, g.s};
+  const size_t sw = layout(make_plan((int)B, dw, 1), false, 0).total;
+  const size_t sr = layout(make_plan(1, dr, 1), false, 0).total;
+  L.solve = o; o += up(std::max(sw, sr));
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+
+size_t rw_hier_workspace_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg) {
+  HierGeo g;
+  if (dtype < RW_U8 || dtype > RW_F32 || !hier_geo(d, dtype, cfg, &g)) return 0;
+  return hier_layout(g).total;
+}
+
+rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d,
+                          const uint8_t* seeds, rw_hier_config cfg, void* workspace,
+                          size_t ws_bytes, float* prob, rw_hier_stats* stats, void* stream) {
+  HierGeo g;
+  if (!vol || !seeds || !prob || !workspace)
+    return fail(RW_EINVAL, "rw_hier_segment: vol, seeds, prob and workspace must be non-NULL");
+  if (dtype < RW_U8 || dtype > RW_F32) return fail(RW_EINVAL, "rw_hier_segment: bad dtype");
+  if (!hier_geo(d, dtype, cfg, &g))
+    return fail(RW_EINVAL, "rw_hier_segment: need a cubic volume of side s*2^k, s %% 4 == 0, "
+                "e in (1, 2] with floor(e s) %% 4 == 0");
+  rw_status v = validate_solve(1, rw_dims{g.se, g.se, g.se}, vol, dtype, nullptr, 1, cfg.eps,
+                               cfg.tol, cfg.max_iter, cfg.tol_mode, workspace);
+  if (v != RW_OK) return v;
+  const HierLayout L = hier_layout(g);
+  if (ws_bytes < L.total)
+    return fail(RW_ENOMEM, "rw_hier_segment: workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  const int sms = num_sms();
+  auto PTR = [&](size_t off) { return (void*)(ws + off); };
+  rw_hier_stats st{};
+  st.levels = g.k + 1;
+
+  // ---- LOD pyramid of the intensities and of the seed bits (R22)
+  const long long N0 = (long long)g.D * g.D * g.D;
+  const void* vlev[16];
+  vlev[0] = vol;
+  if (g.k > 0) {
+    void* outs[16];
+    for (int l = 1; l <= g.k; ++l) outs[l - 1] = PTR(L.volp[l]);
+    rw_status ps = rw_build_pyramid(vol, dtype, d, g.k, outs, stream);
+    if (ps != RW_OK) return ps;
+    for (int l = 1; l <= g.k; ++l) vlev[l] = outs[l - 1];
+  }
+  uint8_t* bits[17];
+  for (int l = 0; l <= g.k; ++l) bits[l] = (uint8_t*)PTR(L.bits[l]);
+  RW_TIMED(RW_K_HIER, s, 1, rw::launch_seed_bits(seeds, N0, bits[0], sms, s));
+  for (int l = 0; l < g.k; ++l)
+    RW_TIMED(RW_K_HIER, s, 1, rw::launch_seed_or(bits[l], g.D >> l, bits[l + 1], sms, s));
+  float* field[17];
+  field[0] = prob;
+  for (int l = 1; l <= g.k; ++l) field[l] = (float*)PTR(L.probp[l]);
+
+  int4* d_org = (int4*)PTR(L.org);
+  int4* d_brick = (int4*)PTR(L.brick);
+  int* d_state = (int*)PTR(L.state);
+  float2* d_range = (float2*)PTR(L.range);
+  int* d_iters = (int*)PTR(L.iters);
+  int* d_status = (int*)PTR(L.status);
+  void* wvol = PTR(L.wvol);
+  uint8_t* wfixed = (uint8_t*)PTR(L.wfixed);
+  float* wval = (float*)PTR(L.wval);
+  float* wx0 = (float*)PTR(L.wx0);
+  float* wprob = (float*)PTR(L.wprob);
+  char* sws = ws + L.solve;
+
+  // solve a chunk of nb windows of side w at level l (x0 from the parent field unless root)
+  std::vector<int> h_state, h_iters;
+  auto solve_chunk = [&](int l, int w, const std::vector<int4>& org, const std::vector<int4>& br,
+                         size_t first, int nb, bool root) -> rw_status {
+    RW_CK(cudaMemcpyAsync(d_org, org.data() + first, nb * sizeof(int4), cudaMemcpyHostToDevice, s));
+    RW_CK(cudaMemcpyAsync(d_brick, br.data() + first, nb * sizeof(int4), cudaMemcpyHostToDevice, s));
+    const int Dl = g.D >> l;
+    RW_TIMED(RW_K_HIER, s, 1,
+             rw::launch_gather(vlev[l], dtype, bits[l], root ? nullptr : field[l + 1], Dl, w,
+                               d_org, nb, wvol, wfixed, wval, wx0, sms, s));
+    const rw_dims dw{w, w, w};
+    const rw::Plan P = make_plan(nb, dw, 1);
+    const Layout Lw = layout(P, false, 0);
+    rw_status r = solve_core(nb, dw, wvol, dtype, nm, nullptr, wfixed, wval, 1, cfg.beta, cfg.eps,
+                             cfg.tol, cfg.max_iter, cfg.tol_mode, root ? nullptr : wx0, sws, Lw,
+                             P, wprob, d_iters, nullptr, d_status, nullptr, s);
+    if (r != RW_OK) return r;
+    RW_TIMED(RW_K_HIER, s, 1,
+             rw::launch_contract(wprob, w, d_org, d_brick, nb, g.s, Dl, bits[l], field[l],
+                                 cfg.t_hom, cfg.t_bin, cfg.prune, d_state, d_range, s));
+    h_state.resize(first + nb);
+    h_iters.resize(first + nb);
+    RW_CK(cudaMemcpyAsync(h_state.data() + first, d_state, nb * sizeof(int), cudaMemcpyDeviceToHost, s));
+    RW_CK(cudaMemcpyAsync(h_iters.data() + first, d_iters, nb * sizeof(int), cudaMemcpyDeviceToHost, s));
+    RW_CK(cudaStreamSynchronize(s));
+    return RW_OK;
+  };
+  auto tally = [&](int l, size_t nb) {
+    st.active[l] = (int64_t)nb;
+    st.solved[l] = (int64_t)nb;
+    for (size_t i = 0; i < nb; ++i) {
+      st.iters[l] += h_iters[i];
+      st.pruned_hom[l] += h_state[i] == 1;
+      st.pruned_dt[l] += h_state[i] == 2;
+      st.conflict[l] += h_state[i] == 3;
+    }
+  };
+
+  // ---- root (Eq. 1): the whole coarsest level, x0 = 0.5
+  std::vector<int4> active{make_int4(0, 0, 0, 0)};
+  {
+    std::vector<int4> org{make_int4(0, 0, 0, 0)};
+    h_state.clear();
+    rw_status r = solve_chunk(g.k, g.s, org, active, 0, 1, true);
+    if (r != RW_OK) return r;
+    tally(g.k, 1);
+  }
+  // ---- levels k-1 .. 0 (Eq. 3, H_p)
+  const int lo = (int)std::ceil((g.se - g.s) / 2.0);
+  for (int l = g.k - 1; l >= 0; --l) {
+    const int Dl = g.D >> l;
+    std::vector<int4> kids;
+    for (size_t i = 0; i < active.size(); ++i) {
+      if (h_state[i] == 1 || h_state[i] == 2) continue;     // prunable: children keep the
+      const int4 b = active[i];                              // upsampled parent field
+      for (int c = 0; c < 8; ++c)
+        kids.push_back(make_int4(2 * b.x + (c & 1), 2 * b.y + ((c >> 1) & 1), 2 * b.z + (c >> 2), 0));
+    }
+    RW_TIMED(RW_K_HIER, s, 1, rw::launch_upsample(field[l + 1], Dl / 2, field[l], Dl, sms, s));
+    std::vector<int4> org(kids.size());
+    auto place = [&](int b) { return std::min(std::max(b * g.s - lo, 0), Dl - g.se); };
+    for (size_t i = 0; i < kids.size(); ++i)
+      org[i] = make_int4(place(kids[i].x), place(kids[i].y), place(kids[i].z), 0);
+    h_state.clear();
+    h_iters.clear();
+    for (size_t f = 0; f < kids.size(); f += g.Bc) {
+      const int nb = (int)std::min((size_t)g.Bc, kids.size() - f);
+      rw_status r = solve_chunk(l, g.se, org, kids, f, nb, false);
+      if (r != RW_OK) return r;
+    }
+    tally(l, kids.size());
+    active.swap(kids);
+  }
+  if (stats) *stats = st;
+  return RW_OK;
+}
 
 rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int32_t z0,
                                 int32_t nzs, int32_t levels, void* const* level_out,

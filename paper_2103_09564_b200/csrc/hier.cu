@@ -1,0 +1,212 @@
+// hier.cu -- SURVEY §8(f) row f1: device kernels of the hierarchical driver.
+// The orchestration (levels, brick lists, batched solves) is rw_hier_segment in api.cu.
+//
+//   k_seed_bits / k_seed_or   rasterised labels -> per-level fg/bg bits (OR over the 2^3
+//                             children; fg+bg = conflict; reading R22)
+//   k_upsample                dense trilinear upsample of the parent level's probability
+//                             field (reading R25): the starting field of every level, so
+//                             pruned regions inherit their nearest solved ancestor (R26)
+//   k_gather                  one expanded window N(n) per active brick (Eq. 3, reading R23):
+//                             intensities, user seeds, continuous border seeds sampled from the
+//                             parent field on window faces interior to the volume (R24),
+//                             initial guess = parent field
+//   k_contract                N^-1: the brick's s^3 of the window solution into the level
+//                             field + min / max / conflict -> prunable
+#include "rw_common.cuh"
+
+namespace rw {
+
+namespace hier {
+
+// parent-voxel coordinate of child voxel centre i, clamped: u = (i + 0.5)/2 - 0.5
+__device__ __forceinline__ void pcoord(int i, int np, int& i0, int& i1, float& f) {
+  float u = fminf(fmaxf(0.5f * (float)i - 0.25f, 0.f), (float)(np - 1));
+  i0 = (int)floorf(u);
+  i1 = min(i0 + 1, np - 1);
+  f = u - (float)i0;
+}
+
+// trilinear sample of the parent field P (np^3) at child voxel (z, y, x)
+__device__ __forceinline__ float sample(const float* __restrict__ P, int np, int z, int y, int x) {
+  int z0, z1, y0, y1, x0, x1;
+  float fz, fy, fx;
+  pcoord(z, np, z0, z1, fz);
+  pcoord(y, np, y0, y1, fy);
+  pcoord(x, np, x0, x1, fx);
+  const long long pl = (long long)np * np;
+  auto at = [&](int a, int b, int c) { return P[(long long)a * pl + (long long)b * np + c]; };
+  const float c00 = __fmaf_rn(fx, at(z0, y0, x1), (1.f - fx) * at(z0, y0, x0));
+  const float c01 = __fmaf_rn(fx, at(z0, y1, x1), (1.f - fx) * at(z0, y1, x0));
+  const float c10 = __fmaf_rn(fx, at(z1, y0, x1), (1.f - fx) * at(z1, y0, x0));
+  const float c11 = __fmaf_rn(fx, at(z1, y1, x1), (1.f - fx) * at(z1, y1, x0));
+  const float c0 = __fmaf_rn(fy, c01, (1.f - fy) * c00);
+  const float c1 = __fmaf_rn(fy, c11, (1.f - fy) * c10);
+  return __fmaf_rn(fz, c1, (1.f - fz) * c0);
+}
+
+}  // namespace hier
+
+__global__ void k_seed_bits(const uint8_t* __restrict__ seeds, long long n, uint8_t* __restrict__ bits) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint8_t s = seeds[i];
+    bits[i] = (s == 1 ? 1 : 0) | (s == 2 ? 2 : 0);
+  }
+}
+
+// level l (D^3) -> level l+1 ((D/2)^3): OR of the 2^3 children
+__global__ void k_seed_or(const uint8_t* __restrict__ in, int D, uint8_t* __restrict__ out) {
+  const int h = D / 2;
+  const long long n = (long long)h * h * h;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % h), y = (int)((i / h) % h), z = (int)(i / ((long long)h * h));
+    uint8_t b = 0;
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx)
+          b |= in[((long long)(2 * z + dz) * D + (2 * y + dy)) * D + (2 * x + dx)];
+    out[i] = b;
+  }
+}
+
+__global__ void k_upsample(const float* __restrict__ P, int np, float* __restrict__ out, int D) {
+  const long long n = (long long)D * D * D;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % D), y = (int)((i / D) % D), z = (int)(i / ((long long)D * D));
+    out[i] = hier::sample(P, np, z, y, x);
+  }
+}
+
+// Window w of active brick list entry j: origin org[j] (level voxels), side se.
+template <typename T>
+__global__ void k_gather(const T* __restrict__ vol, const uint8_t* __restrict__ bits,
+                         const float* __restrict__ Ppar, int D, int se, const int4* __restrict__ org,
+                         int nb, T* __restrict__ wvol, uint8_t* __restrict__ fixed,
+                         float* __restrict__ values, float* __restrict__ x0) {
+  const long long nw = (long long)se * se * se;
+  const long long tot = nw * nb;
+  const int np = D / 2;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / nw);
+    const long long w = i % nw;
+    const int lx = (int)(w % se), ly = (int)((w / se) % se), lz = (int)(w / ((long long)se * se));
+    const int4 o = org[j];
+    const int x = o.x + lx, y = o.y + ly, z = o.z + lz;
+    const long long g = ((long long)z * D + y) * D + x;
+    wvol[i] = vol[g];
+    const uint8_t b = bits[g];
+    bool fx = (b == 1 || b == 2);                       // exactly one of fg / bg (R22)
+    float v = b == 1 ? 1.f : 0.f;
+    const float ps = Ppar ? hier::sample(Ppar, np, z, y, x) : 0.5f;   // root: x0 = 0.5
+    if (!fx) {
+      // continuous border seed on window faces interior to the volume (R24)
+      const bool shell = (lx == 0 && o.x > 0) || (lx == se - 1 && o.x + se < D) ||
+                         (ly == 0 && o.y > 0) || (ly == se - 1 && o.y + se < D) ||
+                         (lz == 0 && o.z > 0) || (lz == se - 1 && o.z + se < D);
+      if (shell) {
+        fx = true;
+        v = ps;
+      }
+    }
+    fixed[i] = fx ? 1 : 0;
+    values[i] = fx ? v : 0.f;
+    x0[i] = ps;
+  }
+}
+
+// One CTA per brick: copy the brick's s^3 of the window solution into the level field and
+// decide prunable.  state: 0 keep (refine children), 1 hom, 2 dt, 3 conflict.
+__global__ void __launch_bounds__(256)
+k_contract(const float* __restrict__ wprob, int se, const int4* __restrict__ org,
+           const int4* __restrict__ brick, int s, int D, const uint8_t* __restrict__ bits,
+           float* __restrict__ P, float t_hom, float t_bin, int prune, int* __restrict__ state,
+           float2* __restrict__ range) {
+  __shared__ float smn[8], smx[8];
+  __shared__ int scf[8];
+  const int j = blockIdx.x;
+  const int4 o = org[j], b = brick[j];
+  const long long nw = (long long)se * se * se;
+  const float* wp = wprob + (long long)j * nw;
+  float mn = 1e30f, mx = -1e30f;
+  int cf = 0;
+  const long long ns = (long long)s * s * s;
+  for (long long t = threadIdx.x; t < ns; t += blockDim.x) {
+    const int bx = (int)(t % s), by = (int)((t / s) % s), bz = (int)(t / ((long long)s * s));
+    const int x = b.x * s + bx, y = b.y * s + by, z = b.z * s + bz;
+    const float v = wp[((long long)(z - o.z) * se + (y - o.y)) * se + (x - o.x)];
+    const long long g = ((long long)z * D + y) * D + x;
+    P[g] = v;
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+    cf |= bits[g] == 3;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    cf |= __shfl_xor_sync(0xffffffffu, cf, off);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { smn[warp] = mn; smx[warp] = mx; scf[warp] = cf; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mn = fminf(mn, smn[w]);
+      mx = fmaxf(mx, smx[w]);
+      cf |= scf[w];
+    }
+    int st = 0;
+    if (cf) st = 3;
+    else if (prune && t_hom >= 0.f && mx - mn < t_hom) st = 1;
+    else if (prune && t_bin >= 0.f && (mn - 0.5f > t_bin || 0.5f - mx > t_bin)) st = 2;
+    state[j] = st;
+    range[j] = make_float2(mn, mx);
+  }
+}
+
+static int grid_n(long long n, int sms) {
+  long long g = (n + 255) / 256;
+  const long long cap = (long long)sms * 16;
+  return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
+}
+
+cudaError_t launch_seed_bits(const uint8_t* seeds, long long n, uint8_t* bits, int sms, cudaStream_t s) {
+  k_seed_bits<<<grid_n(n, sms), 256, 0, s>>>(seeds, n, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seed_or(const uint8_t* in, int D, uint8_t* out, int sms, cudaStream_t s) {
+  const long long h = D / 2;
+  k_seed_or<<<grid_n(h * h * h, sms), 256, 0, s>>>(in, D, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_upsample(const float* P, int np, float* out, int D, int sms, cudaStream_t s) {
+  k_upsample<<<grid_n((long long)D * D * D, sms), 256, 0, s>>>(P, np, out, D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const void* vol, int dtype, const uint8_t* bits, const float* Ppar,
+                          int D, int se, const int4* org, int nb, void* wvol, uint8_t* fixed,
+                          float* values, float* x0, int sms, cudaStream_t s) {
+  const int grid = grid_n((long long)se * se * se * nb, sms);
+  switch (dtype) {
+    case 0: k_gather<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)vol, bits, Ppar, D, se, org, nb, (uint8_t*)wvol, fixed, values, x0); break;
+    case 1: k_gather<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)vol, bits, Ppar, D, se, org, nb, (uint16_t*)wvol, fixed, values, x0); break;
+    case 2: k_gather<int16_t><<<grid, 256, 0, s>>>((const int16_t*)vol, bits, Ppar, D, se, org, nb, (int16_t*)wvol, fixed, values, x0); break;
+    default: k_gather<float><<<grid, 256, 0, s>>>((const float*)vol, bits, Ppar, D, se, org, nb, (float*)wvol, fixed, values, x0); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_contract(const float* wprob, int se, const int4* org, const int4* brick,
+                            int nb, int s, int D, const uint8_t* bits, float* P, float t_hom,
+                            float t_bin, int prune, int* state, float2* range, cudaStream_t st) {
+  k_contract<<<nb, 256, 0, st>>>(wprob, se, org, brick, s, D, bits, P, t_hom, t_bin, prune, state, range);
+  return cudaGetLastError();
+}
+
+}  // namespace rw
