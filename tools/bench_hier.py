@@ -1,0 +1,116 @@
+#!/usr/bin/env python
+"""Hierarchical random walker (rw_hier_segment) on the config-5 vessel volume.
+
+    python tools/bench_hier.py [--scale 0.25] [--s 32] [--e 1.25] [--no-prune-too]
+
+Generates the seeded synthetic vessel network of BASELINE.json config 5 at `scale` (2048^3 x
+scale), rasterised seeds (foreground on vessel centre lines, background in vessel-free
+spots), runs H_p (pruning on) and optionally plain H (no pruning), and prints one JSON line
+per run: wall time (CUDA events, inputs resident), per-level brick statistics, output
+voxels/s and solved-brick voxel-CG-iterations.
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2103_09564_b200 as rwb  # noqa: E402
+import workloads as wl  # noqa: E402
+from workloads.gen import _vessel_segments  # noqa: E402
+
+
+def volume(scale, workers=16):
+    d = wl.cfg5_dims(scale)[0]
+    wl.cfg5_slab(0, 1, scale)          # build the segment cache once
+    step = max(1, d // (workers * 4))
+    with ThreadPoolExecutor(workers) as ex:
+        parts = list(ex.map(lambda z: wl.cfg5_slab(z, min(z + step, d), scale), range(0, d, step)))
+    return np.concatenate(parts, 0)
+
+
+def seed_labels(vol, scale, nfg=400, nbg=400, seed=0):
+    """Foreground seeds at vessel segment mid points, background seeds at random voxels
+    whose 5^3 neighbourhood is vessel-free (intensity well below the vessel level)."""
+    d = vol.shape[0]
+    rng = np.random.default_rng([5, 2, seed])
+    seeds = np.zeros(vol.shape, np.uint8)
+    segs = _vessel_segments(d)
+    pick = rng.choice(len(segs), size=min(nfg, len(segs)), replace=False)
+    for i in pick:
+        p0, p1, r = segs[i]
+        m = np.floor((p0 + p1) / 2).astype(int)
+        x, y, z = np.clip(m, 0, d - 1)
+        if vol[z, y, x] > 15000:
+            seeds[z, y, x] = 1
+    n = 0
+    while n < nbg:
+        z, y, x = rng.integers(2, d - 2, 3)
+        if vol[z - 2:z + 3, y - 2:y + 3, x - 2:x + 3].max() < 10000:
+            seeds[z, y, x] = 2
+            n += 1
+    return seeds
+
+
+def run(vol_d, seeds_d, s, e, prune, reps=2):
+    ws = None
+    out = None
+    ts = []
+    for _ in range(reps + 1):
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0.record()
+        prob, st = rwb.hier_segment(vol_d, seeds_d, s=s, e=e, prune=prune, tol=1e-6,
+                                    max_iter=5000, workspace=ws)
+        t1.record()
+        torch.cuda.synchronize()
+        ts.append(t0.elapsed_time(t1))
+        out = (prob, st)
+    return out, float(np.median(ts[1:]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scale", type=float, default=0.25)
+    ap.add_argument("--s", type=int, default=32)
+    ap.add_argument("--e", type=float, default=1.25)
+    ap.add_argument("--no-prune-too", action="store_true")
+    a = ap.parse_args()
+    t = time.time()
+    vol = volume(a.scale)
+    seeds = seed_labels(vol, a.scale)
+    d = vol.shape[0]
+    print(f"[bench_hier] generated {d}^3 in {time.time() - t:.1f}s; seeds fg {(seeds == 1).sum()} "
+          f"bg {(seeds == 2).sum()}", file=sys.stderr, flush=True)
+    vol_d = torch.from_numpy(vol).cuda()
+    seeds_d = torch.from_numpy(seeds).cuda()
+    se = int(math.floor(a.e * a.s))
+    runs = [True] + ([False] if a.no_prune_too else [])
+    res = {}
+    for prune in runs:
+        (prob, st), ms = run(vol_d, seeds_d, a.s, a.e, prune)
+        total = sum((d // a.s >> l) ** 3 for l in range(st["levels"]))
+        vi = sum(st["iters"][l] * se ** 3 for l in range(st["levels"] - 1)) + st["iters"][-1] * a.s ** 3
+        line = {"config": f"cfg5 vessels {d}^3 u16, hierarchical (s={a.s}, e={a.e}, s_e={se})",
+                "prune": prune, "ms": ms, "output_voxels_per_s": d ** 3 / (ms / 1e3),
+                "bricks_solved": sum(st["solved"]), "bricks_total": total,
+                "solved_voxel_cg_iter_per_s": vi / (ms / 1e3), "stats": st,
+                "fg_fraction": float((prob > 0.5).float().mean())}
+        res[prune] = prob
+        print(json.dumps(line), flush=True)
+    if len(res) == 2:
+        diff = (res[True] - res[False]).abs()
+        agree = ((res[True] > 0.5) == (res[False] > 0.5)).float().mean()
+        print(json.dumps({"pruned_vs_full_max_abs": float(diff.max()),
+                          "label_agreement": float(agree)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
