@@ -105,11 +105,19 @@ def window_origin(brick, s, se, D):
 
 
 def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, eps=1e-6,
-                 tol=1e-10, max_iter=100000, scale=1.0 / 65535, offset=0.0, prune=True):
+                 tol=1e-10, max_iter=100000, scale=1.0 / 65535, offset=0.0, prune=True,
+                 prev=None, t_inc=0.01):
     """Oracle of rw_hier_segment.  vol/seeds [D, D, D] (z, y, x), D = s 2^k.
 
-    Returns dict(prob [D,D,D] fp64 in [0,1], stats per level: solved / pruned_hom /
-    pruned_dt / conflict counts, fields [level] (level 0 first)).
+    prev: the dict a previous call returned (same volume and geometry) -> incremental
+    labelling H_it (reading R27): every solved brick whose previous node was
+    computed, whose new solution differs from the previous one by less than t_inc
+    everywhere in its s^3 and that has no seed conflict involving a changed label
+    keeps its previous values and its whole previous subtree; recomputed bricks start from
+    their previous solution.
+
+    Returns dict(prob [D,D,D] fp64 in [0,1], stats per level, fields [level] (level 0
+    first), computed [level] = set of bricks holding a computed node, bits [level]).
     """
     vol = np.asarray(vol)
     D = vol.shape[0]
@@ -118,42 +126,67 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, ep
     assert s * 2 ** k == D, "volume side must be s * 2^k"
     levels = k + 1
     se = int(math.floor(e * s))
+    inc = prev is not None
     vols = [vol] + (pyramid_oracle.pyramid(vol, k) if k > 0 else [])
     bits = seed_bit_pyramid(seeds, levels)
-    stats = [dict(active=0, solved=0, pruned_hom=0, pruned_dt=0, conflict=0, iters=0)
+    stats = [dict(active=0, solved=0, pruned_hom=0, pruned_dt=0, conflict=0, reused=0, iters=0)
              for _ in range(levels)]
     fields = [None] * levels
+    computed = [set() for _ in range(levels)]
+
+    def region(b):
+        return tuple(slice(c * s, (c + 1) * s) for c in b)
+
+    def decide(l, b, xb, old):
+        """(state, values kept): reuse (R27) before the pruning rule."""
+        if inc and b in prev["computed"][l]:
+            cb, ob = bits[l][region(b)], prev["bits"][l][region(b)]
+            dconf = np.any((cb == 3) & (cb != ob))
+            if not dconf and np.max(np.abs(xb - old)) < t_inc:
+                return "reused", old
+        return _prune_state(b, xb, bits[l], s, t_hom, t_bin, prune), xb
 
     # ---- root (Eq. 1)
     g = ro.normalise(vols[k], scale, offset)
     fixed, val = seeds_from_bits(bits[k])
-    o = ro.solve_brick(g, fixed, val, beta, eps, tol, max_iter)
-    fields[k] = np.where(fixed, val, np.clip(o["x"], 0.0, 1.0))
+    o = ro.solve_brick(g, fixed, val, beta, eps, tol, max_iter,
+                       x0=prev["fields"][k] if inc else None)
+    xr = np.where(fixed, val, np.clip(o["x"], 0.0, 1.0))
+    st, kept = decide(k, (0, 0, 0), xr, prev["fields"][k] if inc else None)
+    fields[k] = kept.copy()
+    computed[k].add((0, 0, 0))
     stats[k].update(active=1, solved=1, iters=o["iters"])
-    active = {(0, 0, 0)}
-    prunable = {}
-    st = _prune_state((0, 0, 0), fields[k], bits[k], s, t_hom, t_bin, prune)
-    prunable[(0, 0, 0)] = st
     _count(stats[k], st)
+    state = {(0, 0, 0): st}            # per brick of the previous (coarser) level
+    reused_desc = set()                # bricks under a reused node
 
-    # ---- levels k-1 .. 0 (Eq. 3 with H_p)
+    # ---- levels k-1 .. 0 (Eq. 3 with H_p and H_it)
     for l in range(k - 1, -1, -1):
         Dl = D >> l
         nb = Dl // s
-        children = set()
-        for (bz, by, bx) in active:
-            if prunable[(bz, by, bx)] in (None, "cfl"):
-                for cz in range(2):
-                    for cy in range(2):
-                        for cx in range(2):
-                            children.add((2 * bz + cz, 2 * by + cy, 2 * bx + cx))
+        active, keep = set(), set()
+        for b, stt in state.items():
+            kids = {(2 * b[0] + cz, 2 * b[1] + cy, 2 * b[2] + cx)
+                    for cz in range(2) for cy in range(2) for cx in range(2)}
+            if stt in (None, "cfl"):
+                active |= kids
+            elif stt == "reused":
+                keep |= kids
+        for b in reused_desc:
+            keep |= {(2 * b[0] + cz, 2 * b[1] + cy, 2 * b[2] + cx)
+                     for cz in range(2) for cy in range(2) for cx in range(2)}
         P_par = fields[l + 1]
-        F = upsample(P_par, (Dl, Dl, Dl))
+        up = upsample(P_par, (Dl, Dl, Dl))
+        F = prev["fields"][l].copy() if inc else up.copy()
+        for b in ((bz, by, bx) for bz in range(nb) for by in range(nb) for bx in range(nb)):
+            if b not in active and b not in keep:
+                F[region(b)] = up[region(b)]           # pruned region: nearest solved ancestor
+        computed[l] = {b for b in keep if inc and b in prev["computed"][l]}
         gl = ro.normalise(vols[l], scale, offset)
         fx_l, val_l = seeds_from_bits(bits[l])
-        stats[l]["active"] = len(children)
-        new_prunable = {}
-        for (bz, by, bx) in sorted(children):
+        stats[l]["active"] = len(active)
+        new_state = {}
+        for (bz, by, bx) in sorted(active):
             w0 = [window_origin(c, s, se, Dl) for c in (bz, by, bx)]
             sl = tuple(slice(a, a + se) for a in w0)
             zs, ys, xs = (np.arange(a, a + se) for a in w0)
@@ -174,21 +207,24 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, ep
             border = shell & ~fixed
             values = np.where(border, samp, values)
             fixed = fixed | border
-            o = ro.solve_brick(gl[sl], fixed, values, beta, eps, tol, max_iter, x0=samp)
+            x0 = prev["fields"][l][sl] if inc else samp
+            o = ro.solve_brick(gl[sl], fixed, values, beta, eps, tol, max_iter, x0=x0)
             xw = np.where(fixed, values, np.clip(o["x"], 0.0, 1.0))
             # contract: the brick's own s^3
             bo = [bz * s - w0[0], by * s - w0[1], bx * s - w0[2]]
             xb = xw[bo[0]:bo[0] + s, bo[1]:bo[1] + s, bo[2]:bo[2] + s]
-            F[bz * s:(bz + 1) * s, by * s:(by + 1) * s, bx * s:(bx + 1) * s] = xb
+            old = prev["fields"][l][region((bz, by, bx))] if inc else None
+            stt, kept = decide(l, (bz, by, bx), xb, old)
+            F[region((bz, by, bx))] = kept
+            computed[l].add((bz, by, bx))
             stats[l]["solved"] += 1
             stats[l]["iters"] += o["iters"]
-            stt = _prune_state((bz, by, bx), xb, bits[l], s, t_hom, t_bin, prune)
-            new_prunable[(bz, by, bx)] = stt
+            new_state[(bz, by, bx)] = stt
             _count(stats[l], stt)
         fields[l] = F
-        active = children
-        prunable = new_prunable
-    return dict(prob=fields[0], stats=stats, fields=fields)
+        reused_desc = keep
+        state = new_state
+    return dict(prob=fields[0], stats=stats, fields=fields, computed=computed, bits=bits)
 
 
 def _prune_state(b, xb, bits_l, s, t_hom, t_bin, prune):
@@ -213,3 +249,5 @@ def _count(stat, st):
         stat["pruned_dt"] += 1
     elif st == "cfl":
         stat["conflict"] += 1
+    elif st == "reused":
+        stat["reused"] += 1

@@ -115,3 +115,41 @@ def test_pruning_soundness_against_unpruned():
     assert np.abs(pr["prob"] - full["prob"]).max() < 0.3 + 0.05
     agree = ((pr["prob"] > 0.5) == (full["prob"] > 0.5)).mean()
     assert agree > 0.99
+
+
+def test_incremental_noop_identity():
+    """S:360 / P:175-181: re-running with unchanged labels reuses the root's subtree: the
+    output equals the previous output voxel for voxel."""
+    vol, seeds = small_volume(32, 5)
+    first = ho.hier_segment(vol, seeds, s=8, e=1.5, beta=50.0, tol=1e-9)
+    again = ho.hier_segment(vol, seeds, s=8, e=1.5, beta=50.0, tol=1e-9, prev=first)
+    assert again["stats"][-1]["reused"] == 1
+    assert sum(st["solved"] for st in again["stats"]) == 1      # only the root is re-solved
+    assert np.array_equal(again["prob"], first["prob"])
+
+
+def test_incremental_new_seed_matches_full_recompute():
+    """one new foreground seed where the solution is already highest (inside the
+    labelled foreground): coarse levels barely change, so subtrees are reused and far fewer
+    bricks are solved; the result agrees with a full run on the new labels."""
+    vol, seeds = small_volume(32, 6)
+    first = ho.hier_segment(vol, seeds, s=8, e=1.5, beta=50.0, tol=1e-9)
+    new = seeds.copy()
+    p = np.where(seeds > 0, -1.0, first["prob"])
+    new[np.unravel_index(np.argmax(p), p.shape)] = 1
+    inc = ho.hier_segment(vol, new, s=8, e=1.5, beta=50.0, tol=1e-9, prev=first)
+    full = ho.hier_segment(vol, new, s=8, e=1.5, beta=50.0, tol=1e-9)
+    assert sum(st["solved"] for st in inc["stats"]) < sum(st["solved"] for st in full["stats"])
+    assert np.abs(inc["prob"] - full["prob"]).max() < 0.3
+    assert ((inc["prob"] > 0.5) == (full["prob"] > 0.5)).mean() > 0.99
+
+
+def test_incremental_conflict_vetoes_reuse():
+    """A changed label that creates a seed conflict in the root brick ("conflicts where
+    at least one of the recently added labels is involved") forces a recomputation."""
+    vol, seeds = small_volume(32, 7)
+    first = ho.hier_segment(vol, seeds, s=8, e=1.5, beta=50.0, tol=1e-9)
+    new = seeds.copy()
+    new[0, 0, 0], new[0, 0, 1] = 1, 2           # fg + bg in one root voxel: a new conflict
+    inc = ho.hier_segment(vol, new, s=8, e=1.5, beta=50.0, tol=1e-9, prev=first)
+    assert inc["stats"][-1]["reused"] == 0 and inc["stats"][-1]["conflict"] == 1
