@@ -218,6 +218,12 @@ rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int
  *            active / solved / pruned_hom / pruned_dt / conflict brick counts, CG iterations.
  *   workspace  device, >= rw_hier_workspace_bytes(d, dtype, cfg).
  *   The call blocks the host (brick lists are built on the host between levels).
+ *   Incremental labelling H_it (cfg.incremental = 1, reading R27): with the previous run's
+ *   workspace and prob passed back unchanged and the new labels in `seeds`, every solved
+ *   brick whose previous node was computed, whose solution moved by less than t_inc over
+ *   its s^3 and that has no seed conflict involving a changed label keeps its previous
+ *   values and its previous subtree (not descended); recomputed windows start from the
+ *   previous solution.
  *   Errors: RW_EINVAL for a non-cubic volume, D != s 2^k, s % 4 != 0, s_e % 4 != 0,
  *   e not in (1, 2], other bad arguments as rw_solve_bricks.
  * ---------------------------------------------------------------------------------- */
@@ -229,10 +235,14 @@ typedef struct {
   float beta, eps, tol; /* Grady weight and solver settings (as rw_solve_bricks)          */
   int32_t max_iter, tol_mode;
   int32_t max_batch;    /* windows per rw_solve_bricks call (workspace size)             */
+  int32_t incremental;  /* 1: H_it -- workspace and prob must hold the previous */
+                        /*    run on the same volume and geometry; updated in place        */
+  float t_inc;          /* reuse threshold max |new - old| (0.01)                    */
 } rw_hier_config;
 typedef struct {
   int32_t levels;
-  int64_t active[16], solved[16], pruned_hom[16], pruned_dt[16], conflict[16], iters[16];
+  int64_t active[16], solved[16], pruned_hom[16], pruned_dt[16], conflict[16], reused[16],
+      iters[16];
 } rw_hier_stats;
 size_t rw_hier_workspace_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg);
 rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d,

@@ -29,13 +29,14 @@ class rw_weight_spec(C.Structure):
 class rw_hier_config(C.Structure):
     _fields_ = [("s", C.c_int32), ("e", C.c_float), ("t_hom", C.c_float), ("t_bin", C.c_float),
                 ("prune", C.c_int32), ("beta", C.c_float), ("eps", C.c_float), ("tol", C.c_float),
-                ("max_iter", C.c_int32), ("tol_mode", C.c_int32), ("max_batch", C.c_int32)]
+                ("max_iter", C.c_int32), ("tol_mode", C.c_int32), ("max_batch", C.c_int32),
+                ("incremental", C.c_int32), ("t_inc", C.c_float)]
 
 
 class rw_hier_stats(C.Structure):
     _fields_ = [("levels", C.c_int32)] + [(f, C.c_int64 * 16) for f in
                                           ("active", "solved", "pruned_hom", "pruned_dt",
-                                           "conflict", "iters")]
+                                           "conflict", "reused", "iters")]
 
 
 P, I32, F32, SZ = C.c_void_p, C.c_int32, C.c_float, C.c_size_t

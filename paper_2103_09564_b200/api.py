@@ -216,31 +216,41 @@ def solve_labels(seeds, K, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6, max
 
 def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True, beta=100.0,
                  eps=1e-6, tol=1e-6, max_iter=5000, tol_mode=0, norm=None, max_batch=1024,
-                 workspace=None, stream=None):
+                 prev=None, t_inc=0.01, workspace=None, stream=None):
     """rw_hier_segment: vol [D,D,D], seeds u8 [D,D,D] (0 / 1 fg / 2 bg), D = s 2^k.
-    Returns (prob fp32 [D,D,D], stats dict of per-level lists, level 0 = full resolution)."""
+
+    Returns (prob fp32 [D,D,D], stats dict of per-level lists (level 0 = full resolution),
+    state).  Passing ``prev=state`` of an earlier call on the same volume and geometry runs
+    the incremental H_it: the previous result is updated in place (the returned
+    prob is the previous tensor)."""
     _need(vol, "vol")
     _need(seeds, "seeds", torch.uint8)
     nz, ny, nx = vol.shape
     d = rw_dims(nx, ny, nz)
     sc, of = norm or DEFAULT_NORM[vol.dtype]
-    cfg = rw_hier_config(s, e, t_hom, t_bin, int(prune), beta, eps, tol, max_iter, tol_mode, max_batch)
+    cfg = rw_hier_config(s, e, t_hom, t_bin, int(prune), beta, eps, tol, max_iter, tol_mode,
+                         max_batch, int(prev is not None), t_inc)
     need = lib().rw_hier_workspace_bytes(d, DTYPES[vol.dtype], cfg)
     if need == 0:
         raise ValueError("hier_segment: need a cubic volume of side s*2^k, s % 4 == 0, "
                          "e in (1, 2] with floor(e*s) % 4 == 0")
-    if workspace is None or workspace.numel() < need:
-        workspace = alloc_workspace(need, vol.device)
-    prob = torch.empty(tuple(vol.shape), dtype=torch.float32, device=vol.device)
+    if prev is not None:
+        workspace, prob = prev["workspace"], prev["prob"]
+        if workspace.numel() < need or tuple(prob.shape) != tuple(vol.shape):
+            raise ValueError("hier_segment: prev state does not match this volume/geometry")
+    else:
+        if workspace is None or workspace.numel() < need:
+            workspace = alloc_workspace(need, vol.device)
+        prob = torch.empty(tuple(vol.shape), dtype=torch.float32, device=vol.device)
     st = rw_hier_stats()
     check(lib().rw_hier_segment(_ptr(vol), DTYPES[vol.dtype], rw_norm(sc, of), d, _ptr(seeds), cfg,
                                 _ptr(workspace), workspace.numel(), _ptr(prob), C.byref(st),
                                 _stream(stream, vol.device)), "rw_hier_segment")
     L = st.levels
     stats = {f: [int(getattr(st, f)[l]) for l in range(L)]
-             for f in ("active", "solved", "pruned_hom", "pruned_dt", "conflict", "iters")}
+             for f in ("active", "solved", "pruned_hom", "pruned_dt", "conflict", "reused", "iters")}
     stats["levels"] = L
-    return prob, stats
+    return prob, stats, {"prob": prob, "workspace": workspace}
 
 
 def level_dims(dims, levels):

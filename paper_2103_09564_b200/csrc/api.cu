@@ -31,11 +31,13 @@ size_t weights_ex_workspace(int kind, int B, long long n);
 cudaError_t launch_seed_bits(const uint8_t*, long long, uint8_t*, int, cudaStream_t);
 cudaError_t launch_seed_or(const uint8_t*, int, uint8_t*, int, cudaStream_t);
 cudaError_t launch_upsample(const float*, int, float*, int, int, cudaStream_t);
-cudaError_t launch_gather(const void*, int, const uint8_t*, const float*, int, int, const int4*,
-                          int, void*, uint8_t*, float*, float*, int, cudaStream_t);
+cudaError_t launch_gather(const void*, int, const uint8_t*, const float*, const float*, int, int,
+                          const int4*, int, void*, uint8_t*, float*, float*, int, cudaStream_t);
 cudaError_t launch_contract(const float*, int, const int4*, const int4*, int, int, int,
-                            const uint8_t*, float*, float, float, int, int*, float2*,
-                            cudaStream_t);
+                            const uint8_t*, const uint8_t*, float*, float, float, int, float,
+                            uint8_t*, int*, float2*, cudaStream_t);
+cudaError_t launch_fill(const float*, int, float*, int, int, const int4*, int, uint8_t*,
+                        cudaStream_t);
 cudaError_t launch_weights_ex(const void*, int, float, float, int, int, int, int, int, float,
                               float, int, float*, void*, int, cudaStream_t);
 }  // namespace rw
@@ -577,8 +579,8 @@ bool hier_geo(rw_dims d, rw_dtype dt, const rw_hier_config& c, HierGeo* g) {
 }
 
 struct HierLayout {
-  size_t volp[16], bits[17], probp[16], org, brick, state, range, iters, status, wvol, wfixed,
-      wval, wx0, wprob, solve, total;
+  size_t volp[16], bits[17], obits[17], comp[17], probp[16], org, brick, state, range, iters,
+      status, wvol, wfixed, wval, wx0, wprob, solve, total;
 };
 
 HierLayout hier_layout(const HierGeo& g) {
@@ -591,6 +593,9 @@ HierLayout hier_layout(const HierGeo& g) {
   for (int l = 0; l <= g.k; ++l) {
     const size_t n = (size_t)(g.D >> l) * (g.D >> l) * (g.D >> l);
     L.bits[l] = o; o += up(n);
+    L.obits[l] = o; o += up(n);              // previous run's seed bits (H_it)
+    const size_t nb = (size_t)((g.D >> l) / g.s);
+    L.comp[l] = o; o += up(nb * nb * nb);    // brick holds a computed node
   }
   for (int l = 1; l <= g.k; ++l) {
     const size_t n = (size_t)(g.D >> l) * (g.D >> l) * (g.D >> l);
@@ -660,7 +665,18 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
     for (int l = 1; l <= g.k; ++l) vlev[l] = outs[l - 1];
   }
   uint8_t* bits[17];
-  for (int l = 0; l <= g.k; ++l) bits[l] = (uint8_t*)PTR(L.bits[l]);
+  uint8_t* obits[17];
+  uint8_t* comp[17];
+  const bool inc = cfg.incremental != 0;
+  for (int l = 0; l <= g.k; ++l) {
+    bits[l] = (uint8_t*)PTR(L.bits[l]);
+    obits[l] = (uint8_t*)PTR(L.obits[l]);
+    comp[l] = (uint8_t*)PTR(L.comp[l]);
+    const size_t n = (size_t)(g.D >> l) * (g.D >> l) * (g.D >> l);
+    const size_t nb = (size_t)((g.D >> l) / g.s);
+    if (inc) RW_CK(cudaMemcpyAsync(obits[l], bits[l], n, cudaMemcpyDeviceToDevice, s));
+    else RW_CK(cudaMemsetAsync(comp[l], 0, nb * nb * nb, s));
+  }
   RW_TIMED(RW_K_HIER, s, 1, rw::launch_seed_bits(seeds, N0, bits[0], sms, s));
   for (int l = 0; l < g.k; ++l)
     RW_TIMED(RW_K_HIER, s, 1, rw::launch_seed_or(bits[l], g.D >> l, bits[l + 1], sms, s));
@@ -689,18 +705,20 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
     RW_CK(cudaMemcpyAsync(d_brick, br.data() + first, nb * sizeof(int4), cudaMemcpyHostToDevice, s));
     const int Dl = g.D >> l;
     RW_TIMED(RW_K_HIER, s, 1,
-             rw::launch_gather(vlev[l], dtype, bits[l], root ? nullptr : field[l + 1], Dl, w,
-                               d_org, nb, wvol, wfixed, wval, wx0, sms, s));
+             rw::launch_gather(vlev[l], dtype, bits[l], root ? nullptr : field[l + 1],
+                               inc ? field[l] : nullptr, Dl, w, d_org, nb, wvol, wfixed, wval,
+                               wx0, sms, s));
     const rw_dims dw{w, w, w};
     const rw::Plan P = make_plan(nb, dw, 1);
     const Layout Lw = layout(P, false, 0);
     rw_status r = solve_core(nb, dw, wvol, dtype, nm, nullptr, wfixed, wval, 1, cfg.beta, cfg.eps,
-                             cfg.tol, cfg.max_iter, cfg.tol_mode, root ? nullptr : wx0, sws, Lw,
-                             P, wprob, d_iters, nullptr, d_status, nullptr, s);
+                             cfg.tol, cfg.max_iter, cfg.tol_mode, (root && !inc) ? nullptr : wx0,
+                             sws, Lw, P, wprob, d_iters, nullptr, d_status, nullptr, s);
     if (r != RW_OK) return r;
     RW_TIMED(RW_K_HIER, s, 1,
-             rw::launch_contract(wprob, w, d_org, d_brick, nb, g.s, Dl, bits[l], field[l],
-                                 cfg.t_hom, cfg.t_bin, cfg.prune, d_state, d_range, s));
+             rw::launch_contract(wprob, w, d_org, d_brick, nb, g.s, Dl, bits[l],
+                                 inc ? obits[l] : nullptr, field[l], cfg.t_hom, cfg.t_bin,
+                                 cfg.prune, cfg.t_inc, comp[l], d_state, d_range, s));
     h_state.resize(first + nb);
     h_iters.resize(first + nb);
     RW_CK(cudaMemcpyAsync(h_state.data() + first, d_state, nb * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -716,10 +734,11 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
       st.pruned_hom[l] += h_state[i] == 1;
       st.pruned_dt[l] += h_state[i] == 2;
       st.conflict[l] += h_state[i] == 3;
+      st.reused[l] += h_state[i] == 4;
     }
   };
 
-  // ---- root (Eq. 1): the whole coarsest level, x0 = 0.5
+  // ---- root (Eq. 1): the whole coarsest level, x0 = 0.5 (incremental: the previous root)
   std::vector<int4> active{make_int4(0, 0, 0, 0)};
   {
     std::vector<int4> org{make_int4(0, 0, 0, 0)};
@@ -728,18 +747,22 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
     if (r != RW_OK) return r;
     tally(g.k, 1);
   }
-  // ---- levels k-1 .. 0 (Eq. 3, H_p)
+  // ---- levels k-1 .. 0 (Eq. 3, H_p, H_it)
   const int lo = (int)std::ceil((g.se - g.s) / 2.0);
+  std::vector<int4> keep;                                   // bricks under a reused node
   for (int l = g.k - 1; l >= 0; --l) {
-    const int Dl = g.D >> l;
-    std::vector<int4> kids;
-    for (size_t i = 0; i < active.size(); ++i) {
-      if (h_state[i] == 1 || h_state[i] == 2) continue;     // prunable: children keep the
-      const int4 b = active[i];                              // upsampled parent field
+    const int Dl = g.D >> l, nbs = Dl / g.s;
+    std::vector<int4> kids, nkeep;
+    auto children = [&](int4 b, std::vector<int4>& out) {
       for (int c = 0; c < 8; ++c)
-        kids.push_back(make_int4(2 * b.x + (c & 1), 2 * b.y + ((c >> 1) & 1), 2 * b.z + (c >> 2), 0));
-    }
-    RW_TIMED(RW_K_HIER, s, 1, rw::launch_upsample(field[l + 1], Dl / 2, field[l], Dl, sms, s));
+        out.push_back(make_int4(2 * b.x + (c & 1), 2 * b.y + ((c >> 1) & 1), 2 * b.z + (c >> 2), 0));
+    };
+    for (size_t i = 0; i < active.size(); ++i) {
+      if (h_state[i] == 0 || h_state[i] == 3) children(active[i], kids);   // refine
+      else if (h_state[i] == 4) children(active[i], nkeep);                 // reused subtree
+    }                                                       // 1, 2: pruned (parent field)
+    for (const int4& b : keep) children(b, nkeep);
+    if (!inc) RW_TIMED(RW_K_HIER, s, 1, rw::launch_upsample(field[l + 1], Dl / 2, field[l], Dl, sms, s));
     std::vector<int4> org(kids.size());
     auto place = [&](int b) { return std::min(std::max(b * g.s - lo, 0), Dl - g.se); };
     for (size_t i = 0; i < kids.size(); ++i)
@@ -751,8 +774,25 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
       rw_status r = solve_chunk(l, g.se, org, kids, f, nb, false);
       if (r != RW_OK) return r;
     }
+    if (inc) {   // pruned regions: upsampled parent field, no computed node
+      std::vector<uint8_t> mark((size_t)nbs * nbs * nbs, 0);
+      for (const int4& b : kids) mark[((size_t)b.z * nbs + b.y) * nbs + b.x] = 1;
+      for (const int4& b : nkeep) mark[((size_t)b.z * nbs + b.y) * nbs + b.x] = 1;
+      std::vector<int4> fill;
+      for (int z = 0; z < nbs; ++z)
+        for (int y = 0; y < nbs; ++y)
+          for (int x = 0; x < nbs; ++x)
+            if (!mark[((size_t)z * nbs + y) * nbs + x]) fill.push_back(make_int4(x, y, z, 0));
+      for (size_t f = 0; f < fill.size(); f += g.Bc) {
+        const int nb = (int)std::min((size_t)g.Bc, fill.size() - f);
+        RW_CK(cudaMemcpyAsync(d_brick, fill.data() + f, nb * sizeof(int4), cudaMemcpyHostToDevice, s));
+        RW_TIMED(RW_K_HIER, s, 1, rw::launch_fill(field[l + 1], Dl / 2, field[l], Dl, g.s, d_brick, nb, comp[l], s));
+        RW_CK(cudaStreamSynchronize(s));
+      }
+    }
     tally(l, kids.size());
     active.swap(kids);
+    keep.swap(nkeep);
   }
   if (stats) *stats = st;
   return RW_OK;

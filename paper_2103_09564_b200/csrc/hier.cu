@@ -82,9 +82,10 @@ __global__ void k_upsample(const float* __restrict__ P, int np, float* __restric
 // Window w of active brick list entry j: origin org[j] (level voxels), side se.
 template <typename T>
 __global__ void k_gather(const T* __restrict__ vol, const uint8_t* __restrict__ bits,
-                         const float* __restrict__ Ppar, int D, int se, const int4* __restrict__ org,
-                         int nb, T* __restrict__ wvol, uint8_t* __restrict__ fixed,
-                         float* __restrict__ values, float* __restrict__ x0) {
+                         const float* __restrict__ Ppar, const float* __restrict__ Pold, int D,
+                         int se, const int4* __restrict__ org, int nb, T* __restrict__ wvol,
+                         uint8_t* __restrict__ fixed, float* __restrict__ values,
+                         float* __restrict__ x0) {
   const long long nw = (long long)se * se * se;
   const long long tot = nw * nb;
   const int np = D / 2;
@@ -113,57 +114,105 @@ __global__ void k_gather(const T* __restrict__ vol, const uint8_t* __restrict__ 
     }
     fixed[i] = fx ? 1 : 0;
     values[i] = fx ? v : 0.f;
-    x0[i] = ps;
+    x0[i] = Pold ? Pold[g] : ps;   // incremental: the previous solution
   }
 }
 
-// One CTA per brick: copy the brick's s^3 of the window solution into the level field and
-// decide prunable.  state: 0 keep (refine children), 1 hom, 2 dt, 3 conflict.
+// One CTA per brick: decide the brick's fate and write its s^3 into the level field.
+// state: 0 keep refining, 1 hom, 2 dt, 3 seed conflict (vetoes pruning),
+// 4 reused (incremental H_it: the previous node was computed, max |new - old| < t_inc over
+// the s^3 and no conflict involving a changed label; the old values stay).
 __global__ void __launch_bounds__(256)
 k_contract(const float* __restrict__ wprob, int se, const int4* __restrict__ org,
            const int4* __restrict__ brick, int s, int D, const uint8_t* __restrict__ bits,
-           float* __restrict__ P, float t_hom, float t_bin, int prune, int* __restrict__ state,
+           const uint8_t* __restrict__ obits, float* __restrict__ P, float t_hom, float t_bin,
+           int prune, float t_inc, uint8_t* __restrict__ computed, int* __restrict__ state,
            float2* __restrict__ range) {
-  __shared__ float smn[8], smx[8];
-  __shared__ int scf[8];
+  __shared__ float smn[8], smx[8], sdf[8];
+  __shared__ int scf[8], sdc[8];
+  __shared__ int s_reuse;
   const int j = blockIdx.x;
   const int4 o = org[j], b = brick[j];
   const long long nw = (long long)se * se * se;
   const float* wp = wprob + (long long)j * nw;
-  float mn = 1e30f, mx = -1e30f;
-  int cf = 0;
+  const int nbs = D / s;
+  const long long bi = ((long long)b.z * nbs + b.y) * nbs + b.x;
+  const bool inc = obits != nullptr;
+  float mn = 1e30f, mx = -1e30f, df = 0.f;
+  int cf = 0, dc = 0;
   const long long ns = (long long)s * s * s;
-  for (long long t = threadIdx.x; t < ns; t += blockDim.x) {
+  auto gidx = [&](long long t, long long& wi) {
     const int bx = (int)(t % s), by = (int)((t / s) % s), bz = (int)(t / ((long long)s * s));
     const int x = b.x * s + bx, y = b.y * s + by, z = b.z * s + bz;
-    const float v = wp[((long long)(z - o.z) * se + (y - o.y)) * se + (x - o.x)];
-    const long long g = ((long long)z * D + y) * D + x;
-    P[g] = v;
+    wi = ((long long)(z - o.z) * se + (y - o.y)) * se + (x - o.x);
+    return ((long long)z * D + y) * D + x;
+  };
+  for (long long t = threadIdx.x; t < ns; t += blockDim.x) {
+    long long wi;
+    const long long g = gidx(t, wi);
+    const float v = wp[wi];
     mn = fminf(mn, v);
     mx = fmaxf(mx, v);
-    cf |= bits[g] == 3;
+    const uint8_t nb = bits[g];
+    cf |= nb == 3;
+    if (inc) {
+      df = fmaxf(df, fabsf(v - P[g]));
+      dc |= (nb == 3) && (nb != obits[g]);
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    df = fmaxf(df, __shfl_xor_sync(0xffffffffu, df, off));
     cf |= __shfl_xor_sync(0xffffffffu, cf, off);
+    dc |= __shfl_xor_sync(0xffffffffu, dc, off);
   }
   const int warp = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) { smn[warp] = mn; smx[warp] = mx; scf[warp] = cf; }
+  if ((threadIdx.x & 31) == 0) { smn[warp] = mn; smx[warp] = mx; sdf[warp] = df; scf[warp] = cf; sdc[warp] = dc; }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
       mn = fminf(mn, smn[w]);
       mx = fmaxf(mx, smx[w]);
+      df = fmaxf(df, sdf[w]);
       cf |= scf[w];
+      dc |= sdc[w];
     }
     int st = 0;
-    if (cf) st = 3;
+    if (inc && computed[bi] && !dc && df < t_inc) st = 4;
+    else if (cf) st = 3;
     else if (prune && t_hom >= 0.f && mx - mn < t_hom) st = 1;
     else if (prune && t_bin >= 0.f && (mn - 0.5f > t_bin || 0.5f - mx > t_bin)) st = 2;
     state[j] = st;
     range[j] = make_float2(mn, mx);
+    computed[bi] = 1;
+    s_reuse = st == 4;
+  }
+  __syncthreads();
+  if (s_reuse) return;                       // the previous node and its values stay
+  for (long long t = threadIdx.x; t < ns; t += blockDim.x) {
+    long long wi;
+    const long long g = gidx(t, wi);
+    P[g] = wp[wi];
+  }
+}
+
+// pruned region (H_p) in incremental mode: the brick's s^3 of the level field becomes the
+// upsampled parent field and the brick no longer holds a computed node
+__global__ void k_fill(const float* __restrict__ Ppar, int np, float* __restrict__ P, int D,
+                       int s, const int4* __restrict__ brick, uint8_t* __restrict__ computed) {
+  const int j = blockIdx.x;
+  const int4 b = brick[j];
+  const long long ns = (long long)s * s * s;
+  for (long long t = threadIdx.x; t < ns; t += blockDim.x) {
+    const int x = b.x * s + (int)(t % s), y = b.y * s + (int)((t / s) % s);
+    const int z = b.z * s + (int)(t / ((long long)s * s));
+    P[((long long)z * D + y) * D + x] = hier::sample(Ppar, np, z, y, x);
+  }
+  if (threadIdx.x == 0) {
+    const int nbs = D / s;
+    computed[((long long)b.z * nbs + b.y) * nbs + b.x] = 0;
   }
 }
 
@@ -190,22 +239,30 @@ cudaError_t launch_upsample(const float* P, int np, float* out, int D, int sms, 
 }
 
 cudaError_t launch_gather(const void* vol, int dtype, const uint8_t* bits, const float* Ppar,
-                          int D, int se, const int4* org, int nb, void* wvol, uint8_t* fixed,
-                          float* values, float* x0, int sms, cudaStream_t s) {
+                          const float* Pold, int D, int se, const int4* org, int nb, void* wvol,
+                          uint8_t* fixed, float* values, float* x0, int sms, cudaStream_t s) {
   const int grid = grid_n((long long)se * se * se * nb, sms);
   switch (dtype) {
-    case 0: k_gather<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)vol, bits, Ppar, D, se, org, nb, (uint8_t*)wvol, fixed, values, x0); break;
-    case 1: k_gather<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)vol, bits, Ppar, D, se, org, nb, (uint16_t*)wvol, fixed, values, x0); break;
-    case 2: k_gather<int16_t><<<grid, 256, 0, s>>>((const int16_t*)vol, bits, Ppar, D, se, org, nb, (int16_t*)wvol, fixed, values, x0); break;
-    default: k_gather<float><<<grid, 256, 0, s>>>((const float*)vol, bits, Ppar, D, se, org, nb, (float*)wvol, fixed, values, x0); break;
+    case 0: k_gather<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)vol, bits, Ppar, Pold, D, se, org, nb, (uint8_t*)wvol, fixed, values, x0); break;
+    case 1: k_gather<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)vol, bits, Ppar, Pold, D, se, org, nb, (uint16_t*)wvol, fixed, values, x0); break;
+    case 2: k_gather<int16_t><<<grid, 256, 0, s>>>((const int16_t*)vol, bits, Ppar, Pold, D, se, org, nb, (int16_t*)wvol, fixed, values, x0); break;
+    default: k_gather<float><<<grid, 256, 0, s>>>((const float*)vol, bits, Ppar, Pold, D, se, org, nb, (float*)wvol, fixed, values, x0); break;
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_contract(const float* wprob, int se, const int4* org, const int4* brick,
-                            int nb, int s, int D, const uint8_t* bits, float* P, float t_hom,
-                            float t_bin, int prune, int* state, float2* range, cudaStream_t st) {
-  k_contract<<<nb, 256, 0, st>>>(wprob, se, org, brick, s, D, bits, P, t_hom, t_bin, prune, state, range);
+                            int nb, int s, int D, const uint8_t* bits, const uint8_t* obits,
+                            float* P, float t_hom, float t_bin, int prune, float t_inc,
+                            uint8_t* computed, int* state, float2* range, cudaStream_t st) {
+  k_contract<<<nb, 256, 0, st>>>(wprob, se, org, brick, s, D, bits, obits, P, t_hom, t_bin,
+                                 prune, t_inc, computed, state, range);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(const float* Ppar, int np, float* P, int D, int s, const int4* brick,
+                        int nb, uint8_t* computed, cudaStream_t st) {
+  k_fill<<<nb, 256, 0, st>>>(Ppar, np, P, D, s, brick, computed);
   return cudaGetLastError();
 }
 

@@ -22,8 +22,8 @@ P_TOL = 1e-4
                                          (64, 16, 2.0, True)])
 def test_hier_matches_oracle(D, s, e, prune):
     vol, seeds = small_volume(D, seed=D + s)
-    prob, st = rwb.hier_segment(dev(vol), dev(seeds), s=s, e=e, prune=prune, beta=50.0,
-                                tol=1e-7, max_iter=20000)
+    prob, st, _ = rwb.hier_segment(dev(vol), dev(seeds), s=s, e=e, prune=prune, beta=50.0,
+                                   tol=1e-7, max_iter=20000)
     torch.cuda.synchronize()
     ref = ho.hier_segment(vol, seeds, s=s, e=e, beta=50.0, tol=1e-10, prune=prune)
     for l, rs in enumerate(ref["stats"]):
@@ -39,7 +39,7 @@ def test_hier_matches_oracle(D, s, e, prune):
 def test_hier_single_level_equals_solve_bricks():
     """D = s: one root brick -> rw_solve_bricks on the whole volume (Eq. 1)."""
     vol, seeds = small_volume(32, seed=7)
-    prob, st = rwb.hier_segment(dev(vol), dev(seeds), s=32, e=1.25, beta=50.0, tol=1e-7)
+    prob, st, _ = rwb.hier_segment(dev(vol), dev(seeds), s=32, e=1.25, beta=50.0, tol=1e-7)
     fixed, val = ho.seeds_from_bits(ho.seed_bits(seeds))
     out = rwb.solve_bricks(dev(fixed.astype(np.uint8)), dev(val.astype(np.float32)),
                            vol=dev(vol), beta=50.0, tol=1e-7)
@@ -56,3 +56,26 @@ def test_hier_rejects_bad_geometry():
         rwb.hier_segment(vol, seeds, s=32)          # 48 != 32 * 2^k
     with pytest.raises(ValueError):
         rwb.hier_segment(vol[:32, :32, :32].contiguous(), seeds[:32, :32, :32].contiguous(), s=16, e=1.1)
+
+
+@pytest.mark.parametrize("case", ["noop", "new_fg", "conflict"])
+def test_hier_incremental_matches_oracle(case):
+    """H_it: the GPU's in-place incremental update against the oracle's, from the
+    same first run; identical per-level solve/reuse counts and |dp| <= 1e-4."""
+    vol, seeds = small_volume(32, seed=6 if case != "conflict" else 7)
+    kw = dict(s=8, e=1.5, beta=50.0)
+    _, _, state = rwb.hier_segment(dev(vol), dev(seeds), tol=1e-7, max_iter=20000, **kw)
+    first = ho.hier_segment(vol, seeds, tol=1e-10, **kw)
+    new = seeds.copy()
+    if case == "new_fg":
+        p = np.where(seeds > 0, -1.0, first["prob"])
+        new[np.unravel_index(np.argmax(p), p.shape)] = 1
+    elif case == "conflict":
+        new[0, 0, 0], new[0, 0, 1] = 1, 2
+    prob, st, _ = rwb.hier_segment(dev(vol), dev(new), tol=1e-7, max_iter=20000, prev=state, **kw)
+    torch.cuda.synchronize()
+    ref = ho.hier_segment(vol, new, tol=1e-10, prev=first, **kw)
+    for l, rs in enumerate(ref["stats"]):
+        assert (st["solved"][l], st["reused"][l], st["conflict"][l]) == \
+            (rs["solved"], rs["reused"], rs["conflict"]), (l, st, ref["stats"])
+    assert np.abs(prob.cpu().numpy().astype(np.float64) - ref["prob"]).max() <= P_TOL
