@@ -260,11 +260,19 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
  * RW_OPT_SOLVER: RW_SOLVER_AUTO (default: resident when available, else streaming),
  * RW_SOLVER_STREAMING, RW_SOLVER_RESIDENT (a solve it cannot serve returns
  * RW_EUNSUPPORTED).  Process-wide setting; not thread-safe against concurrent solves.
+ * RW_OPT_COSCHED: per-mille share (0..500, default 0 = off) of a resident-eligible batch
+ * (>= 64 bricks, vol given, nrhs 1) that runs through the streaming passes on a library
+ * stream concurrently with the resident clusters, on the SMs the 16-CTA clusters cannot use
+ * (the last bricks of the batch; joined back into the caller's stream).  Needs the
+ * workspace rw_solve_workspace_bytes reports (a smaller one disables it).  Those bricks'
+ * results agree with the resident solver's to the solver tolerance, not bitwise.  Off by
+ * default: on B200 the concurrent streaming traffic slows the clusters more than the
+ * 36 spare SMs add.
  * rw_resident_available(d, nrhs): 1 if the resident solver can serve this shape on the
  * current device, else 0.  Results of the two solvers agree to the solver tolerance, not
  * bitwise (different fp64 reduction trees); each is deterministic and batch-invariant.
  * ---------------------------------------------------------------------------------- */
-enum { RW_OPT_SOLVER = 0 };
+enum { RW_OPT_SOLVER = 0, RW_OPT_COSCHED = 1 };
 enum { RW_SOLVER_AUTO = 0, RW_SOLVER_STREAMING = 1, RW_SOLVER_RESIDENT = 2 };
 rw_status rw_set_option(int32_t key, int64_t value);
 int64_t rw_get_option(int32_t key);

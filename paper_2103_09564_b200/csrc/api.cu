@@ -267,16 +267,54 @@ Prof g_prof;
     g_prof.end(kind, s, n);          \
   } while (0)
 
+size_t dtype_size_(rw_dtype t) { return t == RW_U8 ? 1 : (t == RW_F32 ? 4 : 2); }
+
+// share of a batch given to the streaming passes next to the resident clusters (per mille,
+// RW_OPT_COSCHED).  Off by default: measured on B200 (tools/cosched_sweep.py), any
+// concurrent streaming traffic slows the latency-bound clusters by ~30 % (their DSMEM /
+// mbarrier round trips share the memory fabric) -- 512 cfg2 bricks: 70 ms alone, 91-106 ms
+// co-scheduled at 4-26 % streaming share.
+int g_cosched_pm = 0;
+
+int cosched_candidate(int B, rw_dims d, int nrhs, bool weights_given) {
+  const bool shape = (d.nx == 64 && d.ny == 64 && d.nz == 64) || (d.nx == 32 && d.ny == 32 && d.nz == 32);
+  if (!shape || nrhs != 1 || weights_given || B < 64 || g_cosched_pm <= 0) return 0;
+  return (int)((long long)B * g_cosched_pm / 1000);
+}
+
+int cosched_bricks(int B, rw_dims d, int nrhs, bool weights_given, size_t ws_bytes, size_t main_bytes) {
+  const int Bs = cosched_candidate(B, d, nrhs, weights_given);
+  if (Bs <= 0) return 0;
+  const size_t extra = layout(make_plan(Bs, d, nrhs), false, 0).total;
+  return ws_bytes >= main_bytes + extra ? Bs : 0;   // a smaller workspace: no co-scheduling
+}
+
+rw_status cosched_handles(cudaStream_t* s2, cudaEvent_t* fork, cudaEvent_t* join) {
+  static cudaStream_t st = nullptr;
+  static cudaEvent_t ef = nullptr, ej = nullptr;
+  if (!st) {
+    RW_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    RW_CK(cudaEventCreateWithFlags(&ef, cudaEventDisableTiming));
+    RW_CK(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+  }
+  *s2 = st;
+  *fork = ef;
+  *join = ej;
+  return RW_OK;
+}
+
 // Core solve with fixed/values already on the device.
 rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, rw_norm nm,
                      const float* W, const uint8_t* fixed, const float* values, int32_t nrhs,
                      float beta, float eps, float tol, int32_t max_iter, int32_t tol_mode,
                      const float* x0, char* ws, const Layout& Lw, const rw::Plan& P0,
                      float* prob, int32_t* iters, float* resid, int32_t* status,
-                     uint8_t* labels, cudaStream_t s) {
+                     uint8_t* labels, cudaStream_t s, size_t ws_bytes = 0,
+                     bool allow_resident = true) {
   const int sms = num_sms();
   rw::Plan P = P0;
-  const bool res_ok = g_solver != RW_SOLVER_STREAMING && rw::resident_supported(d.nx, d.ny, d.nz, nrhs);
+  const bool res_ok = allow_resident && g_solver != RW_SOLVER_STREAMING &&
+                      rw::resident_supported(d.nx, d.ny, d.nz, nrhs);
   if (g_solver == RW_SOLVER_RESIDENT && !res_ok)
     return fail(RW_EUNSUPPORTED, "resident solver unavailable for %dx%dx%d, nrhs %d on this device",
                 d.nx, d.ny, d.nz, nrhs);
@@ -325,6 +363,7 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
     A.PB = Bf.PB;
     A.PS = Bf.PS;
     A.B = P.B;
+    A.nsolve = P.B;
     A.U = P.U;
     A.next = Bf.ctr + 2;
     A.iters = iters;
@@ -339,7 +378,34 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       RW_CK(cudaMemsetAsync(dbg, 0, 16 * 8 * sizeof(long long), s));
       A.dbg = dbg;
     }
+    // Co-scheduling: the 16-CTA clusters fill 112 of the 148 SMs; the last Bs bricks of a
+    // large batch run through the streaming passes on a second stream, on the SMs the
+    // clusters leave free (they need no shared memory the clusters hold).
+    const int Bs = cosched_bricks(P.B, d, nrhs, W != nullptr, ws_bytes, Lw.total);
+    A.nsolve = P.B - Bs;
     RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, s));
+    if (Bs > 0) {
+      cudaStream_t s2;
+      cudaEvent_t fork, join;
+      rw_status cs = cosched_handles(&s2, &fork, &join);
+      if (cs != RW_OK) return cs;
+      RW_CK(cudaEventRecord(fork, s));
+      RW_CK(cudaStreamWaitEvent(s2, fork, 0));
+      const int Br = P.B - Bs;
+      const size_t n = (size_t)P.n;
+      const size_t es = dtype_size_(dtype);
+      const rw::Plan P2 = make_plan(Bs, d, nrhs);
+      const Layout L2 = layout(P2, false, 0);
+      rw_status r2 = solve_core(Bs, d, (const char*)vol + Br * n * es, dtype, nm, nullptr,
+                                fixed + Br * n, values + Br * n, nrhs, beta, eps, tol, max_iter,
+                                tol_mode, x0 ? x0 + Br * n : nullptr, ws + Lw.total, L2, P2,
+                                prob + Br * n, iters + Br, resid ? resid + Br : nullptr,
+                                status ? status + Br : nullptr, labels ? labels + Br * n : nullptr,
+                                s2, 0, false);
+      if (r2 != RW_OK) return r2;
+      RW_CK(cudaEventRecord(join, s2));
+      RW_CK(cudaStreamWaitEvent(s, join, 0));
+    }
     if (A.dbg) {
       long long h[128];
       RW_CK(cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s));
@@ -410,6 +476,11 @@ rw_status rw_profile_read(int64_t* launches, double* ms) {
 const char* rw_version(void) { return "librw 0.2 (sm_100a)"; }
 
 rw_status rw_set_option(int32_t key, int64_t value) {
+  if (key == RW_OPT_COSCHED) {
+    if (value < 0 || value > 500) return fail(RW_EINVAL, "rw_set_option: co-scheduling share must be 0..500 per mille");
+    g_cosched_pm = (int)value;
+    return RW_OK;
+  }
   if (key != RW_OPT_SOLVER) return fail(RW_EINVAL, "rw_set_option: unknown key %d", key);
   if (value < RW_SOLVER_AUTO || value > RW_SOLVER_RESIDENT)
     return fail(RW_EINVAL, "rw_set_option: bad solver %lld", (long long)value);
@@ -417,7 +488,9 @@ rw_status rw_set_option(int32_t key, int64_t value) {
   return RW_OK;
 }
 
-int64_t rw_get_option(int32_t key) { return key == RW_OPT_SOLVER ? g_solver : -1; }
+int64_t rw_get_option(int32_t key) {
+  return key == RW_OPT_SOLVER ? g_solver : key == RW_OPT_COSCHED ? g_cosched_pm : -1;
+}
 
 int32_t rw_resident_available(rw_dims d, int32_t nrhs) {
   return rw::resident_supported(d.nx, d.ny, d.nz, nrhs) ? 1 : 0;
@@ -476,7 +549,10 @@ rw_status rw_brick_weights_ex(const void* vol, rw_dtype dtype, rw_norm nm, int32
 
 size_t rw_solve_workspace_bytes(int32_t batch, rw_dims d, int32_t nrhs, int32_t weights_given) {
   if (!dims_ok(d) || batch < 1 || nrhs < 1) return 0;
-  return layout(make_plan(batch, d, nrhs), weights_given != 0, 0).total;
+  size_t t = layout(make_plan(batch, d, nrhs), weights_given != 0, 0).total;
+  const int Bs = cosched_candidate(batch, d, nrhs, weights_given != 0);
+  if (Bs > 0) t += layout(make_plan(Bs, d, nrhs), false, 0).total;
+  return t;
 }
 
 size_t rw_solve_labels_workspace_bytes(int32_t batch, rw_dims d, int32_t K, int32_t weights_given) {
@@ -519,7 +595,7 @@ rw_status rw_solve_bricks(int32_t batch, rw_dims d, const void* vol, rw_dtype dt
     return fail(RW_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, Lw.total);
   return solve_core(batch, d, vol, dtype, nm, W, fixed, values, nrhs, beta, eps, tol, max_iter,
                     tol_mode, x0, (char*)workspace, Lw, P, prob, iters, resid, status, labels,
-                    (cudaStream_t)stream);
+                    (cudaStream_t)stream, ws_bytes);
 }
 
 rw_status rw_solve_labels(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype,

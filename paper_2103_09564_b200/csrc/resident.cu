@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     cl_arrive();
     cl_wait();
     const int b = s_brick;
-    if (b >= A.B) break;
+    if (b >= A.nsolve) break;
 
     // ---- load the slab: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
     uint32_t fixm = 0;   // bit 4*it+e: voxel is fixed (dinv == 0)
@@ -600,7 +600,7 @@ static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
   using G = res::Cfg<N, CL>;
   const int nc = resident_clusters<N, CL>();
   if (nc < 1) return cudaErrorNotSupported;
-  const int ncl = nc < A.B ? nc : A.B;
+  const int ncl = nc < A.nsolve ? nc : A.nsolve;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncl * CL);
   cfg.blockDim = dim3(G::T);

@@ -11,7 +11,8 @@ struct ResArgs {
   float* x;            // [B][n]   in: x0 with fixed values (k_setup); out: prob
   const double2* PB;   // [2][B][U] setup partials (r.z, r.r) in slot 0
   const double4* PS;   // [B][U]    (b.b, n_fixed, n_unknown, 0)
-  int B, U;
+  int B, U;            // B: batch of the arrays (plane stride of W); U: setup partials per brick
+  int nsolve;          // bricks 0 .. nsolve-1 are solved (<= B; the rest run elsewhere)
   int* next;           // brick counter (zeroed before the launch)
   int* iters;          // [B]
   int* status;         // [B]
