@@ -24,9 +24,10 @@
 // (persistent, load-balanced over bricks with different iteration counts).  HBM traffic
 // per brick is one read of W/dinv/x/r and one write of the result; per iteration none.
 //
-// Thread map (N = brick x/y extent, QX = N/4 quads per row, T = QX * N/2 threads):
-// thread t owns the x-quad qx = t % QX of rows y = 2j, 2j+1 (j = t / QX) in all ZS planes
-// of its slab: 2*ZS "items" of 4 voxels.  The x-neighbours of a quad come by warp shuffle,
+// Thread map (N = brick x/y extent, QX = N/4 quads per row): a warp holds SPW = 32/QX
+// segments of QX lanes; lane l of warp w owns the x-quad qx = l % QX of rows y = 2j, 2j+1
+// with j = w SPW + l / QX, in all ZS planes of its slab: 2*ZS "items" of 4 voxels.  Lanes
+// past the last segment (N = 40: 2 of 32) own nothing but join the warp-wide operations.  The x-neighbours of a quad come by warp shuffle,
 // the y-neighbours and z-neighbours from the shared p planes.
 #include "cg_device.cuh"
 #include "resident.cuh"
@@ -41,7 +42,11 @@ struct Cfg {
   static constexpr int ZS = 4;              // planes per CTA
   static constexpr int NZ = ZS * CL;        // brick z extent
   static constexpr int QX = N / 4;          // quads per row
-  static constexpr int T = QX * (N / 2);    // threads per CTA
+  static constexpr int SPW = 32 / QX;       // row-pair segments of QX lanes per warp
+  static constexpr int NJ = N / 2;          // row pairs
+  static constexpr int NWARP = (NJ + SPW - 1) / SPW;
+  static constexpr int T = NWARP * 32;      // threads per CTA (idle lanes when QX does not
+                                            // divide 32 or SPW does not divide NJ, e.g. N = 40)
   static constexpr int NI = 2 * ZS;         // items (quads) per thread
   static constexpr int PL = N * N;          // floats per plane
   static constexpr int oP = 0;                          // p   [ZS+2][N][N]  (0, ZS+1 = halo)
@@ -51,8 +56,9 @@ struct Cfg {
   static constexpr int nF = oWZM + PL;
   static constexpr int SMEM = nF * 4;
   static constexpr int NW = T / 32;
-  static constexpr int TCOLS = T >= 512 ? 512 : 128;    // 128 columns per thread
-  static_assert(T % 128 == 0, "thread count must be a multiple of 4 warps");
+  // tensor memory: warp w uses lanes 32 (w % 4) .. +31 and columns 128 (w / 4) .. +127
+  static constexpr int TCOLS = NWARP > 8 ? 512 : (NWARP > 4 ? 256 : 128);
+  static_assert(T <= 512 && N % 4 == 0 && QX <= 32, "brick shape");
 };
 
 __device__ __forceinline__ uint32_t sptr(const void* p) {
@@ -241,9 +247,11 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   __shared__ double2 s_res;
   __shared__ int s_brick;
   __shared__ uint32_t s_taddr;
-  const int t = threadIdx.x, warp = t >> 5;
+  const int t = threadIdx.x, warp = t >> 5, lane_ = t & 31;
   const int rank = cl_rank();
-  const int qx = t % QX, j = t / QX;
+  const int seg = lane_ / QX, jj = warp * G::SPW + seg;
+  const bool act = seg < G::SPW && jj < G::NJ;      // owns voxels
+  const int qx = act ? lane_ % QX : 0, j = act ? jj : 0;
   float* const P = sm + G::oP;
   float* const X = sm + G::oX;
   float* const WYM = sm + G::oWYM;
@@ -278,6 +286,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   // DSMEM: my plane 0 -> rank-1's upper halo, my plane ZS-1 -> rank+1's lower halo, each
   // with st.async completing (in bytes) on the receiver's halo mbarrier
   const uint32_t own_off = (uint32_t)(j * 2 * N + 4 * qx) * 4u;   // row 2j, quad qx (bytes)
+  // x-neighbour quads of the same row: the lanes next to this one inside its segment
+  const int srcl = qx > 0 ? lane_ - 1 : lane_, srcr = qx < QX - 1 ? lane_ + 1 : lane_;
   const uint32_t up_halo = rank > 0 ? mapa(sptr(P + (ZS + 1) * PL), rank - 1) : 0u;
   const uint32_t up_bar = rank > 0 ? mapa(sptr(&s_bar[0]), rank - 1) : 0u;
   const uint32_t dn_halo = rank < CL - 1 ? mapa(sptr(P), rank + 1) : 0u;
@@ -346,26 +356,34 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     if (b >= A.nsolve) break;
 
     // ---- load the slab: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
-    uint32_t fixm = 0;   // bit 4*it+e: voxel is fixed (dinv == 0)
+    uint32_t fixm = act ? 0u : 0xffffffffu;   // bit 4*it+e: voxel fixed (dinv == 0); idle
+                                              // lanes: all fixed, so q = 0 and r stays 0
 #pragma unroll
     for (int it = 0; it < NI; ++it) {
       const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
       const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
-      const float4 dv = ld4(A.dinv + g);
-      tm_st4(cD + 4u * it, dv);
-      tm_st4(cX + 4u * it, ld4(A.W + g));
-      tm_st4(cY + 4u * it, ld4(A.W + BN + g));
-      tm_st4(cZ + 4u * it, ld4(A.W + 2 * BN + g));
-      fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
-      fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
-      fixm |= (dv.z == 0.f ? 4u : 0u) << (4 * it);
-      fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
-      r[it] = ld4(A.r0 + g);
-      const int so = y * N + 4 * qx;
-      st4(X + zl * PL + so, ld4(A.x + g));
-      st4(P + (zl + 1) * PL + so, f4(0.f));
-      if (rr == 0) st4(WYM + (zl * (N / 2) + j) * N + 4 * qx, y > 0 ? ld4(A.W + BN + g - N) : f4(0.f));
-      if (zl == 0) st4(WZM + so, z0 > 0 ? ld4(A.W + 2 * BN + g - PL) : f4(0.f));
+      float4 dv = f4(0.f), wx = f4(0.f), wy = f4(0.f), wz = f4(0.f);
+      r[it] = f4(0.f);
+      if (act) {
+        dv = ld4(A.dinv + g);
+        wx = ld4(A.W + g);
+        wy = ld4(A.W + BN + g);
+        wz = ld4(A.W + 2 * BN + g);
+        fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
+        fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
+        fixm |= (dv.z == 0.f ? 4u : 0u) << (4 * it);
+        fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
+        r[it] = ld4(A.r0 + g);
+        const int so = y * N + 4 * qx;
+        st4(X + zl * PL + so, ld4(A.x + g));
+        st4(P + (zl + 1) * PL + so, f4(0.f));
+        if (rr == 0) st4(WYM + (zl * (N / 2) + j) * N + 4 * qx, y > 0 ? ld4(A.W + BN + g - N) : f4(0.f));
+        if (zl == 0) st4(WZM + so, z0 > 0 ? ld4(A.W + 2 * BN + g - PL) : f4(0.f));
+      }
+      tm_st4(cD + 4u * it, dv);     // warp-collective: every lane takes part
+      tm_st4(cX + 4u * it, wx);
+      tm_st4(cY + 4u * it, wy);
+      tm_st4(cZ + 4u * it, wz);
     }
     res::tm_wait_st();
     // ---- initial scalars from the setup partials (fixed order; same in every thread)
@@ -420,6 +438,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         for (int it = 0; it < NI; ++it) {
           const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
           const int so = y * N + 4 * qx;
+          if (!act) continue;               // idle lane: owns no voxel
           const float4 po = ld4(P + (zl + 1) * PL + so);
           if (k > 0) st4(X + zl * PL + so, fma4(al, po, ld4(X + zl * PL + so)));
           const float4 pn = pnew4(be, po, dv[it], r[it]);
@@ -442,12 +461,12 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         {  // x terms (same term order as stencil1: +x, -x, +y, -y, +z, -z)
           float4 wx0, wx1;
           tm_ld8(cX + 8u * zl, wx0, wx1);
-          const float xl0 = __shfl_up_sync(0xffffffffu, p0.w, 1, QX);
-          const float xr0 = __shfl_down_sync(0xffffffffu, p0.x, 1, QX);
-          const float xl1 = __shfl_up_sync(0xffffffffu, p1.w, 1, QX);
-          const float xr1 = __shfl_down_sync(0xffffffffu, p1.x, 1, QX);
-          const float wl0 = __shfl_up_sync(0xffffffffu, wx0.w, 1, QX);
-          const float wl1 = __shfl_up_sync(0xffffffffu, wx1.w, 1, QX);
+          const float xl0 = __shfl_sync(0xffffffffu, p0.w, srcl);
+          const float xr0 = __shfl_sync(0xffffffffu, p0.x, srcr);
+          const float xl1 = __shfl_sync(0xffffffffu, p1.w, srcl);
+          const float xr1 = __shfl_sync(0xffffffffu, p1.x, srcr);
+          const float wl0 = __shfl_sync(0xffffffffu, wx0.w, srcl);
+          const float wl1 = __shfl_sync(0xffffffffu, wx1.w, srcl);
           q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
           q1 = xterms(p1, xl1, xr1, wx1, qx > 0 ? wl1 : 0.f);
         }
@@ -534,6 +553,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         o[e] = st == ST_ZERO_B ? 0.f : fminf(fmaxf(o[e], 0.f), 1.f);
       }
       const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
+      if (!act) continue;
       st4(A.x + g, make_float4(o[0], o[1], o[2], o[3]));
       if (A.labels)
         *reinterpret_cast<uchar4*>(A.labels + g) =
@@ -561,7 +581,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 }
 
 // ------------------------------------------------------------------------- launcher
-// Supported shapes: N x N x 4*CL bricks with (N, CL) in {(64, 16), (32, 8)}.
+// Supported shapes: N x N x 4*CL bricks with (N, CL) in {(64, 16), (40, 10), (32, 8)};
+// 40^3 is the paper's expanded brick (s = 32, e = 1.25).
 template <int N, int CL>
 static int resident_clusters() {
   static int cached = -1;
@@ -621,11 +642,13 @@ bool resident_supported(int nx, int ny, int nz, int R) {
   if (R != 1) return false;
   if (nx == 64 && ny == 64 && nz == 64) return resident_clusters<64, 16>() > 0;
   if (nx == 32 && ny == 32 && nz == 32) return resident_clusters<32, 8>() > 0;
+  if (nx == 40 && ny == 40 && nz == 40) return resident_clusters<40, 10>() > 0;
   return false;
 }
 
 cudaError_t launch_resident(int nx, const ResArgs& A, cudaStream_t s) {
   if (nx == 64) return launch_res<64, 16>(A, s);
+  if (nx == 40) return launch_res<40, 10>(A, s);
   return launch_res<32, 8>(A, s);
 }
 

@@ -29,6 +29,7 @@ def streaming(p, **kw):
 def test_resident_available_shapes():
     assert rwb.resident_available((64, 64, 64))
     assert rwb.resident_available((32, 32, 32))
+    assert rwb.resident_available((40, 40, 40))       # the paper's s_e = 1.25 * 32
     assert not rwb.resident_available((64, 64, 64), nrhs=2)
     assert not rwb.resident_available((48, 48, 48))
     p = wl.random_brick(48, 8, 8, seed=1, nseed=10)
@@ -66,11 +67,11 @@ def test_cfg2_resident_parity_batch_invariance_and_streaming_agreement():
     np.testing.assert_allclose(s["resid"], o["resid"], rtol=0.05)
 
 
-@pytest.mark.parametrize("n", [32, 64])
+@pytest.mark.parametrize("n", [32, 40, 64])
 def test_resident_random_bricks_many_per_cluster(n):
     """More bricks than co-resident clusters (each cluster solves several), random seeds with
-    continuous values, Dirichlet shell on odd bricks; u16 intensities."""
-    batch = 40 if n == 32 else 10
+    continuous values; u16 intensities.  n = 40 has idle lanes (10 quads per row)."""
+    batch = {32: 40, 40: 40, 64: 10}[n]
     p = wl.random_brick(n, n, n, seed=100 + n, batch=batch, nseed=n ** 3 // 60,
                         continuous=True, dtype="u16")
     o = resident(p, tol=1e-7, max_iter=20000)
