@@ -216,7 +216,7 @@ def solve_labels(seeds, K, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6, max
 
 def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True, beta=100.0,
                  eps=1e-6, tol=1e-6, max_iter=5000, tol_mode=0, norm=None, max_batch=1024,
-                 prev=None, t_inc=0.01, workspace=None, stream=None):
+                 prev=None, t_inc=0.01, workspace=None, out=None, stream=None):
     """rw_hier_segment: vol [D,D,D], seeds u8 [D,D,D] (0 / 1 fg / 2 bg), D = s 2^k.
 
     Returns (prob fp32 [D,D,D], stats dict of per-level lists (level 0 = full resolution),
@@ -241,7 +241,9 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True, be
     else:
         if workspace is None or workspace.numel() < need:
             workspace = alloc_workspace(need, vol.device)
-        prob = torch.empty(tuple(vol.shape), dtype=torch.float32, device=vol.device)
+        prob = out if out is not None else torch.empty(tuple(vol.shape), dtype=torch.float32,
+                                                       device=vol.device)
+        _need(prob, "out", torch.float32)
     st = rw_hier_stats()
     check(lib().rw_hier_segment(_ptr(vol), DTYPES[vol.dtype], rw_norm(sc, of), d, _ptr(seeds), cfg,
                                 _ptr(workspace), workspace.numel(), _ptr(prob), C.byref(st),
