@@ -47,6 +47,7 @@ struct Cfg {
   static constexpr int NWARP = (NJ + SPW - 1) / SPW;
   static constexpr int T = NWARP * 32;      // threads per CTA (idle lanes when QX does not
                                             // divide 32 or SPW does not divide NJ, e.g. N = 40)
+  static constexpr bool EXACT = SPW * QX == 32 && NJ % SPW == 0;   // every lane owns voxels
   static constexpr int NI = 2 * ZS;         // items (quads) per thread
   static constexpr int PL = N * N;          // floats per plane
   static constexpr int oP = 0;                          // p   [ZS+2][N][N]  (0, ZS+1 = halo)
@@ -250,8 +251,9 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   const int t = threadIdx.x, warp = t >> 5, lane_ = t & 31;
   const int rank = cl_rank();
   const int seg = lane_ / QX, jj = warp * G::SPW + seg;
-  const bool act = seg < G::SPW && jj < G::NJ;      // owns voxels
-  const int qx = act ? lane_ % QX : 0, j = act ? jj : 0;
+  const bool act = G::EXACT || (seg < G::SPW && jj < G::NJ);   // owns voxels
+  const int qx = G::EXACT ? t % QX : (act ? lane_ % QX : 0);
+  const int j = G::EXACT ? t / QX : (act ? jj : 0);
   float* const P = sm + G::oP;
   float* const X = sm + G::oX;
   float* const WYM = sm + G::oWYM;
@@ -288,6 +290,12 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   const uint32_t own_off = (uint32_t)(j * 2 * N + 4 * qx) * 4u;   // row 2j, quad qx (bytes)
   // x-neighbour quads of the same row: the lanes next to this one inside its segment
   const int srcl = qx > 0 ? lane_ - 1 : lane_, srcr = qx < QX - 1 ? lane_ + 1 : lane_;
+  auto shl = [&](float v) {   // value of the quad to the left (own value at qx = 0)
+    return G::EXACT ? __shfl_up_sync(0xffffffffu, v, 1, QX) : __shfl_sync(0xffffffffu, v, srcl);
+  };
+  auto shr = [&](float v) {   // value of the quad to the right (own value at qx = QX-1)
+    return G::EXACT ? __shfl_down_sync(0xffffffffu, v, 1, QX) : __shfl_sync(0xffffffffu, v, srcr);
+  };
   const uint32_t up_halo = rank > 0 ? mapa(sptr(P + (ZS + 1) * PL), rank - 1) : 0u;
   const uint32_t up_bar = rank > 0 ? mapa(sptr(&s_bar[0]), rank - 1) : 0u;
   const uint32_t dn_halo = rank < CL - 1 ? mapa(sptr(P), rank + 1) : 0u;
@@ -356,8 +364,31 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     if (b >= A.nsolve) break;
 
     // ---- load the slab: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
-    uint32_t fixm = act ? 0u : 0xffffffffu;   // bit 4*it+e: voxel fixed (dinv == 0); idle
-                                              // lanes: all fixed, so q = 0 and r stays 0
+    uint32_t fixm = 0;   // bit 4*it+e: voxel is fixed (dinv == 0)
+    if constexpr (G::EXACT) {
+#pragma unroll
+      for (int it = 0; it < NI; ++it) {
+        const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+        const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
+        const float4 dv = ld4(A.dinv + g);
+        tm_st4(cD + 4u * it, dv);
+        tm_st4(cX + 4u * it, ld4(A.W + g));
+        tm_st4(cY + 4u * it, ld4(A.W + BN + g));
+        tm_st4(cZ + 4u * it, ld4(A.W + 2 * BN + g));
+        fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
+        fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
+        fixm |= (dv.z == 0.f ? 4u : 0u) << (4 * it);
+        fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
+        r[it] = ld4(A.r0 + g);
+        const int so = y * N + 4 * qx;
+        st4(X + zl * PL + so, ld4(A.x + g));
+        st4(P + (zl + 1) * PL + so, f4(0.f));
+        if (rr == 0) st4(WYM + (zl * (N / 2) + j) * N + 4 * qx, y > 0 ? ld4(A.W + BN + g - N) : f4(0.f));
+        if (zl == 0) st4(WZM + so, z0 > 0 ? ld4(A.W + 2 * BN + g - PL) : f4(0.f));
+      }
+    } else {
+    // idle lanes: all fixed, so q = 0 and r stays 0
+    fixm = act ? 0u : 0xffffffffu;
 #pragma unroll
     for (int it = 0; it < NI; ++it) {
       const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
@@ -384,6 +415,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       tm_st4(cX + 4u * it, wx);
       tm_st4(cY + 4u * it, wy);
       tm_st4(cZ + 4u * it, wz);
+    }
     }
     res::tm_wait_st();
     // ---- initial scalars from the setup partials (fixed order; same in every thread)
@@ -461,12 +493,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         {  // x terms (same term order as stencil1: +x, -x, +y, -y, +z, -z)
           float4 wx0, wx1;
           tm_ld8(cX + 8u * zl, wx0, wx1);
-          const float xl0 = __shfl_sync(0xffffffffu, p0.w, srcl);
-          const float xr0 = __shfl_sync(0xffffffffu, p0.x, srcr);
-          const float xl1 = __shfl_sync(0xffffffffu, p1.w, srcl);
-          const float xr1 = __shfl_sync(0xffffffffu, p1.x, srcr);
-          const float wl0 = __shfl_sync(0xffffffffu, wx0.w, srcl);
-          const float wl1 = __shfl_sync(0xffffffffu, wx1.w, srcl);
+          const float xl0 = shl(p0.w), xr0 = shr(p0.x), xl1 = shl(p1.w), xr1 = shr(p1.x);
+          const float wl0 = shl(wx0.w), wl1 = shl(wx1.w);
           q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
           q1 = xterms(p1, xl1, xr1, wx1, qx > 0 ? wl1 : 0.f);
         }
