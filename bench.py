@@ -193,6 +193,57 @@ def fp32_peak_tflops():
     return SMS * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12, kind
 
 
+def pyramid_and_queue(dev, d=1024, levels=5, slab=32):
+    """SURVEY 8(a) rows a8 (LOD pyramid) and a9 (pinned double-buffered queue), measured in
+    the same run on a seeded 1024^3 u16 volume: resident fused 5-level pyramid (algorithmic
+    bytes = input + all levels) and the volume streamed from pinned host memory in 32-plane
+    slabs through rw_queue into rw_build_pyramid_slab (bound: host-to-device copy)."""
+    import torch
+    import paper_2103_09564_b200 as rwb
+    from paper_2103_09564_b200 import api
+    g = torch.Generator(device=dev).manual_seed(5)
+    vol = torch.randint(0, 65536, (d, d, d), dtype=torch.int32, device=dev, generator=g).to(torch.uint16)
+    outs = rwb.build_pyramid(vol, levels)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        rwb.build_pyramid(vol, levels, outs=outs)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    nbytes = vol.numel() * 2 + sum(o.numel() * 2 for o in outs)
+    peak, kind = measured_peak()
+    host = vol.cpu().numpy()
+    del vol
+    q = rwb.Queue(slab * d * d * 2, depth=3)
+    cs = torch.cuda.Stream(dev)
+    ms_stream = torch.cuda.current_stream(dev)
+    outs2 = [torch.empty_like(o) for o in outs]
+
+    def stream_all():
+        for z0 in range(0, d, slab):
+            ptr, sid = q.push(host[z0:z0 + slab], cs)
+            q.wait(sid, ms_stream)
+            t = api.device_view(ptr, (slab, d, d), torch.uint16, dev)
+            rwb.build_pyramid_slab(t, (d, d, d), z0, levels, outs2)
+            q.release(sid, ms_stream)
+    stream_all()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    stream_all()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    same = all(torch.equal(a, b) for a, b in zip(outs, outs2))
+    q.close()
+    return {"pyramid": {"workload": f"{d}^3 u16 -> {levels} levels (fused, resident)", "ms": ms,
+                        "achieved_GBps": nbytes / ms / 1e6, "peak_GBps": peak, "peak_kind": kind,
+                        "frac": nbytes / ms / 1e6 / peak},
+            "queue": {"workload": f"{d}^3 u16 streamed from pinned host memory, {slab}-plane slabs, "
+                                  "depth 3, pyramid per slab", "wall_ms": wall * 1e3,
+                      "host_GBps": host.nbytes / wall / 1e9, "equals_resident": bool(same)}}
+
+
 def run_b200(args, rank, world, local_rank):
     import torch
     import paper_2103_09564_b200 as rwb
@@ -330,6 +381,9 @@ def run_b200(args, rank, world, local_rank):
     h2d = h_vol.numel() * h_vol.element_size() + h_fixed.numel() + h_values.numel() * 4
     d2h = h_labels.numel() + h_iters.numel() * 4
 
+    # ---------------- rows a8 / a9 beside the headline (not part of the step) ----------------
+    rows = None if (args.no_rows or rank != 0) else pyramid_and_queue(dev)
+
     if rank != 0:
         return
     cpu = None
@@ -354,6 +408,7 @@ def run_b200(args, rank, world, local_rank):
         "solver": solver_used,
         "roofline": roofline,
         "streaming": streaming,
+        "pyramid_queue": rows,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps},
@@ -375,6 +430,8 @@ def main():
     ap.add_argument("--solver", default="auto", choices=["auto", "streaming", "resident"])
     ap.add_argument("--no-streaming", action="store_true",
                     help="skip the secondary streaming-solver timing")
+    ap.add_argument("--no-rows", action="store_true",
+                    help="skip the secondary pyramid / queue measurements")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

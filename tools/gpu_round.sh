@@ -17,7 +17,7 @@ if [ "${SKIP_CFGS:-0}" = "0" ]; then
 timeout 1200 python tools/bench_configs.py > $O/configs.jsonl 2> $O/configs.err; echo "configs rc=$?"
 cat $O/configs.jsonl; tail -3 $O/configs.err
 fi
-CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-streaming"
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-streaming --no-rows"
 $CMD > $O/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $O/launches.csv $CMD > $O/ncu1.log 2>&1; echo "ncu1 rc=$?"
 if [ "${SKIP_FULL:-0}" = "0" ]; then
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_resident -s 3 -c 1 -o $O/resident $CMD > $O/ncu2.log 2>&1; echo "ncu2 rc=$?"
