@@ -268,11 +268,15 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
  * results agree with the resident solver's to the solver tolerance, not bitwise.  Off by
  * default: on B200 the concurrent streaming traffic slows the clusters more than the
  * 36 spare SMs add.
+ * RW_OPT_RESIDUAL_REPLACE: interval (iterations, default 0 = off) at which the streaming
+ * solver replaces the recurrence residual by the true residual b - L_UU x computed in fp32
+ * (and flushes the lagged x update).  Experimental: the fp32 true residual floors near
+ * 1e-5 of ||b||, so tolerances below that are then never met (R5c).
  * rw_resident_available(d, nrhs): 1 if the resident solver can serve this shape on the
  * current device, else 0.  Results of the two solvers agree to the solver tolerance, not
  * bitwise (different fp64 reduction trees); each is deterministic and batch-invariant.
  * ---------------------------------------------------------------------------------- */
-enum { RW_OPT_SOLVER = 0, RW_OPT_COSCHED = 1 };
+enum { RW_OPT_SOLVER = 0, RW_OPT_COSCHED = 1, RW_OPT_RESIDUAL_REPLACE = 2 };
 enum { RW_SOLVER_AUTO = 0, RW_SOLVER_STREAMING = 1, RW_SOLVER_RESIDENT = 2 };
 rw_status rw_set_option(int32_t key, int64_t value);
 int64_t rw_get_option(int32_t key);

@@ -23,6 +23,7 @@ cudaError_t launch_dinv(const float*, int, int, int, int, const uint8_t*, float*
 cudaError_t launch_setup(const Plan&, const Bufs&, const Ctl&, cudaStream_t);
 cudaError_t launch_iteration_A(const Plan&, const Bufs&, const Ctl&, int, const Maps&, cudaStream_t);
 cudaError_t launch_iteration_B(const Plan&, const Bufs&, int, cudaStream_t);
+cudaError_t launch_replace(const Plan&, const Bufs&, const Ctl&, int, cudaStream_t);
 cudaError_t launch_finalize(const Plan&, const Bufs&, const Ctl&, float*, int*, uint8_t*, cudaStream_t);
 cudaError_t launch_labels_prep(const uint8_t*, long long, int, uint8_t*, float*, int, cudaStream_t);
 cudaError_t launch_argmax(const float*, long long, int, uint8_t*, int, cudaStream_t);
@@ -46,6 +47,12 @@ namespace {
 
 thread_local std::string g_err;
 int g_solver = RW_SOLVER_AUTO;
+// streaming solver: residual replacement interval (RW_OPT_RESIDUAL_REPLACE).  Off by default:
+// measured (tools/rr_sweep.py, tools/dbg_rr.py) the fp32 true residual b - L x bottoms out
+// near 1e-5 of ||b|| (rounding of x itself), so with replacement a 1e-6 / 1e-7 relative
+// tolerance is never met and intervals <= 4 diverge; without it the recurrence converges and
+// the solution error stays ~1e-6 (the true residual measures the fp32 roughness of x).
+int g_rr = 0;
 
 rw_status fail(rw_status st, const char* fmt, ...) {
   char buf[512];
@@ -349,7 +356,7 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   Bf.status = reinterpret_cast<int*>(ws + Lw.status);
   Bf.iters = iters;
   Bf.ctr = reinterpret_cast<int*>(ws + Lw.ctr);
-  rw::Ctl C{tol, tol_mode, max_iter, nm.scale, nm.offset, rw::nbl2_of(beta), eps};
+  rw::Ctl C{tol, tol_mode, max_iter, nm.scale, nm.offset, rw::nbl2_of(beta), eps, 0, g_rr};
   rw::Maps M;
   rw_status st = make_maps(P, Bf, &M);
   if (st != RW_OK) return st;
@@ -429,10 +436,19 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   // iterations ahead of the GPU and stops launching once a checkpoint reads 0.
   const int CHECK = 8;
   int j = 0;
+  bool noxlag = false;
   for (int k = 0; k <= max_iter; ++k) {
     RW_CK(cudaMemsetAsync(Bf.ctr + (k & 1), 0, sizeof(int), s));
-    RW_TIMED(RW_K_PASSA, s, nA, rw::launch_iteration_A(P, Bf, C, k, M, s));
+    rw::Ctl Ck = C;
+    Ck.noxlag = noxlag ? 1 : 0;
+    noxlag = false;
+    RW_TIMED(RW_K_PASSA, s, nA, rw::launch_iteration_A(P, Bf, Ck, k, M, s));
     if (k < max_iter) RW_TIMED(RW_K_PASSB, s, nB, rw::launch_iteration_B(P, Bf, k, s));
+    // residual replacement every g_rr iterations (see k_replace); not at the very end
+    if (C.rr > 0 && k < max_iter - 1 && (k + 1) % C.rr == 0) {
+      RW_TIMED(RW_K_OTHER, s, 2, rw::launch_replace(P, Bf, C, k, s));
+      noxlag = true;
+    }
     if (k % CHECK == CHECK - 1 || k == max_iter) {
       const int slot = j & 1;
       RW_CK(cudaMemcpyAsync(g_pin.h + slot, Bf.ctr + (k & 1), sizeof(int),
@@ -477,6 +493,11 @@ rw_status rw_profile_read(int64_t* launches, double* ms) {
 const char* rw_version(void) { return "librw 0.2 (sm_100a)"; }
 
 rw_status rw_set_option(int32_t key, int64_t value) {
+  if (key == RW_OPT_RESIDUAL_REPLACE) {
+    if (value < 0 || value > 1000000) return fail(RW_EINVAL, "rw_set_option: bad replacement interval");
+    g_rr = (int)value;
+    return RW_OK;
+  }
   if (key == RW_OPT_COSCHED) {
     if (value < 0 || value > 500) return fail(RW_EINVAL, "rw_set_option: co-scheduling share must be 0..500 per mille");
     g_cosched_pm = (int)value;
@@ -490,7 +511,8 @@ rw_status rw_set_option(int32_t key, int64_t value) {
 }
 
 int64_t rw_get_option(int32_t key) {
-  return key == RW_OPT_SOLVER ? g_solver : key == RW_OPT_COSCHED ? g_cosched_pm : -1;
+  return key == RW_OPT_SOLVER ? g_solver : key == RW_OPT_COSCHED ? g_cosched_pm
+         : key == RW_OPT_RESIDUAL_REPLACE ? g_rr : -1;
 }
 
 int32_t rw_resident_available(rw_dims d, int32_t nrhs) {

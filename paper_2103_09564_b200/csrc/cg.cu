@@ -178,7 +178,9 @@ k_finalize(Plan P, Bufs Bf, Ctl C, float* resid, int* status_out, uint8_t* label
   if (warp == 0) {
     const double* pb = reinterpret_cast<const double*>(Bf.PB);
     float al = 0.f;
-    if ((st == ST_CONVERGED || st == ST_MAXITER) && k >= 1) {
+    // the lagged update alpha_{k-1} p_{k-1} -- unless a residual replacement flushed it
+    const bool flushed = C.rr > 0 && k % C.rr == 0 && k < C.max_iter;
+    if ((st == ST_CONVERGED || st == ST_MAXITER) && k >= 1 && !flushed) {
       const double rz = warp_sum_array(pb + 2 * (((k - 1) & 1) * RBU + (long long)rb * P.U), P.U, 2, lane);
       const double pq = warp_sum_array(Bf.PA + ((k - 1) & 1) * RBU + (long long)rb * P.U, P.U, 1, lane);
       al = (float)(rz / pq);
@@ -230,6 +232,94 @@ k_finalize(Plan P, Bufs Bf, Ctl C, float* resid, int* status_out, uint8_t* label
   }
 }
 
+// --------------------------------------------------------------------- residual replacement
+// Long fp32 solves (cfg3: ~3 000 iterations) let the recurrence residual drift away from the
+// true one (measured true relative residual 4e-4 at a recurrence 1e-6).  Every few iterations
+// the streaming loop (1) flushes the lagged update x_{k+1} = x_k + alpha_k p_k and (2)
+// replaces r_{k+1} by the true residual b - L_UU x_{k+1} (the k_setup formula on the current
+// iterate) with its partials, so the stopping rule is checked against the true residual
+// (van der Vorst & Ye's residual replacement; p and the Krylov recurrences are kept).
+__global__ void __launch_bounds__(RW_MAX_THREADS)
+k_flush(Plan P, Bufs Bf, int k) {
+  const int u = blockIdx.x, b = blockIdx.y, r = blockIdx.z;
+  const int rb = r * P.B + b;
+  if (Bf.status[rb] != ST_ACTIVE) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long RBU = (long long)P.R * P.B * P.U;
+  const long long RBN = (long long)P.R * P.B * P.n;
+  __shared__ float s_alpha;
+  if (warp == 0) {
+    const double* pb = reinterpret_cast<const double*>(Bf.PB);
+    const double rz = warp_sum_array(pb + 2 * ((k & 1) * RBU + (long long)rb * P.U), P.U, 2, lane);
+    const double pq = warp_sum_array(Bf.PA + (k & 1) * RBU + (long long)rb * P.U, P.U, 1, lane);
+    if (lane == 0) s_alpha = (pq > 0.0 && isfinite(pq)) ? (float)(rz / pq) : 0.f;
+  }
+  __syncthreads();
+  const float al = s_alpha;
+  const Tile t = make_tile(P, u);
+  if (!t.in || al == 0.f) return;
+  const long long BN = (long long)P.B * P.n;
+  const long long plane = (long long)P.nx * P.ny;
+  const float* Pk = Bf.p + (long long)((k + 1) & 1) * RBN;   // p_k, written by pass A(k)
+  for (int z = t.z0; z < t.z1; ++z) {
+    const long long ov = (long long)r * BN + (long long)b * P.n + (long long)z * plane +
+                         (long long)t.y * P.nx + t.x;
+    st4(Bf.x + ov, fma4(al, ld4(Pk + ov), ld4(Bf.x + ov)));
+  }
+}
+
+template <int VM>
+__global__ void __launch_bounds__(RW_MAX_THREADS)
+k_replace(Plan P, Bufs Bf, Ctl C, int slot) {
+  using T = typename VolT<VM>::T;
+  const int u = blockIdx.x, b = blockIdx.y, r = blockIdx.z;
+  const int rb = r * P.B + b;
+  if (Bf.status[rb] != ST_ACTIVE) return;
+  const Tile t = make_tile(P, u);
+  const long long BN = (long long)P.B * P.n;
+  const long long plane = (long long)P.nx * P.ny;
+  const long long dofs[3] = {1, P.nx, plane};
+  const T* vol = reinterpret_cast<const T*>(Bf.vol);
+  auto fw = [&](long long ob, int a) -> float {
+    if (VM == VM_STORED) return Bf.W[a * BN + ob];
+    const float g0 = normv((float)vol[ob], C.scale, C.offset);
+    const float g1 = normv((float)vol[ob + dofs[a]], C.scale, C.offset);
+    return grady(__fsub_rn(g1, g0), C.nbl2, C.eps);
+  };
+  double acc[2] = {0, 0};
+  if (t.in) {
+    for (int z = t.z0; z < t.z1; ++z) {
+      const long long ib = vidx(P, b, z, t.y, t.x);
+      const long long iv = vidx(P, rb, z, t.y, t.x);
+      float rr[4];
+      const float4 dv = ld4(Bf.dinv + ib);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const long long ob = ib + c, ov = iv + c;
+        const int xc = t.x + c;
+        float res = 0.f;
+        if (!Bf.fixed[ob]) {
+          const float xi = Bf.x[ov];
+          const bool okp[3] = {xc + 1 < P.nx, t.y + 1 < P.ny, z + 1 < P.nz};
+          const bool okm[3] = {xc > 0, t.y > 0, z > 0};
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (okp[a]) res = __fmaf_rn(fw(ob, a), __fsub_rn(Bf.x[ov + dofs[a]], xi), res);
+            if (okm[a]) res = __fmaf_rn(fw(ob - dofs[a], a), __fsub_rn(Bf.x[ov - dofs[a]], xi), res);
+          }
+        }
+        rr[c] = res;
+        const float d = comp(dv, c);
+        acc[0] = __fma_rn((double)res, (double)__fmul_rn(d, res), acc[0]);
+        acc[1] = __fma_rn((double)res, (double)res, acc[1]);
+      }
+      st4(Bf.r + iv, make_float4(rr[0], rr[1], rr[2], rr[3]));
+    }
+  }
+  const long long RBU = (long long)P.R * P.B * P.U;
+  block_sum<2>(acc, reinterpret_cast<double*>(Bf.PB + slot * RBU + (long long)rb * P.U + u));
+}
+
 // --------------------------------------------------------------------------- labels (a7)
 // seeds (0 = unseeded, 1..K) -> fixed mask and K-1 one-vs-rest value planes.
 __global__ void k_labels_prep(const uint8_t* __restrict__ seeds, long long BN, int K,
@@ -269,6 +359,20 @@ cudaError_t launch_setup(const Plan& P, const Bufs& Bf, const Ctl& C, cudaStream
     case VM_I16: k_setup<VM_I16><<<g, P.threads, 0, s>>>(P, Bf, C); break;
     case VM_F32: k_setup<VM_F32><<<g, P.threads, 0, s>>>(P, Bf, C); break;
     default: k_setup<VM_STORED><<<g, P.threads, 0, s>>>(P, Bf, C); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_replace(const Plan& P, const Bufs& Bf, const Ctl& C, int k, cudaStream_t s) {
+  const dim3 g(P.U, P.B, P.R);
+  k_flush<<<g, P.threads, 0, s>>>(P, Bf, k);
+  const int slot = (k + 1) & 1;
+  switch (P.vm) {
+    case VM_U8: k_replace<VM_U8><<<g, P.threads, 0, s>>>(P, Bf, C, slot); break;
+    case VM_U16: k_replace<VM_U16><<<g, P.threads, 0, s>>>(P, Bf, C, slot); break;
+    case VM_I16: k_replace<VM_I16><<<g, P.threads, 0, s>>>(P, Bf, C, slot); break;
+    case VM_F32: k_replace<VM_F32><<<g, P.threads, 0, s>>>(P, Bf, C, slot); break;
+    default: k_replace<VM_STORED><<<g, P.threads, 0, s>>>(P, Bf, C, slot); break;
   }
   return cudaGetLastError();
 }

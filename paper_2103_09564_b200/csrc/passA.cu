@@ -82,6 +82,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   const long long ocol = (long long)b * P.n + (long long)t.y * P.nx + t.x;
   float* const Pnew = Bf.p + (long long)((k + 1) & 1) * RBN;
   const int par = k & 1;
+  const bool xup = k > 0 && !C.noxlag;   // lagged x update of this pass
 
   // ---------------------------------------------------------------- producer (tid 0)
   // plane j (z = zs + j) -> ring slot j % kStages; its n-th use completes phase n & 1
@@ -93,7 +94,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
     uint32_t bytes = L.eRP + (VM == VM_STORED ? L.eWx + L.eWy + L.eWz : L.eV);
 #pragma unroll
     for (int c = 0; c < RC; ++c)
-      if (act[c]) bytes += 2 * L.eRP + (k > 0 ? L.eX : 0);
+      if (act[c]) bytes += 2 * L.eRP + (xup ? L.eX : 0);
     mbar_arrive_expect_tx(bj, bytes);
     const int xb = t.x0 - hx, yb = t.y0 - 1;
 #pragma unroll
@@ -103,7 +104,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       const int pp = ((par * P.R + rbase + c) * P.B + b) * nz + zz;
       tma_load_3d(st + L.oR + c * L.bRP, &M.r, bj, xb, yb, pr);
       tma_load_3d(st + L.oP + c * L.bRP, &M.p, bj, xb, yb, pp);
-      if (k > 0) tma_load_3d(st + L.oX + c * L.bX, &M.x, bj, t.x0, t.y0, pr);
+      if (xup) tma_load_3d(st + L.oX + c * L.bX, &M.x, bj, t.x0, t.y0, pr);
     }
     const int pd = b * nz + zz;
     tma_load_3d(st + L.oD, &M.d, bj, xb, yb, pd);
@@ -314,7 +315,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
         q.z = stencil1(p.z, p.w, p.y, yp.z, ym.z, pn[c].z, pm[c].z, wx.z, wxm.z, wy.z, wym.z, wz.z, wzm.z, dvc.z);
         q.w = stencil1(p.w, xr, p.z, yp.w, ym.w, pn[c].w, pm[c].w, wx.w, wxm.w, wy.w, wym.w, wz.w, wzm.w, dvc.w);
         const long long ov = (long long)(rbase + c) * BN + o;
-        if (k > 0) {
+        if (xup) {
           const float4 po = ld4(F(s0, L.oP + c * L.bRP) + crow);
           const float4 xo = ld4(F(s0, L.oX + c * L.bX) + xrow);
           st4(Bf.x + ov, fma4(al[c], po, xo));

@@ -62,6 +62,9 @@ struct Ctl {
   int tol_mode;
   int max_iter;
   float scale, offset, nbl2, eps;  // normalisation + weights (nbl2 = -beta log2 e)
+  int noxlag;       // pass A: the lagged x update was already applied (residual replacement)
+  int rr;           // residual replacement interval (0: off): after pass B(k) with
+                    // (k+1) % rr == 0 and k < max_iter-1, alpha_k p_k is already in x
 };
 
 // Outputs of one fused pyramid group (<= 5 levels).
