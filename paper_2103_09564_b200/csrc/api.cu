@@ -326,12 +326,17 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   if (g_solver == RW_SOLVER_RESIDENT && !res_ok)
     return fail(RW_EUNSUPPORTED, "resident solver unavailable for %dx%dx%d, nrhs %d on this device",
                 d.nx, d.ny, d.nz, nrhs);
-  // the resident solver reads stored weight planes once per brick
+  // the resident solver reads stored weight planes once per brick -- or, for u16 / f32
+  // intensities, assembles weights, dinv, x0 and r0 itself in its brick load phase (fused)
+  const int vm_vol = vol ? choose_vm(P, vol, dtype) : rw::VM_STORED;
+  const bool fused = res_ok && vol && rw::resident_fused(vm_vol);
   set_vm(P, res_ok ? rw::VM_STORED : choose_vm(P, vol, dtype));
   rw::Bufs Bf{};
   float* Wd = W ? const_cast<float*>(W) : reinterpret_cast<float*>(ws + Lw.W);
   float* dinv = reinterpret_cast<float*>(ws + Lw.dinv);
-  if (vol) {
+  if (fused) {
+    // nothing to precompute
+  } else if (vol) {
     // on-the-fly modes need dinv only; stored mode also writes the weight planes
     float* Wout = P.vm == rw::VM_STORED ? Wd : nullptr;
     RW_TIMED(RW_K_WEIGHTS, s, 1,
@@ -361,7 +366,7 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   rw_status st = make_maps(P, Bf, &M);
   if (st != RW_OK) return st;
   RW_CK(cudaMemsetAsync(Bf.status, 0, (size_t)P.R * P.B * sizeof(int), s));
-  RW_TIMED(RW_K_SETUP, s, 1, rw::launch_setup(P, Bf, C, s));
+  if (!fused) RW_TIMED(RW_K_SETUP, s, 1, rw::launch_setup(P, Bf, C, s));
   if (res_ok) {
     rw::ResArgs A{};
     A.W = Wd;
@@ -379,6 +384,13 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
     A.resid = resid;
     A.labels = labels;
     A.C = C;
+    if (fused) {
+      A.vol = vol;
+      A.vdt = vm_vol;
+      A.fixed = fixed;
+      A.values = values;
+      A.x0 = x0;
+    }
     RW_CK(cudaMemsetAsync(A.next, 0, sizeof(int), s));
     static long long* dbg = nullptr;
     if (getenv("RW_DEBUG_RES_TIMING")) {   // debug: phase cycle sums of the resident kernel

@@ -234,14 +234,124 @@ __device__ __forceinline__ float4 mask4(float4 q, uint32_t fm) {
 }  // namespace res
 
 
-template <int N, int CL>
+
+// ---------------------------------------------------------------------------------------
+// Fused implicit assembly of one quad (4 x-consecutive voxels of brick-local row (z, y),
+// x = 4 qx): the same quantities as k_weights + k_setup (readings c1, c4, c6, c8),
+// with their operand and summation orders, from the intensities, the Dirichlet mask and
+// values and the optional initial guess.  Out: forward weights wx/wy/wz, backward wym/wzm,
+// dinv, x0 (values on S), r0 = b - L_UU x0 (0 on S), and the per-thread fp64 partials of
+// r.(dinv r), r.r, b.b plus the fixed / unknown counts.
+struct QuadOut {
+  float4 dv, wx, wy, wz, wym, wzm, xv, rv;
+  uint32_t fm;
+};
+
+template <typename T> struct Quad4;
+template <> struct Quad4<uint16_t> { using V = ushort4; };
+template <> struct Quad4<float> { using V = float4; };
+
+template <typename T, int N, int NZ>
+__device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long base, int z, int y,
+                                                 int x, double (&acc)[5]) {
+  const T* vol = reinterpret_cast<const T*>(A.vol);
+  const float sc = A.C.scale, of = A.C.offset, nb = A.C.nbl2, eps = A.C.eps;
+  const long long PL = (long long)N * N;
+  const long long i0 = base + (long long)z * PL + (long long)y * N + x;
+  // one vector load per neighbour quad (own, +-y, +-z) and scalars for x-1 / x+4 of
+  // intensity, Dirichlet mask, Dirichlet value and initial guess
+  struct NQ { float g[4], xv[4]; bool f[4]; };
+  auto quad = [&](long long i, NQ& q) {
+    const typename Quad4<T>::V v = *reinterpret_cast<const typename Quad4<T>::V*>(vol + i);
+    const uchar4 f = *reinterpret_cast<const uchar4*>(A.fixed + i);
+    const float4 val = *reinterpret_cast<const float4*>(A.values + i);
+    const float4 x0 = A.x0 ? *reinterpret_cast<const float4*>(A.x0 + i) : make_float4(0.5f, 0.5f, 0.5f, 0.5f);
+    const float gv[4] = {(float)v.x, (float)v.y, (float)v.z, (float)v.w};
+    const bool fv[4] = {f.x != 0, f.y != 0, f.z != 0, f.w != 0};
+    const float vv[4] = {val.x, val.y, val.z, val.w}, xx[4] = {x0.x, x0.y, x0.z, x0.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      q.g[c] = normv(gv[c], sc, of);
+      q.f[c] = fv[c];
+      q.xv[c] = fv[c] ? vv[c] : xx[c];
+    }
+  };
+  auto one = [&](long long i, float& g, float& xv, bool& f) {
+    g = normv((float)vol[i], sc, of);
+    f = A.fixed[i] != 0;
+    xv = f ? A.values[i] : (A.x0 ? A.x0[i] : 0.5f);
+  };
+  NQ c0, yp{}, ym{}, zp{}, zm{};
+  quad(i0, c0);
+  if (y + 1 < N) quad(i0 + N, yp);
+  if (y > 0) quad(i0 - N, ym);
+  if (z + 1 < NZ) quad(i0 + PL, zp);
+  if (z > 0) quad(i0 - PL, zm);
+  float gxm = 0.f, gxp = 0.f, xxm = 0.f, xxp = 0.f;
+  bool fxm = false, fxp = false;
+  if (x > 0) one(i0 - 1, gxm, xxm, fxm);
+  if (x + 4 < N) one(i0 + 4, gxp, xxp, fxp);
+  QuadOut o;
+  o.fm = 0;
+  float wxf[4], wxb[4], wyf[4], wyb[4], wzf[4], wzb[4], dv[4], rs[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float gn = c < 3 ? c0.g[c + 1] : gxp, gp = c > 0 ? c0.g[c - 1] : gxm;
+    wxf[c] = x + c + 1 < N ? grady(__fsub_rn(gn, c0.g[c]), nb, eps) : 0.f;
+    wxb[c] = x + c > 0 ? grady(__fsub_rn(c0.g[c], gp), nb, eps) : 0.f;
+    wyf[c] = y + 1 < N ? grady(__fsub_rn(yp.g[c], c0.g[c]), nb, eps) : 0.f;
+    wyb[c] = y > 0 ? grady(__fsub_rn(c0.g[c], ym.g[c]), nb, eps) : 0.f;
+    wzf[c] = z + 1 < NZ ? grady(__fsub_rn(zp.g[c], c0.g[c]), nb, eps) : 0.f;
+    wzb[c] = z > 0 ? grady(__fsub_rn(c0.g[c], zm.g[c]), nb, eps) : 0.f;
+    const bool fx = c0.f[c];
+    const float s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(wxf[c], wxb[c]), wyf[c]), wyb[c]), wzf[c]), wzb[c]);
+    dv[c] = (fx || !(s > 0.f)) ? 0.f : __frcp_rn(s);
+    const float xi = c0.xv[c];
+    float res = 0.f, bi = 0.f;
+    if (!fx) {
+      // k_setup's order: per axis +a then -a
+      const float xj[6] = {c < 3 ? c0.xv[c + 1] : xxp, c > 0 ? c0.xv[c - 1] : xxm, yp.xv[c],
+                           ym.xv[c], zp.xv[c], zm.xv[c]};
+      const bool fj[6] = {c < 3 ? c0.f[c + 1] : fxp, c > 0 ? c0.f[c - 1] : fxm, yp.f[c], ym.f[c],
+                          zp.f[c], zm.f[c]};
+      const float w6[6] = {wxf[c], wxb[c], wyf[c], wyb[c], wzf[c], wzb[c]};
+      const bool ok[6] = {x + c + 1 < N, x + c > 0, y + 1 < N, y > 0, z + 1 < NZ, z > 0};
+#pragma unroll
+      for (int e = 0; e < 6; ++e) {
+        if (!ok[e]) continue;
+        res = __fmaf_rn(w6[e], __fsub_rn(xj[e], xi), res);
+        if (fj[e]) bi = __fmaf_rn(w6[e], xj[e], bi);
+      }
+    } else {
+      o.fm |= 1u << c;
+    }
+    rs[c] = res;
+    acc[0] = __fma_rn((double)res, (double)__fmul_rn(dv[c], res), acc[0]);
+    acc[1] = __fma_rn((double)res, (double)res, acc[1]);
+    acc[2] = __fma_rn((double)bi, (double)bi, acc[2]);
+    acc[3] += fx ? 1.0 : 0.0;
+    acc[4] += fx ? 0.0 : 1.0;
+  }
+  o.dv = make_float4(dv[0], dv[1], dv[2], dv[3]);
+  o.wx = make_float4(wxf[0], wxf[1], wxf[2], wxf[3]);
+  o.wy = make_float4(wyf[0], wyf[1], wyf[2], wyf[3]);
+  o.wz = make_float4(wzf[0], wzf[1], wzf[2], wzf[3]);
+  o.wym = make_float4(wyb[0], wyb[1], wyb[2], wyb[3]);
+  o.wzm = make_float4(wzb[0], wzb[1], wzb[2], wzb[3]);
+  o.xv = make_float4(c0.xv[0], c0.xv[1], c0.xv[2], c0.xv[3]);
+  o.rv = make_float4(rs[0], rs[1], rs[2], rs[3]);
+  return o;
+}
+
+template <int N, int CL, int VM>
 __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   using G = res::Cfg<N, CL>;
   using namespace res;
   constexpr int ZS = G::ZS, QX = G::QX, PL = G::PL, NI = G::NI, NW = G::NW;
   extern __shared__ __align__(16) float sm[];
   // mbarriers: [0] halo planes in, [1] p.q partials in, [2] (r.z, r.r) partials in
-  __shared__ __align__(8) uint64_t s_bar[3];
+  __shared__ __align__(8) uint64_t s_bar[4];   // [3]: brick-start sums (fused assembly)
+  __shared__ __align__(16) double2 s_ini[CL];
   __shared__ __align__(16) double s_pq[CL];      // p.q partial of every CTA (rank order)
   __shared__ __align__(16) double2 s_rz[CL];     // (r.z, r.r) partial of every CTA
   __shared__ double s_bred[NW][2];
@@ -266,7 +376,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (t == 0) {
-    for (int i = 0; i < 3; ++i) mbar_init(&s_bar[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&s_bar[i], 1);
     fence_mbar_init();
   }
   // halo planes start at 0 (the outer ones of ranks 0 and CL-1 are never written)
@@ -302,7 +412,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   const uint32_t dn_bar = rank < CL - 1 ? mapa(sptr(&s_bar[0]), rank + 1) : 0u;
   const uint32_t halo_bytes = (uint32_t)((rank > 0) + (rank < CL - 1)) * PL * 4u;
   const uint32_t brk = sptr(&s_brick);
-  uint32_t ph0 = 0, ph1 = 0, ph2 = 0;   // mbarrier phase parities
+  uint32_t ph0 = 0, ph1 = 0, ph2 = 0, ph3 = 0;   // mbarrier phase parities
 
   // Cluster-wide fp64 sum of nv (1 or 2) values per thread, identical in every thread of
   // every CTA: warp xor-shuffle tree -> per-warp partials -> thread 0 adds them in warp order
@@ -365,7 +475,31 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 
     // ---- load the slab: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
     uint32_t fixm = 0;   // bit 4*it+e: voxel is fixed (dinv == 0)
-    if constexpr (G::EXACT) {
+    double iacc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // fused: r.z, r.r, b.b, n_fixed, n_unknown
+    if constexpr (VM != VM_STORED) {
+      // fused implicit assembly from the intensities (no k_weights / k_setup pass)
+      using T = typename VolT<VM>::T;
+      fixm = act ? 0u : 0xffffffffu;
+#pragma unroll
+      for (int it = 0; it < NI; ++it) {
+        const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+        QuadOut o{};
+        if (act) {
+          o = assemble_quad<T, N, G::NZ>(A, (long long)b * n, z0 + zl, y, 4 * qx, iacc);
+          fixm |= o.fm << (4 * it);
+          const int so = y * N + 4 * qx;
+          st4(X + zl * PL + so, o.xv);
+          st4(P + (zl + 1) * PL + so, f4(0.f));
+          if (rr == 0) st4(WYM + (zl * (N / 2) + j) * N + 4 * qx, o.wym);
+          if (zl == 0) st4(WZM + so, o.wzm);
+        }
+        r[it] = o.rv;
+        tm_st4(cD + 4u * it, o.dv);     // warp-collective: every lane takes part
+        tm_st4(cX + 4u * it, o.wx);
+        tm_st4(cY + 4u * it, o.wy);
+        tm_st4(cZ + 4u * it, o.wz);
+      }
+    } else if constexpr (G::EXACT) {
 #pragma unroll
       for (int it = 0; it < NI; ++it) {
         const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
@@ -418,14 +552,29 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     }
     }
     res::tm_wait_st();
-    // ---- initial scalars from the setup partials (fixed order; same in every thread)
+    // ---- initial scalars: setup partials (fixed order), or, fused, three cluster sums
+    // (slot order pq, ini, rz so that the loop's first pq reduction never overtakes a
+    // reader of the previous use of its slot array)
     double rz = 0.0, rrn = 0.0, bb = 0.0, nf = 0.0, nu = 0.0;
-    for (int u = 0; u < A.U; ++u) {
-      const double2 pb = A.PB[(long long)b * A.U + u];
-      const double4 ps = A.PS[(long long)b * A.U + u];
-      rz += pb.x; rrn += pb.y; bb += ps.x; nf += ps.y; nu += ps.z;
+    if constexpr (VM == VM_STORED) {
+      for (int u = 0; u < A.U; ++u) {
+        const double2 pb = A.PB[(long long)b * A.U + u];
+        const double4 ps = A.PS[(long long)b * A.U + u];
+        rz += pb.x; rrn += pb.y; bb += ps.x; nf += ps.y; nu += ps.z;
+      }
+      __syncthreads();
+    } else {
+      double v0[2] = {iacc[4], 0.0};
+      nu = cluster_sum(v0, 1, 1, s_pq, ph1).x;
+      double v1[2] = {iacc[2], iacc[3]};
+      const double2 a1 = cluster_sum(v1, 2, 3, s_ini, ph3);
+      bb = a1.x;
+      nf = a1.y;
+      double v2[2] = {iacc[0], iacc[1]};
+      const double2 a2 = cluster_sum(v2, 2, 2, s_rz, ph2);
+      rz = a2.x;
+      rrn = a2.y;
     }
-    __syncthreads();
 
     int st = ST_ACTIVE, k = 0;
     double rz_prev = 0.0, pq_prev = 0.0;
@@ -611,15 +760,15 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 // ------------------------------------------------------------------------- launcher
 // Supported shapes: N x N x 4*CL bricks with (N, CL) in {(64, 16), (40, 10), (32, 8)};
 // 40^3 is the paper's expanded brick (s = 32, e = 1.25).
-template <int N, int CL>
+template <int N, int CL, int VM>
 static int resident_clusters() {
   static int cached = -1;
   if (cached >= 0) return cached;
   using G = res::Cfg<N, CL>;
   int nc = 0;
-  if (cudaFuncSetAttribute(k_resident<N, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(k_resident<N, CL, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            G::SMEM) != cudaSuccess ||
-      (CL > 8 && cudaFuncSetAttribute(k_resident<N, CL>,
+      (CL > 8 && cudaFuncSetAttribute(k_resident<N, CL, VM>,
                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
     cudaGetLastError();
     cached = 0;
@@ -636,7 +785,7 @@ static int resident_clusters() {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (cudaOccupancyMaxActiveClusters(&nc, k_resident<N, CL>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&nc, k_resident<N, CL, VM>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     nc = 0;
   }
@@ -644,10 +793,10 @@ static int resident_clusters() {
   return nc;
 }
 
-template <int N, int CL>
+template <int N, int CL, int VM>
 static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
   using G = res::Cfg<N, CL>;
-  const int nc = resident_clusters<N, CL>();
+  const int nc = resident_clusters<N, CL, VM>();
   if (nc < 1) return cudaErrorNotSupported;
   const int ncl = nc < A.nsolve ? nc : A.nsolve;
   cudaLaunchConfig_t cfg = {};
@@ -662,22 +811,32 @@ static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_resident<N, CL>, A);
+  return cudaLaunchKernelEx(&cfg, k_resident<N, CL, VM>, A);
 }
 
 // Is the resident solver available for this brick shape (and device)?
 bool resident_supported(int nx, int ny, int nz, int R) {
   if (R != 1) return false;
-  if (nx == 64 && ny == 64 && nz == 64) return resident_clusters<64, 16>() > 0;
-  if (nx == 32 && ny == 32 && nz == 32) return resident_clusters<32, 8>() > 0;
-  if (nx == 40 && ny == 40 && nz == 40) return resident_clusters<40, 10>() > 0;
+  if (nx == 64 && ny == 64 && nz == 64) return resident_clusters<64, 16, VM_STORED>() > 0;
+  if (nx == 32 && ny == 32 && nz == 32) return resident_clusters<32, 8, VM_STORED>() > 0;
+  if (nx == 40 && ny == 40 && nz == 40) return resident_clusters<40, 10, VM_STORED>() > 0;
   return false;
 }
 
+template <int VM>
+static cudaError_t launch_shape(int nx, const ResArgs& A, cudaStream_t s) {
+  if (nx == 64) return launch_res<64, 16, VM>(A, s);
+  if (nx == 40) return launch_res<40, 10, VM>(A, s);
+  return launch_res<32, 8, VM>(A, s);
+}
+
+// fused assembly for u16 / f32 intensities, stored-weight mode otherwise
+bool resident_fused(int vdt) { return vdt == VM_U16 || vdt == VM_F32; }
+
 cudaError_t launch_resident(int nx, const ResArgs& A, cudaStream_t s) {
-  if (nx == 64) return launch_res<64, 16>(A, s);
-  if (nx == 40) return launch_res<40, 10>(A, s);
-  return launch_res<32, 8>(A, s);
+  if (A.vol && A.vdt == VM_U16) return launch_shape<VM_U16>(nx, A, s);
+  if (A.vol && A.vdt == VM_F32) return launch_shape<VM_F32>(nx, A, s);
+  return launch_shape<VM_STORED>(nx, A, s);
 }
 
 }  // namespace rw

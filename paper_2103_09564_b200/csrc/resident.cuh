@@ -19,10 +19,18 @@ struct ResArgs {
   float* resid;        // [B] or null
   uint8_t* labels;     // [B][n] or null
   Ctl C;
+  // fused assembly (vol != null): weights, dinv, x0 and r0 are formed in the brick load
+  // phase from the intensities, the Dirichlet mask / values and x0 (no k_weights / k_setup)
+  const void* vol;       // [B][n] of dtype vdt, or null (then W / dinv / r0 / x / PB / PS)
+  int vdt;               // VM_U8 .. VM_F32
+  const uint8_t* fixed;  // [B][n]
+  const float* values;   // [B][n]
+  const float* x0;       // [B][n] or null (0.5)
   long long* dbg;      // debug: per-(rank, phase) clock64 sums, or null (RW_DEBUG_RES_TIMING)
 };
 
 bool resident_supported(int nx, int ny, int nz, int R);
+bool resident_fused(int vdt);
 cudaError_t launch_resident(int nx, const ResArgs& A, cudaStream_t s);
 
 }  // namespace rw
