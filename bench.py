@@ -193,7 +193,7 @@ def fp32_peak_tflops():
     return SMS * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12, kind
 
 
-def pyramid_and_queue(dev, d=1024, levels=5, slab=32):
+def pyramid_and_queue(dev, d=1024, levels=5, slab=128):
     """SURVEY 8(a) rows a8 (LOD pyramid) and a9 (pinned double-buffered queue), measured in
     the same run on a seeded 1024^3 u16 volume: resident fused 5-level pyramid (algorithmic
     bytes = input + all levels) and the volume streamed from pinned host memory in 32-plane
@@ -214,7 +214,7 @@ def pyramid_and_queue(dev, d=1024, levels=5, slab=32):
     ms = e0.elapsed_time(e1) / 5
     nbytes = vol.numel() * 2 + sum(o.numel() * 2 for o in outs)
     peak, kind = measured_peak()
-    host = vol.cpu().numpy()
+    host = vol.cpu().pin_memory().numpy()     # pinned host volume: no staging copy (rw_queue_push)
     del vol
     q = rwb.Queue(slab * d * d * 2, depth=3)
     cs = torch.cuda.Stream(dev)
@@ -236,12 +236,27 @@ def pyramid_and_queue(dev, d=1024, levels=5, slab=32):
     wall = time.perf_counter() - t0
     same = all(torch.equal(a, b) for a, b in zip(outs, outs2))
     q.close()
+    # roofline of the queue: plain pinned host -> device copy bandwidth of this box
+    # (1 GiB copies: smaller pinned copies reach less, e.g. 31 GB/s at 64 MiB, 52 at 256 MiB)
+    hp = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+    dd = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    dd.copy_(hp, non_blocking=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(4):
+        dd.copy_(hp, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    h2d_peak = 4 * hp.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del hp, dd
     return {"pyramid": {"workload": f"{d}^3 u16 -> {levels} levels (fused, resident)", "ms": ms,
                         "achieved_GBps": nbytes / ms / 1e6, "peak_GBps": peak, "peak_kind": kind,
                         "frac": nbytes / ms / 1e6 / peak},
             "queue": {"workload": f"{d}^3 u16 streamed from pinned host memory, {slab}-plane slabs, "
                                   "depth 3, pyramid per slab", "wall_ms": wall * 1e3,
-                      "host_GBps": host.nbytes / wall / 1e9, "equals_resident": bool(same)}}
+                      "host_GBps": host.nbytes / wall / 1e9, "equals_resident": bool(same),
+                      "bound": "pcie", "peak_GBps": h2d_peak, "peak_kind": "measured pinned H2D copy",
+                      "frac": host.nbytes / wall / 1e9 / h2d_peak}}
 
 
 def run_b200(args, rank, world, local_rank):

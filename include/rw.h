@@ -287,8 +287,10 @@ int32_t rw_resident_available(rw_dims d, int32_t nrhs);
  * 5; P:105 constant-memory brick-wise loading).  A ring of `depth` (>= 2) slots, each a
  * pinned host buffer plus a device buffer of slot_bytes, allocated once here (library-
  * owned).  push: waits until the slot's previous consumer released it, copies host_src
- * (pageable or pinned, host) into the pinned slot with several host threads, enqueues
- * the H2D copy on copy_stream and returns the device slot pointer and its id.
+ * (pageable, host) into the pinned slot with several host threads -- or, when host_src
+ * is itself pinned (page-locked), skips that staging copy and must stay valid until the
+ * copy completes on copy_stream -- enqueues the H2D copy on copy_stream and returns the
+ * device slot pointer and its id.
  * wait: makes compute_stream wait for that slot's copy.  release: records on
  * compute_stream that the slot's consumers are done (slot reusable after that point).
  * ---------------------------------------------------------------------------------- */

@@ -28,10 +28,13 @@ namespace {
 rw_status qfail(rw_status s, const char* m) { rw::set_last_error(m); return s; }
 
 void parallel_copy(void* dst, const void* src, size_t bytes) {
-  const size_t chunk = 64u << 20;
+  // pageable -> pinned staging copy split over host threads (>= 2 MB each): one thread's
+  // memcpy (~10-20 GB/s) is slower than the PCIe H2D copy it feeds
+  const size_t min_per = 2u << 20;
   unsigned nt = std::thread::hardware_concurrency();
   if (nt > 16) nt = 16;
-  if (bytes < chunk || nt < 2) { std::memcpy(dst, src, bytes); return; }
+  if ((size_t)nt * min_per > bytes) nt = (unsigned)(bytes / min_per);
+  if (nt < 2) { std::memcpy(dst, src, bytes); return; }
   size_t per = (bytes + nt - 1) / nt;
   per = (per + 4095) & ~(size_t)4095;
   std::vector<std::thread> th;
@@ -84,9 +87,19 @@ extern "C" rw_status rw_queue_push(rw_queue* q, const void* host_src, size_t byt
   if (q->used[s] && (cudaEventSynchronize(q->ready[s]) != cudaSuccess ||
                      cudaEventSynchronize(q->freed[s]) != cudaSuccess))
     return qfail(RW_ECUDA, "rw_queue_push: waiting for slot release failed");
-  parallel_copy(q->host[s], host_src, bytes);
+  // a pinned (page-locked / registered) source is copied to the device directly, without
+  // the staging copy; a pageable one goes through the slot's pinned buffer
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, host_src) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();   // pageable pointers may report an error on some drivers
+  const void* src = host_src;
+  if (!pinned) {
+    parallel_copy(q->host[s], host_src, bytes);
+    src = q->host[s];
+  }
   cudaStream_t cs = (cudaStream_t)copy_stream;
-  if (cudaMemcpyAsync(q->dev[s], q->host[s], bytes, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+  if (cudaMemcpyAsync(q->dev[s], src, bytes, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
       cudaEventRecord(q->ready[s], cs) != cudaSuccess)
     return qfail(RW_ECUDA, "rw_queue_push: H2D copy enqueue failed");
   q->used[s] = true;
