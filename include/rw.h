@@ -250,6 +250,34 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
                           size_t ws_bytes, float* prob, rw_hier_stats* stats, void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * rw_hier_segment_labels -- multi-class hierarchical segmentation (P:107
+ *   "The method is run once for each class, where only seeds for the current class are
+ *   considered foreground and all other seeds as background ... the class of a voxel is
+ *   the one that maximizes the foreground probability"; "only homogeneity-based
+ *   pruning ... was applied").  K runs of rw_hier_segment's driver, class k = 1..K as the
+ *   foreground, with dt pruning disabled whatever cfg.t_bin says; the intensity pyramid is
+ *   built once.  After each run a running argmax updates best / out_labels (strict >, so
+ *   ties go to the lowest class id, reading R11).
+ *   labels      device u8 [D][D][D]: 0 unseeded, 1..K class seeds (any other nonzero value
+ *               acts as a background seed for every class).
+ *   prob        out device fp32 [K][D][D][D] (nullable unless incremental): class fields.
+ *   best        out device fp32 [D][D][D]: the winning class's probability.
+ *   out_labels  out device u8 [D][D][D]: argmax class 1..K.
+ *   stats       out host (nullable): K entries, one per class run.
+ *   workspace   device, >= rw_hier_labels_workspace_bytes(d, dtype, K, cfg): one
+ *               rw_hier_segment workspace (K of them when cfg.incremental, each class keeping
+ *               its previous run for H_it) plus one fp32 [D]^3 class field.  A workspace of the incremental size
+ *               (cfg.incremental = 1 in the size query) is always used per class, so a
+ *               first non-incremental run can be followed by incremental ones.
+ *   Errors: as rw_hier_segment; RW_EINVAL for K outside 2..255 or incremental with NULL prob.
+ * ---------------------------------------------------------------------------------- */
+size_t rw_hier_labels_workspace_bytes(rw_dims d, rw_dtype dtype, int32_t K, rw_hier_config cfg);
+rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d,
+                                 const uint8_t* labels, int32_t K, rw_hier_config cfg,
+                                 void* workspace, size_t ws_bytes, float* prob, float* best,
+                                 uint8_t* out_labels, rw_hier_stats* stats, void* stream);
+
+/* ------------------------------------------------------------------------------------
  * Solver selection.  rw_solve_bricks / rw_solve_labels run one of two implementations of
  * the same Jacobi-PCG with the same stopping rule, status codes and outputs:
  *   streaming  -- CG state in HBM, two fused passes per iteration (any brick shape, any

@@ -251,3 +251,24 @@ def _count(stat, st):
         stat["conflict"] += 1
     elif st == "reused":
         stat["reused"] += 1
+
+
+def hier_segment_labels(vol, labels, K, s=32, e=1.25, t_hom=0.3, prune=True, prev=None, **kw):
+    """Multi-class hierarchical segmentation ("run once for each class, where only
+    seeds for the current class are considered foreground and all other seeds as
+    background ... the class of a voxel is the one that maximizes the foreground
+    probability"; only homogeneity pruning, dt disabled).  `labels`:
+    0 unseeded, 1..K class seeds.  `prev`: an earlier result on the same volume -> each class
+    runs H_it from its own previous run.  Returns dict(labels [D,D,D] in 1..K with
+    ties to the lowest class id (reading R11), prob [K][D,D,D], stats [K], runs [K])."""
+    labels = np.asarray(labels)
+    P, S, R = [], [], []
+    for k in range(1, K + 1):
+        seeds = np.where(labels == k, 1, np.where(labels > 0, 2, 0)).astype(np.uint8)
+        o = hier_segment(vol, seeds, s=s, e=e, t_hom=t_hom, t_bin=-1.0, prune=prune,
+                         prev=None if prev is None else prev["runs"][k - 1], **kw)
+        P.append(o["prob"])
+        S.append(o["stats"])
+        R.append(o)
+    P = np.asarray(P)
+    return dict(labels=(np.argmax(P, axis=0) + 1).astype(np.uint8), prob=P, stats=S, runs=R)

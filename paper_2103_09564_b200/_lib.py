@@ -66,6 +66,9 @@ SIGNATURES = {
     "rw_hier_workspace_bytes": (SZ, [rw_dims, I32, rw_hier_config]),
     "rw_hier_segment": (I32, [P, I32, rw_norm, rw_dims, P, rw_hier_config, P, SZ, P,
                               C.POINTER(rw_hier_stats), P]),
+    "rw_hier_labels_workspace_bytes": (SZ, [rw_dims, I32, I32, rw_hier_config]),
+    "rw_hier_segment_labels": (I32, [P, I32, rw_norm, rw_dims, P, I32, rw_hier_config, P, SZ,
+                                     P, P, P, C.POINTER(rw_hier_stats), P]),
     "rw_get_option": (C.c_int64, [I32]),
     "rw_resident_available": (I32, [rw_dims, I32]),
 }

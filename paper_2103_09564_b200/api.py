@@ -255,6 +255,61 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True, be
     return prob, stats, {"prob": prob, "workspace": workspace}
 
 
+def _stats_dict(st):
+    L = st.levels
+    out = {f: [int(getattr(st, f)[l]) for l in range(L)]
+           for f in ("active", "solved", "pruned_hom", "pruned_dt", "conflict", "reused", "iters")}
+    out["levels"] = L
+    return out
+
+
+def hier_segment_labels(vol, labels, K, s=32, e=1.25, t_hom=0.3, prune=True, beta=100.0,
+                        eps=1e-6, tol=1e-6, max_iter=5000, tol_mode=0, norm=None,
+                        max_batch=1024, keep_prob=True, keep_state=False, prev=None, t_inc=0.01,
+                        workspace=None, stream=None):
+    """rw_hier_segment_labels: K one-vs-rest hierarchical runs (homogeneity
+    pruning only) and the argmax class.  labels u8 [D,D,D] in 0..K.
+
+    Returns dict(labels u8 [D,D,D] in 1..K, best fp32 [D,D,D], prob fp32 [K,D,D,D] or None,
+    stats = list of K per-level stats dicts, state).  ``keep_state=True`` keeps one workspace
+    per class (and the class fields) so that a later call with ``prev=state`` runs H_it per
+    class (P:321)."""
+    _need(vol, "vol")
+    _need(labels, "labels", torch.uint8)
+    nz, ny, nx = vol.shape
+    d = rw_dims(nx, ny, nz)
+    sc, of = norm or DEFAULT_NORM[vol.dtype]
+    inc = prev is not None
+    cfg = rw_hier_config(s, e, t_hom, -1.0, int(prune), beta, eps, tol, max_iter, tol_mode,
+                         max_batch, int(inc), t_inc)
+    cfg_size = rw_hier_config(s, e, t_hom, -1.0, int(prune), beta, eps, tol, max_iter, tol_mode,
+                              max_batch, int(inc or keep_state), t_inc)
+    need = lib().rw_hier_labels_workspace_bytes(d, DTYPES[vol.dtype], int(K), cfg_size)
+    if need == 0:
+        raise ValueError("hier_segment_labels: need K in 2..255 and a cubic volume of side "
+                         "s*2^k, s % 4 == 0, e in (1, 2] with floor(e*s) % 4 == 0")
+    shp = tuple(vol.shape)
+    if inc:
+        workspace, prob = prev["workspace"], prev["prob"]
+        if workspace.numel() < need or prob is None or tuple(prob.shape) != (K,) + shp:
+            raise ValueError("hier_segment_labels: prev state does not match this volume/K")
+    else:
+        if workspace is None or workspace.numel() < need:
+            workspace = alloc_workspace(need, vol.device)
+        prob = (torch.empty((K,) + shp, dtype=torch.float32, device=vol.device)
+                if keep_prob or keep_state else None)
+    best = torch.empty(shp, dtype=torch.float32, device=vol.device)
+    lab = torch.empty(shp, dtype=torch.uint8, device=vol.device)
+    st = (rw_hier_stats * int(K))()
+    check(lib().rw_hier_segment_labels(_ptr(vol), DTYPES[vol.dtype], rw_norm(sc, of), d,
+                                       _ptr(labels), int(K), cfg, _ptr(workspace),
+                                       workspace.numel(), _ptr(prob) if prob is not None else None,
+                                       _ptr(best), _ptr(lab), st, _stream(stream, vol.device)),
+          "rw_hier_segment_labels")
+    return dict(labels=lab, best=best, prob=prob, stats=[_stats_dict(x) for x in st],
+                state={"prob": prob, "workspace": workspace})
+
+
 def level_dims(dims, levels):
     nx, ny, nz = dims
     out = []

@@ -29,7 +29,8 @@ cudaError_t launch_labels_prep(const uint8_t*, long long, int, uint8_t*, float*,
 cudaError_t launch_argmax(const float*, long long, int, uint8_t*, int, cudaStream_t);
 int passA_rc(const Plan&);
 size_t weights_ex_workspace(int kind, int B, long long n);
-cudaError_t launch_seed_bits(const uint8_t*, long long, uint8_t*, int, cudaStream_t);
+cudaError_t launch_seed_bits(const uint8_t*, long long, int, uint8_t*, int, cudaStream_t);
+cudaError_t launch_label_max(const float*, long long, int, float*, uint8_t*, int, cudaStream_t);
 cudaError_t launch_seed_or(const uint8_t*, int, uint8_t*, int, cudaStream_t);
 cudaError_t launch_upsample(const float*, int, float*, int, int, cudaStream_t);
 cudaError_t launch_gather(const void*, int, const uint8_t*, const float*, const float*, int, int,
@@ -741,23 +742,25 @@ size_t rw_hier_workspace_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg) {
   return hier_layout(g).total;
 }
 
-rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d,
-                          const uint8_t* seeds, rw_hier_config cfg, void* workspace,
-                          size_t ws_bytes, float* prob, rw_hier_stats* stats, void* stream) {
-  HierGeo g;
-  if (!vol || !seeds || !prob || !workspace)
-    return fail(RW_EINVAL, "rw_hier_segment: vol, seeds, prob and workspace must be non-NULL");
-  if (dtype < RW_U8 || dtype > RW_F32) return fail(RW_EINVAL, "rw_hier_segment: bad dtype");
-  if (!hier_geo(d, dtype, cfg, &g))
-    return fail(RW_EINVAL, "rw_hier_segment: need a cubic volume of side s*2^k, s %% 4 == 0, "
-                "e in (1, 2] with floor(e s) %% 4 == 0");
-  rw_status v = validate_solve(1, rw_dims{g.se, g.se, g.se}, vol, dtype, nullptr, 1, cfg.eps,
-                               cfg.tol, cfg.max_iter, cfg.tol_mode, workspace);
-  if (v != RW_OK) return v;
+static rw_status hier_check(const char* fn, const void* vol, rw_dtype dtype, rw_dims d,
+                            const rw_hier_config& cfg, void* workspace, HierGeo* g) {
+  if (dtype < RW_U8 || dtype > RW_F32) return fail(RW_EINVAL, "%s: bad dtype", fn);
+  if (!hier_geo(d, dtype, cfg, g))
+    return fail(RW_EINVAL, "%s: need a cubic volume of side s*2^k, s %% 4 == 0, "
+                "e in (1, 2] with floor(e s) %% 4 == 0", fn);
+  return validate_solve(1, rw_dims{g->se, g->se, g->se}, vol, dtype, nullptr, 1, cfg.eps,
+                        cfg.tol, cfg.max_iter, cfg.tol_mode, workspace);
+}
+
+// one hierarchical run.  cls = 0: seeds are 0 / 1 fg / 2 bg; cls > 0: one-vs-rest
+// run of class cls over multi-class labels.  pyramid = 0: the intensity pyramid in
+// the workspace is already built for this volume (multi-class runs after the first).
+static rw_status hier_run(const void* vol, rw_dtype dtype, rw_norm nm, const HierGeo& g,
+                          rw_dims d, const uint8_t* seeds, int cls, rw_hier_config cfg,
+                          void* workspace, float* prob, rw_hier_stats* stats, bool pyramid,
+                          cudaStream_t s) {
   const HierLayout L = hier_layout(g);
-  if (ws_bytes < L.total)
-    return fail(RW_ENOMEM, "rw_hier_segment: workspace too small: %zu < %zu bytes", ws_bytes, L.total);
-  cudaStream_t s = (cudaStream_t)stream;
+  void* stream = (void*)s;
   char* ws = (char*)workspace;
   const int sms = num_sms();
   auto PTR = [&](size_t off) { return (void*)(ws + off); };
@@ -771,8 +774,10 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
   if (g.k > 0) {
     void* outs[16];
     for (int l = 1; l <= g.k; ++l) outs[l - 1] = PTR(L.volp[l]);
-    rw_status ps = rw_build_pyramid(vol, dtype, d, g.k, outs, stream);
-    if (ps != RW_OK) return ps;
+    if (pyramid) {
+      rw_status ps = rw_build_pyramid(vol, dtype, d, g.k, outs, stream);
+      if (ps != RW_OK) return ps;
+    }
     for (int l = 1; l <= g.k; ++l) vlev[l] = outs[l - 1];
   }
   uint8_t* bits[17];
@@ -788,7 +793,7 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
     if (inc) RW_CK(cudaMemcpyAsync(obits[l], bits[l], n, cudaMemcpyDeviceToDevice, s));
     else RW_CK(cudaMemsetAsync(comp[l], 0, nb * nb * nb, s));
   }
-  RW_TIMED(RW_K_HIER, s, 1, rw::launch_seed_bits(seeds, N0, bits[0], sms, s));
+  RW_TIMED(RW_K_HIER, s, 1, rw::launch_seed_bits(seeds, N0, cls, bits[0], sms, s));
   for (int l = 0; l < g.k; ++l)
     RW_TIMED(RW_K_HIER, s, 1, rw::launch_seed_or(bits[l], g.D >> l, bits[l + 1], sms, s));
   float* field[17];
@@ -906,6 +911,71 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
     keep.swap(nkeep);
   }
   if (stats) *stats = st;
+  return RW_OK;
+}
+
+rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d,
+                          const uint8_t* seeds, rw_hier_config cfg, void* workspace,
+                          size_t ws_bytes, float* prob, rw_hier_stats* stats, void* stream) {
+  HierGeo g;
+  if (!vol || !seeds || !prob || !workspace)
+    return fail(RW_EINVAL, "rw_hier_segment: vol, seeds, prob and workspace must be non-NULL");
+  rw_status v = hier_check("rw_hier_segment", vol, dtype, d, cfg, workspace, &g);
+  if (v != RW_OK) return v;
+  const size_t need = hier_layout(g).total;
+  if (ws_bytes < need)
+    return fail(RW_ENOMEM, "rw_hier_segment: workspace too small: %zu < %zu bytes", ws_bytes, need);
+  return hier_run(vol, dtype, nm, g, d, seeds, 0, cfg, workspace, prob, stats, true,
+                  (cudaStream_t)stream);
+}
+
+// multi-class: one workspace per class when incremental (each class keeps its own previous
+// run), else one shared workspace; plus the class field when prob is not kept
+size_t rw_hier_labels_workspace_bytes(rw_dims d, rw_dtype dtype, int32_t K, rw_hier_config cfg) {
+  HierGeo g;
+  if (K < 2 || K > 255 || dtype < RW_U8 || dtype > RW_F32 || !hier_geo(d, dtype, cfg, &g)) return 0;
+  const size_t one = hier_layout(g).total;
+  const size_t n = (size_t)g.D * g.D * g.D;
+  return (cfg.incremental ? (size_t)K : 1) * one + up(n * 4);
+}
+
+rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d,
+                                 const uint8_t* labels, int32_t K, rw_hier_config cfg,
+                                 void* workspace, size_t ws_bytes, float* prob, float* best,
+                                 uint8_t* out_labels, rw_hier_stats* stats, void* stream) {
+  HierGeo g;
+  if (!vol || !labels || !best || !out_labels || !workspace)
+    return fail(RW_EINVAL, "rw_hier_segment_labels: vol, labels, best, out_labels and workspace "
+                "must be non-NULL");
+  if (K < 2 || K > 255) return fail(RW_EINVAL, "rw_hier_segment_labels: K must be in 2..255");
+  if (cfg.incremental && !prob)
+    return fail(RW_EINVAL, "rw_hier_segment_labels: incremental runs need the per-class prob "
+                "of the previous run (prob non-NULL)");
+  rw_status v = hier_check("rw_hier_segment_labels", vol, dtype, d, cfg, workspace, &g);
+  if (v != RW_OK) return v;
+  const size_t need = rw_hier_labels_workspace_bytes(d, dtype, K, cfg);
+  if (ws_bytes < need)
+    return fail(RW_ENOMEM, "rw_hier_segment_labels: workspace too small: %zu < %zu bytes",
+                ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t one = hier_layout(g).total;
+  const long long n = (long long)g.D * g.D * g.D;
+  char* ws = (char*)workspace;
+  // per-class workspaces whenever they fit, so a later incremental call finds each class's run
+  rw_hier_config ci = cfg;
+  ci.incremental = 1;
+  const bool per = ws_bytes >= rw_hier_labels_workspace_bytes(d, dtype, K, ci);
+  float* scratch = (float*)(ws + (per ? (size_t)K : 1) * one);
+  rw_hier_config c = cfg;
+  c.t_bin = -1.f;        // the dt assumption does not hold for non-binary segmentation
+  for (int k = 1; k <= K; ++k) {
+    char* wk = ws + (per ? (size_t)(k - 1) * one : 0);
+    float* pk = prob ? prob + (size_t)(k - 1) * n : scratch;
+    rw_status r = hier_run(vol, dtype, nm, g, d, labels, k, c, wk, pk,
+                           stats ? stats + (k - 1) : nullptr, per || k == 1, s);
+    if (r != RW_OK) return r;
+    RW_TIMED(RW_K_HIER, s, 1, rw::launch_label_max(pk, n, k, best, out_labels, num_sms(), s));
+  }
   return RW_OK;
 }
 

@@ -46,11 +46,29 @@ __device__ __forceinline__ float sample(const float* __restrict__ P, int np, int
 
 }  // namespace hier
 
-__global__ void k_seed_bits(const uint8_t* __restrict__ seeds, long long n, uint8_t* __restrict__ bits) {
+// cls == 0: labels are 0 / 1 fg / 2 bg.  cls > 0 (multi-class): class cls is the
+// foreground, every other nonzero label background
+__global__ void k_seed_bits(const uint8_t* __restrict__ seeds, long long n, int cls,
+                            uint8_t* __restrict__ bits) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    const uint8_t s = seeds[i];
-    bits[i] = (s == 1 ? 1 : 0) | (s == 2 ? 2 : 0);
+    const int s = seeds[i];
+    bits[i] = cls == 0 ? ((s == 1 ? 1 : 0) | (s == 2 ? 2 : 0))
+                       : (s == cls ? 1 : (s != 0 ? 2 : 0));
+  }
+}
+
+// running argmax over the class fields ("the class of a voxel is the one that
+// maximizes the foreground probability"): strict > keeps the lowest class id on ties
+__global__ void k_label_max(const float* __restrict__ P, long long n, int cls,
+                            float* __restrict__ best, uint8_t* __restrict__ lab) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float p = P[i];
+    if (cls == 1 || p > best[i]) {
+      best[i] = p;
+      lab[i] = (uint8_t)cls;
+    }
   }
 }
 
@@ -222,8 +240,15 @@ static int grid_n(long long n, int sms) {
   return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
 }
 
-cudaError_t launch_seed_bits(const uint8_t* seeds, long long n, uint8_t* bits, int sms, cudaStream_t s) {
-  k_seed_bits<<<grid_n(n, sms), 256, 0, s>>>(seeds, n, bits);
+cudaError_t launch_seed_bits(const uint8_t* seeds, long long n, int cls, uint8_t* bits, int sms,
+                             cudaStream_t s) {
+  k_seed_bits<<<grid_n(n, sms), 256, 0, s>>>(seeds, n, cls, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_label_max(const float* P, long long n, int cls, float* best, uint8_t* lab,
+                             int sms, cudaStream_t s) {
+  k_label_max<<<grid_n(n, sms), 256, 0, s>>>(P, n, cls, best, lab);
   return cudaGetLastError();
 }
 

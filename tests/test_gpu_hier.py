@@ -79,3 +79,76 @@ def test_hier_incremental_matches_oracle(case):
         assert (st["solved"][l], st["reused"][l], st["conflict"][l]) == \
             (rs["solved"], rs["reused"], rs["conflict"]), (l, st, ref["stats"])
     assert np.abs(prob.cpu().numpy().astype(np.float64) - ref["prob"]).max() <= P_TOL
+
+
+@pytest.mark.parametrize("D,s,e,prune", [(32, 8, 1.5, False), (64, 16, 1.25, True),
+                                         (64, 32, 1.25, True)])
+def test_hier_labels_match_oracle(D, s, e, prune):
+    """rw_hier_segment_labels: K = 3 one-vs-rest runs, homogeneity pruning only,
+    argmax labels; per-class fields within P_TOL, labels equal wherever the oracle's top two
+    classes differ by more than 1e-3 (reading R18), pruning decisions identical."""
+    from test_hier_oracle import multi_volume
+    vol, lab = multi_volume(D, seed=D + s)
+    o = rwb.hier_segment_labels(dev(vol), dev(lab), 3, s=s, e=e, prune=prune, beta=50.0,
+                                tol=1e-7, max_iter=20000)
+    torch.cuda.synchronize()
+    ref = ho.hier_segment_labels(vol, lab, 3, s=s, e=e, beta=50.0, tol=1e-10, prune=prune)
+    P = o["prob"].cpu().numpy().astype(np.float64)
+    for k in range(3):
+        for l, rs in enumerate(ref["stats"][k]):
+            g = o["stats"][k]
+            assert g["solved"][l] == rs["solved"] and g["pruned_hom"][l] == rs["pruned_hom"]
+            assert g["pruned_dt"][l] == 0 and g["conflict"][l] == rs["conflict"]
+        assert np.abs(P[k] - ref["prob"][k]).max() <= P_TOL, k
+    srt = np.sort(ref["prob"], axis=0)
+    sure = srt[-1] - srt[-2] > 1e-3
+    got = o["labels"].cpu().numpy()
+    assert np.array_equal(got[sure], ref["labels"][sure])
+    # best = the winning class's field, bit-exact to the per-class output
+    best = o["best"].cpu().numpy()
+    assert np.array_equal(best, np.take_along_axis(o["prob"].cpu().numpy(),
+                                                   got[None].astype(np.int64) - 1, 0)[0])
+
+
+def test_hier_labels_without_prob():
+    """keep_prob=False gives the same labels / best from the shared class-field scratch."""
+    from test_hier_oracle import multi_volume
+    vol, lab = multi_volume(64, seed=5)
+    a = rwb.hier_segment_labels(dev(vol), dev(lab), 3, s=16, beta=50.0, tol=1e-7, max_iter=20000)
+    b = rwb.hier_segment_labels(dev(vol), dev(lab), 3, s=16, beta=50.0, tol=1e-7, max_iter=20000,
+                                keep_prob=False)
+    torch.cuda.synchronize()
+    assert b["prob"] is None
+    assert torch.equal(a["labels"], b["labels"]) and torch.equal(a["best"], b["best"])
+
+
+@pytest.mark.parametrize("case", ["noop", "new_seed"])
+def test_hier_labels_incremental_matches_oracle(case):
+    """Multi-class H_it (P:321): each class reruns incrementally from its own previous run;
+    per-class solve / reuse counts identical to the oracle's, fields within P_TOL."""
+    from test_hier_oracle import multi_volume
+    vol, lab = multi_volume(32, seed=9)
+    kw = dict(s=8, e=1.5, beta=50.0)
+    a = rwb.hier_segment_labels(dev(vol), dev(lab), 3, tol=1e-7, max_iter=20000,
+                                keep_state=True, **kw)
+    first = ho.hier_segment_labels(vol, lab, 3, tol=1e-10, **kw)
+    new = lab.copy()
+    if case == "new_seed":      # a class-2 seed where class 2 is least likely
+        p = np.where(lab > 0, 2.0, first["prob"][1])
+        new[np.unravel_index(np.argmin(p), p.shape)] = 2
+    c = rwb.hier_segment_labels(dev(vol), dev(new), 3, tol=1e-7, max_iter=20000,
+                                prev=a["state"], **kw)
+    torch.cuda.synchronize()
+    ref = ho.hier_segment_labels(vol, new, 3, tol=1e-10, prev=first, **kw)
+    reused = 0
+    for k in range(3):
+        for l, rs in enumerate(ref["stats"][k]):
+            g = c["stats"][k]
+            assert (g["solved"][l], g["reused"][l]) == (rs["solved"], rs["reused"]), (k, l)
+            reused += g["reused"][l]
+        d = np.abs(c["prob"][k].cpu().numpy().astype(np.float64) - ref["prob"][k]).max()
+        assert d <= P_TOL, (k, d)
+    assert reused > 0
+    srt = np.sort(ref["prob"], axis=0)
+    sure = srt[-1] - srt[-2] > 1e-3
+    assert np.array_equal(c["labels"].cpu().numpy()[sure], ref["labels"][sure])

@@ -32,6 +32,41 @@ def small_volume(D, seed, nblob=2):
     return vol, seeds
 
 
+def multi_volume(D, seed, K=3):
+    """Seeded u16 volume with K-1 blobs + noise and multi-class labels: class k seeds at the
+    centre of blob k, class K (background) near the corners."""
+    rng = np.random.default_rng([23, seed])
+    z, y, x = np.meshgrid(*(np.arange(D),) * 3, indexing="ij")
+    g = np.full((D, D, D), 0.15)
+    labels = np.zeros((D, D, D), np.uint8)
+    for k in range(1, K):
+        c = rng.uniform(0.3, 0.7, 3) * D
+        r = rng.uniform(0.12, 0.2) * D
+        g[(z - c[0]) ** 2 + (y - c[1]) ** 2 + (x - c[2]) ** 2 < r * r] = 0.3 + 0.5 * k / K
+        cs = np.round(c).astype(int)
+        labels[cs[0], cs[1], cs[2]] = k
+        labels[cs[0], cs[1], min(cs[2] + 1, D - 1)] = k
+    g = np.clip(g + rng.normal(0, 0.03, g.shape), 0, 1)
+    labels[1, 1, 1] = labels[D - 2, D - 2, D - 2] = labels[1, D - 2, 1] = K
+    return np.rint(g * 65535).astype(np.uint16), labels
+
+
+def test_multiclass_fields_partition_seeds():
+    """K = 3 on a 3-level volume.  Without pruning every class field keeps its own seeds at 1
+    and the other classes' seeds at 0 (P:107 one-vs-rest), so each seed voxel gets its own
+    class from the argmax; with H_p, dt pruning never fires and a pruned brick
+    carries its ancestor's field (R26), so seeds there are only approximately kept."""
+    vol, lab = multi_volume(32, 3)
+    o = ho.hier_segment_labels(vol, lab, 3, s=8, e=1.5, beta=50.0, tol=1e-9, prune=False)
+    for k in range(3):
+        assert np.all(o["prob"][k][lab == k + 1] == 1.0)
+        assert np.all(o["prob"][k][(lab > 0) & (lab != k + 1)] == 0.0)
+    assert np.array_equal(o["labels"][lab > 0], lab[lab > 0])
+    p = ho.hier_segment_labels(vol, lab, 3, s=8, e=1.5, beta=50.0, tol=1e-9, t_hom=0.3)
+    assert all(st["pruned_dt"] == 0 for k in range(3) for st in p["stats"][k])
+    assert sum(st["pruned_hom"] for k in range(3) for st in p["stats"][k]) > 0
+
+
 def test_single_level_is_the_plain_random_walker():
     """Eq. 1: D = s -> the root solve of the whole volume."""
     vol, seeds = small_volume(16, 0)
@@ -153,3 +188,17 @@ def test_incremental_conflict_vetoes_reuse():
     new[0, 0, 0], new[0, 0, 1] = 1, 2           # fg + bg in one root voxel: a new conflict
     inc = ho.hier_segment(vol, new, s=8, e=1.5, beta=50.0, tol=1e-9, prev=first)
     assert inc["stats"][-1]["reused"] == 0 and inc["stats"][-1]["conflict"] == 1
+
+
+def test_multiclass_two_classes_is_the_binary_run():
+    """K = 2: class 1's probability is the binary run with class-1 seeds foreground; the
+    argmax labels agree with thresholding the binary field at 0.5 wherever the two class
+    fields are not tied."""
+    vol, seeds = small_volume(32, 8)
+    lab = np.where(seeds == 1, 1, np.where(seeds == 2, 2, 0)).astype(np.uint8)
+    mc = ho.hier_segment_labels(vol, lab, 2, s=8, e=1.5, beta=50.0, tol=1e-9)
+    bi = ho.hier_segment(vol, seeds, s=8, e=1.5, beta=50.0, tol=1e-9, t_bin=-1.0)
+    np.testing.assert_allclose(mc["prob"][0], bi["prob"], atol=1e-12)
+    sure = np.abs(mc["prob"][0] - mc["prob"][1]) > 1e-6
+    assert np.array_equal((mc["labels"] == 1)[sure], (mc["prob"][0] > mc["prob"][1])[sure])
+    assert set(np.unique(mc["labels"])) <= {1, 2}
