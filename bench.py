@@ -367,24 +367,26 @@ def run_b200(args, rank, world, local_rank):
                      "gpu_launches": int(sum(v[0] for v in sprof.values()))}
 
     # ---------------- end to end through the API with host buffers ----------------
+    # rw_solve_bricks_host: pinned host inputs -> chunked H2D / solve / D2H pipeline -> host
+    # labels + iterations (the copies are inside the timed region, overlapped with the solve)
     h_vol = torch.from_numpy(p.vol).pin_memory()
     h_fixed = torch.from_numpy(p.fixed).pin_memory()
-    h_values = torch.from_numpy(p.values).pin_memory()
-    h_labels = torch.empty(tuple(fixed.shape), dtype=torch.uint8).pin_memory()
-    h_iters = torch.empty((1, BATCH), dtype=torch.int32).pin_memory()
-    d_vol, d_fixed, d_values = torch.empty_like(vol), torch.empty_like(fixed), torch.empty_like(values)
+    h_values = torch.from_numpy(p.values[0]).pin_memory()
+    h_out = dict(prob=None, labels=torch.empty(tuple(fixed.shape), dtype=torch.uint8).pin_memory(),
+                 iters=torch.empty((1, BATCH), dtype=torch.int32).pin_memory(),
+                 resid=torch.empty((1, BATCH), dtype=torch.float32).pin_memory(),
+                 status=torch.empty((1, BATCH), dtype=torch.int32).pin_memory())
+    h_ws = api.alloc_workspace(api.lib().rw_solve_host_workspace_bytes(
+        BATCH, api.rw_dims(N, N, N), api.DTYPES[torch.uint16], args.e2e_chunk), dev)
 
     def e2e_step():
-        d_vol.copy_(h_vol, non_blocking=True)
-        d_fixed.copy_(h_fixed, non_blocking=True)
-        d_values.copy_(h_values, non_blocking=True)
-        rwb.solve_bricks(d_fixed, d_values, vol=d_vol, beta=p.beta, eps=p.eps, tol=p.tol,
-                         max_iter=p.max_iter, workspace=ws, out=out, stream=stream)
-        h_labels.copy_(out["labels"], non_blocking=True)
-        h_iters.copy_(out["iters"], non_blocking=True)
+        rwb.solve_bricks_host(h_fixed, h_values, h_vol, beta=p.beta, eps=p.eps, tol=p.tol,
+                              max_iter=p.max_iter, chunk=args.e2e_chunk, labels=True,
+                              workspace=h_ws, out=h_out, device=dev, stream=stream)
 
     e2e_step()
     torch.cuda.synchronize()
+    assert torch.equal(h_out["iters"], out["iters"].cpu()), "host pipeline differs from the device solve"
     barrier()
     e0.record(stream)
     for _ in range(args.steps):
@@ -394,7 +396,8 @@ def run_b200(args, rank, world, local_rank):
     ems, _ = reduce_metric(e0.elapsed_time(e1), vox_iters, dev)
     e2e_value = work_all / (ems / args.steps / 1000.0)
     h2d = h_vol.numel() * h_vol.element_size() + h_fixed.numel() + h_values.numel() * 4
-    d2h = h_labels.numel() + h_iters.numel() * 4
+    d2h = h_out["labels"].numel() + BATCH * 12
+    del h_ws
 
     # ---------------- rows a8 / a9 beside the headline (not part of the step) ----------------
     rows = None if (args.no_rows or rank != 0) else pyramid_and_queue(dev)
@@ -426,7 +429,9 @@ def run_b200(args, rank, world, local_rank):
         "pyramid_queue": rows,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps},
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps,
+                "api": "rw_solve_bricks_host (pinned host buffers, chunked H2D/solve/D2H overlap)",
+                "chunk": args.e2e_chunk or -(-BATCH // 16)},
         "gpu_launches": int(gpu_launches),
         "clocks": clocks,
     }
@@ -437,6 +442,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--e2e-chunk", type=int, default=0,
+                    help="bricks per pipeline chunk of the e2e host-buffer solve (0: batch/16)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workers", type=int, default=min(16, os.cpu_count() or 1))

@@ -157,6 +157,33 @@ rw_status rw_solve_bricks(int32_t batch, rw_dims d, const void* vol, rw_dtype dt
                           float* resid, int32_t* status, uint8_t* labels, void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * rw_solve_bricks_host -- rw_solve_bricks (nrhs = 1, weights from vol) on HOST buffers with
+ *   the transfers pipelined against the solve ("H2D on a copy stream
+ *   overlaps compute on the compute stream (events). Results go D2H"; P:105 brick-wise
+ *   loading).  The batch is cut into chunks of `chunk` bricks (0: batch/16 rounded up):
+ *   chunk c+2's inputs go host->device on a copy stream while chunk c is solved and chunk
+ *   c-1's results go device->host on a second copy stream.  Chunk solves alternate between
+ *   two compute streams and two solve workspaces, so chunk c+1's resident clusters start on
+ *   the SMs chunk c leaves idle in its tail.  Device memory is O(chunk): three-slot rings of
+ *   input and output chunks, two chunk workspaces, per-brick scalars of the batch.
+ *   vol_h, fixed_h, values_h   host [batch][n] (page-locked for overlap; pageable works).
+ *   prob_h / labels_h          out host fp32 / u8 [batch][n], either may be NULL.
+ *   iters_h out host int32 [batch];  resid_h, status_h  out host [batch] or NULL.
+ *   workspace  device, >= rw_solve_host_workspace_bytes(batch, d, dtype, chunk).
+ *   Results are identical to rw_solve_bricks on the same bricks (every brick is solved
+ *   independently, fixed-order reductions).  The call blocks until the outputs are in host
+ *   memory; `stream` is waited on at entry and waits for the call's work at exit.
+ *   Errors: as rw_solve_bricks; RW_EINVAL for chunk < 0.
+ * ---------------------------------------------------------------------------------- */
+size_t rw_solve_host_workspace_bytes(int32_t batch, rw_dims d, rw_dtype dtype, int32_t chunk);
+rw_status rw_solve_bricks_host(int32_t batch, rw_dims d, const void* vol_h, rw_dtype dtype,
+                               rw_norm nm, const uint8_t* fixed_h, const float* values_h,
+                               float beta, float eps, float tol, int32_t max_iter,
+                               int32_t tol_mode, int32_t chunk, void* workspace, size_t ws_bytes,
+                               float* prob_h, uint8_t* labels_h, int32_t* iters_h,
+                               float* resid_h, int32_t* status_h, void* stream);
+
+/* ------------------------------------------------------------------------------------
  * rw_solve_labels -- multi-class random walker, P:79 / P:107: class k's probability is the
  *   solution with class-k seeds = 1 and all other seeds = 0; class = argmax.  Classes are
  *   1..K (K in 2..65); classes 1..K-1 are solved as K-1 right-hand sides sharing one

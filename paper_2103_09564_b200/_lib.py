@@ -9,7 +9,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librw.so")
+# RW_LIB_PATH: an in-tree experiment build (tools/ A/B runs); default the package's librw.so
+LIB_PATH = os.environ.get("RW_LIB_PATH") or os.path.join(HERE, "librw.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rw.h")
 
 
@@ -66,6 +67,9 @@ SIGNATURES = {
     "rw_hier_workspace_bytes": (SZ, [rw_dims, I32, rw_hier_config]),
     "rw_hier_segment": (I32, [P, I32, rw_norm, rw_dims, P, rw_hier_config, P, SZ, P,
                               C.POINTER(rw_hier_stats), P]),
+    "rw_solve_host_workspace_bytes": (SZ, [I32, rw_dims, I32, I32]),
+    "rw_solve_bricks_host": (I32, [I32, rw_dims, P, I32, rw_norm, P, P, F32, F32, F32, I32, I32,
+                                   I32, P, SZ, P, P, P, P, P, P]),
     "rw_hier_labels_workspace_bytes": (SZ, [rw_dims, I32, I32, rw_hier_config]),
     "rw_hier_segment_labels": (I32, [P, I32, rw_norm, rw_dims, P, I32, rw_hier_config, P, SZ,
                                      P, P, P, C.POINTER(rw_hier_stats), P]),

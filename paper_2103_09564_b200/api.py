@@ -187,6 +187,58 @@ def solve_bricks(fixed, values, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6
     return out
 
 
+def _need_host(t, name, dtype=None):
+    if t is None:
+        return
+    if t.is_cuda:
+        raise ValueError(f"{name} must be a host (CPU) tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def solve_bricks_host(fixed, values, vol, beta=100.0, eps=1e-6, tol=1e-6, max_iter=5000,
+                      tol_mode=0, norm=None, chunk=0, prob=True, labels=False, workspace=None,
+                      out=None, device=None, stream=None):
+    """rw_solve_bricks_host: the same solve from HOST tensors (pin them for overlap), with the
+    host<->device copies pipelined against the chunked solve (rw.h).  fixed u8 / values fp32 /
+    vol [B,nz,ny,nx] on the CPU.  Returns dict of CPU tensors prob [1,B,...] (if prob),
+    labels [B,...] (if labels), iters / resid / status [1,B].  Blocks until they are filled."""
+    _need_host(fixed, "fixed", torch.uint8)
+    if values.dim() == 5:
+        values = values[0]
+    _need_host(values, "values", torch.float32)
+    _need_host(vol, "vol")
+    if fixed.dim() != 4 or tuple(values.shape) != tuple(fixed.shape) or \
+            tuple(vol.shape) != tuple(fixed.shape):
+        raise ValueError("fixed, values and vol must all be [B,nz,ny,nx]")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    B = fixed.shape[0]
+    d = dims_of(fixed)
+    dt = DTYPES[vol.dtype]
+    sc, of = norm or DEFAULT_NORM[vol.dtype]
+    need = lib().rw_solve_host_workspace_bytes(B, d, dt, int(chunk))
+    if need == 0:
+        raise ValueError("solve_bricks_host: bad dims / dtype / chunk")
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need, dev)
+    if out is None:
+        pin = fixed.is_pinned()
+        mk = lambda shp, dt_: torch.empty(shp, dtype=dt_, pin_memory=pin)
+        out = dict(prob=mk((1,) + tuple(fixed.shape), torch.float32) if prob else None,
+                   labels=mk(tuple(fixed.shape), torch.uint8) if labels else None,
+                   iters=mk((1, B), torch.int32), resid=mk((1, B), torch.float32),
+                   status=mk((1, B), torch.int32))
+    st = lib().rw_solve_bricks_host(B, d, _ptr(vol), dt, rw_norm(sc, of), _ptr(fixed), _ptr(values),
+                                    beta, eps, tol, max_iter, tol_mode, int(chunk),
+                                    _ptr(workspace), workspace.numel(), _ptr(out.get("prob")),
+                                    _ptr(out.get("labels")), _ptr(out["iters"]), _ptr(out["resid"]),
+                                    _ptr(out["status"]), _stream(stream, dev))
+    check(st, "rw_solve_bricks_host")
+    return out
+
+
 def solve_labels(seeds, K, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6, max_iter=5000,
                  tol_mode=0, norm=None, workspace=None, stream=None):
     """rw_solve_labels: seeds u8 [B,nz,ny,nx] (0 unseeded, 1..K).  Returns dict(prob

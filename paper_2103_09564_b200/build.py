@@ -41,12 +41,17 @@ def up_to_date():
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """`out`: build an experiment variant elsewhere (tools/ A/B runs load it through
+    RW_LIB_PATH); RW_NVCC_DEFS adds -D flags for such variants."""
+    lib = out or LIB
+    if out is None and not force and up_to_date():
         return LIB
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-pthread", "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
+           "-Xcompiler", "-pthread", "-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp",
            *sources()]
+    for d in os.environ.get("RW_NVCC_DEFS", "").split():
+        cmd.insert(1, d)
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     if os.environ.get("RW_RES_TIMING"):      # debug: phase timers in the resident kernel
@@ -56,9 +61,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
     if verbose:
         sys.stderr.write(r.stdout + r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv))
+    o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force=True, verbose="--verbose" in sys.argv, out=o))

@@ -634,6 +634,159 @@ rw_status rw_solve_bricks(int32_t batch, rw_dims d, const void* vol, rw_dtype dt
                     (cudaStream_t)stream, ws_bytes);
 }
 
+static size_t dtype_size(rw_dtype t) { return t == RW_U8 ? 1 : (t == RW_F32 ? 4 : 2); }
+
+// ------------------------------------------------------------ host-buffer pipelined solve
+namespace {
+
+struct HostLayout {
+  size_t in_vol, in_fixed, in_val, out_prob, out_lab, iters, resid, status, ws0, ws1, total;
+  size_t slot_vol, slot_fixed, slot_val, slot_prob, slot_lab, ws_one;
+};
+
+// inputs and outputs of `chunk` bricks in rings of 3 slots, two solve workspaces of
+// `chunk` bricks, per-brick scalars of the whole batch
+HostLayout host_layout(int batch, rw_dims d, rw_dtype dtype, int chunk) {
+  HostLayout L{};
+  const size_t n = (size_t)d.nx * d.ny * d.nz, c = (size_t)chunk;
+  L.slot_vol = up(c * n * dtype_size(dtype));
+  L.slot_fixed = up(c * n);
+  L.slot_val = up(c * n * 4);
+  L.slot_prob = up(c * n * 4);
+  L.slot_lab = up(c * n);
+  L.ws_one = up(layout(make_plan(chunk, d, 1), false, 0).total);
+  size_t o = 0;
+  L.in_vol = o; o += 3 * L.slot_vol;
+  L.in_fixed = o; o += 3 * L.slot_fixed;
+  L.in_val = o; o += 3 * L.slot_val;
+  L.out_prob = o; o += 3 * L.slot_prob;
+  L.out_lab = o; o += 3 * L.slot_lab;
+  L.iters = o; o += up((size_t)batch * 4);
+  L.resid = o; o += up((size_t)batch * 4);
+  L.status = o; o += up((size_t)batch * 4);
+  L.ws0 = o; o += L.ws_one;
+  L.ws1 = o; o += L.ws_one;
+  L.total = o;
+  return L;
+}
+
+int host_chunk(int batch, int chunk) {
+  if (chunk > 0) return std::min(chunk, batch);
+  return std::max(1, (batch + 15) / 16);   // auto: 16 chunks (measured: 32 of 512 cfg2 bricks)
+}
+
+}  // namespace
+
+size_t rw_solve_host_workspace_bytes(int32_t batch, rw_dims d, rw_dtype dtype, int32_t chunk) {
+  if (!dims_ok(d) || batch < 1 || chunk < 0 || dtype < RW_U8 || dtype > RW_F32) return 0;
+  return host_layout(batch, d, dtype, host_chunk(batch, chunk)).total;
+}
+
+rw_status rw_solve_bricks_host(int32_t batch, rw_dims d, const void* vol_h, rw_dtype dtype,
+                               rw_norm nm, const uint8_t* fixed_h, const float* values_h,
+                               float beta, float eps, float tol, int32_t max_iter,
+                               int32_t tol_mode, int32_t chunk, void* workspace, size_t ws_bytes,
+                               float* prob_h, uint8_t* labels_h, int32_t* iters_h,
+                               float* resid_h, int32_t* status_h, void* stream) {
+  rw_status v = validate_solve(batch, d, vol_h, dtype, nullptr, 1, eps, tol, max_iter, tol_mode,
+                               workspace);
+  if (v != RW_OK) return v;
+  if (!vol_h || !fixed_h || !values_h || !iters_h)
+    return fail(RW_EINVAL, "rw_solve_bricks_host: vol, fixed, values and iters must be non-NULL");
+  if (chunk < 0) return fail(RW_EINVAL, "rw_solve_bricks_host: chunk must be >= 0");
+  const int C = host_chunk(batch, chunk);
+  const HostLayout L = host_layout(batch, d, dtype, C);
+  if (ws_bytes < L.total)
+    return fail(RW_ENOMEM, "rw_solve_bricks_host: workspace too small: %zu < %zu bytes", ws_bytes,
+                L.total);
+  char* ws = (char*)workspace;
+  const size_t n = (size_t)d.nx * d.ny * d.nz, es = dtype_size(dtype);
+  const int nch = (batch + C - 1) / C;
+  cudaStream_t user = (cudaStream_t)stream;
+  // streams: H2D copies, D2H copies, two compute streams (chunk c on cs[c % 2], so chunk c+1's
+  // solve can start on SMs chunk c leaves idle in its tail); events per chunk
+  cudaStream_t h2d = nullptr, d2h = nullptr, cs[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t e_user = nullptr;
+  auto cleanup = [&]() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (e_user) cudaEventDestroy(e_user);
+    for (cudaStream_t t : {h2d, d2h, cs[0], cs[1]})
+      if (t) cudaStreamDestroy(t);
+  };
+  auto run = [&]() -> rw_status {
+    for (cudaStream_t* t : {&h2d, &d2h, &cs[0], &cs[1]})
+      RW_CK(cudaStreamCreateWithFlags(t, cudaStreamNonBlocking));
+    ev.assign((size_t)3 * nch, nullptr);
+    for (auto& e : ev) RW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    RW_CK(cudaEventCreateWithFlags(&e_user, cudaEventDisableTiming));
+    cudaEvent_t* ev_in = ev.data();              // chunk's inputs are on the device
+    cudaEvent_t* ev_sol = ev.data() + nch;       // chunk solved (input slot + workspace free)
+    cudaEvent_t* ev_out = ev.data() + 2 * nch;   // chunk's outputs are on the host
+    RW_CK(cudaEventRecord(e_user, user));        // work the caller enqueued before this call
+    for (cudaStream_t t : {h2d, d2h, cs[0], cs[1]}) RW_CK(cudaStreamWaitEvent(t, e_user, 0));
+    auto nb_of = [&](int c) { return std::min(C, batch - c * C); };
+    auto enqueue_in = [&](int c) -> rw_status {
+      if (c >= nch) return RW_OK;
+      if (c >= 3) RW_CK(cudaStreamWaitEvent(h2d, ev_sol[c - 3], 0));   // slot c % 3 free
+      const size_t b0 = (size_t)c * C, nb = (size_t)nb_of(c), k = (size_t)(c % 3);
+      RW_CK(cudaMemcpyAsync(ws + L.in_vol + k * L.slot_vol, (const char*)vol_h + b0 * n * es,
+                            nb * n * es, cudaMemcpyHostToDevice, h2d));
+      RW_CK(cudaMemcpyAsync(ws + L.in_fixed + k * L.slot_fixed, fixed_h + b0 * n, nb * n,
+                            cudaMemcpyHostToDevice, h2d));
+      RW_CK(cudaMemcpyAsync(ws + L.in_val + k * L.slot_val, values_h + b0 * n, nb * n * 4,
+                            cudaMemcpyHostToDevice, h2d));
+      RW_CK(cudaEventRecord(ev_in[c], h2d));
+      return RW_OK;
+    };
+    for (int c = 0; c < 2; ++c) {
+      rw_status r = enqueue_in(c);
+      if (r != RW_OK) return r;
+    }
+    for (int c = 0; c < nch; ++c) {
+      rw_status r = enqueue_in(c + 2);
+      if (r != RW_OK) return r;
+      const int nb = nb_of(c);
+      const size_t b0 = (size_t)c * C, k = (size_t)(c % 3);
+      cudaStream_t s = cs[c % 2];
+      RW_CK(cudaStreamWaitEvent(s, ev_in[c], 0));
+      if (c >= 3) RW_CK(cudaStreamWaitEvent(s, ev_out[c - 3], 0));      // output slot free
+      float* prob = (float*)(ws + L.out_prob + k * L.slot_prob);
+      uint8_t* lab = (uint8_t*)(ws + L.out_lab + k * L.slot_lab);
+      int32_t* it = (int32_t*)(ws + L.iters) + b0;
+      float* rs = (float*)(ws + L.resid) + b0;
+      int32_t* stt = (int32_t*)(ws + L.status) + b0;
+      const rw::Plan P = make_plan(nb, d, 1);
+      const Layout Lw = layout(P, false, 0);
+      r = solve_core(nb, d, ws + L.in_vol + k * L.slot_vol, dtype, nm, nullptr,
+                     (const uint8_t*)(ws + L.in_fixed + k * L.slot_fixed),
+                     (const float*)(ws + L.in_val + k * L.slot_val), 1, beta, eps, tol, max_iter,
+                     tol_mode, nullptr, ws + (c % 2 ? L.ws1 : L.ws0), Lw, P, prob, it, rs, stt,
+                     labels_h ? lab : nullptr, s, L.ws_one);
+      if (r != RW_OK) return r;
+      RW_CK(cudaEventRecord(ev_sol[c], s));
+      RW_CK(cudaStreamWaitEvent(d2h, ev_sol[c], 0));
+      if (prob_h)
+        RW_CK(cudaMemcpyAsync(prob_h + b0 * n, prob, nb * n * 4, cudaMemcpyDeviceToHost, d2h));
+      if (labels_h)
+        RW_CK(cudaMemcpyAsync(labels_h + b0 * n, lab, nb * n, cudaMemcpyDeviceToHost, d2h));
+      RW_CK(cudaEventRecord(ev_out[c], d2h));
+    }
+    RW_CK(cudaMemcpyAsync(iters_h, ws + L.iters, (size_t)batch * 4, cudaMemcpyDeviceToHost, d2h));
+    if (resid_h)
+      RW_CK(cudaMemcpyAsync(resid_h, ws + L.resid, (size_t)batch * 4, cudaMemcpyDeviceToHost, d2h));
+    if (status_h)
+      RW_CK(cudaMemcpyAsync(status_h, ws + L.status, (size_t)batch * 4, cudaMemcpyDeviceToHost, d2h));
+    RW_CK(cudaEventRecord(e_user, d2h));
+    RW_CK(cudaStreamWaitEvent(user, e_user, 0));   // the caller's stream sees the whole call
+    RW_CK(cudaStreamSynchronize(d2h));
+    return RW_OK;
+  };
+  const rw_status r = run();
+  cleanup();
+  return r;
+}
+
 rw_status rw_solve_labels(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype,
                           rw_norm nm, const float* W, const uint8_t* seeds, int32_t K,
                           float beta, float eps, float tol, int32_t max_iter,
@@ -665,7 +818,6 @@ rw_status rw_solve_labels(int32_t batch, rw_dims d, const void* vol, rw_dtype dt
   return RW_OK;
 }
 
-static size_t dtype_size(rw_dtype t) { return t == RW_U8 ? 1 : (t == RW_F32 ? 4 : 2); }
 
 // ------------------------------------------------------------------ hierarchical driver
 namespace {

@@ -1,0 +1,11 @@
+# A/B of resident-kernel variants built into abtest/ (librw_<v>.so and timing builds
+# librw_t<v>.so): correctness + throughput on 512 cfg2 bricks, phase cycles on 64
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/${AB_TAG:-ab}
+mkdir -p $O
+for v in ${AB_VARIANTS:-old new}; do
+  RW_LIB_PATH=$PWD/abtest/librw_$v.so timeout 300 python tools/res_time.py 512 > $O/$v.log 2>&1
+  echo "== $v rc=$?"; grep -E '"resident"|max_abs' $O/$v.log | cut -c1-200
+  RW_LIB_PATH=$PWD/abtest/librw_t$v.so RW_DEBUG_RES_TIMING=1 timeout 300 python tools/res_time.py 64 > $O/t$v.log 2>&1
+  grep "res-timing" $O/t$v.log | head -4
+done
