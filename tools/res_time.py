@@ -35,6 +35,8 @@ for name in ("resident", "streaming"):
                           "iters": [int(it.min()), float(np.median(it)), int(it.max())],
                           "kernels": res[name]["kernels"]}), flush=True)
 a, b = res["resident"], res["streaming"]
+if os.environ.get("RES_DUMP"):     # A/B: keep the resident outputs for a bitwise comparison
+    np.savez(os.environ["RES_DUMP"], prob=a["prob"], it=a["it"])
 print(json.dumps({"max_abs_dprob": float(np.abs(a["prob"] - b["prob"]).max()),
                   "max_abs_diters": int(np.abs(a["it"].astype(int) - b["it"].astype(int)).max()),
                   "speedup": b["ms"] / a["ms"]}))
