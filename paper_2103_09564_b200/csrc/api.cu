@@ -1165,7 +1165,7 @@ rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int
     CUtensorMap map;
     const int es = (int)dtype_size(dtype);
     const bool use_tma = ((size_t)nx[l0] * es) % 16 == 0 && ((uintptr_t)in & 15u) == 0 &&
-                         tmap(&map, in, es == 4 ? 4 : es, nx[l0], ny[l0], lzc, 32, 32, 32);
+                         tmap(&map, in, es == 4 ? 4 : es, nx[l0], ny[l0], lzc, 32, 32, 16);
     RW_TIMED(RW_K_PYRAMID, s, 1,
              rw::launch_pyramid_group(in, dtype, nx[l0], ny[l0], nz[l0], lz0, lzc, L, o,
                                       use_tma ? &map : nullptr, s));

@@ -70,23 +70,29 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
   using A = typename std::conditional<std::is_same<T, float>::value, float, int>::type;
   extern __shared__ __align__(128) unsigned char dsm[];
   const T* box = reinterpret_cast<const T*>(dsm);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(dsm + 32 * 32 * 32 * sizeof(T));
   if (USE_TMA) {
-    uint64_t* bar = reinterpret_cast<uint64_t*>(dsm + 32 * 32 * 32 * sizeof(T));
+    // two 32x32x16 loads on two mbarriers: level 1's lower half (output planes 0..7)
+    // starts as soon as the lower half of the box has landed
     if (threadIdx.x == 0) {
-      mbar_init(bar, 1);
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
       fence_mbar_init();
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      mbar_arrive_expect_tx(bar, 32 * 32 * 32 * sizeof(T));
-      tma_load_3d(dsm, &map, bar, blockIdx.x * 32, blockIdx.y * 32, blockIdx.z * 32);
+      constexpr uint32_t half = 32 * 32 * 16 * sizeof(T);
+      mbar_arrive_expect_tx(&bar[0], half);
+      tma_load_3d(dsm, &map, &bar[0], blockIdx.x * 32, blockIdx.y * 32, blockIdx.z * 32);
+      mbar_arrive_expect_tx(&bar[1], half);
+      tma_load_3d(dsm + half, &map, &bar[1], blockIdx.x * 32, blockIdx.y * 32, blockIdx.z * 32 + 16);
     }
-    mbar_wait(bar, 0);
   }
-  // level buffers 1..4 (16^3, 8^3, 4^3, 2^3) in one array; offsets computed, not indexed
+  // level buffers 1..4 (16^3, 8^3, 4^3, 2^3) in one array of the input type (every level
+  // mean fits it), so three CTAs of a 2-byte type fit one SM; offsets computed, not indexed
   // through a pointer table (which would live in local memory)
-  __shared__ A lv[4096 + 512 + 64 + 8];
-  A* s1 = lv;
+  __shared__ T lv[4096 + 512 + 64 + 8];
+  T* s1 = lv;
   const long long pin = (long long)nx * ny;
   // level 1 from global
   {
@@ -94,6 +100,7 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
     T* out = (T*)o.p[0];
     const long long po = (long long)o.nx[0] * o.ny[0];
     for (int idx = threadIdx.x; idx < 4096; idx += 256) {
+      if (USE_TMA && (idx & 2047) < 256) mbar_wait(&bar[idx >> 11], 0);   // half 0, then 1
       const int lx = idx & 15, ly = (idx >> 4) & 15, lz = idx >> 8;
       const int X = X0 + lx, Y = Y0 + ly, Z = Z0 + lz;
       A v = 0;
@@ -123,7 +130,7 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
         out[(long long)Z * po + (long long)Y * o.nx[0] + X] = r;
         v = (A)r;
       }
-      s1[idx] = v;
+      s1[idx] = (T)v;
     }
   }
   // levels 2..L from shared memory
@@ -134,8 +141,8 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
     const int e = 16 >> l;                // box extent at this level
     const int X0 = blockIdx.x * e, Y0 = blockIdx.y * e, Z0 = (zb >> (l + 1)) + blockIdx.z * e;
     const int off_src = l == 1 ? 0 : (l == 2 ? 4096 : (l == 3 ? 4608 : 4672));
-    const A* src = lv + off_src;
-    A* dst = (l < 4) ? lv + off_src + pe3(l) : nullptr;
+    const T* src = lv + off_src;
+    T* dst = (l < 4) ? lv + off_src + pe3(l) : nullptr;
     T* out = (T*)o.p[l];
     const long long po = (long long)o.nx[l] * o.ny[l];
     const int pe = 2 * e;                 // child box extent
@@ -146,7 +153,7 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
       const int zend = (zb + zc + (1 << l) - 1) >> l;   // slab end at the child level
       if (2 * X + 1 < o.nx[l - 1] && 2 * Y + 1 < o.ny[l - 1] && 2 * Z + 1 < o.nz[l - 1] &&
           2 * Z + 1 < zend) {                           // interior: 8 children present
-        const A* c = src + ((2 * lz) * pe + 2 * ly) * pe + 2 * lx;
+        const T* c = src + ((2 * lz) * pe + 2 * ly) * pe + 2 * lx;
         const int pp = pe * pe;
         T r;
         if (std::is_same<T, float>::value) {
@@ -164,13 +171,13 @@ k_pyramid(const T* __restrict__ in, int nx, int ny, int nz, int zb, int zc, int 
         const T r = mean8<T, A>([&](int dx, int dy, int dz, A& val) {
           const int x = 2 * X + dx, y = 2 * Y + dy, z = 2 * Z + dz;
           if (x >= o.nx[l - 1] || y >= o.ny[l - 1] || z >= o.nz[l - 1]) return false;
-          val = src[((2 * lz + dz) * pe + (2 * ly + dy)) * pe + (2 * lx + dx)];
+          val = (A)src[((2 * lz + dz) * pe + (2 * ly + dy)) * pe + (2 * lx + dx)];
           return true;
         });
         out[(long long)Z * po + (long long)Y * o.nx[l] + X] = r;
         v = (A)r;
       }
-      if (dst) dst[idx] = v;
+      if (dst) dst[idx] = (T)v;
     }
   }
 }
@@ -180,7 +187,7 @@ static cudaError_t launch_t(const void* in, int nx, int ny, int nz, int zb, int 
                            const PyrOut& o, const CUtensorMap* map, cudaStream_t s) {
   const dim3 g((nx + 31) / 32, (ny + 31) / 32, (zc + 31) / 32);
   if (map) {
-    const int smem = 32 * 32 * 32 * sizeof(T) + 8;
+    const int smem = 32 * 32 * 32 * sizeof(T) + 16;
     static int attr = 0;
     if (attr < smem) {
       const cudaError_t e = cudaFuncSetAttribute(k_pyramid<T, true>,
