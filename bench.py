@@ -41,7 +41,8 @@ BATCH, N = 512, 64
 # algorithmic bytes per active voxel per launch.  Pass A (weights recomputed
 # from the u16 intensities, VM_U16) reads r, p, dinv, x (16 B) + the intensity (2 B) and
 # writes p, x, q (12 B); at k = 0 there is no x traffic.  Pass B reads r, q, dinv, writes r.
-BYTES_A, BYTES_A0, BYTES_B = 30, 22, 16
+BYTES_A, BYTES_A0, BYTES_B = 30, 22, 16       # two-pass streaming CG (RW_OPT_STREAM_PASSES 2)
+BYTES_1, BYTES_10 = 38, 26                      # one-pass (default): pass k >= 1, pass 0
 # fp32 flops per voxel-iteration of the resident kernel: edge-difference
 # SpMV 6 sub + 6 mul/fma (18), p = dinv r + beta p (3), x += alpha p (2), r -= alpha q (2),
 # dots p.q (2), r.(dinv r) (3), r.r (2)
@@ -161,9 +162,12 @@ def run_reference(args, rank, world):
 def streaming_roofline(kms, vox_iters, steps, nbr):
     """HBM roofline of the streaming passes from the profile of `steps` solves."""
     vox = float(N ** 3)
-    alg_A = steps * (BYTES_A * vox_iters - (BYTES_A - BYTES_A0) * vox * nbr)
-    alg_B = steps * BYTES_B * vox_iters
-    alg = {"passA": alg_A, "passB": alg_B}
+    one = kms.get("passB", 0.0) == 0.0
+    if one:   # one pass per iteration: iters_b full passes + pass 0 per brick (rw.h)
+        alg = {"passA": steps * (BYTES_1 * vox_iters + BYTES_10 * vox * nbr), "passB": 0.0}
+    else:
+        alg = {"passA": steps * (BYTES_A * vox_iters - (BYTES_A - BYTES_A0) * vox * nbr),
+               "passB": steps * BYTES_B * vox_iters}
     dom = max(("passA", "passB"), key=lambda k: kms.get(k, 0.0))
     peak, peak_kind = measured_peak()
     achieved = alg[dom] / (kms[dom] / 1000.0) / 1e9
@@ -171,7 +175,9 @@ def streaming_roofline(kms, vox_iters, steps, nbr):
             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
             "traffic": ncu_traffic(dom),
             "per_kernel_ms_per_step": {k: v / steps for k, v in kms.items() if v > 0},
-            "alg_bytes_per_voxel_iter": {"passA": BYTES_A, "passB": BYTES_B}}
+            "alg_bytes_per_voxel_iter": ({"passA": BYTES_1, "passA_k0": BYTES_10} if one else
+                                         {"passA": BYTES_A, "passB": BYTES_B}),
+            "passes_per_iteration": 1 if one else 2}
 
 
 def ncu_traffic(kernel):

@@ -307,8 +307,8 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
 /* ------------------------------------------------------------------------------------
  * Solver selection.  rw_solve_bricks / rw_solve_labels run one of two implementations of
  * the same Jacobi-PCG with the same stopping rule, status codes and outputs:
- *   streaming  -- CG state in HBM, two fused passes per iteration (any brick shape, any
- *                 nrhs);
+ *   streaming  -- CG state in HBM, one fused pass per iteration by default (any brick
+ *                 shape, any nrhs, see RW_OPT_STREAM_PASSES);
  *   resident   -- one thread-block cluster per brick keeps the whole CG state on chip
  *                 (shared + tensor memory, registers) for all iterations (SURVEY 8(f)
  *                 f2/f4); bricks of 64x64x64 or 32x32x32, nrhs == 1, device permitting.
@@ -327,11 +327,20 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
  * solver replaces the recurrence residual by the true residual b - L_UU x computed in fp32
  * (and flushes the lagged x update).  Experimental: the fp32 true residual floors near
  * 1e-5 of ||b||, so tolerances below that are then never met (R5c).
+ * RW_OPT_STREAM_PASSES: 1 (default) or 2 HBM passes per streaming CG iteration.  1: pass
+ * B (r -= alpha q and its dots) is folded into the next pass A, which also forms q.D r and
+ * q.D q so that beta comes from the one-step expansion r'.z' = r.z - 2 alpha q.D r +
+ * alpha^2 q.D q of the true r.z of the same pass (38 instead of 46 bytes per voxel and
+ * iteration, one launch instead of two); the stop test uses the true ||r_k|| one pass
+ * later, so one extra SpMV runs per (rhs, brick).  2: the classical two-pass form.  The
+ * residual-replacement option implies 2.  Iteration counts and probabilities agree to the
+ * solver tolerance, not bitwise.
  * rw_resident_available(d, nrhs): 1 if the resident solver can serve this shape on the
  * current device, else 0.  Results of the two solvers agree to the solver tolerance, not
  * bitwise (different fp64 reduction trees); each is deterministic and batch-invariant.
  * ---------------------------------------------------------------------------------- */
-enum { RW_OPT_SOLVER = 0, RW_OPT_COSCHED = 1, RW_OPT_RESIDUAL_REPLACE = 2 };
+enum { RW_OPT_SOLVER = 0, RW_OPT_COSCHED = 1, RW_OPT_RESIDUAL_REPLACE = 2,
+       RW_OPT_STREAM_PASSES = 3 };
 enum { RW_SOLVER_AUTO = 0, RW_SOLVER_STREAMING = 1, RW_SOLVER_RESIDENT = 2 };
 rw_status rw_set_option(int32_t key, int64_t value);
 int64_t rw_get_option(int32_t key);

@@ -70,6 +70,26 @@ def solver(name):
         set_solver(old)
 
 
+def set_stream_passes(n):
+    """rw_set_option(RW_OPT_STREAM_PASSES): 1 (default, one fused pass per streaming CG
+    iteration) or 2 (classical passes A + B)."""
+    check(lib().rw_set_option(3, int(n)), "rw_set_option")
+
+
+def get_stream_passes():
+    return int(lib().rw_get_option(3))
+
+
+@contextlib.contextmanager
+def stream_passes(n):
+    old = get_stream_passes()
+    set_stream_passes(n)
+    try:
+        yield
+    finally:
+        set_stream_passes(old)
+
+
 def resident_available(dims, nrhs=1):
     """rw_resident_available: can the brick-resident (on-chip) solver serve this shape?"""
     nx, ny, nz = dims

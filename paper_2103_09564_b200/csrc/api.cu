@@ -54,6 +54,7 @@ int g_solver = RW_SOLVER_AUTO;
 // tolerance is never met and intervals <= 4 diverge; without it the recurrence converges and
 // the solution error stays ~1e-6 (the true residual measures the fp32 roughness of x).
 int g_rr = 0;
+int g_passes = 1;   // RW_OPT_STREAM_PASSES
 
 rw_status fail(rw_status st, const char* fmt, ...) {
   char buf[512];
@@ -107,6 +108,7 @@ rw::Plan make_plan(int B, rw_dims d, int R) {
   P.tiles_z = (d.nz + zc - 1) / zc;
   P.U = P.tiles_x * P.tiles_y * P.tiles_z;
   P.vm = rw::VM_STORED;
+  P.one = 0;
   P.hxv = P.hx;
   P.TXhv = P.TXh;
   return P;
@@ -142,10 +144,10 @@ Layout layout(const rw::Plan& P, bool weights_given, int label_K) {
   size_t o = 0;
   L.W = o;      o += weights_given ? 0 : up(3 * BN * sizeof(float));
   L.dinv = o;   o += up(BN * sizeof(float));
-  L.r = o;      o += up(RBN * sizeof(float));
+  L.r = o;      o += up(2 * RBN * sizeof(float));
   L.p = o;      o += up(2 * RBN * sizeof(float));
-  L.q = o;      o += up(RBN * sizeof(float));
-  L.PA = o;     o += up(2 * RB * P.U * sizeof(double));
+  L.q = o;      o += up(2 * RBN * sizeof(float));
+  L.PA = o;     o += up(2 * RB * P.U * 5 * sizeof(double));
   L.PB = o;     o += up(2 * RB * P.U * sizeof(double2));
   L.PS = o;     o += up(RB * P.U * sizeof(double4));
   L.status = o; o += up(RB * sizeof(int));
@@ -194,8 +196,9 @@ bool tmap(CUtensorMap* m, const void* base, int es, int nx, int ny, long long pl
 rw_status make_maps(const rw::Plan& P, const rw::Bufs& Bf, rw::Maps* M) {
   std::memset(M, 0, sizeof(*M));
   const long long BZ = (long long)P.B * P.nz, RBZ = (long long)P.R * BZ;
-  bool ok = tmap(&M->r, Bf.r, 4, P.nx, P.ny, RBZ, P.TXh, P.TY + 2) &&
+  bool ok = tmap(&M->r, Bf.r, 4, P.nx, P.ny, 2 * RBZ, P.TXh, P.TY + 2) &&
             tmap(&M->p, Bf.p, 4, P.nx, P.ny, 2 * RBZ, P.TXh, P.TY + 2) &&
+            tmap(&M->q, Bf.q, 4, P.nx, P.ny, 2 * RBZ, P.TXh, P.TY + 2) &&
             tmap(&M->x, Bf.x, 4, P.nx, P.ny, RBZ, P.TX, P.TY) &&
             tmap(&M->d, Bf.dinv, 4, P.nx, P.ny, BZ, P.TXh, P.TY + 2);
   if (ok && P.vm == rw::VM_STORED)
@@ -332,6 +335,9 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   const int vm_vol = vol ? choose_vm(P, vol, dtype) : rw::VM_STORED;
   const bool fused = res_ok && vol && rw::resident_fused(vm_vol);
   set_vm(P, res_ok ? rw::VM_STORED : choose_vm(P, vol, dtype));
+  // one pass per iteration unless (measured, tools/passes_ab.py) a single-rhs system whose
+  // tiles carry an x halo, where the two lighter passes stream faster (cfg3: 1.83 vs 1.92 s)
+  P.one = (!res_ok && g_passes == 1 && g_rr == 0 && (P.hx == 0 || P.R > 1)) ? 1 : 0;
   rw::Bufs Bf{};
   float* Wd = W ? const_cast<float*>(W) : reinterpret_cast<float*>(ws + Lw.W);
   float* dinv = reinterpret_cast<float*>(ws + Lw.dinv);
@@ -442,6 +448,7 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   }
   const int nA = (P.R + rw::passA_rc(P) - 1) / rw::passA_rc(P);
   const int nB = (P.R + 3) / 4;
+  const bool one = P.one != 0;
   st = ensure_pinned();
   if (st != RW_OK) return st;
   // Host-polled loop: every CHECK iterations the active-pair count is copied to pinned
@@ -450,19 +457,21 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   const int CHECK = 8;
   int j = 0;
   bool noxlag = false;
-  for (int k = 0; k <= max_iter; ++k) {
+  // one-pass mode: pass k decides on the state after pass k-1, so it runs to max_iter + 1
+  const int kend = one ? max_iter + 1 : max_iter;
+  for (int k = 0; k <= kend; ++k) {
     RW_CK(cudaMemsetAsync(Bf.ctr + (k & 1), 0, sizeof(int), s));
     rw::Ctl Ck = C;
     Ck.noxlag = noxlag ? 1 : 0;
     noxlag = false;
     RW_TIMED(RW_K_PASSA, s, nA, rw::launch_iteration_A(P, Bf, Ck, k, M, s));
-    if (k < max_iter) RW_TIMED(RW_K_PASSB, s, nB, rw::launch_iteration_B(P, Bf, k, s));
+    if (!one && k < max_iter) RW_TIMED(RW_K_PASSB, s, nB, rw::launch_iteration_B(P, Bf, k, s));
     // residual replacement every g_rr iterations (see k_replace); not at the very end
     if (C.rr > 0 && k < max_iter - 1 && (k + 1) % C.rr == 0) {
       RW_TIMED(RW_K_OTHER, s, 2, rw::launch_replace(P, Bf, C, k, s));
       noxlag = true;
     }
-    if (k % CHECK == CHECK - 1 || k == max_iter) {
+    if (k % CHECK == CHECK - 1 || k == kend) {
       const int slot = j & 1;
       RW_CK(cudaMemcpyAsync(g_pin.h + slot, Bf.ctr + (k & 1), sizeof(int),
                             cudaMemcpyDeviceToHost, s));
@@ -511,6 +520,11 @@ rw_status rw_set_option(int32_t key, int64_t value) {
     g_rr = (int)value;
     return RW_OK;
   }
+  if (key == RW_OPT_STREAM_PASSES) {
+    if (value != 1 && value != 2) return fail(RW_EINVAL, "rw_set_option: passes must be 1 or 2");
+    g_passes = (int)value;
+    return RW_OK;
+  }
   if (key == RW_OPT_COSCHED) {
     if (value < 0 || value > 500) return fail(RW_EINVAL, "rw_set_option: co-scheduling share must be 0..500 per mille");
     g_cosched_pm = (int)value;
@@ -525,7 +539,7 @@ rw_status rw_set_option(int32_t key, int64_t value) {
 
 int64_t rw_get_option(int32_t key) {
   return key == RW_OPT_SOLVER ? g_solver : key == RW_OPT_COSCHED ? g_cosched_pm
-         : key == RW_OPT_RESIDUAL_REPLACE ? g_rr : -1;
+         : key == RW_OPT_RESIDUAL_REPLACE ? g_rr : key == RW_OPT_STREAM_PASSES ? g_passes : -1;
 }
 
 int32_t rw_resident_available(rw_dims d, int32_t nrhs) {

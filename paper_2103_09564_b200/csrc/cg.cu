@@ -180,7 +180,7 @@ k_finalize(Plan P, Bufs Bf, Ctl C, float* resid, int* status_out, uint8_t* label
     float al = 0.f;
     // the lagged update alpha_{k-1} p_{k-1} -- unless a residual replacement flushed it
     const bool flushed = C.rr > 0 && k % C.rr == 0 && k < C.max_iter;
-    if ((st == ST_CONVERGED || st == ST_MAXITER) && k >= 1 && !flushed) {
+    if (!P.one && (st == ST_CONVERGED || st == ST_MAXITER) && k >= 1 && !flushed) {
       const double rz = warp_sum_array(pb + 2 * (((k - 1) & 1) * RBU + (long long)rb * P.U), P.U, 2, lane);
       const double pq = warp_sum_array(Bf.PA + ((k - 1) & 1) * RBU + (long long)rb * P.U, P.U, 1, lane);
       al = (float)(rz / pq);
@@ -188,7 +188,10 @@ k_finalize(Plan P, Bufs Bf, Ctl C, float* resid, int* status_out, uint8_t* label
     if (u == 0) {
       double res = 0.0;
       if (st == ST_CONVERGED || st == ST_MAXITER || st == ST_BREAKDOWN) {
-        const double rr = warp_sum_array(pb + 2 * ((k & 1) * RBU + (long long)rb * P.U) + 1, P.U, 2, lane);
+        // one-pass mode: ||r_k||^2 of the stopping iterate from pass k's partials
+        const double rr = (P.one && k >= 1)
+            ? warp_sum_array(Bf.PA + 5 * ((k & 1) * RBU + (long long)rb * P.U) + 1, P.U, 5, lane)
+            : warp_sum_array(pb + 2 * ((P.one ? 0 : (k & 1)) * RBU + (long long)rb * P.U) + 1, P.U, 2, lane);
         const double* ps = reinterpret_cast<const double*>(Bf.PS) + 4LL * rb * P.U;
         const double bb = warp_sum_array(ps, P.U, 4, lane);
         res = sqrt(rr);

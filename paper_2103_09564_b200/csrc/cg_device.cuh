@@ -172,4 +172,59 @@ __device__ inline Scal passA_scalars(const Plan& P, const Bufs& Bf, const Ctl& C
   return s;
 }
 
+// One-pass mode (passA.cu): at the start of pass k the partials of pass k-1 give the TRUE
+// r_{k-1}.z_{k-1}, ||r_{k-1}||^2 and p.q, q.D r, q.D q of iteration k-1.  Decisions run on the
+// true residual of r_{k-1} (x_{k-1} was written by pass k-1, so it is the result), alpha_{k-1}
+// = r.z / p.q, beta_{k-1} from the one-step expansion of r_k.z_k.  iters = k-1 at a stop.
+__device__ inline Scal passA_scalars1(const Plan& P, const Bufs& Bf, const Ctl& C, int rb, int k,
+                                      int u, int lane) {
+  Scal s = {0, 0.f, 0.f};
+  const int st = Bf.status[rb];
+  if (st != ST_ACTIVE) return s;
+  const long long RBU = (long long)P.R * P.B * P.U;
+  const double* ps = reinterpret_cast<const double*>(Bf.PS) + 4LL * rb * P.U;
+  const double bb = warp_sum_array(ps + 0, P.U, 4, lane);
+  const double t2 = (double)C.tol * (double)C.tol;
+  auto conv = [&](double rr) { return (C.tol_mode == 0) ? (rr <= t2 * bb) : (rr <= t2); };
+  int nst = ST_ACTIVE, it = 0;
+  double rz = 0.0, pq = 0.0, qdr = 0.0, qdq = 0.0;
+  if (k == 0) {
+    const double* pb = reinterpret_cast<const double*>(Bf.PB);     // setup: (r0.z0, r0.r0)
+    const double rr0 = warp_sum_array(pb + 2 * ((long long)rb * P.U) + 1, P.U, 2, lane);
+    const double nf = warp_sum_array(ps + 1, P.U, 4, lane);
+    const double nu = warp_sum_array(ps + 2, P.U, 4, lane);
+    if (nf == 0.0 || nu == 0.0) nst = ST_TRIVIAL;
+    else if (bb == 0.0) nst = ST_ZERO_B;
+    else if (conv(rr0)) nst = ST_CONVERGED;
+  } else {
+    const double* pa = Bf.PA + 5 * (((k - 1) & 1) * RBU + (long long)rb * P.U);
+    rz = warp_sum_array(pa + 0, P.U, 5, lane);
+    const double rr = warp_sum_array(pa + 1, P.U, 5, lane);
+    pq = warp_sum_array(pa + 2, P.U, 5, lane);
+    qdr = warp_sum_array(pa + 3, P.U, 5, lane);
+    qdq = warp_sum_array(pa + 4, P.U, 5, lane);
+    it = k - 1;
+    if (k > 1 && conv(rr)) nst = ST_CONVERGED;
+    else if (it >= C.max_iter) nst = ST_MAXITER;
+    else if (!(pq > 0.0) || !isfinite(pq) || !isfinite(rz) || !(rz > 0.0)) nst = ST_BREAKDOWN;
+  }
+  if (nst != ST_ACTIVE) {
+    if (u == 0 && lane == 0) {
+      Bf.status[rb] = nst;
+      Bf.iters[rb] = it;
+    }
+    return s;
+  }
+  if (u == 0 && lane == 0) atomicAdd(Bf.ctr + (k & 1), 1);
+  s.active = 1;
+  if (k > 0) {
+    s.alpha = (float)(rz / pq);
+    const double a = (double)s.alpha;
+    double rz1 = rz - 2.0 * a * qdr + a * a * qdq;
+    if (!(rz1 > 0.0)) rz1 = 0.0;        // below the rounding level: restart the direction
+    s.beta = (float)(rz1 / rz);
+  }
+  return s;
+}
+
 }  // namespace rw

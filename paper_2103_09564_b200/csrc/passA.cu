@@ -6,6 +6,14 @@
 //   q   = L_UU p_k   as  q_i = sum_j w_ij (p_i - p_j),  q = 0 on fixed voxels
 //   partial p_k . q  (fp64, fixed order)
 //
+// One-pass mode (ONE, the default streaming loop): pass B is folded in.  Pass k first forms
+//   r_k = r_{k-1} - alpha_{k-1} q_{k-1}   (centre and x/y halo, from double-buffered r, q)
+// then p_k, x_k, q_k as above, and writes r_k, p_k, x_k, q_k with the partials of r_k.z_k,
+// r_k.r_k, p_k.q_k, q_k.D r_k, q_k.D q_k.  alpha_k = r.z / p.q as in plain CG; beta_k uses
+// r_{k+1}.z_{k+1} = r.z - 2 alpha q.D r + alpha^2 q.D q, a one-step expansion anchored on
+// the true dot of the same pass (passA_scalars1).  One HBM pass per iteration: 38 B per
+// voxel-iteration (r, q, p, x, dinv, u16 in; r, p, x, q out) instead of 30 + 16.
+//
 // B200 design.  A CTA owns a TX x TY column tile of one brick and marches over ZC planes.
 // One elected thread streams each plane's boxes (r, p_{k-1}, x, dinv and either the three
 // weight planes or the raw intensities) into a 3-stage shared-memory ring with TMA
@@ -22,10 +30,12 @@
 
 namespace rw {
 
-template <int RC, int VM>
+template <int RC, int VM, bool ONE, int NS>
 __global__ void __launch_bounds__(RW_MAX_THREADS, 2)
 k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps M) {
   using T = typename VolT<VM>::T;
+  // NS = a_stages(P): ring depth, a compile-time constant (a runtime modulo in the ring
+  // indexing measured 7 % slower)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ float s_beta[RC], s_alpha[RC];
   __shared__ int s_act[RC];
@@ -36,12 +46,14 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bars);
   if (warp < RC) {
     Scal s = {0, 0.f, 0.f};
-    if (rbase + warp < P.R) s = passA_scalars(P, Bf, C, (rbase + warp) * P.B + b, k, u, lane);
+    if (rbase + warp < P.R)
+      s = ONE ? passA_scalars1(P, Bf, C, (rbase + warp) * P.B + b, k, u, lane)
+              : passA_scalars(P, Bf, C, (rbase + warp) * P.B + b, k, u, lane);
     if (lane == 0) { s_act[warp] = s.active; s_beta[warp] = s.beta; s_alpha[warp] = s.alpha; }
   }
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);
+    for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -83,18 +95,21 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   float* const Pnew = Bf.p + (long long)((k + 1) & 1) * RBN;
   const int par = k & 1;
   const bool xup = k > 0 && !C.noxlag;   // lagged x update of this pass
+  const bool qin = ONE && k > 0;         // one-pass: r_k = r_{k-1} - alpha q_{k-1}
+  float* const Rout = Bf.r + (long long)((k + 1) & 1) * RBN;
+  float* const Qout = ONE ? Bf.q + (long long)((k + 1) & 1) * RBN : Bf.q;
 
   // ---------------------------------------------------------------- producer (tid 0)
-  // plane j (z = zs + j) -> ring slot j % kStages; its n-th use completes phase n & 1
+  // plane j (z = zs + j) -> ring slot j % NS; its n-th use completes phase n & 1
   auto issue = [&](int j) {
     if (j >= np) return;
     const int zz = zs + j;
-    unsigned char* st = smem + (j % kStages) * L.stage;
-    uint64_t* bj = bar + (j % kStages);
+    unsigned char* st = smem + (j % NS) * L.stage;
+    uint64_t* bj = bar + (j % NS);
     uint32_t bytes = L.eRP + (VM == VM_STORED ? L.eWx + L.eWy + L.eWz : L.eV);
 #pragma unroll
     for (int c = 0; c < RC; ++c)
-      if (act[c]) bytes += 2 * L.eRP + (xup ? L.eX : 0);
+      if (act[c]) bytes += (qin ? 3 : 2) * L.eRP + (xup ? L.eX : 0);
     mbar_arrive_expect_tx(bj, bytes);
     const int xb = t.x0 - hx, yb = t.y0 - 1;
 #pragma unroll
@@ -102,8 +117,9 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       if (!act[c]) continue;
       const int pr = ((rbase + c) * P.B + b) * nz + zz;
       const int pp = ((par * P.R + rbase + c) * P.B + b) * nz + zz;
-      tma_load_3d(st + L.oR + c * L.bRP, &M.r, bj, xb, yb, pr);
+      tma_load_3d(st + L.oR + c * L.bRP, &M.r, bj, xb, yb, ONE ? pp : pr);
       tma_load_3d(st + L.oP + c * L.bRP, &M.p, bj, xb, yb, pp);
+      if (qin) tma_load_3d(st + L.oQ + c * L.bRP, &M.q, bj, xb, yb, pp);
       if (xup) tma_load_3d(st + L.oX + c * L.bX, &M.x, bj, t.x0, t.y0, pr);
     }
     const int pd = b * nz + zz;
@@ -116,12 +132,21 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       tma_load_3d(st + L.oW, &M.v, bj, t.x0 - P.hxv, yb, pd);
     }
   };
-  auto wait = [&](int j) { mbar_wait(bar + (j % kStages), (uint32_t)((j / kStages) & 1)); };
-  auto stg = [&](int j) -> const unsigned char* { return smem + (j % kStages) * L.stage; };
+  auto wait = [&](int j) { mbar_wait(bar + (j % NS), (uint32_t)((j / NS) & 1)); };
+  auto stg = [&](int j) -> const unsigned char* { return smem + (j % NS) * L.stage; };
   auto F = [](const unsigned char* st, int off) { return reinterpret_cast<const float*>(st + off); };
+  // r of this iteration at box offset `off` (one-pass: r_{k-1} - alpha_{k-1} q_{k-1})
+  auto rk4 = [&](const unsigned char* st, int c, int off) -> float4 {
+    const float4 r = ld4(F(st, L.oR + c * L.bRP) + off);
+    return qin ? fma4(-al[c], ld4(F(st, L.oQ + c * L.bRP) + off), r) : r;
+  };
+  auto rk1 = [&](const unsigned char* st, int c, int off) -> float {
+    const float r = F(st, L.oR + c * L.bRP)[off];
+    return qin ? __fmaf_rn(-al[c], F(st, L.oQ + c * L.bRP)[off], r) : r;
+  };
   auto centre_pnew = [&](const unsigned char* st, int c) -> float4 {
     return pnew4(be[c], ld4(F(st, L.oP + c * L.bRP) + crow), ld4(F(st, L.oD) + crow),
-                 ld4(F(st, L.oR + c * L.bRP) + crow));
+                 rk4(st, c, crow));
   };
   // normalised intensities of 4 consecutive intensity-box elements (one vector smem load)
   auto gvol4 = [&](const unsigned char* st, int off, float g[4]) {
@@ -150,8 +175,8 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
     prefetch_tmap(&M.p);
     prefetch_tmap(&M.d);
     prefetch_tmap(VM == VM_STORED ? &M.wx : &M.v);
-    // planes 0 .. jz0 + kStages - 2 now; step z issues plane (z - zs) + kStages - 1
-    for (int j = 0; j <= (t.z0 - zs) + kStages - 2; ++j) issue(j);
+    // planes 0 .. jz0 + NS - 2 now; step z issues plane (z - zs) + NS - 1
+    for (int j = 0; j <= (t.z0 - zs) + NS - 2; ++j) issue(j);
   }
   // out-of-tile halo columns of the p_new planes stay zero when the tile spans the brick
   if (hx == 0) {
@@ -195,8 +220,13 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   }
 
   double acc[RC];
+  double acc1[RC][4];   // one-pass: r.z, r.r, q.D r, q.D q
 #pragma unroll
-  for (int c = 0; c < RC; ++c) acc[c] = 0.0;
+  for (int c = 0; c < RC; ++c) {
+    acc[c] = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc1[c][e] = 0.0;
+  }
   const int nrow = 2 * tpx;                   // row-halo float4 items per rhs
   const int nhalo = nrow + (hx ? 2 * TY : 0); // + column-halo scalar items
 
@@ -227,7 +257,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
           float4 v = f4(0.f);
           if (act[c])
             v = pnew4(be[c], ld4(F(s0, L.oP + c * L.bRP) + off), ld4(F(s0, L.oD) + off),
-                      ld4(F(s0, L.oR + c * L.bRP) + off));
+                      rk4(s0, c, off));
           st4(spz + c * spc + brow * TXP + 4 + 4 * g, v);
         }
       } else {                               // columns x0-1 / x0+TX (tile narrower than brick)
@@ -238,8 +268,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
         for (int c = 0; c < RC; ++c) {
           float v = 0.f;
           if (act[c])
-            v = pnew1(be[c], F(s0, L.oP + c * L.bRP)[off], F(s0, L.oD)[off],
-                      F(s0, L.oR + c * L.bRP)[off]);
+            v = pnew1(be[c], F(s0, L.oP + c * L.bRP)[off], F(s0, L.oD)[off], rk1(s0, c, off));
           spz[c * spc + (ry + 1) * TXP + (side ? TX + 4 : 3)] = v;
         }
       }
@@ -285,7 +314,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       }
     }
     __syncthreads();                          // p_new plane + Wys of plane z complete
-    if (tid == 0) issue(jz + kStages - 1);    // refill the slot of plane z-1 (all done with it)
+    if (tid == 0) issue(jz + NS - 1);    // refill the slot of plane z-1 (all done with it)
     if (in) {
       if (VM == VM_STORED) {
         const float* Wxb = F(s0, L.oW);
@@ -321,8 +350,17 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
           st4(Bf.x + ov, fma4(al[c], po, xo));
         }
         st4(Pnew + ov, p);
-        st4(Bf.q + ov, q);
+        st4(Qout + ov, q);
         acc[c] += (double)dot4f(p, q);
+        if (ONE) {
+          const float4 rk = rk4(s0, c, crow);
+          st4(Rout + ov, rk);
+          const float4 dr = mul4(dvc, rk), dq = mul4(dvc, q);
+          acc1[c][0] += (double)dot4f(rk, dr);
+          acc1[c][1] += (double)dot4f(rk, rk);
+          acc1[c][2] += (double)dot4f(q, dr);
+          acc1[c][3] += (double)dot4f(q, dq);
+        }
       }
       wzm = wz;
 #pragma unroll
@@ -335,26 +373,40 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   const long long RBU = (long long)P.R * P.B * P.U;
 #pragma unroll
   for (int c = 0; c < RC; ++c) {
-    double v[1] = {acc[c]};
     __syncthreads();
-    if (act[c]) block_sum<1>(v, Bf.PA + (k & 1) * RBU + (long long)((rbase + c) * P.B + b) * P.U + u);
+    if (ONE) {
+      double v[5] = {acc1[c][0], acc1[c][1], acc[c], acc1[c][2], acc1[c][3]};
+      if (act[c])
+        block_sum<5>(v, Bf.PA + 5 * ((k & 1) * RBU + (long long)((rbase + c) * P.B + b) * P.U + u));
+    } else {
+      double v[1] = {acc[c]};
+      if (act[c]) block_sum<1>(v, Bf.PA + (k & 1) * RBU + (long long)((rbase + c) * P.B + b) * P.U + u);
+    }
   }
 }
 
 // ------------------------------------------------------------------------- launcher
-template <int RC, int VM>
-static cudaError_t launch_rc(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0,
-                             const Maps& M, cudaStream_t s) {
+template <int RC, int VM, bool ONE, int NS>
+static cudaError_t launch_one(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0,
+                              const Maps& M, cudaStream_t s) {
   static int attr = 48 * 1024;   // largest dynamic smem opted in so far for this instance
   const ALayout L = a_layout(P, RC, VM);
   if (L.total > attr) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(k_passA<RC, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+    const cudaError_t e = cudaFuncSetAttribute(k_passA<RC, VM, ONE, NS>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
     if (e != cudaSuccess) return e;
     attr = L.total;
   }
-  k_passA<RC, VM><<<dim3(P.U, P.B, 1), P.threads, L.total, s>>>(P, Bf, C, k, r0, M);
+  k_passA<RC, VM, ONE, NS><<<dim3(P.U, P.B, 1), P.threads, L.total, s>>>(P, Bf, C, k, r0, M);
   return cudaGetLastError();
+}
+
+template <int RC, int VM>
+static cudaError_t launch_rc(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0,
+                             const Maps& M, cudaStream_t s) {
+  if (!P.one) return launch_one<RC, VM, false, kStages>(P, Bf, C, k, r0, M, s);
+  return a_stages(P) == 3 ? launch_one<RC, VM, true, 3>(P, Bf, C, k, r0, M, s)
+                          : launch_one<RC, VM, true, kStages>(P, Bf, C, k, r0, M, s);
 }
 
 template <int VM>

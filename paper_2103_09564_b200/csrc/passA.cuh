@@ -9,7 +9,8 @@ namespace rw {
 // 3-D tiled tensor maps (x, y, plane) over the arrays pass A streams.  Arrays indexed
 // [q][b][z] collapse (q, b, z) into one plane coordinate (q*B + b)*nz + z.
 struct Maps {
-  CUtensorMap r;    // r      [R][B] planes, box {TXh, TY+2, 1}
+  CUtensorMap r;    // r      [2][R][B] planes, box {TXh, TY+2, 1}
+  CUtensorMap q;    // q      [2][R][B],    box {TXh, TY+2, 1}   (one-pass mode)
   CUtensorMap p;    // P      [2][R][B],    box {TXh, TY+2, 1}
   CUtensorMap x;    // x      [R][B],       box {TX, TY, 1}
   CUtensorMap d;    // dinv   [B],          box {TXh, TY+2, 1}
@@ -20,6 +21,12 @@ struct Maps {
 };
 
 constexpr int kStages = 4;  // TMA ring depth (planes issued ~2 steps before use)
+// one-pass mode streams one more box per rhs per stage; for single-rhs tiles spanning the
+// brick in x (no x halo, e.g. 64^3 bricks) 3 stages keep two CTAs per SM, which measured
+// faster than 4 stages at one CTA per SM (tools/passes_ab.py)
+__host__ __device__ inline int a_stages(const Plan& P) {
+  return (P.one && P.hx == 0 && P.R == 1) ? 3 : kStages;
+}
 
 __host__ __device__ inline int rup128(int b) { return (b + 127) & ~127; }
 __host__ __device__ inline int vm_esize(int vm) {
@@ -29,7 +36,7 @@ __host__ __device__ inline int vm_esize(int vm) {
 struct ALayout {
   int eRP, eX, eWx, eWy, eWz, eV;   // exact box bytes (mbarrier transaction counts)
   int bRP, bX, bWx, bWy, bWz, bV;   // 128-byte rounded smem footprints
-  int oR, oP, oX, oD, oW;           // offsets inside a stage (rhs c adds c * b..)
+  int oR, oP, oQ, oX, oD, oW;       // offsets inside a stage (rhs c adds c * b..)
   int stage, sp, wys, bars, total;  // stage size; p_new planes; +y weights; mbarriers; total
 };
 
@@ -49,14 +56,15 @@ __host__ __device__ inline ALayout a_layout(const Plan& P, int RC, int vm) {
   L.bV = rup128(L.eV);
   L.oR = 0;
   L.oP = RC * L.bRP;
-  L.oX = 2 * RC * L.bRP;
+  L.oQ = 2 * RC * L.bRP;                      // one-pass mode: q_{k-1} boxes
+  L.oX = (P.one ? 3 : 2) * RC * L.bRP;
   L.oD = L.oX + RC * L.bX;
   L.oW = L.oD + L.bRP;
   L.stage = L.oW + (vm == VM_STORED ? L.bWx + L.bWy + L.bWz : L.bV);
-  L.sp = kStages * L.stage;
+  L.sp = a_stages(P) * L.stage;
   L.wys = L.sp + rup128(2 * RC * (P.TY + 2) * P.TXP * 4);
   L.bars = L.wys + (vm == VM_STORED ? 0 : rup128(2 * P.TY * P.TX * 4));
-  L.total = L.bars + kStages * 8;
+  L.total = L.bars + a_stages(P) * 8;
   return L;
 }
 

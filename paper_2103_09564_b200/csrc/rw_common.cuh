@@ -32,6 +32,7 @@ struct Plan {
   int tiles_x, tiles_y, tiles_z, U;
   int TXP;              // smem row pitch (floats) of p_new planes = TX + 8 (cols -1..TX)
   int vm;               // VM_* weight mode
+  int one;              // 1: one-pass CG (pass A only, see passA.cu), 0: passes A + B
 };
 
 // Per-(rhs,brick) status (0 = active); values match include/rw.h RW_ST_*.
@@ -46,10 +47,12 @@ struct Bufs {
   const float* values;   // [R][B][n]
   const float* x0;       // [R][B][n] or null
   float* x;           // [R][B][n]   iterate (aliases the prob output)
-  float* r;           // [R][B][n]
+  float* r;           // [2][R][B][n] (two-pass mode uses slot 0 only; one-pass: R[k&1]
+                      //               holds r_{k-1} at the start of iteration k)
   float* p;           // [2][R][B][n]  P[k&1] holds p_{k-1} at the start of iteration k
-  float* q;           // [R][B][n]
-  double* PA;         // [2][R*B][U]       p.q partials (slot k&1 written by pass A(k))
+  float* q;           // [2][R][B][n]  (as r)
+  double* PA;         // [2][R*B][U][5] p.q partials (slot k&1 written by pass A(k)); one-pass
+                      //               mode: (r.z, r.r, p.q, q.D r, q.D q) of iteration k
   double2* PB;        // [2][R*B][U]       (r.z, r.r) partials (slot k&1 = state k)
   double4* PS;        // [R*B][U]          (b.b, n_fixed, n_unknown, 0) from setup
   int* status;        // [R*B]
