@@ -234,3 +234,31 @@ def test_queue_streams_batches_intact():
     torch.cuda.synchronize()
     q.close()
     np.testing.assert_array_equal(torch.cat(got).cpu().numpy(), vol)
+
+
+# ------------------------------------------------------------------ streaming passes
+@pytest.mark.parametrize("passes", [1, 2])
+@pytest.mark.parametrize("dims,batch,nrhs,dtype", [
+    ((68, 33, 17), 2, 1, "u16"),          # x halo (tiles_x = 2), ragged tiles
+    ((24, 10, 9), 2, 5, "f32"),           # 5 rhs (chunks of 4 + 1 / 1 + ...)
+    ((16, 8, 8), 3, 1, "u8"),
+])
+def test_stream_passes_parity(passes, dims, batch, nrhs, dtype):
+    """RW_OPT_STREAM_PASSES 1 (pass B folded into the next pass A, one-step beta expansion)
+    and 2 (classical) on the streaming solver: both against the fp64 oracle, and against
+    each other (iterations within 1, |dp| <= 1e-5)."""
+    nx, ny, nz = dims
+    p = wl.random_brick(nx, ny, nz, seed=3 * nx + nrhs, batch=batch, nseed=max(4, nx * ny * nz // 60),
+                        nrhs=nrhs, dtype=dtype, continuous=True)
+    with rwb.solver("streaming"), rwb.stream_passes(passes):
+        o = gpu_solve(p, tol=1e-7, max_iter=50000)
+    with rwb.solver("streaming"), rwb.stream_passes(3 - passes):
+        other = gpu_solve(p, tol=1e-7, max_iter=50000)
+    ref = ro.solve_problem(p, tol=1e-11)
+    assert_prob_parity(o["prob"], ref["prob"])
+    assert (o["status"] == 1).all()
+    assert np.abs(o["iters"].astype(int) - other["iters"].astype(int)).max() <= 1
+    assert np.abs(o["prob"] - other["prob"]).max() <= 1e-5
+    with rwb.solver("streaming"), rwb.stream_passes(passes):
+        m = gpu_solve(p, tol=1e-12, max_iter=4)
+    assert (m["iters"] == 4).all() and (m["status"] == 2).all()
