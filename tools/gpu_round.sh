@@ -21,5 +21,8 @@ CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-streaming --no-
 $CMD > $O/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $O/launches.csv $CMD > $O/ncu1.log 2>&1; echo "ncu1 rc=$?"
 if [ "${SKIP_FULL:-0}" = "0" ]; then
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_resident -s 3 -c 1 -o $O/resident $CMD > $O/ncu2.log 2>&1; echo "ncu2 rc=$?"
+# the streaming solver's dominant kernel (one-pass pass A) at a steady-state iteration
+SCMD="python bench.py --solver streaming --steps 1 --warmup 3 --no-cpu-baseline --no-rows"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_passA -s 60 -c 1 -o $O/passA $SCMD > $O/ncu3.log 2>&1; echo "ncu3 rc=$?"
 fi
 ls -la $O
