@@ -47,14 +47,27 @@ __device__ __forceinline__ float sample(const float* __restrict__ P, int np, int
 }  // namespace hier
 
 // cls == 0: labels are 0 / 1 fg / 2 bg.  cls > 0 (multi-class): class cls is the
-// foreground, every other nonzero label background
+// foreground, every other nonzero label background.  16 voxels per thread (n % 16 == 0,
+// 16-byte aligned buffers: D = s 2^k with s % 4 == 0).
+__device__ __forceinline__ uint32_t seed_bits4(uint32_t w, int cls) {
+  uint32_t o = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int s = (w >> (8 * e)) & 0xff;
+    const uint32_t b = cls == 0 ? ((s == 1 ? 1u : 0u) | (s == 2 ? 2u : 0u))
+                                : (s == cls ? 1u : (s != 0 ? 2u : 0u));
+    o |= b << (8 * e);
+  }
+  return o;
+}
 __global__ void k_seed_bits(const uint8_t* __restrict__ seeds, long long n, int cls,
                             uint8_t* __restrict__ bits) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+  const long long n16 = n / 16;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n16;
        i += (long long)gridDim.x * blockDim.x) {
-    const int s = seeds[i];
-    bits[i] = cls == 0 ? ((s == 1 ? 1 : 0) | (s == 2 ? 2 : 0))
-                       : (s == cls ? 1 : (s != 0 ? 2 : 0));
+    const uint4 v = reinterpret_cast<const uint4*>(seeds)[i];
+    reinterpret_cast<uint4*>(bits)[i] =
+        make_uint4(seed_bits4(v.x, cls), seed_bits4(v.y, cls), seed_bits4(v.z, cls), seed_bits4(v.w, cls));
   }
 }
 
@@ -72,28 +85,86 @@ __global__ void k_label_max(const float* __restrict__ P, long long n, int cls,
   }
 }
 
-// level l (D^3) -> level l+1 ((D/2)^3): OR of the 2^3 children
+// level l (D^3) -> level l+1 ((D/2)^3): OR of the 2^3 children.  One block-stride loop over
+// output rows (z, y); a thread ORs 4 outputs from 8-byte loads of the 4 child rows
+// (D % 8 == 0 whenever a coarser level exists).
 __global__ void k_seed_or(const uint8_t* __restrict__ in, int D, uint8_t* __restrict__ out) {
-  const int h = D / 2;
-  const long long n = (long long)h * h * h;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(i % h), y = (int)((i / h) % h), z = (int)(i / ((long long)h * h));
-    uint8_t b = 0;
-    for (int dz = 0; dz < 2; ++dz)
-      for (int dy = 0; dy < 2; ++dy)
-        for (int dx = 0; dx < 2; ++dx)
-          b |= in[((long long)(2 * z + dz) * D + (2 * y + dy)) * D + (2 * x + dx)];
-    out[i] = b;
+  const int h = D / 2, hq = h / 4;
+  for (long long row = blockIdx.x; row < (long long)h * h; row += gridDim.x) {
+    const int z = (int)(row / h), y = (int)(row % h);
+    for (int g = threadIdx.x; g < hq; g += blockDim.x) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy) {
+          const uint2 v = *reinterpret_cast<const uint2*>(
+              in + ((long long)(2 * z + dz) * D + (2 * y + dy)) * D + 8 * g);
+          // output byte e = OR of input bytes 2e, 2e+1
+          const uint32_t a = v.x | (v.x >> 8), b = v.y | (v.y >> 8);
+          acc |= (a & 0xffu) | ((a >> 8) & 0xff00u) | ((b & 0xffu) << 16) | ((b & 0xff0000u) << 8);
+        }
+      reinterpret_cast<uint32_t*>(out + row * h)[g] = acc;
+    }
   }
 }
 
+// Dense trilinear upsample (reading R25), one block-stride loop over output rows: the parent
+// coordinates of the row (z, y) are computed once, a thread writes 4 consecutive outputs
+// with one 16-byte store.  Same arithmetic as hier::sample (bit-identical values).
 __global__ void k_upsample(const float* __restrict__ P, int np, float* __restrict__ out, int D) {
-  const long long n = (long long)D * D * D;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(i % D), y = (int)((i / D) % D), z = (int)(i / ((long long)D * D));
-    out[i] = hier::sample(P, np, z, y, x);
+  const long long pl = (long long)np * np;
+  for (long long row = blockIdx.x; row < (long long)D * D; row += gridDim.x) {
+    const int z = (int)(row / D), y = (int)(row % D);
+    int z0, z1, y0, y1;
+    float fz, fy;
+    hier::pcoord(z, np, z0, z1, fz);
+    hier::pcoord(y, np, y0, y1, fy);
+    const float* r00 = P + (long long)z0 * pl + (long long)y0 * np;
+    const float* r01 = P + (long long)z0 * pl + (long long)y1 * np;
+    const float* r10 = P + (long long)z1 * pl + (long long)y0 * np;
+    const float* r11 = P + (long long)z1 * pl + (long long)y1 * np;
+    const float* rr[4] = {r00, r01, r10, r11};
+    for (int g = threadIdx.x; g < D / 4; g += blockDim.x) {
+      float o[4];
+      if (g > 0 && 2 * g + 2 <= np - 1) {
+        // interior: outputs 4g..4g+3 use parents 2g-1..2g+2 with (x0, x1, fx) =
+        // (2g-1, 2g, .75), (2g, 2g+1, .25), (2g, 2g+1, .75), (2g+1, 2g+2, .25) -- exactly
+        // what pcoord gives; three 8-byte loads per parent row instead of eight scalars
+        float c[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 a = *reinterpret_cast<const float2*>(rr[q] + 2 * g - 2);
+          const float2 b = *reinterpret_cast<const float2*>(rr[q] + 2 * g);
+          const float2 d = *reinterpret_cast<const float2*>(rr[q] + 2 * g + 2);
+          c[q][0] = __fmaf_rn(0.75f, b.x, (1.f - 0.75f) * a.y);
+          c[q][1] = __fmaf_rn(0.25f, b.y, (1.f - 0.25f) * b.x);
+          c[q][2] = __fmaf_rn(0.75f, b.y, (1.f - 0.75f) * b.x);
+          c[q][3] = __fmaf_rn(0.25f, d.x, (1.f - 0.25f) * b.y);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float c0 = __fmaf_rn(fy, c[1][e], (1.f - fy) * c[0][e]);
+          const float c1 = __fmaf_rn(fy, c[3][e], (1.f - fy) * c[2][e]);
+          o[e] = __fmaf_rn(fz, c1, (1.f - fz) * c0);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          int x0, x1;
+          float fx;
+          hier::pcoord(4 * g + e, np, x0, x1, fx);
+          const float c00 = __fmaf_rn(fx, r00[x1], (1.f - fx) * r00[x0]);
+          const float c01 = __fmaf_rn(fx, r01[x1], (1.f - fx) * r01[x0]);
+          const float c10 = __fmaf_rn(fx, r10[x1], (1.f - fx) * r10[x0]);
+          const float c11 = __fmaf_rn(fx, r11[x1], (1.f - fx) * r11[x0]);
+          const float c0 = __fmaf_rn(fy, c01, (1.f - fy) * c00);
+          const float c1 = __fmaf_rn(fy, c11, (1.f - fy) * c10);
+          o[e] = __fmaf_rn(fz, c1, (1.f - fz) * c0);
+        }
+      }
+      reinterpret_cast<float4*>(out + row * D)[g] = make_float4(o[0], o[1], o[2], o[3]);
+    }
   }
 }
 
@@ -242,8 +313,13 @@ static int grid_n(long long n, int sms) {
 
 cudaError_t launch_seed_bits(const uint8_t* seeds, long long n, int cls, uint8_t* bits, int sms,
                              cudaStream_t s) {
-  k_seed_bits<<<grid_n(n, sms), 256, 0, s>>>(seeds, n, cls, bits);
+  k_seed_bits<<<grid_n(n / 16, sms), 256, 0, s>>>(seeds, n, cls, bits);
   return cudaGetLastError();
+}
+
+static int grid_rows(long long rows, int sms) {
+  const long long cap = (long long)sms * 8;
+  return (int)(rows < cap ? (rows < 1 ? 1 : rows) : cap);
 }
 
 cudaError_t launch_label_max(const float* P, long long n, int cls, float* best, uint8_t* lab,
@@ -254,12 +330,13 @@ cudaError_t launch_label_max(const float* P, long long n, int cls, float* best, 
 
 cudaError_t launch_seed_or(const uint8_t* in, int D, uint8_t* out, int sms, cudaStream_t s) {
   const long long h = D / 2;
-  k_seed_or<<<grid_n(h * h * h, sms), 256, 0, s>>>(in, D, out);
+  k_seed_or<<<grid_rows(h * h, sms), h / 4 < 256 ? (int)((h / 4 + 31) / 32 * 32) : 256, 0, s>>>(in, D, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_upsample(const float* P, int np, float* out, int D, int sms, cudaStream_t s) {
-  k_upsample<<<grid_n((long long)D * D * D, sms), 256, 0, s>>>(P, np, out, D);
+  const int th = D / 4 < 256 ? (D / 4 + 31) / 32 * 32 : 256;
+  k_upsample<<<grid_rows((long long)D * D, sms), th, 0, s>>>(P, np, out, D);
   return cudaGetLastError();
 }
 

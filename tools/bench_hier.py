@@ -117,8 +117,12 @@ def main():
     runs = [True] + ([False] if a.no_prune_too else [])
     res = {}
     ws = buf = None
+    from paper_2103_09564_b200 import api
     for prune in runs:
+        api.profile_enable(True)
         (prob, st, state), ms = run(vol_d, seeds_d, a.s, a.e, prune, ws=ws, prob_buf=buf)
+        prof = api.profile_read()
+        api.profile_enable(False)
         ws, buf = state["workspace"], prob
         total = sum((d // a.s >> l) ** 3 for l in range(st["levels"]))
         vi = sum(st["iters"][l] * se ** 3 for l in range(st["levels"] - 1)) + st["iters"][-1] * a.s ** 3
@@ -126,7 +130,9 @@ def main():
                 "prune": prune, "ms": ms, "output_voxels_per_s": d ** 3 / (ms / 1e3),
                 "bricks_solved": sum(st["solved"]), "bricks_total": total,
                 "solved_voxel_cg_iter_per_s": vi / (ms / 1e3), "stats": st,
-                "fg_fraction": float((prob > 0.5).float().mean())}
+                "fg_fraction": float((prob > 0.5).float().mean()),
+                "kernel_ms_all_reps": {k: round(v[1], 2) for k, v in prof.items() if v[1] > 0},
+                "launches_all_reps": {k: v[0] for k, v in prof.items() if v[0] > 0}}
         if a.no_prune_too:
             res[prune] = (prob > 0.5).cpu() if d > 1024 else prob.clone()
         print(json.dumps(line), flush=True)
