@@ -152,3 +152,26 @@ def test_hier_labels_incremental_matches_oracle(case):
     srt = np.sort(ref["prob"], axis=0)
     sure = srt[-1] - srt[-2] > 1e-3
     assert np.array_equal(c["labels"].cpu().numpy()[sure], ref["labels"][sure])
+
+
+def test_hier_labels_two_classes_equals_binary_run():
+    """K = 2: class 1's field is rw_hier_segment with t_bin disabled on the same seeds
+    (bit-identical: the same driver and kernels), and the labels are its > / == split
+    against class 2's field."""
+    vol, seeds = small_volume(64, seed=4)
+    o = rwb.hier_segment_labels(dev(vol), dev(seeds), 2, s=16, beta=50.0, tol=1e-7, max_iter=20000)
+    b, st, _ = rwb.hier_segment(dev(vol), dev(seeds), s=16, beta=50.0, tol=1e-7, max_iter=20000,
+                                t_bin=-1.0)
+    torch.cuda.synchronize()
+    assert torch.equal(o["prob"][0], b)
+    assert [s_["pruned_dt"] for s_ in o["stats"]] == [[0] * st["levels"]] * 2
+    want = torch.where(o["prob"][0] >= o["prob"][1], 1, 2).to(torch.uint8)
+    assert torch.equal(o["labels"], want)
+
+
+def test_hier_labels_rejects_bad_arguments():
+    vol, seeds = small_volume(32, seed=2)
+    with pytest.raises(ValueError):
+        rwb.hier_segment_labels(dev(vol), dev(seeds), 1, s=8, e=1.5)      # K < 2
+    with pytest.raises(ValueError):
+        rwb.hier_segment_labels(dev(vol), dev(seeds), 3, s=12)            # 32 != 12 * 2^k

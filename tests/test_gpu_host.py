@@ -54,3 +54,20 @@ def test_host_pipeline_rejects_device_tensors():
     p = wl.cfg2(batch=2)
     with pytest.raises(ValueError):
         rwb.solve_bricks_host(dev(p.fixed), _host(p.values[0], False), _host(p.vol, False))
+
+
+def test_host_pipeline_prob_only_and_labels_only():
+    p = wl.cfg2(batch=5)
+    ref = rwb.solve_bricks(dev(p.fixed), dev(p.values), vol=dev(p.vol), beta=p.beta, eps=p.eps,
+                           tol=p.tol, max_iter=p.max_iter, labels=True)
+    torch.cuda.synchronize()
+    a = rwb.solve_bricks_host(_host(p.fixed, True), _host(p.values[0], True), _host(p.vol, True),
+                              beta=p.beta, eps=p.eps, tol=p.tol, max_iter=p.max_iter, chunk=2,
+                              prob=True, labels=False)
+    b = rwb.solve_bricks_host(_host(p.fixed, False), _host(p.values[0], False), _host(p.vol, False),
+                              beta=p.beta, eps=p.eps, tol=p.tol, max_iter=p.max_iter, chunk=3,
+                              prob=False, labels=True)
+    assert a["labels"] is None and b["prob"] is None
+    assert torch.equal(a["prob"], ref["prob"].cpu())
+    assert torch.equal(b["labels"], ref["labels"].cpu())
+    assert torch.equal(a["iters"], b["iters"])
