@@ -235,7 +235,7 @@ rw_status rw_build_pyramid_slab(const void* slab, rw_dtype dtype, rw_dims d, int
  *   seeded with its user seeds plus continuous seeds sampled (trilinear) from the parent
  *   level's probability field on window faces interior to the volume (Eq. 2), initialised
  *   from that field, and all such windows of a level are solved as one batch with
- *   rw_solve_bricks (resident solver when s_e is 32 or 64).  The brick's s^3 of each
+ *   rw_solve_bricks (resident solver when s_e is 32, 40 or 64).  The brick's s^3 of each
  *   window solution goes into the level's field; prunable = (hom: max-min < t_hom or
  *   dt: min-0.5 > t_bin or 0.5-max > t_bin) and no seed conflict in the brick;
  *   children of prunable bricks keep the upsampled parent field.
@@ -311,7 +311,8 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
  *                 shape, any nrhs, see RW_OPT_STREAM_PASSES);
  *   resident   -- one thread-block cluster per brick keeps the whole CG state on chip
  *                 (shared + tensor memory, registers) for all iterations (SURVEY 8(f)
- *                 f2/f4); bricks of 64x64x64 or 32x32x32, nrhs == 1, device permitting.
+ *                 f2/f4); bricks of 64^3, 40^3 (s_e of P:119) or 32^3, nrhs == 1, device
+ *                 permitting.
  * RW_OPT_SOLVER: RW_SOLVER_AUTO (default: resident when available, else streaming),
  * RW_SOLVER_STREAMING, RW_SOLVER_RESIDENT (a solve it cannot serve returns
  * RW_EUNSUPPORTED).  Process-wide setting; not thread-safe against concurrent solves.
