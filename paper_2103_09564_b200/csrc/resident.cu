@@ -51,9 +51,9 @@ struct Cfg {
   static constexpr int NI = 2 * ZS;         // items (quads) per thread
   static constexpr int PL = N * N;          // floats per plane
   static constexpr int oP = 0;                          // p   [ZS+2][N][N]  (0, ZS+1 = halo)
-  static constexpr int oX = oP + (ZS + 2) * PL;         // x   [ZS][N][N]
-  static constexpr int oWYM = oX + ZS * PL;             // -y weight of rows 2j [ZS][N/2][N]
-  static constexpr int oWZM = oWYM + ZS * (N / 2) * N;  // -z weight of plane 0 [N][N]
+  static constexpr int oWY = oP + (ZS + 2) * PL;        // +y weight [ZS][N][N] (row y's is
+                                                        // also row y+1's -y weight)
+  static constexpr int oWZM = oWY + ZS * PL;            // -z weight of plane 0 [N][N]
   static constexpr int nF = oWZM + PL;
   static constexpr int SMEM = nF * 4;
   static constexpr int NW = T / 32;
@@ -144,6 +144,14 @@ __device__ __forceinline__ void tm_ld32(uint32_t ta, float4 (&v)[8]) {
   for (int i = 0; i < 8; ++i)
     v[i] = make_float4(__uint_as_float(a[4 * i]), __uint_as_float(a[4 * i + 1]),
                        __uint_as_float(a[4 * i + 2]), __uint_as_float(a[4 * i + 3]));
+}
+// 8 columns (2 float4) store
+__device__ __forceinline__ void tm_st8(uint32_t ta, float4 u, float4 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+               :: "r"(ta), "r"(__float_as_uint(u.x)), "r"(__float_as_uint(u.y)),
+                  "r"(__float_as_uint(u.z)), "r"(__float_as_uint(u.w)), "r"(__float_as_uint(v.x)),
+                  "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)), "r"(__float_as_uint(v.w))
+               : "memory");
 }
 // 8 columns (2 float4)
 __device__ __forceinline__ void tm_ld8(uint32_t ta, float4& u, float4& v) {
@@ -365,8 +373,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   const int qx = G::EXACT ? t % QX : (act ? lane_ % QX : 0);
   const int j = G::EXACT ? t / QX : (act ? jj : 0);
   float* const P = sm + G::oP;
-  float* const X = sm + G::oX;
-  float* const WYM = sm + G::oWYM;
+  float* const WY = sm + G::oWY;
   float* const WZM = sm + G::oWZM;
 
   // ---- tensor memory: 128 columns per thread (lane = 32*(warp%4) + lane id)
@@ -388,9 +395,11 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2);
-  // column map: dinv(it) = 4it, wx(it) = 32+4it, wy(it) = 64+4it, wz(it) = 96+4it;
-  // the two items of plane zl (it = 2zl, 2zl+1) are 8 adjacent columns of each weight
-  const uint32_t cD = tb, cX = tb + 32u, cY = tb + 64u, cZ = tb + 96u;
+  // column map: dinv(it) = 4it, wx(it) = 32+4it, x(it) = 64+4it, wz(it) = 96+4it;
+  // the two items of plane zl (it = 2zl, 2zl+1) are 8 adjacent columns of each array.  The
+  // iterate x lives here (its update is a TMEM read-modify-write, 3x the bandwidth of shared
+  // memory), the +y weights in shared memory where rows 2j+1 / 2j-1 serve as -y weights.
+  const uint32_t cD = tb, cX = tb + 32u, cV = tb + 64u, cZ = tb + 96u;
 
   const int z0 = rank * ZS;
   const long long n = (long long)PL * G::NZ;
@@ -488,15 +497,14 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
           o = assemble_quad<T, N, G::NZ>(A, (long long)b * n, z0 + zl, y, 4 * qx, iacc);
           fixm |= o.fm << (4 * it);
           const int so = y * N + 4 * qx;
-          st4(X + zl * PL + so, o.xv);
+          st4(WY + zl * PL + so, o.wy);
           st4(P + (zl + 1) * PL + so, f4(0.f));
-          if (rr == 0) st4(WYM + (zl * (N / 2) + j) * N + 4 * qx, o.wym);
           if (zl == 0) st4(WZM + so, o.wzm);
         }
         r[it] = o.rv;
         tm_st4(cD + 4u * it, o.dv);     // warp-collective: every lane takes part
         tm_st4(cX + 4u * it, o.wx);
-        tm_st4(cY + 4u * it, o.wy);
+        tm_st4(cV + 4u * it, o.xv);
         tm_st4(cZ + 4u * it, o.wz);
       }
     } else if constexpr (G::EXACT) {
@@ -507,7 +515,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         const float4 dv = ld4(A.dinv + g);
         tm_st4(cD + 4u * it, dv);
         tm_st4(cX + 4u * it, ld4(A.W + g));
-        tm_st4(cY + 4u * it, ld4(A.W + BN + g));
+        tm_st4(cV + 4u * it, ld4(A.x + g));
         tm_st4(cZ + 4u * it, ld4(A.W + 2 * BN + g));
         fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
         fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
@@ -515,9 +523,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
         r[it] = ld4(A.r0 + g);
         const int so = y * N + 4 * qx;
-        st4(X + zl * PL + so, ld4(A.x + g));
+        st4(WY + zl * PL + so, ld4(A.W + BN + g));
         st4(P + (zl + 1) * PL + so, f4(0.f));
-        if (rr == 0) st4(WYM + (zl * (N / 2) + j) * N + 4 * qx, y > 0 ? ld4(A.W + BN + g - N) : f4(0.f));
         if (zl == 0) st4(WZM + so, z0 > 0 ? ld4(A.W + 2 * BN + g - PL) : f4(0.f));
       }
     } else {
@@ -527,12 +534,12 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     for (int it = 0; it < NI; ++it) {
       const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
       const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
-      float4 dv = f4(0.f), wx = f4(0.f), wy = f4(0.f), wz = f4(0.f);
+      float4 dv = f4(0.f), wx = f4(0.f), xv = f4(0.f), wz = f4(0.f);
       r[it] = f4(0.f);
       if (act) {
         dv = ld4(A.dinv + g);
         wx = ld4(A.W + g);
-        wy = ld4(A.W + BN + g);
+        xv = ld4(A.x + g);
         wz = ld4(A.W + 2 * BN + g);
         fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
         fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
@@ -540,14 +547,13 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
         r[it] = ld4(A.r0 + g);
         const int so = y * N + 4 * qx;
-        st4(X + zl * PL + so, ld4(A.x + g));
+        st4(WY + zl * PL + so, ld4(A.W + BN + g));
         st4(P + (zl + 1) * PL + so, f4(0.f));
-        if (rr == 0) st4(WYM + (zl * (N / 2) + j) * N + 4 * qx, y > 0 ? ld4(A.W + BN + g - N) : f4(0.f));
         if (zl == 0) st4(WZM + so, z0 > 0 ? ld4(A.W + 2 * BN + g - PL) : f4(0.f));
       }
       tm_st4(cD + 4u * it, dv);     // warp-collective: every lane takes part
       tm_st4(cX + 4u * it, wx);
-      tm_st4(cY + 4u * it, wy);
+      tm_st4(cV + 4u * it, xv);
       tm_st4(cZ + 4u * it, wz);
     }
     }
@@ -612,22 +618,26 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 #endif
       // ---- step 1: x += alpha_{k-1} p_{k-1} (lagged);  p_k = dinv r + beta p_{k-1}
       if (t == 0) mbar_arrive_expect_tx(&s_bar[0], halo_bytes);
-      {
-        float4 dv[NI];
-        tm_ld32(cD, dv);
 #pragma unroll
-        for (int it = 0; it < NI; ++it) {
-          const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+      for (int zl = 0; zl < ZS; ++zl) {   // one plane (2 items) of dinv and x at a time
+        float4 dv[2], xv[2];
+        tm_ld8(cD + 8u * zl, dv[0], dv[1]);
+        if (k > 0) tm_ld8(cV + 8u * zl, xv[0], xv[1]);
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int it = 2 * zl + rr, y = 2 * j + rr;
           const int so = y * N + 4 * qx;
           if (!act) continue;               // idle lane: owns no voxel
           const float4 po = ld4(P + (zl + 1) * PL + so);
-          if (k > 0) st4(X + zl * PL + so, fma4(al, po, ld4(X + zl * PL + so)));
-          const float4 pn = pnew4(be, po, dv[it], r[it]);
+          if (k > 0) xv[rr] = fma4(al, po, xv[rr]);
+          const float4 pn = pnew4(be, po, dv[rr], r[it]);
           st4(P + (zl + 1) * PL + so, pn);
           if (zl == 0 && rank > 0) st_async4(up_halo + own_off + rr * N * 4, pn, up_bar);
           if (zl == ZS - 1 && rank < CL - 1) st_async4(dn_halo + own_off + rr * N * 4, pn, dn_bar);
         }
+        if (k > 0) tm_st8(cV + 8u * zl, xv[0], xv[1]);   // warp-collective
       }
+      tm_wait_st();
       __syncthreads();
       TP(0);
 
@@ -648,11 +658,11 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
           q1 = xterms(p1, xl1, xr1, wx1, qx > 0 ? wl1 : 0.f);
         }
         {  // y terms: row 2j+1 is +y of row 2j (and row 2j is -y of row 2j+1)
-          float4 wy0, wy1;
-          tm_ld8(cY + 8u * zl, wy0, wy1);
+          const float* Wz = WY + zl * PL;
+          const float4 wy0 = ld4(Wz + so), wy1 = ld4(Wz + so + N);
           const float4 pym = j > 0 ? ld4(Pz + so - N) : f4(0.f);
           const float4 pyp = j < N / 2 - 1 ? ld4(Pz + so + 2 * N) : f4(0.f);
-          const float4 wym0 = ld4(WYM + (zl * (N / 2) + j) * N + 4 * qx);
+          const float4 wym0 = j > 0 ? ld4(Wz + so - N) : f4(0.f);
           q0 = terms2(q0, p0, p1, pym, wy0, wym0);
           q1 = terms2(q1, p1, pyp, p0, wy1, wy0);
         }
@@ -720,7 +730,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     for (int it = 0; it < NI; ++it) {
       const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
       const int so = y * N + 4 * qx;
-      float4 xv = ld4(X + zl * PL + so);
+      float4 xv = tm_ld4(cV + 4u * it);   // warp-collective
       if (upd && al != 0.f) xv = fma4(al, ld4(P + (zl + 1) * PL + so), xv);
       const uint32_t fm = fixm >> (4 * it);
       float o[4] = {xv.x, xv.y, xv.z, xv.w};
