@@ -1,6 +1,7 @@
 # A/B of abtest/librw_{old,new}.so on tools/res_n.py (brick side N, batch B)
 cd $GRAFT_REPO_ROOT
-for v in old new; do
+RW_LIB_PATH=$PWD/abtest/librw_old.so timeout 300 python tools/res_n.py ${N:-40} ${B:-1024} > /dev/null 2>&1   # clocks up
+for v in old new old new; do
   RES_DUMP=/tmp/abn_$v.npz RW_LIB_PATH=$PWD/abtest/librw_$v.so timeout 300 python tools/res_n.py ${N:-40} ${B:-1024}
 done
 python -c "
