@@ -81,7 +81,7 @@ def rep(path):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
-    ap.add_argument("--rep")
+    ap.add_argument("--rep", nargs="*", default=[])
     ap.add_argument("--bench")
     ap.add_argument("--out", required=True)
     ap.add_argument("--note", default="")
@@ -100,7 +100,7 @@ def main():
         md += [f"| {k} | {v['launches']} | {v['ms']:.3f} | {v['share']:.3f} |" for k, v in L.items()]
         md.append("")
     if a.rep:
-        R = rep(a.rep)
+        R = [d for r_ in a.rep for d in rep(r_)]
         S["full_capture"] = R
         md += ["## ncu --set full (one launch each, all bricks active)", ""]
         for d in R:
