@@ -678,9 +678,10 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
           q0 = terms2(q0, p0, ld4(Pz + PL + so), ld4(Pz - PL + so), wz0, wzm0);
           q1 = terms2(q1, p1, ld4(Pz + PL + so + N), ld4(Pz - PL + so + N), wz1, wzm1);
         }
-        const uint32_t fm = fixm >> (8 * zl);
-        q0 = mask4(q0, fm);
-        q1 = mask4(q1, fm >> 4);
+        // no mask on fixed voxels here: p = dinv r + beta p is exactly 0 there (dinv = 0,
+        // r = 0), so they add nothing to p.q, and step 3 keeps their r at 0.  (Testing the
+        // 32 mask bits here made the compiler hoist them into 32 registers and spill.)
+        if (!G::EXACT && !act) q0 = q1 = f4(0.f);   // idle lanes computed from row 0's p
         q[2 * zl] = q0;
         q[2 * zl + 1] = q1;
         apq = __fadd_rn(apq, __fadd_rn(dot4f(p0, q0), dot4f(p1, q1)));
@@ -706,7 +707,11 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         tm_ld32(cD, dv);
 #pragma unroll
         for (int it = 0; it < NI; ++it) {
-          const float4 rn = fma4(-al, q[it], r[it]);
+          float4 rn = fma4(-al, q[it], r[it]);
+          if (dv[it].x == 0.f) rn.x = 0.f;   // fixed voxel (dinv = 0): r stays 0
+          if (dv[it].y == 0.f) rn.y = 0.f;
+          if (dv[it].z == 0.f) rn.z = 0.f;
+          if (dv[it].w == 0.f) rn.w = 0.f;
           r[it] = rn;
           arz = __fadd_rn(arz, dot4f(rn, mul4(dv[it], rn)));
           arr = __fadd_rn(arr, dot4f(rn, rn));
