@@ -176,14 +176,14 @@ __global__ void k_gather(const T* __restrict__ vol, const uint8_t* __restrict__ 
                          uint8_t* __restrict__ fixed, float* __restrict__ values,
                          float* __restrict__ x0) {
   const long long nw = (long long)se * se * se;
-  const long long tot = nw * nb;
-  const int np = D / 2;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(i / nw);
-    const long long w = i % nw;
-    const int lx = (int)(w % se), ly = (int)((w / se) % se), lz = (int)(w / ((long long)se * se));
-    const int4 o = org[j];
+  const int np = D / 2, pl = se * se;
+  // one block-stride loop over (window, plane) pairs; threads over the plane (32-bit math)
+  for (long long jp = blockIdx.x; jp < (long long)nb * se; jp += gridDim.x) {
+   const int j = (int)(jp / se), lz = (int)(jp % se);
+   const int4 o = org[j];
+   for (int t = threadIdx.x; t < pl; t += blockDim.x) {
+    const int lx = t % se, ly = t / se;
+    const long long i = (long long)j * nw + (long long)lz * pl + t;
     const int x = o.x + lx, y = o.y + ly, z = o.z + lz;
     const long long g = ((long long)z * D + y) * D + x;
     wvol[i] = vol[g];
@@ -204,6 +204,7 @@ __global__ void k_gather(const T* __restrict__ vol, const uint8_t* __restrict__ 
     fixed[i] = fx ? 1 : 0;
     values[i] = fx ? v : 0.f;
     x0[i] = Pold ? Pold[g] : ps;   // incremental: the previous solution
+   }
   }
 }
 
@@ -343,7 +344,7 @@ cudaError_t launch_upsample(const float* P, int np, float* out, int D, int sms, 
 cudaError_t launch_gather(const void* vol, int dtype, const uint8_t* bits, const float* Ppar,
                           const float* Pold, int D, int se, const int4* org, int nb, void* wvol,
                           uint8_t* fixed, float* values, float* x0, int sms, cudaStream_t s) {
-  const int grid = grid_n((long long)se * se * se * nb, sms);
+  const int grid = grid_rows((long long)nb * se, sms);
   switch (dtype) {
     case 0: k_gather<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)vol, bits, Ppar, Pold, D, se, org, nb, (uint8_t*)wvol, fixed, values, x0); break;
     case 1: k_gather<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)vol, bits, Ppar, Pold, D, se, org, nb, (uint16_t*)wvol, fixed, values, x0); break;
