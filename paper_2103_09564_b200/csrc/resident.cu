@@ -230,15 +230,6 @@ __device__ __forceinline__ float4 terms2(float4 q, float4 p, float4 pp, float4 p
   q.w = __fmaf_rn(wm.w, __fsub_rn(p.w, pm.w), __fmaf_rn(wp.w, __fsub_rn(p.w, pp.w), q.w));
   return q;
 }
-// q = 0 on fixed voxels (bit e of fm)
-__device__ __forceinline__ float4 mask4(float4 q, uint32_t fm) {
-  if (fm & 1u) q.x = 0.f;
-  if (fm & 2u) q.y = 0.f;
-  if (fm & 4u) q.z = 0.f;
-  if (fm & 8u) q.w = 0.f;
-  return q;
-}
-
 }  // namespace res
 
 
