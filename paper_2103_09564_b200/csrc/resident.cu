@@ -37,18 +37,22 @@ namespace rw {
 
 namespace res {
 
+// A CTA owns ZS = N / CL planes.  ZS = 4: a thread owns a row pair (NR = 2 rows) in each
+// plane; ZS = 8: one row (NR = 1), so a cluster of half the size keeps the same registers
+// per thread (8 quads) with twice the warps per CTA.
 template <int N, int CL>
 struct Cfg {
-  static constexpr int ZS = 4;              // planes per CTA
+  static constexpr int ZS = N / CL;         // planes per CTA
+  static constexpr int NR = ZS == 4 ? 2 : 1;   // rows per thread per plane
   static constexpr int NZ = ZS * CL;        // brick z extent
   static constexpr int QX = N / 4;          // quads per row
-  static constexpr int SPW = 32 / QX;       // row-pair segments of QX lanes per warp
-  static constexpr int NJ = N / 2;          // row pairs
+  static constexpr int SPW = 32 / QX;       // row-group segments of QX lanes per warp
+  static constexpr int NJ = N / NR;         // row groups
   static constexpr int NWARP = (NJ + SPW - 1) / SPW;
   static constexpr int T = NWARP * 32;      // threads per CTA (idle lanes when QX does not
                                             // divide 32 or SPW does not divide NJ, e.g. N = 40)
   static constexpr bool EXACT = SPW * QX == 32 && NJ % SPW == 0;   // every lane owns voxels
-  static constexpr int NI = 2 * ZS;         // items (quads) per thread
+  static constexpr int NI = NR * ZS;        // items (quads) per thread
   static constexpr int PL = N * N;          // floats per plane
   static constexpr int oP = 0;                          // p   [ZS+2][N][N]  (0, ZS+1 = halo)
   static constexpr int oWY = oP + (ZS + 2) * PL;        // +y weight [ZS][N][N] (row y's is
@@ -59,7 +63,7 @@ struct Cfg {
   static constexpr int NW = T / 32;
   // tensor memory: warp w uses lanes 32 (w % 4) .. +31 and columns 128 (w / 4) .. +127
   static constexpr int TCOLS = NWARP > 8 ? 512 : (NWARP > 4 ? 256 : 128);
-  static_assert(T <= 512 && N % 4 == 0 && QX <= 32, "brick shape");
+  static_assert(T <= 512 && N % 4 == 0 && QX <= 32 && NI == 8 && N == NZ, "brick shape");
 };
 
 __device__ __forceinline__ uint32_t sptr(const void* p) {
@@ -152,6 +156,15 @@ __device__ __forceinline__ void tm_st8(uint32_t ta, float4 u, float4 v) {
                   "r"(__float_as_uint(u.z)), "r"(__float_as_uint(u.w)), "r"(__float_as_uint(v.x)),
                   "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)), "r"(__float_as_uint(v.w))
                : "memory");
+}
+// 4 columns (1 float4)
+__device__ __forceinline__ void tm_ld4x(uint32_t ta, float4& u) {
+  uint32_t a[4];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]) : "r"(ta));
+  u = make_float4(__uint_as_float(a[0]), __uint_as_float(a[1]), __uint_as_float(a[2]), __uint_as_float(a[3]));
 }
 // 8 columns (2 float4)
 __device__ __forceinline__ void tm_ld8(uint32_t ta, float4& u, float4& v) {
@@ -391,13 +404,23 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   // iterate x lives here (its update is a TMEM read-modify-write, 3x the bandwidth of shared
   // memory), the +y weights in shared memory where rows 2j+1 / 2j-1 serve as -y weights.
   const uint32_t cD = tb, cX = tb + 32u, cV = tb + 64u, cZ = tb + 96u;
+  // the NR items of plane zl of one array: columns base + 4 NR zl ..
+  auto tm_plane = [](uint32_t base, int zl, float4 (&v)[G::NR]) {
+    if constexpr (G::NR == 2) tm_ld8(base + 8u * zl, v[0], v[1]);
+    else tm_ld4x(base + 4u * zl, v[0]);
+  };
+  auto tm_plane_st = [](uint32_t base, int zl, const float4 (&v)[G::NR]) {
+    if constexpr (G::NR == 2) tm_st8(base + 8u * zl, v[0], v[1]);
+    else tm_st4(base + 4u * zl, v[0]);
+  };
 
   const int z0 = rank * ZS;
   const long long n = (long long)PL * G::NZ;
   const long long BN = (long long)A.B * n;
   // DSMEM: my plane 0 -> rank-1's upper halo, my plane ZS-1 -> rank+1's lower halo, each
   // with st.async completing (in bytes) on the receiver's halo mbarrier
-  const uint32_t own_off = (uint32_t)(j * 2 * N + 4 * qx) * 4u;   // row 2j, quad qx (bytes)
+  constexpr int NR = G::NR;
+  const uint32_t own_off = (uint32_t)(j * NR * N + 4 * qx) * 4u;   // row NR j, quad qx (bytes)
   // x-neighbour quads of the same row: the lanes next to this one inside its segment
   const int srcl = qx > 0 ? lane_ - 1 : lane_, srcr = qx < QX - 1 ? lane_ + 1 : lane_;
   auto shl = [&](float v) {   // value of the quad to the left (own value at qx = 0)
@@ -482,7 +505,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       fixm = act ? 0u : 0xffffffffu;
 #pragma unroll
       for (int it = 0; it < NI; ++it) {
-        const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+        const int zl = it / NR, rr = it % NR, y = NR * j + rr;
         QuadOut o{};
         if (act) {
           o = assemble_quad<T, N, G::NZ>(A, (long long)b * n, z0 + zl, y, 4 * qx, iacc);
@@ -501,7 +524,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     } else if constexpr (G::EXACT) {
 #pragma unroll
       for (int it = 0; it < NI; ++it) {
-        const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+        const int zl = it / NR, rr = it % NR, y = NR * j + rr;
         const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
         const float4 dv = ld4(A.dinv + g);
         tm_st4(cD + 4u * it, dv);
@@ -523,7 +546,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     fixm = act ? 0u : 0xffffffffu;
 #pragma unroll
     for (int it = 0; it < NI; ++it) {
-      const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+      const int zl = it / NR, rr = it % NR, y = NR * j + rr;
       const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
       float4 dv = f4(0.f), wx = f4(0.f), xv = f4(0.f), wz = f4(0.f);
       r[it] = f4(0.f);
@@ -610,13 +633,13 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       // ---- step 1: x += alpha_{k-1} p_{k-1} (lagged);  p_k = dinv r + beta p_{k-1}
       if (t == 0) mbar_arrive_expect_tx(&s_bar[0], halo_bytes);
 #pragma unroll
-      for (int zl = 0; zl < ZS; ++zl) {   // one plane (2 items) of dinv and x at a time
-        float4 dv[2], xv[2];
-        tm_ld8(cD + 8u * zl, dv[0], dv[1]);
-        if (k > 0) tm_ld8(cV + 8u * zl, xv[0], xv[1]);
+      for (int zl = 0; zl < ZS; ++zl) {   // one plane (NR items) of dinv and x at a time
+        float4 dv[NR], xv[NR];
+        tm_plane(cD, zl, dv);
+        if (k > 0) tm_plane(cV, zl, xv);
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int it = 2 * zl + rr, y = 2 * j + rr;
+        for (int rr = 0; rr < NR; ++rr) {
+          const int it = NR * zl + rr, y = NR * j + rr;
           const int so = y * N + 4 * qx;
           if (!act) continue;               // idle lane: owns no voxel
           const float4 po = ld4(P + (zl + 1) * PL + so);
@@ -626,7 +649,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
           if (zl == 0 && rank > 0) st_async4(up_halo + own_off + rr * N * 4, pn, up_bar);
           if (zl == ZS - 1 && rank < CL - 1) st_async4(dn_halo + own_off + rr * N * 4, pn, dn_bar);
         }
-        if (k > 0) tm_st8(cV + 8u * zl, xv[0], xv[1]);   // warp-collective
+        if (k > 0) tm_plane_st(cV, zl, xv);   // warp-collective
       }
       tm_wait_st();
       __syncthreads();
@@ -636,6 +659,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       // (items 2zl, 2zl+1) at a time
       float apq = 0.f;   // this thread's p.q (fp32 over its 32 voxels; fp64 beyond)
       auto spmv = [&](int zl) {
+       if constexpr (NR == 2) {
         const float* Pz = P + (zl + 1) * PL;
         const int so = 2 * j * N + 4 * qx;
         const float4 p0 = ld4(Pz + so), p1 = ld4(Pz + so + N);
@@ -676,6 +700,37 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         q[2 * zl] = q0;
         q[2 * zl + 1] = q1;
         apq = __fadd_rn(apq, __fadd_rn(dot4f(p0, q0), dot4f(p1, q1)));
+       } else {
+        // one row per thread: both y-neighbour rows come from shared memory
+        const float* Pz = P + (zl + 1) * PL;
+        const int so = j * N + 4 * qx;
+        const float4 p0 = ld4(Pz + so);
+        float4 q0;
+        {
+          float4 wx0;
+          tm_ld4x(cX + 4u * zl, wx0);
+          const float xl0 = shl(p0.w), xr0 = shr(p0.x), wl0 = shl(wx0.w);
+          q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
+        }
+        {
+          const float* Wz = WY + zl * PL;
+          const float4 wy0 = ld4(Wz + so);
+          const float4 wym0 = j > 0 ? ld4(Wz + so - N) : f4(0.f);
+          const float4 pym = j > 0 ? ld4(Pz + so - N) : f4(0.f);
+          const float4 pyp = j < N - 1 ? ld4(Pz + so + N) : f4(0.f);
+          q0 = terms2(q0, p0, pyp, pym, wy0, wym0);
+        }
+        {
+          float4 wz0, wzm0;
+          tm_ld4x(cZ + 4u * zl, wz0);
+          if (zl == 0) wzm0 = ld4(WZM + so);
+          else tm_ld4x(cZ + 4u * (zl - 1), wzm0);
+          q0 = terms2(q0, p0, ld4(Pz + PL + so), ld4(Pz - PL + so), wz0, wzm0);
+        }
+        if (!G::EXACT && !act) q0 = f4(0.f);
+        q[zl] = q0;
+        apq = __fadd_rn(apq, dot4f(p0, q0));
+       }
       };
 #pragma unroll
       for (int zl = 1; zl < ZS - 1; ++zl) spmv(zl);
@@ -724,7 +779,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     const bool upd = (st == ST_CONVERGED || st == ST_MAXITER) && k >= 1;
 #pragma unroll
     for (int it = 0; it < NI; ++it) {
-      const int zl = it >> 1, rr = it & 1, y = 2 * j + rr;
+      const int zl = it / NR, rr = it % NR, y = NR * j + rr;
       const int so = y * N + 4 * qx;
       float4 xv = tm_ld4(cV + 4u * it);   // warp-collective
       if (upd && al != 0.f) xv = fma4(al, ld4(P + (zl + 1) * PL + so), xv);
@@ -820,20 +875,26 @@ static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, k_resident<N, CL, VM>, A);
 }
 
+#ifdef RW_RES_WIDE_SMALL
+constexpr int CL40 = 10, CL32 = 8;   // 4 planes per CTA, row pairs per thread
+#else
+constexpr int CL40 = 5, CL32 = 4;    // 8 planes per CTA, one row per thread
+#endif
+
 // Is the resident solver available for this brick shape (and device)?
 bool resident_supported(int nx, int ny, int nz, int R) {
   if (R != 1) return false;
   if (nx == 64 && ny == 64 && nz == 64) return resident_clusters<64, 16, VM_STORED>() > 0;
-  if (nx == 32 && ny == 32 && nz == 32) return resident_clusters<32, 8, VM_STORED>() > 0;
-  if (nx == 40 && ny == 40 && nz == 40) return resident_clusters<40, 10, VM_STORED>() > 0;
+  if (nx == 32 && ny == 32 && nz == 32) return resident_clusters<32, CL32, VM_STORED>() > 0;
+  if (nx == 40 && ny == 40 && nz == 40) return resident_clusters<40, CL40, VM_STORED>() > 0;
   return false;
 }
 
 template <int VM>
 static cudaError_t launch_shape(int nx, const ResArgs& A, cudaStream_t s) {
   if (nx == 64) return launch_res<64, 16, VM>(A, s);
-  if (nx == 40) return launch_res<40, 10, VM>(A, s);
-  return launch_res<32, 8, VM>(A, s);
+  if (nx == 40) return launch_res<40, CL40, VM>(A, s);
+  return launch_res<32, CL32, VM>(A, s);
 }
 
 // fused assembly for u16 / f32 intensities, stored-weight mode otherwise
