@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 }
 
 // ------------------------------------------------------------------------- launcher
-// Supported shapes: N x N x 4*CL bricks with (N, CL) in {(64, 16), (40, 10), (32, 8)};
+// Supported shapes: N^3 bricks with (N, CL) in {(64, 16), (40, 5), (32, 4)} (CL40 / CL32 below);
 // 40^3 is the paper's expanded brick (s = 32, e = 1.25).
 template <int N, int CL, int VM>
 static int resident_clusters() {
