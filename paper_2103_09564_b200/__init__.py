@@ -9,5 +9,5 @@ from .api import (  # noqa: F401
     brick_weights, brick_weights_ex, solve_bricks, solve_bricks_host, solve_labels, build_pyramid, build_pyramid_slab, Queue,
     solve_workspace_bytes, solve_labels_workspace_bytes, level_dims, set_solver, get_solver,
     solver, resident_available, hier_segment, hier_segment_labels, stream_passes,
-    set_stream_passes, get_stream_passes,
+    set_stream_passes, get_stream_passes, set_resident_wide, get_resident_wide,
 )

@@ -70,6 +70,15 @@ def solver(name):
         set_solver(old)
 
 
+def set_resident_wide(on):
+    """rw_set_option(RW_OPT_RESIDENT_WIDE): latency-shaped clusters for 40^3 / 32^3 bricks."""
+    check(lib().rw_set_option(4, int(bool(on))), "rw_set_option")
+
+
+def get_resident_wide():
+    return bool(lib().rw_get_option(4))
+
+
 def set_stream_passes(n):
     """rw_set_option(RW_OPT_STREAM_PASSES): 1 (default, one fused pass per streaming CG
     iteration) or 2 (classical passes A + B)."""

@@ -55,6 +55,7 @@ int g_solver = RW_SOLVER_AUTO;
 // the solution error stays ~1e-6 (the true residual measures the fp32 roughness of x).
 int g_rr = 0;
 int g_passes = 1;   // RW_OPT_STREAM_PASSES
+int g_res_wide = 0; // RW_OPT_RESIDENT_WIDE
 
 rw_status fail(rw_status st, const char* fmt, ...) {
   char buf[512];
@@ -410,7 +411,7 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
     // clusters leave free (they need no shared memory the clusters hold).
     const int Bs = cosched_bricks(P.B, d, nrhs, W != nullptr, ws_bytes, Lw.total);
     A.nsolve = P.B - Bs;
-    RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, s));
+    RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, g_res_wide, s));
     if (Bs > 0) {
       cudaStream_t s2;
       cudaEvent_t fork, join;
@@ -520,6 +521,11 @@ rw_status rw_set_option(int32_t key, int64_t value) {
     g_rr = (int)value;
     return RW_OK;
   }
+  if (key == RW_OPT_RESIDENT_WIDE) {
+    if (value != 0 && value != 1) return fail(RW_EINVAL, "rw_set_option: resident wide must be 0 or 1");
+    g_res_wide = (int)value;
+    return RW_OK;
+  }
   if (key == RW_OPT_STREAM_PASSES) {
     if (value != 1 && value != 2) return fail(RW_EINVAL, "rw_set_option: passes must be 1 or 2");
     g_passes = (int)value;
@@ -539,7 +545,8 @@ rw_status rw_set_option(int32_t key, int64_t value) {
 
 int64_t rw_get_option(int32_t key) {
   return key == RW_OPT_SOLVER ? g_solver : key == RW_OPT_COSCHED ? g_cosched_pm
-         : key == RW_OPT_RESIDUAL_REPLACE ? g_rr : key == RW_OPT_STREAM_PASSES ? g_passes : -1;
+         : key == RW_OPT_RESIDUAL_REPLACE ? g_rr : key == RW_OPT_STREAM_PASSES ? g_passes
+         : key == RW_OPT_RESIDENT_WIDE ? g_res_wide : -1;
 }
 
 int32_t rw_resident_available(rw_dims d, int32_t nrhs) {

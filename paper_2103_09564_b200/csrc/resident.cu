@@ -875,35 +875,32 @@ static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, k_resident<N, CL, VM>, A);
 }
 
-#ifdef RW_RES_WIDE_SMALL
-constexpr int CL40 = 10, CL32 = 8;   // 4 planes per CTA, row pairs per thread
-#else
-constexpr int CL40 = 5, CL32 = 4;    // 8 planes per CTA, one row per thread
-#endif
-
-// Is the resident solver available for this brick shape (and device)?
+// 40^3 / 32^3 bricks: throughput shape (default) = 8 planes per CTA, one row per thread,
+// 5- / 4-CTA clusters; latency shape (wide = 1, RW_OPT_RESIDENT_WIDE) = 4 planes per CTA,
+// row pairs, 10- / 8-CTA clusters -- twice the SMs per brick, for a single brick (cfg1).
+// Each shape is deterministic and batch-invariant; the two agree to the solver tolerance.
 bool resident_supported(int nx, int ny, int nz, int R) {
   if (R != 1) return false;
   if (nx == 64 && ny == 64 && nz == 64) return resident_clusters<64, 16, VM_STORED>() > 0;
-  if (nx == 32 && ny == 32 && nz == 32) return resident_clusters<32, CL32, VM_STORED>() > 0;
-  if (nx == 40 && ny == 40 && nz == 40) return resident_clusters<40, CL40, VM_STORED>() > 0;
+  if (nx == 32 && ny == 32 && nz == 32) return resident_clusters<32, 4, VM_STORED>() > 0;
+  if (nx == 40 && ny == 40 && nz == 40) return resident_clusters<40, 5, VM_STORED>() > 0;
   return false;
 }
 
 template <int VM>
-static cudaError_t launch_shape(int nx, const ResArgs& A, cudaStream_t s) {
+static cudaError_t launch_shape(int nx, const ResArgs& A, int wide, cudaStream_t s) {
   if (nx == 64) return launch_res<64, 16, VM>(A, s);
-  if (nx == 40) return launch_res<40, CL40, VM>(A, s);
-  return launch_res<32, CL32, VM>(A, s);
+  if (nx == 40) return wide ? launch_res<40, 10, VM>(A, s) : launch_res<40, 5, VM>(A, s);
+  return wide ? launch_res<32, 8, VM>(A, s) : launch_res<32, 4, VM>(A, s);
 }
 
 // fused assembly for u16 / f32 intensities, stored-weight mode otherwise
 bool resident_fused(int vdt) { return vdt == VM_U16 || vdt == VM_F32; }
 
-cudaError_t launch_resident(int nx, const ResArgs& A, cudaStream_t s) {
-  if (A.vol && A.vdt == VM_U16) return launch_shape<VM_U16>(nx, A, s);
-  if (A.vol && A.vdt == VM_F32) return launch_shape<VM_F32>(nx, A, s);
-  return launch_shape<VM_STORED>(nx, A, s);
+cudaError_t launch_resident(int nx, const ResArgs& A, int wide, cudaStream_t s) {
+  if (A.vol && A.vdt == VM_U16) return launch_shape<VM_U16>(nx, A, wide, s);
+  if (A.vol && A.vdt == VM_F32) return launch_shape<VM_F32>(nx, A, wide, s);
+  return launch_shape<VM_STORED>(nx, A, wide, s);
 }
 
 }  // namespace rw

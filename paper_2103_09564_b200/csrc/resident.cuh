@@ -31,6 +31,6 @@ struct ResArgs {
 
 bool resident_supported(int nx, int ny, int nz, int R);
 bool resident_fused(int vdt);
-cudaError_t launch_resident(int nx, const ResArgs& A, cudaStream_t s);
+cudaError_t launch_resident(int nx, const ResArgs& A, int wide, cudaStream_t s);
 
 }  // namespace rw

@@ -83,6 +83,27 @@ def test_resident_random_bricks_many_per_cluster(n):
         assert_prob_parity(o["prob"][:, j:j + 1], ref["prob"])
 
 
+@pytest.mark.parametrize("n", [32, 40])
+def test_resident_wide_shape(n):
+    """RW_OPT_RESIDENT_WIDE (10- / 8-CTA clusters of 4 planes for 40^3 / 32^3) against the
+    oracle and the default 5- / 4-CTA shape; batch invariance within the wide shape."""
+    p = wl.random_brick(n, n, n, seed=200 + n, batch=6, nseed=n ** 3 // 60, continuous=True,
+                        dtype="u16")
+    d = resident(p, tol=1e-7, max_iter=20000)
+    rwb.set_resident_wide(True)
+    try:
+        w = resident(p, tol=1e-7, max_iter=20000)
+        one = resident(p.subset([4]), tol=1e-7, max_iter=20000)
+    finally:
+        rwb.set_resident_wide(False)
+    assert (w["status"] == 1).all()
+    assert np.abs(w["prob"] - d["prob"]).max() <= 2e-5
+    assert np.abs(w["iters"].astype(int) - d["iters"].astype(int)).max() <= 2
+    assert np.array_equal(one["prob"][0, 0], w["prob"][0, 4])
+    ref = ro.solve_problem(p, tol=1e-11, bricks=[0])
+    assert_prob_parity(w["prob"][:, 0:1], ref["prob"])
+
+
 def test_resident_degenerate_bricks():
     """As test_degenerate_bricks on 32^3: no fixed voxel -> TRIVIAL 0.5; all fixed ->
     TRIVIAL values; all fixed values 0 -> ZERO_B; a normal brick vs the oracle."""

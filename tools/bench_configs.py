@@ -157,6 +157,12 @@ def main():
     a = ap.parse_args()
     if 1 in a.cfg:
         print(json.dumps(solve_cfg(wl.cfg1(), "cfg1 32^3 f32 sphere", a.check)), flush=True)
+        rwb.set_resident_wide(True)       # latency-shaped 8-CTA cluster for the single brick
+        try:
+            print(json.dumps(solve_cfg(wl.cfg1(), "cfg1 32^3 f32 sphere (RW_OPT_RESIDENT_WIDE)",
+                                       a.check)), flush=True)
+        finally:
+            rwb.set_resident_wide(False)
     if 3 in a.cfg:
         p = wl.cfg3()
         print(json.dumps(solve_cfg(p, "cfg3 512x512x256 i16 CT phantom", a.check)), flush=True)
