@@ -67,6 +67,7 @@ def run(vol_d, seeds_d, s, e, prune, reps=2, prev=None, ws=None, prob_buf=None):
         torch.cuda.synchronize()
         t0.record()
         prob, st, state = rwb.hier_segment(vol_d, seeds_d, s=s, e=e, prune=prune, tol=1e-6,
+                                           max_batch=int(os.environ.get("HIER_MAX_BATCH", "1024")),
                                            max_iter=5000, workspace=ws, prev=prev, out=prob_buf)
         t1.record()
         torch.cuda.synchronize()
