@@ -437,7 +437,7 @@ def run_b200(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps,
                 "api": "rw_solve_bricks_host (pinned host buffers, chunked H2D/solve/D2H overlap)",
-                "chunk": args.e2e_chunk or -(-BATCH // 16)},
+                "chunk": args.e2e_chunk or -(-BATCH // 32)},
         "gpu_launches": int(gpu_launches),
         "clocks": clocks,
     }
@@ -449,7 +449,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--e2e-chunk", type=int, default=0,
-                    help="bricks per pipeline chunk of the e2e host-buffer solve (0: batch/16)")
+                    help="bricks per pipeline chunk of the e2e host-buffer solve (0: batch/32)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workers", type=int, default=min(16, os.cpu_count() or 1))

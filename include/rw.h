@@ -160,7 +160,7 @@ rw_status rw_solve_bricks(int32_t batch, rw_dims d, const void* vol, rw_dtype dt
  * rw_solve_bricks_host -- rw_solve_bricks (nrhs = 1, weights from vol) on HOST buffers with
  *   the transfers pipelined against the solve ("H2D on a copy stream
  *   overlaps compute on the compute stream (events). Results go D2H"; P:105 brick-wise
- *   loading).  The batch is cut into chunks of `chunk` bricks (0: batch/16 rounded up):
+ *   loading).  The batch is cut into chunks of `chunk` bricks (0: batch/32 rounded up):
  *   chunk c+2's inputs go host->device on a copy stream while chunk c is solved and chunk
  *   c-1's results go device->host on a second copy stream.  Chunk solves alternate between
  *   two compute streams and two solve workspaces, so chunk c+1's resident clusters start on
