@@ -30,6 +30,9 @@
 // past the last segment (N = 40: 2 of 32) own nothing but join the warp-wide operations.  The x-neighbours of a quad come by warp shuffle,
 // the y-neighbours and z-neighbours from the shared p planes.
 #include "cg_device.cuh"
+#include <cstdio>
+#include <cstdlib>
+
 #include "resident.cuh"
 #include "tma.cuh"
 
@@ -851,6 +854,8 @@ static int resident_clusters() {
     nc = 0;
   }
   cached = nc;
+  if (getenv("RW_DEBUG_RES_CLUSTERS"))   // debug: co-resident clusters of this shape
+    fprintf(stderr, "[resident] N=%d CL=%d VM=%d: %d co-resident clusters\n", N, CL, VM, nc);
   return nc;
 }
 
