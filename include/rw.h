@@ -2,7 +2,8 @@
  * rw.h -- C ABI of librw: the B200 (sm_100a) hot path of the hierarchical random walker
  * of Drees, Eilers & Jiang, arXiv 2103.09564 ("PAPER.md").
  *
- * Citations: P:n = PAPER.md line n.  Readings c1..c17 = DESIGN.md section 3.
+ * Citations: P:n = PAPER.md line n.  Readings c1..c17 are R1..R17 of
+ * DESIGN.md section 3, which adds R19..R29.
  *
  * Conventions for every entry point
  * ---------------------------------
