@@ -336,9 +336,9 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   const int vm_vol = vol ? choose_vm(P, vol, dtype) : rw::VM_STORED;
   const bool fused = res_ok && vol && rw::resident_fused(vm_vol);
   set_vm(P, res_ok ? rw::VM_STORED : choose_vm(P, vol, dtype));
-  // one pass per iteration unless (measured, tools/passes_ab.py) a single-rhs system whose
-  // tiles carry an x halo, where the two lighter passes stream faster (cfg3: 1.83 vs 1.92 s)
-  P.one = (!res_ok && g_passes == 1 && g_rr == 0 && (P.hx == 0 || P.R > 1)) ? 1 : 0;
+  // one HBM pass per iteration (measured, tools/passes_ab.py: cfg2 512 bricks 167 vs 193 ms,
+  // cfg3 1.61 vs 1.87 s, cfg4 0.89 vs 0.99 s, identical iteration counts)
+  P.one = (!res_ok && g_passes == 1 && g_rr == 0) ? 1 : 0;
   rw::Bufs Bf{};
   float* Wd = W ? const_cast<float*>(W) : reinterpret_cast<float*>(ws + Lw.W);
   float* dinv = reinterpret_cast<float*>(ws + Lw.dinv);

@@ -109,7 +109,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
     uint32_t bytes = L.eRP + (VM == VM_STORED ? L.eWx + L.eWy + L.eWz : L.eV);
 #pragma unroll
     for (int c = 0; c < RC; ++c)
-      if (act[c]) bytes += (qin ? 3 : 2) * L.eRP + (xup ? L.eX : 0);
+      if (act[c]) bytes += (qin ? 3 : 2) * L.eRP + ((xup && !ONE) ? L.eX : 0);
     mbar_arrive_expect_tx(bj, bytes);
     const int xb = t.x0 - hx, yb = t.y0 - 1;
 #pragma unroll
@@ -120,7 +120,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       tma_load_3d(st + L.oR + c * L.bRP, &M.r, bj, xb, yb, ONE ? pp : pr);
       tma_load_3d(st + L.oP + c * L.bRP, &M.p, bj, xb, yb, pp);
       if (qin) tma_load_3d(st + L.oQ + c * L.bRP, &M.q, bj, xb, yb, pp);
-      if (xup) tma_load_3d(st + L.oX + c * L.bX, &M.x, bj, t.x0, t.y0, pr);
+      if (xup && !ONE) tma_load_3d(st + L.oX + c * L.bX, &M.x, bj, t.x0, t.y0, pr);
     }
     const int pd = b * nz + zz;
     tma_load_3d(st + L.oD, &M.d, bj, xb, yb, pd);
@@ -233,6 +233,13 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   for (int z = t.z0; z < t.z1; ++z) {
     const int jz = z - zs;
     const bool hasn = z + 1 <= ze;
+    float4 xz[RC];                            // one-pass: x_{k-1} of plane z, loaded early
+    if (ONE && xup && in) {
+#pragma unroll
+      for (int c = 0; c < RC; ++c)
+        xz[c] = act[c] ? ld4(Bf.x + (long long)(rbase + c) * BN + ocol + (long long)z * plane)
+                       : f4(0.f);
+    }
     const unsigned char* s0 = stg(jz);
     const unsigned char* s1 = stg(jz + 1);
     const int buf = z & 1;
@@ -346,7 +353,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
         const long long ov = (long long)(rbase + c) * BN + o;
         if (xup) {
           const float4 po = ld4(F(s0, L.oP + c * L.bRP) + crow);
-          const float4 xo = ld4(F(s0, L.oX + c * L.bX) + xrow);
+          const float4 xo = ONE ? xz[c] : ld4(F(s0, L.oX + c * L.bX) + xrow);
           st4(Bf.x + ov, fma4(al[c], po, xo));
         }
         st4(Pnew + ov, p);
@@ -404,9 +411,8 @@ static cudaError_t launch_one(const Plan& P, const Bufs& Bf, const Ctl& C, int k
 template <int RC, int VM>
 static cudaError_t launch_rc(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0,
                              const Maps& M, cudaStream_t s) {
-  if (!P.one) return launch_one<RC, VM, false, kStages>(P, Bf, C, k, r0, M, s);
-  return a_stages(P) == 3 ? launch_one<RC, VM, true, 3>(P, Bf, C, k, r0, M, s)
-                          : launch_one<RC, VM, true, kStages>(P, Bf, C, k, r0, M, s);
+  return P.one ? launch_one<RC, VM, true, kStages>(P, Bf, C, k, r0, M, s)
+               : launch_one<RC, VM, false, kStages>(P, Bf, C, k, r0, M, s);
 }
 
 template <int VM>

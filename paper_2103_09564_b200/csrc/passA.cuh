@@ -21,12 +21,9 @@ struct Maps {
 };
 
 constexpr int kStages = 4;  // TMA ring depth (planes issued ~2 steps before use)
-// one-pass mode streams one more box per rhs per stage; for single-rhs tiles spanning the
-// brick in x (no x halo, e.g. 64^3 bricks) 3 stages keep two CTAs per SM, which measured
-// faster than 4 stages at one CTA per SM (tools/passes_ab.py)
-__host__ __device__ inline int a_stages(const Plan& P) {
-  return (P.one && P.hx == 0 && P.R == 1) ? 3 : kStages;
-}
+// one-pass mode streams the q box instead of the x box (x is read straight from global
+// memory, it has no halo), so 4 stages still fit two CTAs per SM
+__host__ __device__ inline int a_stages(const Plan& P) { return kStages; }
 
 __host__ __device__ inline int rup128(int b) { return (b + 127) & ~127; }
 __host__ __device__ inline int vm_esize(int vm) {
@@ -49,7 +46,7 @@ __host__ __device__ inline ALayout a_layout(const Plan& P, int RC, int vm) {
   L.eWz = L.eX;
   L.eV = P.TXhv * (P.TY + 2) * vm_esize(vm);
   L.bRP = rup128(L.eRP);
-  L.bX = rup128(L.eX);
+  L.bX = P.one ? 0 : rup128(L.eX);   // one-pass mode reads x straight from global memory
   L.bWx = rup128(L.eWx);
   L.bWy = rup128(L.eWy);
   L.bWz = rup128(L.eWz);
