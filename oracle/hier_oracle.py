@@ -104,6 +104,37 @@ def window_origin(brick, s, se, D):
     return int(min(max(o, 0), D - se))
 
 
+def window_system(P_par, fx_l, val_l, brick, s, se, Dl):
+    """The Dirichlet data of one expanded window N(n) at level l (Eq. 3).
+
+    Returns (w0, fixed, values, samp): the window origin (reading R23), the fixed mask and
+    values = the user seeds inside the window plus the continuous border seeds of
+    sample_border (reading R24): every voxel of the window's one-voxel shell on a face
+    interior to the volume (w0 > 0 for the low face, w0 + se < Dl for the high face) that is
+    not a user seed takes the parent field sampled at its centre (reading R25); faces on
+    the volume boundary stay Neumann (reading c4).  samp = the parent field sampled at every
+    window voxel (the initial guess)."""
+    w0 = [window_origin(c, s, se, Dl) for c in brick]
+    sl = tuple(slice(a, a + se) for a in w0)
+    zs, ys, xs = (np.arange(a, a + se) for a in w0)
+    samp = sample_parent(P_par, zs, ys, xs)
+    fixed = fx_l[sl].copy()
+    values = np.where(fixed, val_l[sl], 0.0)
+    shell = np.zeros((se, se, se), bool)
+    for ax in range(3):
+        lo = [slice(None)] * 3
+        hi = [slice(None)] * 3
+        lo[ax] = 0
+        hi[ax] = se - 1
+        if w0[ax] > 0:
+            shell[tuple(lo)] = True
+        if w0[ax] + se < Dl:
+            shell[tuple(hi)] = True
+    border = shell & ~fixed
+    values = np.where(border, samp, values)
+    return w0, fixed | border, values, samp
+
+
 def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, eps=1e-6,
                  tol=1e-10, max_iter=100000, scale=1.0 / 65535, offset=0.0, prune=True,
                  prev=None, t_inc=0.01):
@@ -187,26 +218,8 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, ep
         stats[l]["active"] = len(active)
         new_state = {}
         for (bz, by, bx) in sorted(active):
-            w0 = [window_origin(c, s, se, Dl) for c in (bz, by, bx)]
+            w0, fixed, values, samp = window_system(P_par, fx_l, val_l, (bz, by, bx), s, se, Dl)
             sl = tuple(slice(a, a + se) for a in w0)
-            zs, ys, xs = (np.arange(a, a + se) for a in w0)
-            samp = sample_parent(P_par, zs, ys, xs)
-            fixed = fx_l[sl].copy()
-            values = np.where(fixed, val_l[sl], 0.0)
-            # continuous border seeds on window faces interior to the volume (user seeds win)
-            shell = np.zeros((se, se, se), bool)
-            for ax in range(3):
-                lo = [slice(None)] * 3
-                hi = [slice(None)] * 3
-                lo[ax] = 0
-                hi[ax] = se - 1
-                if w0[ax] > 0:
-                    shell[tuple(lo)] = True
-                if w0[ax] + se < Dl:
-                    shell[tuple(hi)] = True
-            border = shell & ~fixed
-            values = np.where(border, samp, values)
-            fixed = fixed | border
             x0 = prev["fields"][l][sl] if inc else samp
             o = ro.solve_brick(gl[sl], fixed, values, beta, eps, tol, max_iter, x0=x0)
             xw = np.where(fixed, values, np.clip(o["x"], 0.0, 1.0))

@@ -11,6 +11,7 @@ from conftest import read_golden
 from oracle import rw_oracle as ro
 from oracle import energy
 import workloads as wl
+from workloads import gen
 
 
 # ------------------------------------------------------------------ weights
@@ -196,7 +197,7 @@ def test_energy_decrease():
 
 def test_multilabel_sum_to_one_and_argmax():
     """K one-vs-rest probabilities sum to 1 (S:231: linearity of the Dirichlet problem);
-    argmax picks the class of each seed; ties -> lowest id."""
+    argmax picks the class of each seed."""
     rng = np.random.default_rng(70)
     n = 6
     vol = rng.uniform(0, 1, (1, n, n, n)).astype(np.float32)
@@ -209,9 +210,7 @@ def test_multilabel_sum_to_one_and_argmax():
     np.testing.assert_allclose(o["x"].sum(axis=0), 1.0, atol=1e-9)
     seeded = labels[0] > 0
     assert np.array_equal(o["labels"][0][seeded], labels[0][seeded])
-    # tie rule: two classes with identical probability -> lower id
-    P = np.zeros((3, 1, 1, 1, 2)); P[0] = 0.4; P[1] = 0.4; P[2] = 0.2
-    assert (np.argmax(P, axis=0) + 1).ravel().tolist() == [1, 1]
+    # the tie rule is pinned through solve_labels in test_solve_labels_tie_goes_to_lowest_class
 
 
 def test_degenerate_cases():
@@ -229,3 +228,28 @@ def test_degenerate_cases():
 def test_threshold_golden():
     p, m = read_golden("threshold_ramp.txt")
     assert ro.threshold(np.array(p, float)).tolist() == [int(v) for v in m]
+
+
+def test_normalise_golden():
+    """Worked values of reading c2 (tests/golden/normalise.txt) through the per-dtype
+    scale / offset the workloads and the ABI use (workloads.NORM)."""
+    for dt, v, g in read_golden("normalise.txt"):
+        sc, off = gen.NORM[dt]
+        raw = np.array([float(v)]).astype(gen.NP_DTYPE[dt])
+        assert abs(ro.normalise(raw, sc, off)[0] - float(g)) <= 1e-12, (dt, v, g)
+
+
+@pytest.mark.parametrize("order", [(1, 2), (2, 1)])
+def test_solve_labels_tie_goes_to_lowest_class(order):
+    """Reading c11 / S:337 through solve_labels itself: a mirror-symmetric 1 x 1 x 5 chain of
+    uniform intensity with a class-a seed at x = 0 and a class-b seed at x = 4.  By symmetry
+    both classes' probabilities at the centre are exactly 0.5 (the CG iterates stay
+    antisymmetric about it), so the centre voxel takes class 1 whichever end class 1 is
+    seeded at; voxels 1 and 3 take the class of their nearer seed."""
+    a, b = order
+    vol = np.full((1, 1, 1, 5), 0.5, np.float32)
+    labels = np.zeros((1, 1, 1, 5), np.uint8)
+    labels[0, 0, 0, 0], labels[0, 0, 0, 4] = a, b
+    o = ro.solve_labels(wl.LabelProblem("tie", vol, "f32", labels, 2, beta=10.0))
+    assert o["prob"][0, 0, 0, 0, 2] == 0.5 and o["prob"][1, 0, 0, 0, 2] == 0.5
+    assert o["labels"][0, 0, 0].tolist() == [a, a, 1, b, b]
