@@ -365,6 +365,9 @@ int32_t rw_resident_available(rw_dims d, int32_t nrhs);
  * device slot pointer and its id.
  * wait: makes compute_stream wait for that slot's copy.  release: records on
  * compute_stream that the slot's consumers are done (slot reusable after that point).
+ * Every push must be matched by a release before the ring comes round to its slot again:
+ * a push into a slot that was pushed and not yet released returns RW_EINVAL (nothing is
+ * enqueued), so at most `depth` slots are in flight.
  * ---------------------------------------------------------------------------------- */
 typedef struct rw_queue rw_queue;
 rw_status rw_queue_create(size_t slot_bytes, int32_t depth, rw_queue** q);

@@ -30,6 +30,18 @@ def _stream(stream=None, device=None):
     return C.c_void_p(s.cuda_stream)
 
 
+def _retain(stream, *ts):
+    """Tensors this binding allocated (workspace, outputs) are used by work enqueued on
+    ``stream``; the calls return before that work ends (rw.h: stream-ordered).  When
+    ``stream`` is not torch's current stream, tell the caching allocator so it does not
+    hand their memory to new work before the stream reaches this point."""
+    if stream is None:
+        return
+    for t in ts:
+        if t is not None and t.is_cuda:
+            t.record_stream(stream)
+
+
 def _need(t, name, dtype=None):
     if t is None:
         return
@@ -133,6 +145,7 @@ def brick_weights(vol, beta=100.0, eps=1e-6, fixed=None, norm=None, want_dinv=Tr
     st = lib().rw_brick_weights(_ptr(vol), DTYPES[vol.dtype], rw_norm(sc, of), B, dims_of(vol),
                                 beta, eps, _ptr(W), _ptr(dinv), _ptr(fixed), _stream(stream, vol.device))
     check(st, "rw_brick_weights")
+    _retain(stream, W, dinv)
     return W, dinv
 
 
@@ -159,6 +172,7 @@ def brick_weights_ex(vol, kind="ttest", beta=100.0, eps=1e-6, count_scale=1.0, r
                                    _ptr(W), _ptr(dinv), _ptr(fixed), _ptr(ws),
                                    0 if ws is None else ws.numel(), _stream(stream, vol.device))
     check(st, "rw_brick_weights_ex")
+    _retain(stream, W, dinv, ws)
     return W, dinv
 
 
@@ -168,8 +182,8 @@ def solve_bricks(fixed, values, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6
     """rw_solve_bricks.  ``values``/``x0``: [nrhs, B, nz, ny, nx] (or [B, ...] for nrhs=1).
 
     Returns dict(prob [nrhs,B,nz,ny,nx], iters [nrhs,B], resid [nrhs,B], status [nrhs,B],
-    labels [B,nz,ny,nx] u8 or None).  Stream-ordered; the call itself blocks only until the
-    device iteration loop has been fully enqueued/finished (see rw.h).
+      labels [B,nz,ny,nx] u8 or None).  Stream-ordered: outputs are valid once ``stream`` (default:
+    the current stream) reaches this point (see rw.h).
     """
     _need(fixed, "fixed", torch.uint8)
     if fixed.dim() == 3:                       # a single brick
@@ -213,6 +227,7 @@ def solve_bricks(fixed, values, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6
                                _ptr(out["iters"]), _ptr(out["resid"]), _ptr(out["status"]),
                                _ptr(out["labels"]), _stream(stream, dev))
     check(st, "rw_solve_bricks")
+    _retain(stream, workspace, *out.values())
     return out
 
 
@@ -292,6 +307,7 @@ def solve_labels(seeds, K, vol=None, W=None, beta=100.0, eps=1e-6, tol=1e-6, max
                                workspace.numel(), _ptr(prob), _ptr(iters), _ptr(resid),
                                _ptr(labels), _stream(stream, dev))
     check(st, "rw_solve_labels")
+    _retain(stream, workspace, prob, labels, iters, resid)
     return dict(prob=prob, labels=labels, iters=iters, resid=resid)
 
 

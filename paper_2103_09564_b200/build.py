@@ -47,20 +47,36 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     lib = out or LIB
     if out is None and not force and up_to_date():
         return LIB
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-pthread", "-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp",
-           *sources()]
-    for d in os.environ.get("RW_NVCC_DEFS", "").split():
-        cmd.insert(1, d)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
+             "-pthread", "-I", os.path.join(ROOT, "include")]
+    flags += os.environ.get("RW_NVCC_DEFS", "").split()
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
+        flags.append("-Xptxas=-v")
     if os.environ.get("RW_RES_TIMING"):      # debug: phase timers in the resident kernel
-        cmd.insert(1, "-DRW_RES_TIMING")
-    r = subprocess.run(cmd, capture_output=True, text=True)
+        flags.append("-DRW_RES_TIMING")
+    # one nvcc per translation unit, in parallel (no cross-unit device code), then one link
+    import concurrent.futures as cf
+    import tempfile
+    tmp = tempfile.mkdtemp(prefix="rwbuild_")
+    objs = [os.path.join(tmp, os.path.basename(f) + ".o") for f in sources()]
+
+    def compile_one(src_obj):
+        src, obj = src_obj
+        return subprocess.run([nvcc(), *flags, "-c", src, "-o", obj], capture_output=True, text=True)
+
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(objs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, zip(sources(), objs)))
+    log = "".join(r.stdout + r.stderr for r in results)
+    if any(r.returncode != 0 for r in results):
+        shutil.rmtree(tmp, ignore_errors=True)
+        raise RuntimeError("nvcc failed:\n" + log)
+    r = subprocess.run([nvcc(), *ARCH, "-shared", "-Xcompiler", "-pthread", "-o", lib + ".tmp",
+                        *objs], capture_output=True, text=True)
+    shutil.rmtree(tmp, ignore_errors=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
     if verbose:
-        sys.stderr.write(r.stdout + r.stderr)
+        sys.stderr.write(log + r.stdout + r.stderr)
     os.replace(lib + ".tmp", lib)
     return lib
 

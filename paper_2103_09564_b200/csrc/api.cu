@@ -49,7 +49,7 @@ namespace {
 thread_local std::string g_err;
 int g_solver = RW_SOLVER_AUTO;
 // streaming solver: residual replacement interval (RW_OPT_RESIDUAL_REPLACE).  Off by default:
-// measured (tools/rr_sweep.py, tools/dbg_rr.py) the fp32 true residual b - L x bottoms out
+// measured (tools/rr_sweep.py) the fp32 true residual b - L x bottoms out
 // near 1e-5 of ||b|| (rounding of x itself), so with replacement a 1e-6 / 1e-7 relative
 // tolerance is never met and intervals <= 4 diverge; without it the recurrence converges and
 // the solution error stays ~1e-6 (the true residual measures the fp32 roughness of x).
@@ -326,14 +326,17 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
                      bool allow_resident = true) {
   const int sms = num_sms();
   rw::Plan P = P0;
+  // the resident variant that would run: fused from u16 / f32 intensities, else stored
+  // weights (a vol of another dtype gets its weight planes from k_weights first)
+  const int vm_vol = vol ? choose_vm(P, vol, dtype) : rw::VM_STORED;
+  const int vm_res = (vol && rw::resident_fused(vm_vol)) ? vm_vol : rw::VM_STORED;
   const bool res_ok = allow_resident && g_solver != RW_SOLVER_STREAMING &&
-                      rw::resident_supported(d.nx, d.ny, d.nz, nrhs);
+                      rw::resident_supported(d.nx, d.ny, d.nz, nrhs, vm_res, g_res_wide);
   if (g_solver == RW_SOLVER_RESIDENT && !res_ok)
     return fail(RW_EUNSUPPORTED, "resident solver unavailable for %dx%dx%d, nrhs %d on this device",
                 d.nx, d.ny, d.nz, nrhs);
   // the resident solver reads stored weight planes once per brick -- or, for u16 / f32
   // intensities, assembles weights, dinv, x0 and r0 itself in its brick load phase (fused)
-  const int vm_vol = vol ? choose_vm(P, vol, dtype) : rw::VM_STORED;
   const bool fused = res_ok && vol && rw::resident_fused(vm_vol);
   set_vm(P, res_ok ? rw::VM_STORED : choose_vm(P, vol, dtype));
   // one HBM pass per iteration (measured, tools/passes_ab.py: cfg2 512 bricks 167 vs 193 ms,
@@ -400,25 +403,22 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       A.x0 = x0;
     }
     RW_CK(cudaMemsetAsync(A.next, 0, sizeof(int), s));
-    static long long* dbg = nullptr;
-    if (getenv("RW_DEBUG_RES_TIMING")) {   // debug: phase cycle sums of the resident kernel
-      if (!dbg) RW_CK(cudaMalloc(&dbg, 16 * 8 * sizeof(long long)));
-      RW_CK(cudaMemsetAsync(dbg, 0, 16 * 8 * sizeof(long long), s));
-      A.dbg = dbg;
-    }
     // Co-scheduling: the 16-CTA clusters fill 112 of the 148 SMs; the last Bs bricks of a
     // large batch run through the streaming passes on a second stream, on the SMs the
-    // clusters leave free (they need no shared memory the clusters hold).
+    // clusters leave free (they need no shared memory the clusters hold).  The fork is
+    // recorded before the resident launch, so the streaming bricks start with it.
     const int Bs = cosched_bricks(P.B, d, nrhs, W != nullptr, ws_bytes, Lw.total);
     A.nsolve = P.B - Bs;
-    RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, g_res_wide, s));
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
     if (Bs > 0) {
-      cudaStream_t s2;
-      cudaEvent_t fork, join;
       rw_status cs = cosched_handles(&s2, &fork, &join);
       if (cs != RW_OK) return cs;
       RW_CK(cudaEventRecord(fork, s));
       RW_CK(cudaStreamWaitEvent(s2, fork, 0));
+    }
+    RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, g_res_wide, s));
+    if (Bs > 0) {
       const int Br = P.B - Bs;
       const size_t n = (size_t)P.n;
       const size_t es = dtype_size_(dtype);
@@ -433,17 +433,6 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       if (r2 != RW_OK) return r2;
       RW_CK(cudaEventRecord(join, s2));
       RW_CK(cudaStreamWaitEvent(s, join, 0));
-    }
-    if (A.dbg) {
-      long long h[128];
-      RW_CK(cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s));
-      RW_CK(cudaStreamSynchronize(s));
-      const char* names[7] = {"step1+sync", "spmv-int", "halo-wait", "spmv-bnd", "red-pq", "step3", "red-rz"};
-      for (int r = 0; r < 16; r += 5) {
-        fprintf(stderr, "[res-timing rank %2d]", r);
-        for (int i = 0; i < 7; ++i) fprintf(stderr, " %s=%lld", names[i], h[r * 8 + i]);
-        fprintf(stderr, "\n");
-      }
     }
     return RW_OK;
   }
@@ -550,7 +539,7 @@ int64_t rw_get_option(int32_t key) {
 }
 
 int32_t rw_resident_available(rw_dims d, int32_t nrhs) {
-  return rw::resident_supported(d.nx, d.ny, d.nz, nrhs) ? 1 : 0;
+  return rw::resident_supported(d.nx, d.ny, d.nz, nrhs, rw::VM_STORED, g_res_wide) ? 1 : 0;
 }
 
 rw_status rw_brick_weights(const void* vol, rw_dtype dtype, rw_norm nm, int32_t batch,

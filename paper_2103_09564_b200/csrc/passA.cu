@@ -16,7 +16,8 @@
 //
 // B200 design.  A CTA owns a TX x TY column tile of one brick and marches over ZC planes.
 // One elected thread streams each plane's boxes (r, p_{k-1}, x, dinv and either the three
-// weight planes or the raw intensities) into a 3-stage shared-memory ring with TMA
+// weight planes or the raw intensities) into a 4-stage (default; 3 for the multi-rhs
+// variants) shared-memory ring with TMA
 // (cp.async.bulk.tensor, mbarrier completion), so HBM reads run two planes ahead of the
 // math with no register cost.  The y/x halo of r, p, dinv (needed to form p_k at the
 // tile's neighbours) comes in the same boxes; out-of-brick cells are zero-filled by TMA.

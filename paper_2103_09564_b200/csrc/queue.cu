@@ -20,6 +20,7 @@ struct rw_queue {
   std::vector<void*> host, dev;
   std::vector<cudaEvent_t> ready, freed;
   std::vector<bool> used;
+  std::vector<bool> released;   // released since its last push (or never pushed)
 };
 
 namespace rw { void set_last_error(const char* msg); }
@@ -71,6 +72,7 @@ extern "C" rw_status rw_queue_create(size_t slot_bytes, int32_t depth, rw_queue*
     Q->ready.push_back(a);
     Q->freed.push_back(b);
     Q->used.push_back(false);
+    Q->released.push_back(true);
   }
   *q = Q;
   return RW_OK;
@@ -81,6 +83,11 @@ extern "C" rw_status rw_queue_push(rw_queue* q, const void* host_src, size_t byt
   if (!q || !host_src || !dev_slot || bytes > q->slot_bytes)
     return qfail(RW_EINVAL, "rw_queue_push: bad arguments or bytes > slot_bytes");
   const int s = q->next;
+  // pushing more than `depth` slots ahead of rw_queue_release would overwrite a slot whose
+  // consumers were never enqueued: refuse instead of racing
+  if (!q->released[s])
+    return qfail(RW_EINVAL, "rw_queue_push: the next slot has not been released (more than "
+                            "depth pushes ahead of rw_queue_release)");
   q->next = (q->next + 1) % q->depth;
   // the slot's previous H2D copy must be done (host buffer reuse) and its consumers must
   // have released it (device buffer reuse)
@@ -103,6 +110,7 @@ extern "C" rw_status rw_queue_push(rw_queue* q, const void* host_src, size_t byt
       cudaEventRecord(q->ready[s], cs) != cudaSuccess)
     return qfail(RW_ECUDA, "rw_queue_push: H2D copy enqueue failed");
   q->used[s] = true;
+  q->released[s] = false;
   *dev_slot = q->dev[s];
   if (slot_id) *slot_id = s;
   return RW_OK;
@@ -119,6 +127,7 @@ extern "C" rw_status rw_queue_release(rw_queue* q, int32_t slot_id, void* comput
   if (!q || slot_id < 0 || slot_id >= q->depth) return qfail(RW_EINVAL, "rw_queue_release: bad slot");
   if (cudaEventRecord(q->freed[slot_id], (cudaStream_t)compute_stream) != cudaSuccess)
     return qfail(RW_ECUDA, "rw_queue_release: cudaEventRecord failed");
+  q->released[slot_id] = true;
   return RW_OK;
 }
 

@@ -9,10 +9,12 @@
 // P:167): the brick is split into CL z-slabs of ZS = 4 planes, one CTA (one SM) per slab,
 // and every iteration runs on chip:
 //
-//   shared memory : p (own planes + one halo plane on each side), x, the -y / -z weights
-//                   this thread does not own                          (208 KB at 64^3)
-//   tensor memory : dinv and the three forward edge weights of the thread's 32 voxels
-//                   (tcgen05.st once per brick, tcgen05.ld every iteration; 128 columns)
+//   shared memory : p of the own planes + one halo plane on each side, the +y weights
+//                   (row y's also serves row y+1 as its -y weight), the -z weights of
+//                   plane 0                                           (180 KB at 64^3)
+//   tensor memory : dinv, the +x and +z weights and the iterate x of the thread's 32 voxels
+//                   (tcgen05.st once per brick; tcgen05.ld every iteration, the x update a
+//                   TMEM read-modify-write; all 512 columns at 64^3)
 //   registers     : r and q of the thread's 32 voxels
 //
 // Halo planes of p travel to the neighbouring CTAs through distributed shared memory
@@ -826,8 +828,16 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 // 40^3 is the paper's expanded brick (s = 32, e = 1.25).
 template <int N, int CL, int VM>
 static int resident_clusters() {
-  static int cached = -1;
-  if (cached >= 0) return cached;
+  // per device: the shared-memory / cluster-size attributes are set on the current device
+  // and the co-resident cluster count is a property of that device
+  constexpr int MAXDEV = 64;
+  static int cached[MAXDEV] = {};   // 0 = not yet queried, else count + 1
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAXDEV) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (cached[dev] > 0) return cached[dev] - 1;
   using G = res::Cfg<N, CL>;
   int nc = 0;
   if (cudaFuncSetAttribute(k_resident<N, CL, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -835,7 +845,7 @@ static int resident_clusters() {
       (CL > 8 && cudaFuncSetAttribute(k_resident<N, CL, VM>,
                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
     cudaGetLastError();
-    cached = 0;
+    cached[dev] = 1;
     return 0;
   }
   cudaLaunchConfig_t cfg = {};
@@ -853,9 +863,10 @@ static int resident_clusters() {
     cudaGetLastError();
     nc = 0;
   }
-  cached = nc;
+  cached[dev] = nc + 1;
   if (getenv("RW_DEBUG_RES_CLUSTERS"))   // debug: co-resident clusters of this shape
-    fprintf(stderr, "[resident] N=%d CL=%d VM=%d: %d co-resident clusters\n", N, CL, VM, nc);
+    fprintf(stderr, "[resident] dev %d N=%d CL=%d VM=%d: %d co-resident clusters\n", dev, N, CL,
+            VM, nc);
   return nc;
 }
 
@@ -884,12 +895,20 @@ static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
 // 5- / 4-CTA clusters; latency shape (wide = 1, RW_OPT_RESIDENT_WIDE) = 4 planes per CTA,
 // row pairs, 10- / 8-CTA clusters -- twice the SMs per brick, for a single brick (cfg1).
 // Each shape is deterministic and batch-invariant; the two agree to the solver tolerance.
-bool resident_supported(int nx, int ny, int nz, int R) {
+template <int VM>
+static bool supported_vm(int nx, int wide) {
+  if (nx == 64) return resident_clusters<64, 16, VM>() > 0;
+  if (nx == 40) return wide ? resident_clusters<40, 10, VM>() > 0 : resident_clusters<40, 5, VM>() > 0;
+  return wide ? resident_clusters<32, 8, VM>() > 0 : resident_clusters<32, 4, VM>() > 0;
+}
+
+// the exact variant launch_resident will pick for (shape, vdt, wide) must be launchable
+bool resident_supported(int nx, int ny, int nz, int R, int vdt, int wide) {
   if (R != 1) return false;
-  if (nx == 64 && ny == 64 && nz == 64) return resident_clusters<64, 16, VM_STORED>() > 0;
-  if (nx == 32 && ny == 32 && nz == 32) return resident_clusters<32, 4, VM_STORED>() > 0;
-  if (nx == 40 && ny == 40 && nz == 40) return resident_clusters<40, 5, VM_STORED>() > 0;
-  return false;
+  if (!((nx == 64 || nx == 40 || nx == 32) && ny == nx && nz == nx)) return false;
+  if (vdt == VM_U16) return supported_vm<VM_U16>(nx, wide);
+  if (vdt == VM_F32) return supported_vm<VM_F32>(nx, wide);
+  return supported_vm<VM_STORED>(nx, wide);
 }
 
 template <int VM>

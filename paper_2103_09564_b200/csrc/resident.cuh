@@ -26,10 +26,13 @@ struct ResArgs {
   const uint8_t* fixed;  // [B][n]
   const float* values;   // [B][n]
   const float* x0;       // [B][n] or null (0.5)
-  long long* dbg;      // debug: per-(rank, phase) clock64 sums, or null (RW_DEBUG_RES_TIMING)
+  long long* dbg;      // debug builds only (-DRW_RES_TIMING): per-(rank, phase) clock64 sums
+                       // in a caller-provided buffer; null in the library
 };
 
-bool resident_supported(int nx, int ny, int nz, int R);
+// vdt: the VM_* mode the launch will use (VM_U16 / VM_F32 fused from intensities, else
+// VM_STORED); wide: RW_OPT_RESIDENT_WIDE
+bool resident_supported(int nx, int ny, int nz, int R, int vdt, int wide);
 bool resident_fused(int vdt);
 cudaError_t launch_resident(int nx, const ResArgs& A, int wide, cudaStream_t s);
 

@@ -62,9 +62,19 @@ def local_parity(g, fixed, values, x, beta, eps, z0, y0, x0, m):
     return float(np.abs(ref - x[sl])[1:-1, 1:-1, 1:-1].max())
 
 
+def _oracle_brick(sub):
+    """One cfg2 brick through the fp64 oracle (run in a worker process)."""
+    return ro.solve_problem(sub, tol=1e-10)["prob"]
+
+
 def test_cfg2_full_batch_in_bench_configuration():
     """The whole 512 x 64^3 batch through the default (auto -> resident) solver exactly as
-    bench.py runs it; 3 sampled bricks against the fp64 oracle, 8 by the fp64 residual."""
+    bench.py runs it.  34 bricks element by element against the fp64 oracle: the bricks
+    with the most and the fewest iterations plus 32 spread over the batch; every brick by
+    the fp64 residual of the plain definition."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    import os
     p = wl.cfg2(batch=512, workers=8)
     out = rwb.solve_bricks(dev(p.fixed), dev(p.values), vol=dev(p.vol), beta=p.beta, eps=p.eps,
                            tol=p.tol, max_iter=p.max_iter, labels=True)
@@ -75,11 +85,15 @@ def test_cfg2_full_batch_in_bench_configuration():
     assert (st == 1).all() and it.min() > 100 and it.max() < p.max_iter
     assert prob.min() >= 0.0 and prob.max() <= 1.0
     labels = out["labels"].cpu().numpy()
-    for b in (0, 255, 511):
-        ref = ro.solve_problem(p, tol=1e-10, bricks=[b])
-        assert_prob_parity(prob[:, b:b + 1], ref["prob"])
-        assert_label_parity(labels[b], ref["prob"][0, 0])
-    for b in range(3, 512, 64):
+    ids = sorted({int(np.argmax(it[0])), int(np.argmin(it[0]))} | set(range(0, 512, 16)))
+    assert len(ids) >= 32
+    with cf.ProcessPoolExecutor(max_workers=min(16, os.cpu_count() or 1),
+                                mp_context=mp.get_context("spawn")) as ex:
+        refs = list(ex.map(_oracle_brick, [p.subset([b]) for b in ids]))
+    for b, ref in zip(ids, refs):
+        assert_prob_parity(prob[:, b:b + 1], ref)
+        assert_label_parity(labels[b], ref[0, 0])
+    for b in range(3, 512, 8):
         g = ro.normalise(p.vol[b], p.scale, p.offset)
         rel = residual_fp64(g, p.fixed[b], p.values[0, b], prob[0, b], p.beta, p.eps)
         assert rel <= 2e-5, (b, rel)       # fp32 iterate at rel. tol 1e-6
@@ -127,8 +141,16 @@ def test_cfg4_full_size_multilabel_properties():
         vk = (seeds == k + 1).astype(np.float64)
         rel = residual_fp64(g, fixed, vk, prob[k], lp.beta, lp.eps)
         assert rel <= 1e-3, (k, rel)          # fp32 floor, see the cfg3 test
-        d = local_parity(g, fixed, vk, prob[k].astype(np.float64), lp.beta, lp.eps, 100, 110, 90, 24)
-        assert d <= 1e-4, (k, d)
+    # element-wise: every solved class and the derived class K = 1 - sum (R11) inside 24^3
+    # sub-blocks that straddle class boundaries, solved by the oracle with the GPU solution
+    # on their shell (the discrete equations of P:77 restricted to the block)
+    pK = np.clip(1.0 - prob.astype(np.float64).sum(0), 0.0, 1.0)
+    fields = [prob[k].astype(np.float64) for k in range(lp.K - 1)] + [pK]
+    for k, xk in enumerate(fields):
+        vk = (seeds == k + 1).astype(np.float64)
+        for (z0, y0, x0) in [(100, 110, 90), (60, 128, 150), (150, 40, 120)]:
+            d = local_parity(g, fixed, vk, xk, lp.beta, lp.eps, z0, y0, x0, 24)
+            assert d <= 1e-4, (k, (z0, y0, x0), d)
 
 
 def test_pyramid_2048_aligned_subcubes_bit_exact():

@@ -138,3 +138,25 @@ def test_resident_max_iter_abs_mode_warm_start_and_W():
     v = resident(p)
     u = resident(p, use_W=True)
     assert np.array_equal(v["prob"], u["prob"]) and np.array_equal(v["iters"], u["iters"])
+
+
+def test_cosched_matches_resident_only():
+    """RW_OPT_COSCHED (include/rw.h): the last share of a 64^3 batch runs through the
+    streaming passes on a second stream next to the resident clusters.  Results agree with
+    the resident-only solve to the solver tolerance, iteration counts within 3."""
+    from paper_2103_09564_b200._lib import lib
+    ids = list(range(0, 512, 4))
+    p = wl.cfg2(bricks=ids)
+    a = resident(p)
+    old = lib().rw_get_option(1)
+    lib().rw_set_option(1, 250)
+    try:
+        ws = rwb.api.alloc_workspace(rwb.solve_workspace_bytes(p.batch, p.dims, 1) * 2, "cuda")
+        b = gpu_solve(p, workspace=ws)
+    finally:
+        lib().rw_set_option(1, old)
+    assert (b["status"] == 1).all()
+    assert np.abs(a["prob"] - b["prob"]).max() <= 2e-5
+    assert np.abs(a["iters"].astype(int) - b["iters"].astype(int)).max() <= 3
+    nres = len(ids) - len(ids) * 250 // 1000
+    assert np.array_equal(a["prob"][:, :nres], b["prob"][:, :nres])     # resident part bitwise

@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-python tools/dbg_cases.py
 timeout 900 python -m pytest tests -m gpu -q -x --timeout 180 2>&1 | tail -5
 echo "tests rc=${PIPESTATUS[0]}"
 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
