@@ -417,7 +417,29 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       RW_CK(cudaEventRecord(fork, s));
       RW_CK(cudaStreamWaitEvent(s2, fork, 0));
     }
+#ifdef RW_RES_TIMING
+    // debug builds only (tools/ab_res.sh): phase cycle sums of the resident kernel
+    static long long* dbg = nullptr;
+    if (getenv("RW_DEBUG_RES_TIMING")) {
+      if (!dbg) RW_CK(cudaMalloc(&dbg, 16 * 8 * sizeof(long long)));
+      RW_CK(cudaMemsetAsync(dbg, 0, 16 * 8 * sizeof(long long), s));
+      A.dbg = dbg;
+    }
+#endif
     RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, g_res_wide, s));
+#ifdef RW_RES_TIMING
+    if (A.dbg) {
+      long long h[128];
+      RW_CK(cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s));
+      RW_CK(cudaStreamSynchronize(s));
+      const char* names[7] = {"step1+sync", "spmv-int", "halo-wait", "spmv-bnd", "red-pq", "step3", "red-rz"};
+      for (int r = 0; r < 16; r += 5) {
+        fprintf(stderr, "[res-timing rank %2d]", r);
+        for (int i = 0; i < 7; ++i) fprintf(stderr, " %s=%lld", names[i], h[r * 8 + i]);
+        fprintf(stderr, "\n");
+      }
+    }
+#endif
     if (Bs > 0) {
       const int Br = P.B - Bs;
       const size_t n = (size_t)P.n;
