@@ -230,23 +230,58 @@ __device__ __forceinline__ float4 stencil4(float4 p, float xl, float xr, float4 
   q.w = stencil1(p.w, xr, p.z, yp.w, ym.w, zp.w, zm.w, wx.w, wxm.w, wy.w, wym.w, wz.w, wzm.w, 1.f);
   return q;
 }
-// edge-difference stencil (reading c8) split by axis, same term order as stencil1:
-// q = wx (p - p[+x]);  q += wxm (p - p[-x]);  then +y, -y, +z, -z the same way
-__device__ __forceinline__ float4 xterms(float4 p, float xl, float xr, float4 wx, float wl) {
-  float4 q;
-  q.x = __fmaf_rn(wl, __fsub_rn(p.x, xl), __fmul_rn(wx.x, __fsub_rn(p.x, p.y)));
-  q.y = __fmaf_rn(wx.x, __fsub_rn(p.y, p.x), __fmul_rn(wx.y, __fsub_rn(p.y, p.z)));
-  q.z = __fmaf_rn(wx.y, __fsub_rn(p.z, p.y), __fmul_rn(wx.z, __fsub_rn(p.z, p.w)));
-  q.w = __fmaf_rn(wx.z, __fsub_rn(p.w, p.z), __fmul_rn(wx.w, __fsub_rn(p.w, xr)));
-  return q;
+// ---- packed fp32 pairs (sm_100a FFMA2 / FADD2 / FMUL2: one issue slot for two lanes' worth
+// of IEEE round-to-nearest fp32 arithmetic; every lane computes exactly what the scalar op
+// would).  A float4 quad is the aligned register pairs (x, y) and (z, w).
+__device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float4 cat2(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
 }
+// a * x + y, scalar a broadcast to both lanes
+__device__ __forceinline__ float4 fma4p(float a, float4 x, float4 y) {
+  const float2 aa = make_float2(a, a);
+  return cat2(__ffma2_rn(aa, lo2(x), lo2(y)), __ffma2_rn(aa, hi2(x), hi2(y)));
+}
+// p_new = beta p_old + dinv r (z = dinv r never stored), as pnew4
+__device__ __forceinline__ float4 pnew4p(float be, float4 po, float4 d, float4 r) {
+  const float2 bb = make_float2(be, be);
+  return cat2(__ffma2_rn(bb, lo2(po), __fmul2_rn(lo2(d), lo2(r))),
+              __ffma2_rn(bb, hi2(po), __fmul2_rn(hi2(d), hi2(r))));
+}
+// acc += a . b, per lane of the pair accumulators (fixed order over a thread's quads)
+__device__ __forceinline__ void dot4acc(float4 a, float4 b, float2& acc0, float2& acc1) {
+  acc0 = __ffma2_rn(lo2(a), lo2(b), acc0);
+  acc1 = __ffma2_rn(hi2(a), hi2(b), acc1);
+}
+__device__ __forceinline__ float hsum(float2 a, float2 b) {
+  return __fadd_rn(__fadd_rn(a.x, a.y), __fadd_rn(b.x, b.y));
+}
+
+// edge-difference stencil (reading c8) split by axis, same term order as stencil1:
+// q = wx (p - p[+x]);  q += wxm (p - p[-x]);  then +y, -y, +z, -z the same way.
+// x terms: the forward differences d_i = p_i - p_{i+1} (d3 = p.w - xr) are computed once;
+// the -x difference of voxel i+1 is -d_i exactly (IEEE subtraction is antisymmetric), and
+// that of voxel x is -dl, dl = the left quad's d3 (passed in by shuffle).
+__device__ __forceinline__ float4 xterms(float4 p, float xr, float dl, float4 wx, float wl,
+                                         float& d3) {
+  const float d0 = __fsub_rn(p.x, p.y), d1 = __fsub_rn(p.y, p.z), d2 = __fsub_rn(p.z, p.w);
+  d3 = __fsub_rn(p.w, xr);
+  const float2 m0 = __fmul2_rn(lo2(wx), make_float2(d0, d1));
+  const float2 m1 = __fmul2_rn(hi2(wx), make_float2(d2, d3));
+  return make_float4(__fmaf_rn(wl, -dl, m0.x), __fmaf_rn(wx.x, -d0, m0.y),
+                     __fmaf_rn(wx.y, -d1, m1.x), __fmaf_rn(wx.z, -d2, m1.y));
+}
+// the forward differences only (d3 is what the right neighbour needs)
+__device__ __forceinline__ float xd3(float4 p, float xr) { return __fsub_rn(p.w, xr); }
 __device__ __forceinline__ float4 terms2(float4 q, float4 p, float4 pp, float4 pm, float4 wp,
                                          float4 wm) {
-  q.x = __fmaf_rn(wm.x, __fsub_rn(p.x, pm.x), __fmaf_rn(wp.x, __fsub_rn(p.x, pp.x), q.x));
-  q.y = __fmaf_rn(wm.y, __fsub_rn(p.y, pm.y), __fmaf_rn(wp.y, __fsub_rn(p.y, pp.y), q.y));
-  q.z = __fmaf_rn(wm.z, __fsub_rn(p.z, pm.z), __fmaf_rn(wp.z, __fsub_rn(p.z, pp.z), q.z));
-  q.w = __fmaf_rn(wm.w, __fsub_rn(p.w, pm.w), __fmaf_rn(wp.w, __fsub_rn(p.w, pp.w), q.w));
-  return q;
+  float2 a = __ffma2_rn(lo2(wp), sub2(lo2(p), lo2(pp)), lo2(q));
+  float2 b = __ffma2_rn(hi2(wp), sub2(hi2(p), hi2(pp)), hi2(q));
+  a = __ffma2_rn(lo2(wm), sub2(lo2(p), lo2(pm)), a);
+  b = __ffma2_rn(hi2(wm), sub2(hi2(p), hi2(pm)), b);
+  return cat2(a, b);
 }
 }  // namespace res
 
@@ -648,8 +683,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
           const int so = y * N + 4 * qx;
           if (!act) continue;               // idle lane: owns no voxel
           const float4 po = ld4(P + (zl + 1) * PL + so);
-          if (k > 0) xv[rr] = fma4(al, po, xv[rr]);
-          const float4 pn = pnew4(be, po, dv[rr], r[it]);
+          if (k > 0) xv[rr] = fma4p(al, po, xv[rr]);
+          const float4 pn = pnew4p(be, po, dv[rr], r[it]);
           st4(P + (zl + 1) * PL + so, pn);
           if (zl == 0 && rank > 0) st_async4(up_halo + own_off + rr * N * 4, pn, up_bar);
           if (zl == ZS - 1 && rank < CL - 1) st_async4(dn_halo + own_off + rr * N * 4, pn, dn_bar);
@@ -662,7 +697,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 
       // ---- step 2: q = L_UU p (edge-difference stencil), partial p.q; one row pair
       // (items 2zl, 2zl+1) at a time
-      float apq = 0.f;   // this thread's p.q (fp32 over its 32 voxels; fp64 beyond)
+      // this thread's p.q: fp32 pair accumulators over its 32 voxels (fp64 beyond)
+      float2 apq0 = make_float2(0.f, 0.f), apq1 = make_float2(0.f, 0.f);
       auto spmv = [&](int zl) {
        if constexpr (NR == 2) {
         const float* Pz = P + (zl + 1) * PL;
@@ -672,10 +708,12 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         {  // x terms (same term order as stencil1: +x, -x, +y, -y, +z, -z)
           float4 wx0, wx1;
           tm_ld8(cX + 8u * zl, wx0, wx1);
-          const float xl0 = shl(p0.w), xr0 = shr(p0.x), xl1 = shl(p1.w), xr1 = shr(p1.x);
+          const float xr0 = shr(p0.x), xr1 = shr(p1.x);
           const float wl0 = shl(wx0.w), wl1 = shl(wx1.w);
-          q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
-          q1 = xterms(p1, xl1, xr1, wx1, qx > 0 ? wl1 : 0.f);
+          const float dl0 = shl(xd3(p0, xr0)), dl1 = shl(xd3(p1, xr1));
+          float d30, d31;
+          q0 = xterms(p0, xr0, dl0, wx0, qx > 0 ? wl0 : 0.f, d30);
+          q1 = xterms(p1, xr1, dl1, wx1, qx > 0 ? wl1 : 0.f, d31);
         }
         {  // y terms: row 2j+1 is +y of row 2j (and row 2j is -y of row 2j+1)
           const float* Wz = WY + zl * PL;
@@ -704,7 +742,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         if (!G::EXACT && !act) q0 = q1 = f4(0.f);   // idle lanes computed from row 0's p
         q[2 * zl] = q0;
         q[2 * zl + 1] = q1;
-        apq = __fadd_rn(apq, __fadd_rn(dot4f(p0, q0), dot4f(p1, q1)));
+        dot4acc(p0, q0, apq0, apq1);
+        dot4acc(p1, q1, apq0, apq1);
        } else {
         // one row per thread: both y-neighbour rows come from shared memory
         const float* Pz = P + (zl + 1) * PL;
@@ -714,8 +753,10 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         {
           float4 wx0;
           tm_ld4x(cX + 4u * zl, wx0);
-          const float xl0 = shl(p0.w), xr0 = shr(p0.x), wl0 = shl(wx0.w);
-          q0 = xterms(p0, xl0, xr0, wx0, qx > 0 ? wl0 : 0.f);
+          const float xr0 = shr(p0.x), wl0 = shl(wx0.w);
+          const float dl0 = shl(xd3(p0, xr0));
+          float d30;
+          q0 = xterms(p0, xr0, dl0, wx0, qx > 0 ? wl0 : 0.f, d30);
         }
         {
           const float* Wz = WY + zl * PL;
@@ -734,7 +775,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         }
         if (!G::EXACT && !act) q0 = f4(0.f);
         q[zl] = q0;
-        apq = __fadd_rn(apq, dot4f(p0, q0));
+        dot4acc(p0, q0, apq0, apq1);
        }
       };
 #pragma unroll
@@ -746,30 +787,32 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       spmv(0);
       spmv(ZS - 1);
       TP(3);
-      double v1[2] = {(double)apq, 0.0};
+      double v1[2] = {(double)hsum(apq0, apq1), 0.0};
       const double pq = cluster_sum(v1, 1, 1, s_pq, ph1).x;
       al = (pq > 0.0 && isfinite(pq)) ? (float)(rz / pq) : 0.f;
       TP(4);
 
       // ---- step 3: r -= alpha q;  partials r.(dinv r), r.r
-      float arz = 0.f, arr = 0.f;
+      float2 az0 = make_float2(0.f, 0.f), az1 = az0, ar0 = az0, ar1 = az0;
       {
         float4 dv[NI];
         tm_ld32(cD, dv);
 #pragma unroll
         for (int it = 0; it < NI; ++it) {
-          float4 rn = fma4(-al, q[it], r[it]);
+          float4 rn = fma4p(-al, q[it], r[it]);
           if (dv[it].x == 0.f) rn.x = 0.f;   // fixed voxel (dinv = 0): r stays 0
           if (dv[it].y == 0.f) rn.y = 0.f;
           if (dv[it].z == 0.f) rn.z = 0.f;
           if (dv[it].w == 0.f) rn.w = 0.f;
           r[it] = rn;
-          arz = __fadd_rn(arz, dot4f(rn, mul4(dv[it], rn)));
-          arr = __fadd_rn(arr, dot4f(rn, rn));
+          const float2 z0 = __fmul2_rn(lo2(dv[it]), lo2(rn)), z1 = __fmul2_rn(hi2(dv[it]), hi2(rn));
+          az0 = __ffma2_rn(lo2(rn), z0, az0);
+          az1 = __ffma2_rn(hi2(rn), z1, az1);
+          dot4acc(rn, rn, ar0, ar1);
         }
       }
       TP(5);
-      double v2[2] = {(double)arz, (double)arr};
+      double v2[2] = {(double)hsum(az0, az1), (double)hsum(ar0, ar1)};
       const double2 srr = cluster_sum(v2, 2, 2, s_rz, ph2);
       const double srz = srr.x;
       TP(6);
@@ -787,7 +830,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       const int zl = it / NR, rr = it % NR, y = NR * j + rr;
       const int so = y * N + 4 * qx;
       float4 xv = tm_ld4(cV + 4u * it);   // warp-collective
-      if (upd && al != 0.f) xv = fma4(al, ld4(P + (zl + 1) * PL + so), xv);
+      if (upd && al != 0.f) xv = fma4p(al, ld4(P + (zl + 1) * PL + so), xv);
       const uint32_t fm = fixm >> (4 * it);
       float o[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
