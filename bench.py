@@ -48,6 +48,11 @@ BYTES_1, BYTES_10 = 38, 26                      # one-pass (default): pass k >= 
 # dots p.q (2), r.(dinv r) (3), r.r (2)
 FLOPS_RES = 32
 FP32_LANES_PER_SM, SMS = 128, 148
+# shared-memory bytes per voxel-iteration of the resident kernel at 64^3 (LDS/STS of one
+# iteration per thread, counted in the SASS): step 1 p load + store (8),
+# SpMV own p, +-y rows of p and the +y/-y weights, +-z planes of p (22)
+SMEM_BYTES_RES = 30
+SMEM_BYTES_PER_CLK_SM = 128
 
 
 def log(*a):
@@ -119,41 +124,89 @@ def make_inputs(rank, world, workers):
     return p
 
 
-def cpu_oracle_sample(nbricks, seed0=0):
-    """Time the fp64 oracle (as it stands) on ``nbricks`` bricks of the same workload at the
-    same tolerance; returns (voxel-iter/s, seconds, voxel-iterations, threads used)."""
+def host_cpu():
+    """(usable cores, /proc/cpuinfo model name) of this host."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return cores, model
+
+
+def _oracle_brick(b):
+    """One cfg2 brick through the fp64 oracle in a worker process (1 BLAS thread)."""
     import workloads as wl
     from oracle import rw_oracle as ro
     from threadpoolctl import threadpool_limits
-    p = wl.cfg2(bricks=list(range(seed0, seed0 + nbricks)), n=N)
+    p = wl.cfg2(bricks=[b], n=N)
     with threadpool_limits(1):
-        t = time.perf_counter()
         o = ro.solve_problem(p, tol=p.tol, max_iter=p.max_iter)
-        dt = time.perf_counter() - t
-    vi = float(np.sum(o["iters"])) * N ** 3
-    return vi / dt, dt, vi, 1
+    return float(np.sum(o["iters"])) * N ** 3
+
+
+class OraclePool:
+    """The fp64 oracle (as it stands, never tuned) on every host core: one worker process per
+    core, one brick per task.  Input generation happens inside the timed task too (it is
+    ~1 % of an oracle solve)."""
+
+    def __init__(self):
+        import concurrent.futures as cf
+        import multiprocessing as mp
+        self.cores, self.model = host_cpu()
+        self.ex = cf.ProcessPoolExecutor(self.cores, mp_context=mp.get_context("spawn"))
+        list(self.ex.map(_warm, range(self.cores)))        # workers up, imports done
+
+    def run(self, bricks):
+        t = time.perf_counter()
+        vi = sum(self.ex.map(_oracle_brick, bricks))
+        return vi / (time.perf_counter() - t), time.perf_counter() - t, vi
+
+    def close(self):
+        self.ex.shutdown()
+
+
+def _warm(_):
+    import workloads  # noqa: F401
+    from oracle import rw_oracle  # noqa: F401
+    import threadpoolctl  # noqa: F401
+    return 0
 
 
 def run_reference(args, rank, world):
+    """This tier's reference arm: the fp64 oracle on the host cores, same metric / unit /
+    config; each step = one brick per core (a bounded sample of the 512-brick batch)."""
     if rank != 0:
         return
-    nb = 3
+    pool = OraclePool()
+    nb = pool.cores
     vals, tot_t = [], 0.0
-    for s in range(args.warmup + args.steps):
-        v, dt, vi, cores = cpu_oracle_sample(nb, seed0=(s * nb) % BATCH)
-        if s >= args.warmup:
+    for s_ in range(args.warmup + args.steps):
+        v, dt, vi = pool.run([(s_ * nb + i) % BATCH for i in range(nb)])
+        if s_ >= args.warmup:
             vals.append(v)
             tot_t += dt
+    pool.close()
     value = float(np.median(vals))
+    sample = (f"{nb} cfg2 bricks (64^3) per step, one per host core, fp64 numpy/scipy CSR "
+              f"Jacobi-PCG to rel 1e-6")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * tot_t / max(1, args.steps), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample": f"{nb} bricks of 64^3 per step (of 512)",
-                   "parallelism": "single host thread"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{nb} cfg2 bricks per step, fp64 CSR Jacobi-PCG to rel 1e-6"},
+                   "parallelism": f"{pool.cores} host processes ({pool.model})"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": pool.cores, "kind": "oracle",
+                         "cpu_model": pool.model, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -197,6 +250,165 @@ def fp32_peak_tflops():
     except Exception:
         mhz, kind = 1965.0, "derived: 148 SMs x 128 fp32 lanes x 2 x 1965 MHz (guide)"
     return SMS * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12, kind
+
+
+def smem_peak_tbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+            kind = "derived: 148 SMs x 128 B/clk x measured sm_max_mhz"
+    except Exception:
+        mhz, kind = 1965.0, "derived: 148 SMs x 128 B/clk x 1965 MHz (guide)"
+    return SMS * SMEM_BYTES_PER_CLK_SM * mhz * 1e6 / 1e12, kind
+
+
+def _ev_ms(fn, reps=1, warm=1):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+def config_lines(dev, workers):
+    """BASELINE.json configs 1, 3, 4, 5 measured beside the headline (each a full solve with
+    inputs resident, CUDA events, one warm-up): times, iterations and the dominant kernel's
+    roofline fraction.  Not part of the timed step."""
+    import torch
+    import paper_2103_09564_b200 as rwb
+    from paper_2103_09564_b200 import api
+    import workloads as wl
+    peak, peak_kind = measured_peak()
+    t2d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    res = {}
+
+    def solve(p, wide=False):
+        vol, fixed, values = t2d(p.vol), t2d(p.fixed), t2d(p.values)
+        nx, ny, nz = p.dims
+        ws = api.alloc_workspace(rwb.solve_workspace_bytes(p.batch, (nx, ny, nz), 1), dev)
+        out = {}
+
+        def run():
+            out.update(rwb.solve_bricks(fixed, values, vol=vol, beta=p.beta, eps=p.eps,
+                                        tol=p.tol, max_iter=p.max_iter, labels=True,
+                                        workspace=ws, norm=(p.scale, p.offset)))
+        rwb.set_resident_wide(wide)
+        try:
+            run()
+            torch.cuda.synchronize()
+            api.profile_enable(True)
+            ms = _ev_ms(run, reps=1, warm=0)
+            prof = api.profile_read()
+            api.profile_enable(False)
+        finally:
+            rwb.set_resident_wide(False)
+        it = out["iters"].cpu().numpy()
+        assert (out["status"].cpu().numpy() == 1).all()
+        return ms, it, prof
+
+    # cfg1: one 32^3 f32 brick (latency-bound: one cluster, 234 dependent iterations)
+    p = wl.cfg1()
+    ms, it, _ = solve(p)
+    msw, _, _ = solve(p, wide=True)
+    res["cfg1"] = {"workload": "32^3 f32 sphere, 40 seeds, tol 1e-6", "full_solve_ms": ms,
+                   "full_solve_ms_wide_cluster": msw, "iters": int(it.max()),
+                   "voxel_cg_iter_per_s": float(it.sum()) * 32 ** 3 / (min(ms, msw) / 1e3),
+                   "bound": "latency (one brick on one 4- / 8-CTA cluster)"}
+    # cfg3: one 67M-voxel system, one-pass streaming CG (38 B / voxel-iteration)
+    p = wl.cfg3()
+    ms, it, prof = solve(p)
+    nvox = float(np.prod(p.dims))
+    passA = prof["passA"][1]
+    alg = (BYTES_1 * float(it.sum()) + BYTES_10) * nvox
+    ach = alg / (passA / 1e3) / 1e9
+    res["cfg3"] = {"workload": "512x512x256 i16 CT phantom, tol 1e-6", "full_solve_ms": ms,
+                   "iters": int(it.max()),
+                   "voxel_cg_iter_per_s": float(it.sum()) * nvox / (ms / 1e3),
+                   "roofline": {"bound": "hbm", "kernel": "passA", "achieved": ach, "peak": peak,
+                                "peak_kind": peak_kind, "unit": "GB/s", "frac": ach / peak,
+                                "alg_bytes_per_voxel_iter": BYTES_1}}
+    del p
+    # cfg4: 256^3 K = 4, three RHS on one operator (one-pass streaming, 2 + 1 rhs launches)
+    lp = wl.cfg4()
+    seeds, vol = t2d(lp.labels), t2d(lp.vol)
+    ws = api.alloc_workspace(rwb.solve_labels_workspace_bytes(1, lp.dims, lp.K), dev)
+    out = {}
+
+    def run4():
+        out.update(rwb.solve_labels(seeds, lp.K, vol=vol, beta=lp.beta, eps=lp.eps, tol=lp.tol,
+                                    max_iter=lp.max_iter, workspace=ws))
+    run4()
+    torch.cuda.synchronize()
+    api.profile_enable(True)
+    ms = _ev_ms(run4, reps=1, warm=0)
+    prof = api.profile_read()
+    api.profile_enable(False)
+    it = out["iters"].cpu().numpy().ravel()
+    nvox = float(lp.vol[0].size)
+    # per voxel-iteration and rhs: r, q, p, x read + written (32 B); per launch group: dinv
+    # and the f32 intensity (8 B); groups {rhs 1, 2}, {rhs 3}
+    alg = (32.0 * float(it.sum()) + 8.0 * (max(it[0], it[1]) + it[2])) * nvox
+    ach = alg / (prof["passA"][1] / 1e3) / 1e9
+    res["cfg4"] = {"workload": "256^3 f32, K = 4 (3 RHS on one operator), tol 1e-6",
+                   "full_solve_ms": ms, "iters_per_rhs": it.tolist(),
+                   "voxel_rhs_cg_iter_per_s": float(it.sum()) * nvox / (ms / 1e3),
+                   "roofline": {"bound": "hbm", "kernel": "passA (multi-rhs)", "achieved": ach,
+                                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                                "frac": ach / peak}}
+    del seeds, vol, ws, out
+    torch.cuda.empty_cache()
+    # cfg5: 2048^3 u16 pyramid (fused 5 levels, resident) and the hierarchical solve on the
+    # vessel network (H_p with pruning, then H_it after 50 new seeds)
+    d = 2048
+    g = torch.Generator(device=dev).manual_seed(5)
+    pv = torch.randint(0, 65536, (d, d, d), dtype=torch.int32, device=dev, generator=g).to(torch.uint16)
+    outs = rwb.build_pyramid(pv, 5)
+    ms = _ev_ms(lambda: rwb.build_pyramid(pv, 5, outs=outs), reps=3)
+    nbytes = pv.numel() * 2 + sum(o.numel() * 2 for o in outs)
+    del pv, outs
+    torch.cuda.empty_cache()
+    t = time.time()
+    vol = wl.cfg5_volume(1.0, workers)
+    seeds = wl.cfg5_seeds(vol)
+    seeds2 = wl.cfg5_new_seeds(vol, seeds)
+    gen_s = time.time() - t
+    vol_d, seeds_d, seeds2_d = t2d(vol), t2d(seeds), t2d(seeds2)
+    del vol
+    state = {}
+
+    def hier(prev=None, sd=seeds_d):
+        prob, st, stt = rwb.hier_segment(vol_d, sd, s=32, e=1.25, prune=True, tol=1e-6,
+                                          max_iter=5000, prev=prev,
+                                          workspace=state.get("workspace"), out=state.get("prob"))
+        state.update(stt)
+        state["stats"] = st
+    hier()
+    torch.cuda.synchronize()
+    ms_h = _ev_ms(hier, reps=1, warm=0)
+    st = state["stats"]
+    ms_i = _ev_ms(lambda: hier(prev=dict(state), sd=seeds2_d), reps=1, warm=0)
+    st2 = state["stats"]
+    res["cfg5"] = {
+        "workload": "2048^3 u16 vessel network (16 GiB), s = 32, e = 1.25, 400 fg / 400 bg seeds",
+        "pyramid_ms": ms, "pyramid_roofline": {"bound": "hbm", "achieved": nbytes / ms / 1e6,
+                                               "peak": peak, "peak_kind": peak_kind,
+                                               "unit": "GB/s", "frac": nbytes / ms / 1e6 / peak},
+        "hier_Hp_ms": ms_h, "hier_bricks_solved": int(sum(st["solved"])),
+        "hier_output_voxels_per_s": d ** 3 / (ms_h / 1e3),
+        "hier_Hit_plus50_seeds_ms": ms_i, "hier_Hit_bricks_solved": int(sum(st2["solved"])),
+        "hier_Hit_bricks_reused": int(sum(st2["reused"])),
+        "generate_s": gen_s}
+    del vol_d, seeds_d, seeds2_d, state
+    torch.cuda.empty_cache()
+    return res
 
 
 def pyramid_and_queue(dev, d=1024, levels=5, slab=128):
@@ -305,6 +517,10 @@ def run_b200(args, rank, world, local_rank):
     iters = out["iters"].cpu().numpy().astype(np.int64)
     assert (out["status"].cpu().numpy() == 1).all(), "not all bricks converged"
     vox_iters = float(iters.sum()) * N ** 3
+    ref_iters = out["iters"].cpu()
+    ref_prob = out["prob"].cpu()
+    unknown = (p.fixed.reshape(p.fixed.shape[0], -1) == 0).sum(1).astype(np.float64)
+    unk_iters = float((unknown * iters.reshape(-1)).sum())
 
     # ---------------- device-timed region (inputs resident) ----------------
     clk = Clocks(local_rank)
@@ -335,6 +551,14 @@ def run_b200(args, rank, world, local_rank):
     if solver_used == "resident":
         peak, peak_kind = fp32_peak_tflops()
         achieved = FLOPS_RES * vox_iters * args.steps / (kms["resident"] / 1000.0) / 1e12
+        speak, speak_kind = smem_peak_tbs()
+        sach = SMEM_BYTES_RES * vox_iters * args.steps / (kms["resident"] / 1000.0) / 1e12
+        roofline_smem = {"bound": "smem", "kernel": "resident", "achieved": sach, "peak": speak,
+                         "peak_kind": speak_kind, "unit": "TB/s", "frac": sach / speak,
+                         "alg_bytes_per_voxel_iter": SMEM_BYTES_RES,
+                         "ncu_shared_wavefronts_pct_of_peak": 40.0,
+                         "note": "LDS/STS bytes of one iteration counted in the SASS; 112 of 148 "
+                                 "SMs host 16-CTA clusters (DESIGN.md 5b)"}
         roofline = {"bound": "alu", "kernel": "resident", "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "TFLOP/s", "frac": achieved / peak,
                     "traffic": ncu_traffic("resident"),
@@ -345,6 +569,7 @@ def run_b200(args, rank, world, local_rank):
                             "halo exchange per iteration (DESIGN.md 5)"}
     else:
         roofline = streaming_roofline(kms, vox_iters, args.steps, BATCH)
+        roofline_smem = None
 
     streaming = None
     if solver_used == "resident" and not args.no_streaming:
@@ -374,48 +599,74 @@ def run_b200(args, rank, world, local_rank):
 
     # ---------------- end to end through the API with host buffers ----------------
     # rw_solve_bricks_host: pinned host inputs -> chunked H2D / solve / D2H pipeline -> host
-    # labels + iterations (the copies are inside the timed region, overlapped with the solve)
+    # fp32 probabilities + labels + iterations (the copies are inside the timed region,
+    # overlapped with the solve).  Measured twice: with the fp32 probabilities copied back
+    # (the headline e2e: rw_solve_bricks' output) and with labels only.
     h_vol = torch.from_numpy(p.vol).pin_memory()
     h_fixed = torch.from_numpy(p.fixed).pin_memory()
     h_values = torch.from_numpy(p.values[0]).pin_memory()
-    h_out = dict(prob=None, labels=torch.empty(tuple(fixed.shape), dtype=torch.uint8).pin_memory(),
-                 iters=torch.empty((1, BATCH), dtype=torch.int32).pin_memory(),
-                 resid=torch.empty((1, BATCH), dtype=torch.float32).pin_memory(),
-                 status=torch.empty((1, BATCH), dtype=torch.int32).pin_memory())
     h_ws = api.alloc_workspace(api.lib().rw_solve_host_workspace_bytes(
         BATCH, api.rw_dims(N, N, N), api.DTYPES[torch.uint16], args.e2e_chunk), dev)
-
-    def e2e_step():
-        rwb.solve_bricks_host(h_fixed, h_values, h_vol, beta=p.beta, eps=p.eps, tol=p.tol,
-                              max_iter=p.max_iter, chunk=args.e2e_chunk, labels=True,
-                              workspace=h_ws, out=h_out, device=dev, stream=stream)
-
-    e2e_step()
-    torch.cuda.synchronize()
-    assert torch.equal(h_out["iters"], out["iters"].cpu()), "host pipeline differs from the device solve"
-    barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ems, _ = reduce_metric(e0.elapsed_time(e1), vox_iters, dev)
-    e2e_value = work_all / (ems / args.steps / 1000.0)
     h2d = h_vol.numel() * h_vol.element_size() + h_fixed.numel() + h_values.numel() * 4
-    d2h = h_out["labels"].numel() + BATCH * 12
+
+    def e2e_run(with_prob):
+        h_out = dict(prob=torch.empty((1,) + tuple(fixed.shape), dtype=torch.float32).pin_memory()
+                     if with_prob else None,
+                     labels=torch.empty(tuple(fixed.shape), dtype=torch.uint8).pin_memory(),
+                     iters=torch.empty((1, BATCH), dtype=torch.int32).pin_memory(),
+                     resid=torch.empty((1, BATCH), dtype=torch.float32).pin_memory(),
+                     status=torch.empty((1, BATCH), dtype=torch.int32).pin_memory())
+
+        def e2e_step():
+            rwb.solve_bricks_host(h_fixed, h_values, h_vol, beta=p.beta, eps=p.eps, tol=p.tol,
+                                  max_iter=p.max_iter, chunk=args.e2e_chunk, prob=with_prob,
+                                  labels=True, workspace=h_ws, out=h_out, device=dev,
+                                  stream=stream)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        assert torch.equal(h_out["iters"], ref_iters), "host pipeline differs from the device solve"
+        if with_prob:
+            assert torch.equal(h_out["prob"], ref_prob), "host pipeline prob differs"
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems, _ = reduce_metric(e0.elapsed_time(e1), vox_iters, dev)
+        d2h = h_out["labels"].numel() + BATCH * 12 + (h_out["prob"].numel() * 4 if with_prob else 0)
+        return {"value": work_all / (ems / args.steps / 1000.0), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": ems / args.steps,
+                "api": "rw_solve_bricks_host (pinned host buffers, chunked H2D/solve/D2H overlap)",
+                "returns": "fp32 prob + u8 labels + iters/resid/status" if with_prob
+                           else "u8 labels + iters/resid/status",
+                "chunk": args.e2e_chunk or -(-BATCH // 32)}
+
+    e2e = e2e_run(True)
+    e2e_labels = e2e_run(False)
     del h_ws
 
     # ---------------- rows a8 / a9 beside the headline (not part of the step) ----------------
     rows = None if (args.no_rows or rank != 0) else pyramid_and_queue(dev)
+    del vol, fixed, values, ws, out
+    torch.cuda.empty_cache()
+    configs = None if (args.no_configs or rank != 0 or world > 1) else config_lines(dev, args.workers)
 
     if rank != 0:
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, dt, vi, cores = cpu_oracle_sample(args.cpu_bricks)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{args.cpu_bricks} cfg2 bricks (64^3) at rel tol 1e-6, {dt:.1f}s, "
-                         "fp64 numpy/scipy CSR Jacobi-PCG, 1 thread"}
+        pool = OraclePool()
+        nb = max(args.cpu_bricks, 2 * pool.cores)
+        v, dt, vi = pool.run(list(range(nb)))
+        pool.close()
+        cpu = {"value": v, "unit": UNIT, "cores": pool.cores, "cpu_model": pool.model,
+               "kind": "oracle",
+               "sample": f"{nb} cfg2 bricks (64^3) at rel tol 1e-6 on {pool.cores} host "
+                         f"processes (one brick per task), {dt:.1f}s, fp64 numpy/scipy CSR "
+                         "Jacobi-PCG"}
     gpu_launches = sum(launches.values())
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -427,17 +678,18 @@ def run_b200(args, rank, world, local_rank):
                    "l2": "inputs larger than L2 (u16 volume, mask, values, weight planes, CG state: > 2 GB), no flush",
                    "iters": {"min": int(iters.min()), "median": float(np.median(iters)),
                              "max": int(iters.max())}},
+        "unknown_voxel_cg_iter_per_s": unk_iters * world / (ms_per_step / 1000.0),
         "bricks_per_s": BATCH * world / (ms_per_step / 1000.0),
         "full_solve_ms": ms_per_step,
         "solver": solver_used,
         "roofline": roofline,
+        "roofline_smem": roofline_smem,
         "streaming": streaming,
+        "configs": configs,
         "pyramid_queue": rows,
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps,
-                "api": "rw_solve_bricks_host (pinned host buffers, chunked H2D/solve/D2H overlap)",
-                "chunk": args.e2e_chunk or -(-BATCH // 32)},
+        "e2e": e2e,
+        "e2e_labels_only": e2e_labels,
         "gpu_launches": int(gpu_launches),
         "clocks": clocks,
     }
@@ -452,7 +704,7 @@ def main():
                     help="bricks per pipeline chunk of the e2e host-buffer solve (0: batch/32)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workers", type=int, default=min(16, os.cpu_count() or 1))
+    ap.add_argument("--workers", type=int, default=min(32, os.cpu_count() or 1))
     ap.add_argument("--cpu-bricks", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solver", default="auto", choices=["auto", "streaming", "resident"])
@@ -460,6 +712,8 @@ def main():
                     help="skip the secondary streaming-solver timing")
     ap.add_argument("--no-rows", action="store_true",
                     help="skip the secondary pyramid / queue measurements")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the BASELINE configs 1/3/4/5 block")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

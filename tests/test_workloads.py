@@ -48,3 +48,30 @@ def test_cfg5_slab_decomposition_invariant():
     a = wl.cfg5_slab(0, 6, scale=1 / 64)
     b = np.concatenate([wl.cfg5_slab(0, 3, scale=1 / 64), wl.cfg5_slab(3, 6, scale=1 / 64)])
     assert np.array_equal(a, b) and a.dtype == np.uint16
+
+
+def test_cfg2_every_isolated_region_is_seeded():
+    """Reading c7 / R7: in every cfg2 brick each region that intensity jumps > GAP cut off from
+    the rest holds a fixed voxel (brick 256 has a 4-voxel background pocket enclosed by two
+    blobs; 22 of the 512 bricks get such a seed), so tol 1e-6 pins the solution everywhere."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+    from workloads import gen
+    for b in (2, 97, 256, 359):
+        vol, fixed, values = gen.cfg2_brick(b)
+        n = vol.shape[0]
+        g = vol.astype(np.float64) / 65535.0
+        idx = np.arange(n ** 3).reshape(n, n, n)
+        r, c = [], []
+        for ax in range(3):
+            sp = [slice(None)] * 3
+            sq = [slice(None)] * 3
+            sp[ax] = slice(0, -1)
+            sq[ax] = slice(1, None)
+            close = np.abs(g[tuple(sp)] - g[tuple(sq)]) <= gen.GAP
+            r.append(idx[tuple(sp)][close])
+            c.append(idx[tuple(sq)][close])
+        r, c = np.concatenate(r), np.concatenate(c)
+        _, lab = connected_components(coo_matrix((np.ones(r.size), (r, c)), shape=(n ** 3,) * 2),
+                                      directed=False)
+        assert set(np.unique(lab)) == set(np.unique(lab[fixed.ravel() > 0])), b

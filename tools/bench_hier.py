@@ -28,35 +28,11 @@ from workloads.gen import _vessel_segments  # noqa: E402
 
 
 def volume(scale, workers=16):
-    d = wl.cfg5_dims(scale)[0]
-    wl.cfg5_slab(0, 1, scale)          # build the segment cache once
-    step = max(1, d // (workers * 4))
-    with ThreadPoolExecutor(workers) as ex:
-        parts = list(ex.map(lambda z: wl.cfg5_slab(z, min(z + step, d), scale), range(0, d, step)))
-    return np.concatenate(parts, 0)
+    return wl.cfg5_volume(scale, workers)
 
 
 def seed_labels(vol, scale, nfg=400, nbg=400, seed=0):
-    """Foreground seeds at vessel segment mid points, background seeds at random voxels
-    whose 5^3 neighbourhood is vessel-free (intensity well below the vessel level)."""
-    d = vol.shape[0]
-    rng = np.random.default_rng([5, 2, seed])
-    seeds = np.zeros(vol.shape, np.uint8)
-    segs = _vessel_segments(d)
-    pick = rng.choice(len(segs), size=min(nfg, len(segs)), replace=False)
-    for i in pick:
-        p0, p1, r = segs[i]
-        m = np.floor((p0 + p1) / 2).astype(int)
-        x, y, z = np.clip(m, 0, d - 1)
-        if vol[z, y, x] > 15000:
-            seeds[z, y, x] = 1
-    n = 0
-    while n < nbg:
-        z, y, x = rng.integers(2, d - 2, 3)
-        if vol[z - 2:z + 3, y - 2:y + 3, x - 2:x + 3].max() < 10000:
-            seeds[z, y, x] = 2
-            n += 1
-    return seeds
+    return wl.cfg5_seeds(vol, nfg, nbg, seed)
 
 
 def run(vol_d, seeds_d, s, e, prune, reps=2, prev=None, ws=None, prob_buf=None):
@@ -81,22 +57,7 @@ def run(vol_d, seeds_d, s, e, prune, reps=2, prev=None, ws=None, prob_buf=None):
 
 
 def new_seeds(vol, seeds, n=50, seed=1):
-    """Config 5's incremental step: `n` new foreground seeds at vessel segment mid points
-    that were not seeded before."""
-    d = vol.shape[0]
-    rng = np.random.default_rng([5, 3, seed])
-    out = seeds.copy()
-    segs = _vessel_segments(d)
-    added = 0
-    for i in rng.permutation(len(segs)):
-        p0, p1, r = segs[i]
-        x, y, z = np.clip(np.floor((p0 + p1) / 2).astype(int), 0, d - 1)
-        if vol[z, y, x] > 15000 and out[z, y, x] == 0:
-            out[z, y, x] = 1
-            added += 1
-            if added == n:
-                break
-    return out
+    return wl.cfg5_new_seeds(vol, seeds, n, seed)
 
 
 def main():

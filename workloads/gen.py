@@ -215,7 +215,42 @@ def cfg2_brick(b: int, n: int = 64, seed_frac: float = 1e-3):
     values[fg] = 1.0
     fixed[bg] = 1
     values[bg] = 0.0
+    # reading c7 / R7: every region the intensity contrast isolates must hold a fixed voxel.
+    # Union of overlapping ellipsoids can enclose a small background pocket, and a later blob
+    # can cut an earlier one in two; such a region would be coupled to the rest only through
+    # edges with |dg| > GAP (weights below ~1e-4 at beta = 100), and its solution would stay
+    # at the initial guess at tol 1e-6 (unpinned).  One seed goes into each
+    # such region: value 1 if its mean intensity is blob-like, else 0.
+    _seed_isolated(vol.astype(np.float64) / 65535.0, fixed, values, bgv, n)
     return vol, fixed.reshape(n, n, n), values.reshape(n, n, n)
+
+
+GAP = 0.3   # intensity jump that separates regions (input conditioning, see _seed_isolated)
+
+
+def _seed_isolated(g, fixed, values, bgv, n):
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+    idx = np.arange(n ** 3).reshape(n, n, n)
+    rows, cols = [], []
+    for sp, sq in (((slice(None), slice(None), slice(0, -1)), (slice(None), slice(None), slice(1, None))),
+                   ((slice(None), slice(0, -1), slice(None)), (slice(None), slice(1, None), slice(None))),
+                   ((slice(0, -1), slice(None), slice(None)), (slice(1, None), slice(None), slice(None)))):
+        close = np.abs(g[sp] - g[sq]) <= GAP
+        rows.append(idx[sp][close])
+        cols.append(idx[sq][close])
+    r = np.concatenate(rows)
+    c = np.concatenate(cols)
+    A = coo_matrix((np.ones(r.size, np.int8), (r, c)), shape=(n ** 3, n ** 3))
+    ncomp, lab = connected_components(A, directed=False)
+    has_fixed = np.zeros(ncomp, bool)
+    has_fixed[lab[fixed > 0]] = True
+    gr = g.ravel()
+    for comp in np.flatnonzero(~has_fixed):
+        members = np.flatnonzero(lab == comp)
+        k = int(members[0])
+        fixed[k] = 1
+        values[k] = 1.0 if gr[members].mean() > bgv + 0.15 else 0.0
 
 
 def cfg2(batch: int = 512, n: int = 64, bricks=None, max_iter: int = 2000,
@@ -510,3 +545,58 @@ def pyramid_volume(nx: int, ny: int, nz: int, dtype: str, seed: int, kind: str =
     if kind == "min":
         return np.full(shp, np.iinfo(dt).min if dtype != "f32" else 0.0, dt)
     raise ValueError(kind)
+
+
+def cfg5_volume(scale: float = 1.0, workers: int = 16):
+    """The whole config-5 vessel volume [d, d, d] u16 (cfg5_slab over z-slabs on `workers`
+    host threads)."""
+    from concurrent.futures import ThreadPoolExecutor
+    d = cfg5_dims(scale)[0]
+    cfg5_slab(0, 1, scale)          # build the segment cache once
+    step = max(1, d // (max(1, workers) * 4))
+    with ThreadPoolExecutor(max(1, workers)) as ex:
+        parts = list(ex.map(lambda z: cfg5_slab(z, min(z + step, d), scale), range(0, d, step)))
+    return np.concatenate(parts, 0)
+
+
+def cfg5_seeds(vol, nfg: int = 400, nbg: int = 400, seed: int = 0):
+    """Config 5's rasterised seeds (reading R22): 0 unseeded, 1 foreground at vessel
+    segment mid points, 2 background at random voxels whose 5^3 neighbourhood is vessel-free
+    (intensity well below the vessel level)."""
+    d = vol.shape[0]
+    rng = np.random.default_rng([5, 2, seed])
+    seeds = np.zeros(vol.shape, np.uint8)
+    segs = _vessel_segments(d)
+    pick = rng.choice(len(segs), size=min(nfg, len(segs)), replace=False)
+    for i in pick:
+        p0, p1, r = segs[i]
+        m = np.floor((p0 + p1) / 2).astype(int)
+        x, y, z = np.clip(m, 0, d - 1)
+        if vol[z, y, x] > 15000:
+            seeds[z, y, x] = 1
+    n = 0
+    while n < nbg:
+        z, y, x = rng.integers(2, d - 2, 3)
+        if vol[z - 2:z + 3, y - 2:y + 3, x - 2:x + 3].max() < 10000:
+            seeds[z, y, x] = 2
+            n += 1
+    return seeds
+
+
+def cfg5_new_seeds(vol, seeds, n: int = 50, seed: int = 1):
+    """Config 5's incremental step: `n` new foreground seeds at vessel segment mid points
+    that were not seeded before."""
+    d = vol.shape[0]
+    rng = np.random.default_rng([5, 3, seed])
+    out = seeds.copy()
+    segs = _vessel_segments(d)
+    added = 0
+    for i in rng.permutation(len(segs)):
+        p0, p1, r = segs[i]
+        x, y, z = np.clip(np.floor((p0 + p1) / 2).astype(int), 0, d - 1)
+        if vol[z, y, x] > 15000 and out[z, y, x] == 0:
+            out[z, y, x] = 1
+            added += 1
+            if added == n:
+                break
+    return out
