@@ -147,8 +147,12 @@ size_t rw_solve_workspace_bytes(int32_t batch, rw_dims d, int32_t nrhs, int32_t 
  *   labels out   device u8 [batch][n] or NULL: prob[0] > 0.5 (0.5 -> 0, c10).
  *   Not errors: non-convergence (iters = max_iter, status MAXITER); a brick without fixed
  *   voxels (prob = x0 clamped, iters 0, status TRIVIAL).
- *   The call blocks the host until the iteration loop has finished (it polls a device
- *   counter every few iterations); all work is ordered on `stream`.
+ *   Stream-ordered and asynchronous: all work is enqueued on `stream` and the call returns
+ *   without waiting for it (resident solver: one kernel; streaming solver: one CUDA graph
+ *   whose WHILE node runs the iterations on the device, RW_OPT_DEVICE_LOOP).  Outputs are
+ *   valid once `stream` reaches this point.  Exceptions that block the host until the loop
+ *   has been enqueued: RW_OPT_DEVICE_LOOP = 0, RW_OPT_STREAM_PASSES = 2, residual
+ *   replacement, and RW_OPT_COSCHED when it applies.
  * ---------------------------------------------------------------------------------- */
 rw_status rw_solve_bricks(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype,
                           rw_norm nm, const float* W, const uint8_t* fixed,
@@ -322,9 +326,15 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
  * stream concurrently with the resident clusters, on the SMs the 16-CTA clusters cannot use
  * (the last bricks of the batch; joined back into the caller's stream).  Needs the
  * workspace rw_solve_workspace_bytes reports (a smaller one disables it).  Those bricks'
- * results agree with the resident solver's to the solver tolerance, not bitwise.  Off by
- * default: on B200 the concurrent streaming traffic slows the clusters more than the
- * 36 spare SMs add.
+ * results agree with the resident solver's to the solver tolerance, not bitwise, so a
+ * brick's bits then depend on its position in the batch.  Off by default for that reason
+ * (measured on B200: 100 per mille = +4.5 % on the 512 x 64^3 batch, larger shares slower;
+ * DESIGN.md 5b).
+ * RW_OPT_DEVICE_LOOP: 1 (default) = the streaming solver's iteration loop is device-driven:
+ * one CUDA graph whose conditional WHILE node repeats {pass A, loop control} on the GPU, so
+ * rw_solve_bricks / rw_solve_labels never block the host (fully stream-ordered; one-pass
+ * mode without residual replacement).  0 = host-driven loop (the host polls the active-pair
+ * count every 8 iterations and blocks until the loop has been enqueued).  Bit-identical.
  * RW_OPT_RESIDUAL_REPLACE: interval (iterations, default 0 = off) at which the streaming
  * solver replaces the recurrence residual by the true residual b - L_UU x computed in fp32
  * (and flushes the lagged x update).  Experimental: the fp32 true residual floors near
@@ -348,7 +358,7 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
  * bitwise (different fp64 reduction trees); each is deterministic and batch-invariant.
  * ---------------------------------------------------------------------------------- */
 enum { RW_OPT_SOLVER = 0, RW_OPT_COSCHED = 1, RW_OPT_RESIDUAL_REPLACE = 2,
-       RW_OPT_STREAM_PASSES = 3, RW_OPT_RESIDENT_WIDE = 4 };
+       RW_OPT_STREAM_PASSES = 3, RW_OPT_RESIDENT_WIDE = 4, RW_OPT_DEVICE_LOOP = 5 };
 enum { RW_SOLVER_AUTO = 0, RW_SOLVER_STREAMING = 1, RW_SOLVER_RESIDENT = 2 };
 rw_status rw_set_option(int32_t key, int64_t value);
 int64_t rw_get_option(int32_t key);

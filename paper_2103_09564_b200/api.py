@@ -91,6 +91,27 @@ def get_resident_wide():
     return bool(lib().rw_get_option(4))
 
 
+def set_device_loop(on):
+    """rw_set_option(RW_OPT_DEVICE_LOOP): 1 (default) = the streaming CG loop runs on the
+    device (one CUDA graph with a conditional WHILE node, the call does not block the host);
+    0 = host-driven loop."""
+    check(lib().rw_set_option(5, int(bool(on))), "rw_set_option")
+
+
+def get_device_loop():
+    return bool(lib().rw_get_option(5))
+
+
+@contextlib.contextmanager
+def device_loop(on):
+    old = get_device_loop()
+    set_device_loop(on)
+    try:
+        yield
+    finally:
+        set_device_loop(old)
+
+
 def set_stream_passes(n):
     """rw_set_option(RW_OPT_STREAM_PASSES): 1 (default, one fused pass per streaming CG
     iteration) or 2 (classical passes A + B)."""

@@ -23,6 +23,7 @@ cudaError_t launch_dinv(const float*, int, int, int, int, const uint8_t*, float*
 cudaError_t launch_setup(const Plan&, const Bufs&, const Ctl&, cudaStream_t);
 cudaError_t launch_iteration_A(const Plan&, const Bufs&, const Ctl&, int, const Maps&, cudaStream_t);
 cudaError_t launch_iteration_B(const Plan&, const Bufs&, int, cudaStream_t);
+cudaError_t launch_loop_ctl(cudaGraphConditionalHandle, int*, int, cudaStream_t);
 cudaError_t launch_replace(const Plan&, const Bufs&, const Ctl&, int, cudaStream_t);
 cudaError_t launch_finalize(const Plan&, const Bufs&, const Ctl&, float*, int*, uint8_t*, cudaStream_t);
 cudaError_t launch_labels_prep(const uint8_t*, long long, int, uint8_t*, float*, int, cudaStream_t);
@@ -56,6 +57,7 @@ int g_solver = RW_SOLVER_AUTO;
 int g_rr = 0;
 int g_passes = 1;   // RW_OPT_STREAM_PASSES
 int g_res_wide = 0; // RW_OPT_RESIDENT_WIDE
+int g_dev_loop = 1; // RW_OPT_DEVICE_LOOP
 
 rw_status fail(rw_status st, const char* fmt, ...) {
   char buf[512];
@@ -316,6 +318,84 @@ rw_status cosched_handles(cudaStream_t* s2, cudaEvent_t* fork, cudaEvent_t* join
   return RW_OK;
 }
 
+// The device-driven streaming loop: a graph with one conditional WHILE node whose body is
+// captured once from the ordinary launchers (pass A with Bf.kdev set, then k_loop_ctl).
+// The graph is built and instantiated per call (tens of microseconds against solves of
+// milliseconds or more) and released asynchronously after its launch.
+struct ParkedGraph {
+  cudaGraphExec_t x;
+  cudaGraph_t g;
+  cudaEvent_t done;
+};
+thread_local std::vector<ParkedGraph> g_graphs;
+
+void release_finished_graphs() {
+  size_t k = 0;
+  for (auto& pg : g_graphs) {
+    if (cudaEventQuery(pg.done) == cudaSuccess) {
+      cudaGraphExecDestroy(pg.x);
+      cudaGraphDestroy(pg.g);
+      cudaEventDestroy(pg.done);
+    } else {
+      g_graphs[k++] = pg;
+    }
+  }
+  g_graphs.resize(k);
+  cudaGetLastError();   // cudaErrorNotReady from the queries
+}
+
+rw_status device_loop(const rw::Plan& P, const rw::Bufs& Bf, const rw::Ctl& C, const rw::Maps& M,
+                      int kend, cudaStream_t s) {
+  release_finished_graphs();
+  static thread_local cudaStream_t cap = nullptr;
+  if (!cap) RW_CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t x = nullptr;
+  RW_CK(cudaGraphCreate(&g, 0));
+  auto bail = [&](cudaError_t e, const char* what) {
+    if (x) cudaGraphExecDestroy(x);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return fail(RW_ECUDA, "device loop: %s: %s", what, cudaGetErrorString(e));
+  };
+  cudaGraphConditionalHandle h;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  if (e != cudaSuccess) return bail(e, "conditional handle");
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  e = cudaGraphAddNode(&node, g, nullptr, 0, &np);
+  if (e != cudaSuccess) return bail(e, "while node");
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  e = cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+  if (e != cudaSuccess) return bail(e, "capture");
+  cudaError_t e1 = rw::launch_iteration_A(P, Bf, C, 0, M, cap);
+  cudaError_t e2 = rw::launch_loop_ctl(h, Bf.ctr, kend, cap);
+  e = cudaStreamEndCapture(cap, &body);
+  if (e1 != cudaSuccess) return bail(e1, "pass A capture");
+  if (e2 != cudaSuccess) return bail(e2, "control capture");
+  if (e != cudaSuccess) return bail(e, "end capture");
+  e = cudaGraphInstantiate(&x, g, 0);
+  if (e != cudaSuccess) return bail(e, "instantiate");
+  // pass 0 counts into ctr[0]; the loop index starts at 0
+  RW_CK(cudaMemsetAsync(Bf.ctr, 0, sizeof(int), s));
+  RW_CK(cudaMemsetAsync(Bf.ctr + 3, 0, sizeof(int), s));
+  g_prof.begin(s);
+  e = cudaGraphLaunch(x, s);
+  if (e != cudaSuccess) return bail(e, "launch");
+  g_prof.end(RW_K_PASSA, s, 1);
+  // destroying an executable graph waits for it, so launched graphs are parked and released
+  // by a later call once their completion event has fired (the host never waits here)
+  cudaEvent_t done;
+  RW_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  RW_CK(cudaEventRecord(done, s));
+  g_graphs.push_back({x, g, done});
+  return RW_OK;
+}
+
 // Core solve with fixed/values already on the device.
 rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, rw_norm nm,
                      const float* W, const uint8_t* fixed, const float* values, int32_t nrhs,
@@ -461,6 +541,17 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   const int nA = (P.R + rw::passA_rc(P) - 1) / rw::passA_rc(P);
   const int nB = (P.R + 3) / 4;
   const bool one = P.one != 0;
+  if (one && C.rr == 0 && g_dev_loop) {
+    // Device-driven loop ("the CG iterations run on the GPU"): one CUDA graph whose
+    // WHILE node repeats { pass A(k), loop control } until a pass finds no active
+    // (rhs, brick) pair or k reaches max_iter + 1; the pass reads k from the workspace.
+    // Nothing blocks the host; results are bit-identical to the host-driven loop.
+    Bf.kdev = Bf.ctr + 3;
+    st = device_loop(P, Bf, C, M, max_iter + 1, s);
+    if (st != RW_OK) return st;
+    RW_TIMED(RW_K_FINALIZE, s, 1, rw::launch_finalize(P, Bf, C, resid, status, labels, s));
+    return RW_OK;
+  }
   st = ensure_pinned();
   if (st != RW_OK) return st;
   // Host-polled loop: every CHECK iterations the active-pair count is copied to pinned
@@ -532,6 +623,11 @@ rw_status rw_set_option(int32_t key, int64_t value) {
     g_rr = (int)value;
     return RW_OK;
   }
+  if (key == RW_OPT_DEVICE_LOOP) {
+    if (value != 0 && value != 1) return fail(RW_EINVAL, "rw_set_option: device loop must be 0 or 1");
+    g_dev_loop = (int)value;
+    return RW_OK;
+  }
   if (key == RW_OPT_RESIDENT_WIDE) {
     if (value != 0 && value != 1) return fail(RW_EINVAL, "rw_set_option: resident wide must be 0 or 1");
     g_res_wide = (int)value;
@@ -557,7 +653,7 @@ rw_status rw_set_option(int32_t key, int64_t value) {
 int64_t rw_get_option(int32_t key) {
   return key == RW_OPT_SOLVER ? g_solver : key == RW_OPT_COSCHED ? g_cosched_pm
          : key == RW_OPT_RESIDUAL_REPLACE ? g_rr : key == RW_OPT_STREAM_PASSES ? g_passes
-         : key == RW_OPT_RESIDENT_WIDE ? g_res_wide : -1;
+         : key == RW_OPT_RESIDENT_WIDE ? g_res_wide : key == RW_OPT_DEVICE_LOOP ? g_dev_loop : -1;
 }
 
 int32_t rw_resident_available(rw_dims d, int32_t nrhs) {

@@ -380,6 +380,22 @@ cudaError_t launch_replace(const Plan& P, const Bufs& Bf, const Ctl& C, int k, c
   return cudaGetLastError();
 }
 
+// Device-driven loop control (one thread), after pass A(k) inside the body of a CUDA-graph
+// WHILE node: continue while pass k still found active (rhs, brick) pairs and k < kend,
+// zero the counter of pass k+1 and advance the device iteration index.
+__global__ void k_loop_ctl(cudaGraphConditionalHandle h, int* ctr, int kend) {
+  const int k = ctr[3];
+  const bool more = ctr[k & 1] > 0 && k < kend;
+  ctr[(k + 1) & 1] = 0;
+  ctr[3] = k + 1;
+  cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+cudaError_t launch_loop_ctl(cudaGraphConditionalHandle h, int* ctr, int kend, cudaStream_t s) {
+  k_loop_ctl<<<1, 1, 0, s>>>(h, ctr, kend);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_iteration_B(const Plan& P, const Bufs& Bf, int k, cudaStream_t s) {
   for (int r0 = 0; r0 < P.R; r0 += 4) {
     const int rc = P.R - r0 < 4 ? P.R - r0 : 4;

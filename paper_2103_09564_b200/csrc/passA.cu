@@ -38,6 +38,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   // NS = a_stages(P): ring depth, a compile-time constant (a runtime modulo in the ring
   // indexing measured 7 % slower)
   extern __shared__ __align__(128) unsigned char smem[];
+  if (Bf.kdev) k = *reinterpret_cast<const volatile int*>(Bf.kdev);   // device-driven loop
   __shared__ float s_beta[RC], s_alpha[RC];
   __shared__ int s_act[RC];
   const int u = blockIdx.x, b = blockIdx.y;

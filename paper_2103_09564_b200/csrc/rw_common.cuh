@@ -57,7 +57,10 @@ struct Bufs {
   double4* PS;        // [R*B][U]          (b.b, n_fixed, n_unknown, 0) from setup
   int* status;        // [R*B]
   int* iters;         // [R*B]
-  int* ctr;           // [2] active (rhs,brick) count per iteration parity
+  int* ctr;           // [4]: [0..1] active (rhs,brick) count per iteration parity,
+                      //      [2] resident brick counter, [3] iteration index (device loop)
+  const int* kdev;    // device-driven loop: pass A reads its iteration index here (ctr + 3);
+                      // null: the index is the kernel argument (host-driven loop)
 };
 
 struct Ctl {
