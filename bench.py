@@ -714,7 +714,13 @@ def main():
                     help="skip the secondary pyramid / queue measurements")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the BASELINE configs 1/3/4/5 block")
+    ap.add_argument("--host-loop", action="store_true",
+                    help="streaming solver: host-driven iteration loop (RW_OPT_DEVICE_LOOP = 0); "
+                         "ncu cannot profile kernels inside conditional CUDA graphs")
     args = ap.parse_args()
+    if args.host_loop:
+        import paper_2103_09564_b200 as rwb
+        rwb.set_device_loop(False)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

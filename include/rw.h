@@ -353,12 +353,16 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
  * clusters of 4 planes (latency: twice the SMs per brick -- a single 32^3 brick solves in
  * 0.55 instead of 0.74 ms).  Within one setting results are batch-invariant; across the
  * two they agree to the solver tolerance.
+ * RW_OPT_STREAM_ZC: 0 (default, automatic) or the streaming solver's z-chunk (planes per
+ * CTA column tile, 4..4096).  The chunk fixes the fp64 partial-sum tree, so results are
+ * bitwise reproducible for a given chunk; different chunks agree to the solver tolerance.
  * rw_resident_available(d, nrhs): 1 if the resident solver can serve this shape on the
  * current device, else 0.  Results of the two solvers agree to the solver tolerance, not
  * bitwise (different fp64 reduction trees); each is deterministic and batch-invariant.
  * ---------------------------------------------------------------------------------- */
 enum { RW_OPT_SOLVER = 0, RW_OPT_COSCHED = 1, RW_OPT_RESIDUAL_REPLACE = 2,
-       RW_OPT_STREAM_PASSES = 3, RW_OPT_RESIDENT_WIDE = 4, RW_OPT_DEVICE_LOOP = 5 };
+       RW_OPT_STREAM_PASSES = 3, RW_OPT_RESIDENT_WIDE = 4, RW_OPT_DEVICE_LOOP = 5,
+       RW_OPT_STREAM_ZC = 6 };
 enum { RW_SOLVER_AUTO = 0, RW_SOLVER_STREAMING = 1, RW_SOLVER_RESIDENT = 2 };
 rw_status rw_set_option(int32_t key, int64_t value);
 int64_t rw_get_option(int32_t key);

@@ -10,5 +10,5 @@ from .api import (  # noqa: F401
     solve_workspace_bytes, solve_labels_workspace_bytes, level_dims, set_solver, get_solver,
     solver, resident_available, hier_segment, hier_segment_labels, stream_passes,
     set_stream_passes, get_stream_passes, set_resident_wide, get_resident_wide,
-    set_device_loop, get_device_loop, device_loop,
+    set_device_loop, get_device_loop, device_loop, set_stream_zc, get_stream_zc, stream_zc,
 )

@@ -132,6 +132,26 @@ def stream_passes(n):
         set_stream_passes(old)
 
 
+def set_stream_zc(zc):
+    """rw_set_option(RW_OPT_STREAM_ZC): 0 (default, automatic) or the streaming solver's
+    z-chunk in planes (4..4096)."""
+    check(lib().rw_set_option(6, int(zc)), "rw_set_option")
+
+
+def get_stream_zc():
+    return int(lib().rw_get_option(6))
+
+
+@contextlib.contextmanager
+def stream_zc(zc):
+    old = get_stream_zc()
+    set_stream_zc(zc)
+    try:
+        yield
+    finally:
+        set_stream_zc(old)
+
+
 def resident_available(dims, nrhs=1):
     """rw_resident_available: can the brick-resident (on-chip) solver serve this shape?"""
     nx, ny, nz = dims

@@ -29,6 +29,7 @@ cudaError_t launch_finalize(const Plan&, const Bufs&, const Ctl&, float*, int*, 
 cudaError_t launch_labels_prep(const uint8_t*, long long, int, uint8_t*, float*, int, cudaStream_t);
 cudaError_t launch_argmax(const float*, long long, int, uint8_t*, int, cudaStream_t);
 int passA_rc(const Plan&);
+void passA_stages(Plan&);
 size_t weights_ex_workspace(int kind, int B, long long n);
 cudaError_t launch_seed_bits(const uint8_t*, long long, int, uint8_t*, int, cudaStream_t);
 cudaError_t launch_label_max(const float*, long long, int, float*, uint8_t*, int, cudaStream_t);
@@ -57,6 +58,7 @@ int g_solver = RW_SOLVER_AUTO;
 int g_rr = 0;
 int g_passes = 1;   // RW_OPT_STREAM_PASSES
 int g_res_wide = 0; // RW_OPT_RESIDENT_WIDE
+int g_zc = 0;       // RW_OPT_STREAM_ZC (0 = auto)
 int g_dev_loop = 1; // RW_OPT_DEVICE_LOOP
 
 rw_status fail(rw_status st, const char* fmt, ...) {
@@ -78,6 +80,21 @@ rw_status fail(rw_status st, const char* fmt, ...) {
   } while (0)
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// Plan.lastdec threshold (rw::kLastDecMinU; env RW_LASTDEC_MIN_U for A/B runs -- the two
+// schemes are bit-identical by construction)
+int lastdec_min_u() {
+  static int v = [] {
+    const char* e = getenv("RW_LASTDEC_MIN_U");
+    return e ? atoi(e) : rw::kLastDecMinU;
+  }();
+  return v;
+}
 
 int num_sms() {
   int dev = 0, n = 148;
@@ -107,11 +124,15 @@ rw::Plan make_plan(int B, rw_dims d, int R) {
   P.tiles_y = (d.ny + P.TY - 1) / P.TY;
   int zc = 64;
   while (zc > 8 && P.tiles_x * P.tiles_y * ((d.nz + zc - 1) / zc) < 4) zc /= 2;
+  if (g_zc > 0) zc = g_zc;
   P.ZC = zc;
   P.tiles_z = (d.nz + zc - 1) / zc;
   P.U = P.tiles_x * P.tiles_y * P.tiles_z;
   P.vm = rw::VM_STORED;
   P.one = 0;
+  P.lastdec = 0;
+  P.rc = env_int("RW_PASSA_RC", 0);   // A/B knob: right-hand sides per pass-A CTA
+  P.ns = 0;
   P.hxv = P.hx;
   P.TXhv = P.TXh;
   return P;
@@ -136,7 +157,7 @@ void set_vm(rw::Plan& P, int vm) {
 }
 
 struct Layout {
-  size_t W, dinv, r, p, q, PA, PB, PS, status, ctr, fixed, values, total;
+  size_t W, dinv, r, p, q, PA, PB, PS, status, ctr, SD, cnt, fixed, values, total;
 };
 
 size_t up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -155,6 +176,8 @@ Layout layout(const rw::Plan& P, bool weights_given, int label_K) {
   L.PS = o;     o += up(RB * P.U * sizeof(double4));
   L.status = o; o += up(RB * sizeof(int));
   L.ctr = o;    o += up(4 * sizeof(int));   // [0..1] active counts, [2] resident brick counter
+  L.SD = o;     o += up(2 * RB * sizeof(float4));   // last-CTA decisions (Plan.lastdec)
+  L.cnt = o;    o += up(RB * sizeof(int));
   L.fixed = o;  o += label_K ? up(BN) : 0;
   L.values = o; o += label_K ? up((size_t)(label_K - 1) * BN * sizeof(float)) : 0;
   L.total = o;
@@ -422,6 +445,8 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   // one HBM pass per iteration (measured, tools/passes_ab.py: cfg2 512 bricks 167 vs 193 ms,
   // cfg3 1.61 vs 1.87 s, cfg4 0.89 vs 0.99 s, identical iteration counts)
   P.one = (!res_ok && g_passes == 1 && g_rr == 0) ? 1 : 0;
+  P.lastdec = (P.one && P.U >= lastdec_min_u()) ? 1 : 0;
+  rw::passA_stages(P);
   rw::Bufs Bf{};
   float* Wd = W ? const_cast<float*>(W) : reinterpret_cast<float*>(ws + Lw.W);
   float* dinv = reinterpret_cast<float*>(ws + Lw.dinv);
@@ -452,11 +477,14 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
   Bf.status = reinterpret_cast<int*>(ws + Lw.status);
   Bf.iters = iters;
   Bf.ctr = reinterpret_cast<int*>(ws + Lw.ctr);
+  Bf.SD = reinterpret_cast<float4*>(ws + Lw.SD);
+  Bf.cnt = reinterpret_cast<int*>(ws + Lw.cnt);
   rw::Ctl C{tol, tol_mode, max_iter, nm.scale, nm.offset, rw::nbl2_of(beta), eps, 0, g_rr};
   rw::Maps M;
   rw_status st = make_maps(P, Bf, &M);
   if (st != RW_OK) return st;
   RW_CK(cudaMemsetAsync(Bf.status, 0, (size_t)P.R * P.B * sizeof(int), s));
+  if (P.lastdec) RW_CK(cudaMemsetAsync(Bf.cnt, 0, (size_t)P.R * P.B * sizeof(int), s));
   if (!fused) RW_TIMED(RW_K_SETUP, s, 1, rw::launch_setup(P, Bf, C, s));
   if (res_ok) {
     rw::ResArgs A{};
@@ -538,7 +566,8 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
     }
     return RW_OK;
   }
-  const int nA = (P.R + rw::passA_rc(P) - 1) / rw::passA_rc(P);
+  const int rcm = rw::passA_rc(P), rcl = P.R % rcm == 0 ? P.R : rcm;   // rhs per launch
+  const int nA = (P.R + rcl - 1) / rcl;
   const int nB = (P.R + 3) / 4;
   const bool one = P.one != 0;
   if (one && C.rr == 0 && g_dev_loop) {
@@ -633,6 +662,11 @@ rw_status rw_set_option(int32_t key, int64_t value) {
     g_res_wide = (int)value;
     return RW_OK;
   }
+  if (key == RW_OPT_STREAM_ZC) {
+    if (value != 0 && (value < 4 || value > 4096)) return fail(RW_EINVAL, "rw_set_option: z chunk must be 0 or 4..4096");
+    g_zc = (int)value;
+    return RW_OK;
+  }
   if (key == RW_OPT_STREAM_PASSES) {
     if (value != 1 && value != 2) return fail(RW_EINVAL, "rw_set_option: passes must be 1 or 2");
     g_passes = (int)value;
@@ -653,7 +687,8 @@ rw_status rw_set_option(int32_t key, int64_t value) {
 int64_t rw_get_option(int32_t key) {
   return key == RW_OPT_SOLVER ? g_solver : key == RW_OPT_COSCHED ? g_cosched_pm
          : key == RW_OPT_RESIDUAL_REPLACE ? g_rr : key == RW_OPT_STREAM_PASSES ? g_passes
-         : key == RW_OPT_RESIDENT_WIDE ? g_res_wide : key == RW_OPT_DEVICE_LOOP ? g_dev_loop : -1;
+         : key == RW_OPT_RESIDENT_WIDE ? g_res_wide : key == RW_OPT_DEVICE_LOOP ? g_dev_loop
+         : key == RW_OPT_STREAM_ZC ? g_zc : -1;
 }
 
 int32_t rw_resident_available(rw_dims d, int32_t nrhs) {

@@ -18,6 +18,13 @@ __device__ __forceinline__ double warp_sum_array(const double* a, int U, int str
   return warp_sum(s);
 }
 
+// As warp_sum_array, reading through L2 (partials written by other CTAs of the same launch).
+__device__ __forceinline__ double warp_sum_array_cg(const double* a, int U, int stride, int lane) {
+  double s = 0.0;
+  for (int u = lane; u < U; u += 32) s += __ldcg(a + (long long)u * stride);
+  return warp_sum(s);
+}
+
 // Block-wide fixed-order reduction of NV values per thread; result written by thread 0.
 // Callers separate consecutive calls with __syncthreads().
 template <int NV>
@@ -172,50 +179,45 @@ __device__ inline Scal passA_scalars(const Plan& P, const Bufs& Bf, const Ctl& C
   return s;
 }
 
-// One-pass mode (passA.cu): at the start of pass k the partials of pass k-1 give the TRUE
-// r_{k-1}.z_{k-1}, ||r_{k-1}||^2 and p.q, q.D r, q.D q of iteration k-1.  Decisions run on the
-// true residual of r_{k-1} (x_{k-1} was written by pass k-1, so it is the result), alpha_{k-1}
-// = r.z / p.q, beta_{k-1} from the one-step expansion of r_k.z_k.  iters = k-1 at a stop.
-__device__ inline Scal passA_scalars1(const Plan& P, const Bufs& Bf, const Ctl& C, int rb, int k,
-                                      int u, int lane) {
-  Scal s = {0, 0.f, 0.f};
-  const int st = Bf.status[rb];
-  if (st != ST_ACTIVE) return s;
+// Decision of pass k for (rhs, brick) rb from pass k-1's partials (the math of
+// passA_scalars1).  CG = true: the partials come from other CTAs of the running launch (read
+// through L2).  Out: status (ST_ACTIVE or the stop reason), iters at a stop, alpha / beta.
+template <bool CG>
+__device__ inline int passA_decide1(const Plan& P, const Bufs& Bf, const Ctl& C, int rb, int k,
+                                    int lane, Scal& s, int& it) {
+  auto wsum = [&](const double* a, int stride) {
+    return CG ? warp_sum_array_cg(a, P.U, stride, lane) : warp_sum_array(a, P.U, stride, lane);
+  };
   const long long RBU = (long long)P.R * P.B * P.U;
   const double* ps = reinterpret_cast<const double*>(Bf.PS) + 4LL * rb * P.U;
-  const double bb = warp_sum_array(ps + 0, P.U, 4, lane);
+  const double bb = wsum(ps + 0, 4);
   const double t2 = (double)C.tol * (double)C.tol;
   auto conv = [&](double rr) { return (C.tol_mode == 0) ? (rr <= t2 * bb) : (rr <= t2); };
-  int nst = ST_ACTIVE, it = 0;
+  int nst = ST_ACTIVE;
+  it = 0;
   double rz = 0.0, pq = 0.0, qdr = 0.0, qdq = 0.0;
   if (k == 0) {
     const double* pb = reinterpret_cast<const double*>(Bf.PB);     // setup: (r0.z0, r0.r0)
-    const double rr0 = warp_sum_array(pb + 2 * ((long long)rb * P.U) + 1, P.U, 2, lane);
-    const double nf = warp_sum_array(ps + 1, P.U, 4, lane);
-    const double nu = warp_sum_array(ps + 2, P.U, 4, lane);
+    const double rr0 = wsum(pb + 2 * ((long long)rb * P.U) + 1, 2);
+    const double nf = wsum(ps + 1, 4);
+    const double nu = wsum(ps + 2, 4);
     if (nf == 0.0 || nu == 0.0) nst = ST_TRIVIAL;
     else if (bb == 0.0) nst = ST_ZERO_B;
     else if (conv(rr0)) nst = ST_CONVERGED;
   } else {
     const double* pa = Bf.PA + 5 * (((k - 1) & 1) * RBU + (long long)rb * P.U);
-    rz = warp_sum_array(pa + 0, P.U, 5, lane);
-    const double rr = warp_sum_array(pa + 1, P.U, 5, lane);
-    pq = warp_sum_array(pa + 2, P.U, 5, lane);
-    qdr = warp_sum_array(pa + 3, P.U, 5, lane);
-    qdq = warp_sum_array(pa + 4, P.U, 5, lane);
+    rz = wsum(pa + 0, 5);
+    const double rr = wsum(pa + 1, 5);
+    pq = wsum(pa + 2, 5);
+    qdr = wsum(pa + 3, 5);
+    qdq = wsum(pa + 4, 5);
     it = k - 1;
     if (k > 1 && conv(rr)) nst = ST_CONVERGED;
     else if (it >= C.max_iter) nst = ST_MAXITER;
     else if (!(pq > 0.0) || !isfinite(pq) || !isfinite(rz) || !(rz > 0.0)) nst = ST_BREAKDOWN;
   }
-  if (nst != ST_ACTIVE) {
-    if (u == 0 && lane == 0) {
-      Bf.status[rb] = nst;
-      Bf.iters[rb] = it;
-    }
-    return s;
-  }
-  if (u == 0 && lane == 0) atomicAdd(Bf.ctr + (k & 1), 1);
+  s = {0, 0.f, 0.f};
+  if (nst != ST_ACTIVE) return nst;
   s.active = 1;
   if (k > 0) {
     s.alpha = (float)(rz / pq);
@@ -224,7 +226,56 @@ __device__ inline Scal passA_scalars1(const Plan& P, const Bufs& Bf, const Ctl& 
     if (!(rz1 > 0.0)) rz1 = 0.0;        // below the rounding level: restart the direction
     s.beta = (float)(rz1 / rz);
   }
+  return nst;
+}
+
+// One-pass mode (passA.cu): at the start of pass k the partials of pass k-1 give the TRUE
+// r_{k-1}.z_{k-1}, ||r_{k-1}||^2 and p.q, q.D r, q.D q of iteration k-1.  Decisions run on the
+// true residual of r_{k-1} (x_{k-1} was written by pass k-1, so it is the result), alpha_{k-1}
+// = r.z / p.q, beta_{k-1} from the one-step expansion of r_k.z_k.  iters = k-1 at a stop.
+// With P.lastdec the decision of pass k >= 1 was taken by the last CTA of pass k-1
+// (passA_last_decide) and is read from Bufs.SD; a stop was already written to status.
+__device__ inline Scal passA_scalars1(const Plan& P, const Bufs& Bf, const Ctl& C, int rb, int k,
+                                      int u, int lane) {
+  Scal s = {0, 0.f, 0.f};
+  const int st = Bf.status[rb];
+  if (st != ST_ACTIVE) return s;
+  if (P.lastdec && k > 0) {
+    const float4 d = Bf.SD[(long long)(k & 1) * P.R * P.B + rb];
+    s.active = 1;
+    s.alpha = d.x;
+    s.beta = d.y;
+  } else {
+    int it = 0;
+    const int nst = passA_decide1<false>(P, Bf, C, rb, k, lane, s, it);
+    if (nst != ST_ACTIVE) {
+      if (u == 0 && lane == 0) {
+        Bf.status[rb] = nst;
+        Bf.iters[rb] = it;
+      }
+      return s;
+    }
+  }
+  if (u == 0 && lane == 0) atomicAdd(Bf.ctr + (k & 1), 1);
   return s;
+}
+
+// P.lastdec, end of pass k, one warp of the CTA that finished (rhs, brick) rb last: the
+// decision of pass k+1 -- a stop goes to status / iters, else (alpha, beta) to SD[(k+1)&1].
+__device__ inline void passA_last_decide(const Plan& P, const Bufs& Bf, const Ctl& C, int rb,
+                                         int k, int lane) {
+  Scal s;
+  int it = 0;
+  const int nst = passA_decide1<true>(P, Bf, C, rb, k + 1, lane, s, it);
+  if (lane == 0) {
+    if (nst != ST_ACTIVE) {
+      Bf.status[rb] = nst;
+      Bf.iters[rb] = it;
+    } else {
+      Bf.SD[(long long)((k + 1) & 1) * P.R * P.B + rb] = make_float4(s.alpha, s.beta, 0.f, 0.f);
+    }
+    Bf.cnt[rb] = 0;
+  }
 }
 
 }  // namespace rw

@@ -392,11 +392,27 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       if (act[c]) block_sum<1>(v, Bf.PA + (k & 1) * RBU + (long long)((rbase + c) * P.B + b) * P.U + u);
     }
   }
+  if (ONE && P.lastdec) {
+    // the CTA that completes a (rhs, brick)'s U partials takes the decision of pass k+1 once
+    // (threadfence reduction: partial stores -> fence -> arrival count)
+    __shared__ int s_last[RC];
+    if (tid == 0) {
+      __threadfence();
+#pragma unroll
+      for (int c = 0; c < RC; ++c)
+        s_last[c] = act[c] ? (atomicAdd(Bf.cnt + (rbase + c) * P.B + b, 1) == P.U - 1) : 0;
+    }
+    __syncthreads();
+    if (warp < RC && s_last[warp]) {
+      __threadfence();
+      passA_last_decide(P, Bf, C, (rbase + warp) * P.B + b, k, lane);
+    }
+  }
 }
 
 // ------------------------------------------------------------------------- launcher
 template <int RC, int VM, bool ONE, int NS>
-static cudaError_t launch_one(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0,
+static cudaError_t launch_one(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0, int nz,
                               const Maps& M, cudaStream_t s) {
   static int attr = 48 * 1024;   // largest dynamic smem opted in so far for this instance
   const ALayout L = a_layout(P, RC, VM);
@@ -406,49 +422,67 @@ static cudaError_t launch_one(const Plan& P, const Bufs& Bf, const Ctl& C, int k
     if (e != cudaSuccess) return e;
     attr = L.total;
   }
-  k_passA<RC, VM, ONE, NS><<<dim3(P.U, P.B, 1), P.threads, L.total, s>>>(P, Bf, C, k, r0, M);
+  k_passA<RC, VM, ONE, NS><<<dim3(P.U, P.B, nz), P.threads, L.total, s>>>(P, Bf, C, k, r0, M);
   return cudaGetLastError();
 }
 
 template <int RC, int VM>
-static cudaError_t launch_rc(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0,
+static cudaError_t launch_rc(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0, int nz,
                              const Maps& M, cudaStream_t s) {
-  return P.one ? launch_one<RC, VM, true, kStages>(P, Bf, C, k, r0, M, s)
-               : launch_one<RC, VM, false, kStages>(P, Bf, C, k, r0, M, s);
+  if (P.one && a_stages(P) == kStages - 1)
+    return launch_one<RC, VM, true, kStages - 1>(P, Bf, C, k, r0, nz, M, s);
+  return P.one ? launch_one<RC, VM, true, kStages>(P, Bf, C, k, r0, nz, M, s)
+               : launch_one<RC, VM, false, kStages>(P, Bf, C, k, r0, nz, M, s);
 }
 
 template <int VM>
 static cudaError_t launch_vm(const Plan& P, const Bufs& Bf, const Ctl& C, int k, int r0, int rc,
-                             const Maps& M, cudaStream_t s) {
+                             int nz, const Maps& M, cudaStream_t s) {
   switch (rc) {
-    case 1: return launch_rc<1, VM>(P, Bf, C, k, r0, M, s);
-    case 2: return launch_rc<2, VM>(P, Bf, C, k, r0, M, s);
-    case 3: return launch_rc<3, VM>(P, Bf, C, k, r0, M, s);
-    default: return launch_rc<4, VM>(P, Bf, C, k, r0, M, s);
+    case 1: return launch_rc<1, VM>(P, Bf, C, k, r0, nz, M, s);
+    case 2: return launch_rc<2, VM>(P, Bf, C, k, r0, nz, M, s);
+    case 3: return launch_rc<3, VM>(P, Bf, C, k, r0, nz, M, s);
+    default: return launch_rc<4, VM>(P, Bf, C, k, r0, nz, M, s);
   }
 }
 
-// right-hand sides per CTA: up to 4 sharing one operator load, fewer if smem is short
+// right-hand sides per CTA: up to 4 sharing one operator load, as long as two CTAs still fit
+// one SM (measured on cfg4, 256^3 with 3 rhs: one launch of 3 single-rhs CTA layers 884 ms
+// vs 2 + 1 rhs per CTA at one CTA per SM 1060 ms, bit-identical); P.rc > 0: fixed by the
+// caller (RW_PASSA_RC)
 int passA_rc(const Plan& P) {
+  if (P.rc > 0) return P.rc < P.R ? P.rc : P.R;
   int rc = P.R < 4 ? P.R : 4;
-  while (rc > 1 && a_layout(P, rc, P.vm).total > 220 * 1024) --rc;
+  while (rc > 1 && a_layout(P, rc, P.vm).total > 112 * 1024) --rc;
   return rc;
+}
+
+// One-pass mode: a ring of kStages - 1 planes where kStages would leave one CTA per SM
+// (e.g. f32 intensities with x halos: 123 KB at 4 stages, 97 KB at 3; cfg4 256^3 f32 runs
+// at 12 % warp occupancy with 4 stages, ncu gpurun_out/c4)
+void passA_stages(Plan& P) {
+  P.ns = kStages;
+  if (!P.one) return;
+  if (a_layout(P, passA_rc(P), P.vm).total > 112 * 1024) P.ns = kStages - 1;
 }
 
 size_t passA_smem(const Plan& P, int rc) { return (size_t)a_layout(P, rc, P.vm).total; }
 
+// One launch per group of right-hand sides: R / rc CTA layers (grid z) when rc divides R,
+// else ceil(R / rc) launches (the last one narrower).
 cudaError_t launch_iteration_A(const Plan& P, const Bufs& Bf, const Ctl& C, int k,
                                const Maps& M, cudaStream_t s) {
   const int rcmax = passA_rc(P);
-  for (int r0 = 0; r0 < P.R; r0 += rcmax) {
+  const int layers = P.R % rcmax == 0 ? P.R / rcmax : 1;
+  for (int r0 = 0; r0 < P.R; r0 += rcmax * layers) {
     const int rc = P.R - r0 < rcmax ? P.R - r0 : rcmax;
     cudaError_t e;
     switch (P.vm) {
-      case VM_U8: e = launch_vm<VM_U8>(P, Bf, C, k, r0, rc, M, s); break;
-      case VM_U16: e = launch_vm<VM_U16>(P, Bf, C, k, r0, rc, M, s); break;
-      case VM_I16: e = launch_vm<VM_I16>(P, Bf, C, k, r0, rc, M, s); break;
-      case VM_F32: e = launch_vm<VM_F32>(P, Bf, C, k, r0, rc, M, s); break;
-      default: e = launch_vm<VM_STORED>(P, Bf, C, k, r0, rc, M, s); break;
+      case VM_U8: e = launch_vm<VM_U8>(P, Bf, C, k, r0, rc, layers, M, s); break;
+      case VM_U16: e = launch_vm<VM_U16>(P, Bf, C, k, r0, rc, layers, M, s); break;
+      case VM_I16: e = launch_vm<VM_I16>(P, Bf, C, k, r0, rc, layers, M, s); break;
+      case VM_F32: e = launch_vm<VM_F32>(P, Bf, C, k, r0, rc, layers, M, s); break;
+      default: e = launch_vm<VM_STORED>(P, Bf, C, k, r0, rc, layers, M, s); break;
     }
     if (e != cudaSuccess) return e;
   }

@@ -23,7 +23,8 @@ struct Maps {
 constexpr int kStages = 4;  // TMA ring depth (planes issued ~2 steps before use)
 // one-pass mode streams the q box instead of the x box (x is read straight from global
 // memory, it has no halo), so 4 stages still fit two CTAs per SM
-__host__ __device__ inline int a_stages(const Plan& P) { return kStages; }
+// (kStages - 1 when the one-pass layout would otherwise drop to one CTA per SM, passA_stages)
+__host__ __device__ inline int a_stages(const Plan& P) { return P.ns > 0 ? P.ns : kStages; }
 
 __host__ __device__ inline int rup128(int b) { return (b + 127) & ~127; }
 __host__ __device__ inline int vm_esize(int vm) {

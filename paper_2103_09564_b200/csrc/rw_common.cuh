@@ -33,7 +33,16 @@ struct Plan {
   int TXP;              // smem row pitch (floats) of p_new planes = TX + 8 (cols -1..TX)
   int vm;               // VM_* weight mode
   int one;              // 1: one-pass CG (pass A only, see passA.cu), 0: passes A + B
+  int rc;               // right-hand sides per pass-A CTA (0: automatic, passA_rc)
+  int ns;               // pass-A TMA ring depth (0: kStages; passA_stages)
+  int lastdec;          // one-pass mode, large bricks (U >= kLastDecMinU): the last CTA of a
+                        // (rhs, brick) to finish pass k sums the U partials once and stores the
+                        // decision of pass k+1 (Bufs.SD) instead of every CTA of pass k+1
+                        // re-summing them (same sums, same order: bit-identical)
 };
+
+// U from which the last-CTA decision is used (api.cu; env RW_LASTDEC_MIN_U overrides)
+constexpr int kLastDecMinU = 16;
 
 // Per-(rhs,brick) status (0 = active); values match include/rw.h RW_ST_*.
 enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_TRIVIAL = 3, ST_ZERO_B = 4,
@@ -61,6 +70,8 @@ struct Bufs {
                       //      [2] resident brick counter, [3] iteration index (device loop)
   const int* kdev;    // device-driven loop: pass A reads its iteration index here (ctr + 3);
                       // null: the index is the kernel argument (host-driven loop)
+  float4* SD;         // [2][R*B] (Plan.lastdec) decision of pass k in slot k&1: (alpha, beta)
+  int* cnt;           // [R*B]    (Plan.lastdec) CTAs of pass k done with their partials
 };
 
 struct Ctl {

@@ -22,7 +22,7 @@ $CMD > $O/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --c
 if [ "${SKIP_FULL:-0}" = "0" ]; then
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_resident -s 3 -c 1 -o $O/resident $CMD > $O/ncu2.log 2>&1; echo "ncu2 rc=$?"
 # the streaming solver's dominant kernel (one-pass pass A) at a steady-state iteration
-SCMD="python bench.py --solver streaming --steps 1 --warmup 3 --no-cpu-baseline --no-rows"
+SCMD="python bench.py --solver streaming --host-loop --steps 1 --warmup 3 --no-cpu-baseline --no-rows --no-configs"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_passA -s 60 -c 1 -o $O/passA $SCMD > $O/ncu3.log 2>&1; echo "ncu3 rc=$?"
 fi
 ls -la $O

@@ -9,6 +9,7 @@ import workloads as wl
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 p = wl.cfg3()
 d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+rwb.set_device_loop(False)
 with rwb.solver("streaming"), rwb.stream_passes(n):
     o = rwb.solve_bricks(d(p.fixed), d(p.values), vol=d(p.vol), beta=p.beta, eps=p.eps, tol=p.tol,
                          max_iter=24, norm=(p.scale, p.offset))
