@@ -316,8 +316,10 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
  *                 shape, any nrhs, see RW_OPT_STREAM_PASSES);
  *   resident   -- one thread-block cluster per brick keeps the whole CG state on chip
  *                 (shared + tensor memory, registers) for all iterations (SURVEY 8(f)
- *                 f2/f4); bricks of 64^3, 40^3 (s_e of P:119) or 32^3, nrhs == 1, device
- *                 permitting.
+ *                 f2/f4); bricks of 64^3, 40^3 (s_e of P:119) or 32^3, device
+ *                 permitting.  nrhs > 1: every (rhs, brick) pair is its own resident
+ *                 solve on the brick's operator (pairs drawn rhs-major from one counter),
+ *                 bit-identical to nrhs separate single-rhs calls.
  * RW_OPT_SOLVER: RW_SOLVER_AUTO (default: resident when available, else streaming),
  * RW_SOLVER_STREAMING, RW_SOLVER_RESIDENT (a solve it cannot serve returns
  * RW_EUNSUPPORTED).  Process-wide setting; not thread-safe against concurrent solves.

@@ -516,7 +516,8 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
     // clusters leave free (they need no shared memory the clusters hold).  The fork is
     // recorded before the resident launch, so the streaming bricks start with it.
     const int Bs = cosched_bricks(P.B, d, nrhs, W != nullptr, ws_bytes, Lw.total);
-    A.nsolve = P.B - Bs;
+    A.nb = P.B - Bs;
+    A.nsolve = P.R * A.nb;   // (rhs, brick) pairs: each rhs is its own resident solve
     cudaStream_t s2 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     if (Bs > 0) {

@@ -304,8 +304,8 @@ template <> struct Quad4<uint16_t> { using V = ushort4; };
 template <> struct Quad4<float> { using V = float4; };
 
 template <typename T, int N, int NZ>
-__device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long base, int z, int y,
-                                                 int x, double (&acc)[5]) {
+__device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long base, long long voff,
+                                                 int z, int y, int x, double (&acc)[5]) {
   const T* vol = reinterpret_cast<const T*>(A.vol);
   const float sc = A.C.scale, of = A.C.offset, nb = A.C.nbl2, eps = A.C.eps;
   const long long PL = (long long)N * N;
@@ -316,8 +316,8 @@ __device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long bas
   auto quad = [&](long long i, NQ& q) {
     const typename Quad4<T>::V v = *reinterpret_cast<const typename Quad4<T>::V*>(vol + i);
     const uchar4 f = *reinterpret_cast<const uchar4*>(A.fixed + i);
-    const float4 val = *reinterpret_cast<const float4*>(A.values + i);
-    const float4 x0 = A.x0 ? *reinterpret_cast<const float4*>(A.x0 + i) : make_float4(0.5f, 0.5f, 0.5f, 0.5f);
+    const float4 val = *reinterpret_cast<const float4*>(A.values + voff + i);
+    const float4 x0 = A.x0 ? *reinterpret_cast<const float4*>(A.x0 + voff + i) : make_float4(0.5f, 0.5f, 0.5f, 0.5f);
     const float gv[4] = {(float)v.x, (float)v.y, (float)v.z, (float)v.w};
     const bool fv[4] = {f.x != 0, f.y != 0, f.z != 0, f.w != 0};
     const float vv[4] = {val.x, val.y, val.z, val.w}, xx[4] = {x0.x, x0.y, x0.z, x0.w};
@@ -331,7 +331,7 @@ __device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long bas
   auto one = [&](long long i, float& g, float& xv, bool& f) {
     g = normv((float)vol[i], sc, of);
     f = A.fixed[i] != 0;
-    xv = f ? A.values[i] : (A.x0 ? A.x0[i] : 0.5f);
+    xv = f ? A.values[voff + i] : (A.x0 ? A.x0[voff + i] : 0.5f);
   };
   NQ c0, yp{}, ym{}, zp{}, zm{};
   quad(i0, c0);
@@ -533,8 +533,13 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     }
     cl_arrive();
     cl_wait();
-    const int b = s_brick;
-    if (b >= A.nsolve) break;
+    const int pr = s_brick;
+    if (pr >= A.nsolve) break;
+    // (rhs, brick) pair: the operator is the brick's; values / x0 / x / r0 / partials /
+    // outputs are the pair's (offset rb n)
+    const int b = pr % A.nb;
+    const long long rb = (long long)(pr / A.nb) * A.B + b;
+    const long long xoff = (rb - b) * n;   // rhs offset of the pair's arrays
 
     // ---- load the slab: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
     uint32_t fixm = 0;   // bit 4*it+e: voxel is fixed (dinv == 0)
@@ -548,7 +553,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         const int zl = it / NR, rr = it % NR, y = NR * j + rr;
         QuadOut o{};
         if (act) {
-          o = assemble_quad<T, N, G::NZ>(A, (long long)b * n, z0 + zl, y, 4 * qx, iacc);
+          o = assemble_quad<T, N, G::NZ>(A, (long long)b * n, xoff, z0 + zl, y, 4 * qx, iacc);
           fixm |= o.fm << (4 * it);
           const int so = y * N + 4 * qx;
           st4(WY + zl * PL + so, o.wy);
@@ -569,13 +574,13 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         const float4 dv = ld4(A.dinv + g);
         tm_st4(cD + 4u * it, dv);
         tm_st4(cX + 4u * it, ld4(A.W + g));
-        tm_st4(cV + 4u * it, ld4(A.x + g));
+        tm_st4(cV + 4u * it, ld4(A.x + xoff + g));
         tm_st4(cZ + 4u * it, ld4(A.W + 2 * BN + g));
         fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
         fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
         fixm |= (dv.z == 0.f ? 4u : 0u) << (4 * it);
         fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
-        r[it] = ld4(A.r0 + g);
+        r[it] = ld4(A.r0 + xoff + g);
         const int so = y * N + 4 * qx;
         st4(WY + zl * PL + so, ld4(A.W + BN + g));
         st4(P + (zl + 1) * PL + so, f4(0.f));
@@ -593,13 +598,13 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       if (act) {
         dv = ld4(A.dinv + g);
         wx = ld4(A.W + g);
-        xv = ld4(A.x + g);
+        xv = ld4(A.x + xoff + g);
         wz = ld4(A.W + 2 * BN + g);
         fixm |= (dv.x == 0.f ? 1u : 0u) << (4 * it);
         fixm |= (dv.y == 0.f ? 2u : 0u) << (4 * it);
         fixm |= (dv.z == 0.f ? 4u : 0u) << (4 * it);
         fixm |= (dv.w == 0.f ? 8u : 0u) << (4 * it);
-        r[it] = ld4(A.r0 + g);
+        r[it] = ld4(A.r0 + xoff + g);
         const int so = y * N + 4 * qx;
         st4(WY + zl * PL + so, ld4(A.W + BN + g));
         st4(P + (zl + 1) * PL + so, f4(0.f));
@@ -618,8 +623,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     double rz = 0.0, rrn = 0.0, bb = 0.0, nf = 0.0, nu = 0.0;
     if constexpr (VM == VM_STORED) {
       for (int u = 0; u < A.U; ++u) {
-        const double2 pb = A.PB[(long long)b * A.U + u];
-        const double4 ps = A.PS[(long long)b * A.U + u];
+        const double2 pb = A.PB[rb * A.U + u];
+        const double4 ps = A.PS[rb * A.U + u];
         rz += pb.x; rrn += pb.y; bb += ps.x; nf += ps.y; nu += ps.z;
       }
       __syncthreads();
@@ -840,21 +845,21 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       }
       const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
       if (!act) continue;
-      st4(A.x + g, make_float4(o[0], o[1], o[2], o[3]));
-      if (A.labels)
+      st4(A.x + xoff + g, make_float4(o[0], o[1], o[2], o[3]));
+      if (A.labels && xoff == 0)   // labels = prob[0] > 0.5 (rw.h)
         *reinterpret_cast<uchar4*>(A.labels + g) =
             make_uchar4(o[0] > 0.5f, o[1] > 0.5f, o[2] > 0.5f, o[3] > 0.5f);
     }
     if (rank == 0 && t == 0) {
-      A.status[b] = st;
-      A.iters[b] = (st == ST_TRIVIAL || st == ST_ZERO_B) ? 0 : k;
+      A.status[rb] = st;
+      A.iters[rb] = (st == ST_TRIVIAL || st == ST_ZERO_B) ? 0 : k;
       if (A.resid) {
         double res = 0.0;
         if (st == ST_CONVERGED || st == ST_MAXITER || st == ST_BREAKDOWN) {
           res = sqrt(rrn);
           if (A.C.tol_mode == 0) res = bb > 0.0 ? res / sqrt(bb) : 0.0;
         }
-        A.resid[b] = (float)res;
+        A.resid[rb] = (float)res;
       }
     }
   }
@@ -947,7 +952,7 @@ static bool supported_vm(int nx, int wide) {
 
 // the exact variant launch_resident will pick for (shape, vdt, wide) must be launchable
 bool resident_supported(int nx, int ny, int nz, int R, int vdt, int wide) {
-  if (R != 1) return false;
+  if (R < 1) return false;
   if (!((nx == 64 || nx == 40 || nx == 32) && ny == nx && nz == nx)) return false;
   if (vdt == VM_U16) return supported_vm<VM_U16>(nx, wide);
   if (vdt == VM_F32) return supported_vm<VM_F32>(nx, wide);

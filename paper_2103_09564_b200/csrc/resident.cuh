@@ -7,25 +7,27 @@ namespace rw {
 struct ResArgs {
   const float* W;      // [3][B][n]
   const float* dinv;   // [B][n]   0 on fixed voxels
-  const float* r0;     // [B][n]   initial residual (k_setup)
-  float* x;            // [B][n]   in: x0 with fixed values (k_setup); out: prob
-  const double2* PB;   // [2][B][U] setup partials (r.z, r.r) in slot 0
-  const double4* PS;   // [B][U]    (b.b, n_fixed, n_unknown, 0)
+  const float* r0;     // [R][B][n] initial residual (k_setup)
+  float* x;            // [R][B][n] in: x0 with fixed values (k_setup); out: prob
+  const double2* PB;   // [2][R][B][U] setup partials (r.z, r.r) in slot 0
+  const double4* PS;   // [R][B][U]    (b.b, n_fixed, n_unknown, 0)
   int B, U;            // B: batch of the arrays (plane stride of W); U: setup partials per brick
-  int nsolve;          // bricks 0 .. nsolve-1 are solved (<= B; the rest run elsewhere)
-  int* next;           // brick counter (zeroed before the launch)
-  int* iters;          // [B]
-  int* status;         // [B]
-  float* resid;        // [B] or null
-  uint8_t* labels;     // [B][n] or null
+  int nb;              // bricks 0 .. nb-1 of every rhs are solved here (<= B; the rest run
+                       // elsewhere)
+  int nsolve;          // (rhs, brick) pairs solved = R * nb; pair i = (i / nb, i % nb)
+  int* next;           // pair counter (zeroed before the launch)
+  int* iters;          // [R][B]
+  int* status;         // [R][B]
+  float* resid;        // [R][B] or null
+  uint8_t* labels;     // [B][n] or null (R == 1 only)
   Ctl C;
   // fused assembly (vol != null): weights, dinv, x0 and r0 are formed in the brick load
   // phase from the intensities, the Dirichlet mask / values and x0 (no k_weights / k_setup)
   const void* vol;       // [B][n] of dtype vdt, or null (then W / dinv / r0 / x / PB / PS)
   int vdt;               // VM_U8 .. VM_F32
   const uint8_t* fixed;  // [B][n]
-  const float* values;   // [B][n]
-  const float* x0;       // [B][n] or null (0.5)
+  const float* values;   // [R][B][n]
+  const float* x0;       // [R][B][n] or null (0.5)
   long long* dbg;      // debug builds only (-DRW_RES_TIMING): per-(rank, phase) clock64 sums
                        // in a caller-provided buffer; null in the library
 };

@@ -30,7 +30,7 @@ def test_resident_available_shapes():
     assert rwb.resident_available((64, 64, 64))
     assert rwb.resident_available((32, 32, 32))
     assert rwb.resident_available((40, 40, 40))       # the paper's s_e = 1.25 * 32
-    assert not rwb.resident_available((64, 64, 64), nrhs=2)
+    assert rwb.resident_available((64, 64, 64), nrhs=3)   # (rhs, brick) pairs
     assert not rwb.resident_available((48, 48, 48))
     p = wl.random_brick(48, 8, 8, seed=1, nseed=10)
     with rwb.solver("resident"), pytest.raises(RWError, match="RW_EUNSUPPORTED"):
@@ -160,3 +160,53 @@ def test_cosched_matches_resident_only():
     assert np.abs(a["iters"].astype(int) - b["iters"].astype(int)).max() <= 3
     nres = len(ids) - len(ids) * 250 // 1000
     assert np.array_equal(a["prob"][:, :nres], b["prob"][:, :nres])     # resident part bitwise
+
+
+@pytest.mark.parametrize("n", [32, 40, 64])
+def test_resident_multilabel_parity(n):
+    """rw_solve_labels on the resident solver (K-1 = 3 rhs as (rhs, brick) pairs on one
+    operator) against K explicit fp64 oracle solves (reading R11)."""
+    lp = wl.cfg4(n=n, seeds_per_label=max(20, n // 2))
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    outs = {}
+    for name in ("resident", "streaming"):
+        with rwb.solver(name):
+            o = rwb.solve_labels(dv(lp.labels), lp.K, vol=dv(lp.vol), beta=lp.beta, eps=lp.eps,
+                                 tol=lp.tol, max_iter=lp.max_iter)
+        torch.cuda.synchronize()
+        outs[name] = {k: v.cpu().numpy() for k, v in o.items() if v is not None}
+    prob, lab = outs["resident"]["prob"], outs["resident"]["labels"]
+    ref = ro.solve_labels(lp, tol=1e-10)
+    assert_prob_parity(prob, ref["prob"][: lp.K - 1])
+    derived = np.clip(1.0 - prob.astype(np.float64).sum(axis=0), 0, 1)
+    assert np.abs(derived - ref["prob"][lp.K - 1]).max() <= 3e-4
+    P = np.sort(ref["prob"], axis=0)
+    sure = (P[-1] - P[-2]) > 1e-3
+    assert np.array_equal(lab[sure], ref["labels"][sure])
+    # the two solvers agree to the solver tolerance, with the same iteration counts (+-3)
+    assert np.abs(outs["streaming"]["prob"] - prob).max() <= 2e-5
+    it_r = outs["resident"]["iters"].astype(int)
+    it_s = outs["streaming"]["iters"].astype(int)
+    assert np.abs(it_r - it_s).max() <= 3, (it_r, it_s)
+
+
+def test_resident_multi_rhs_bitwise_and_linearity():
+    """nrhs = 2 on 64^3 bricks: each (rhs, brick) pair equals its own single-rhs resident solve
+    bit for bit; values' = 1 - values gives x' = 1 - x (linearity of L_UU x_U = -B^T x_S)
+    to the solver tolerance."""
+    p = wl.cfg2(bricks=[3, 77, 200])
+    two = wl.Problem("two", p.vol, p.dtype, p.fixed,
+                     np.concatenate([p.values, (1.0 - p.values).astype(np.float32)]),
+                     p.beta, p.eps, p.tol, p.max_iter, p.tol_mode, p.scale, p.offset)
+    o = resident(two)
+    assert o["prob"].shape[0] == 2
+    for r in range(2):
+        one = wl.Problem("one", p.vol, p.dtype, p.fixed, two.values[r:r + 1].copy(), p.beta,
+                         p.eps, p.tol, p.max_iter, p.tol_mode, p.scale, p.offset)
+        s = resident(one)
+        assert np.array_equal(s["prob"][0], o["prob"][r])
+        assert np.array_equal(s["iters"][0], o["iters"][r])
+        assert np.array_equal(s["resid"][0], o["resid"][r])
+        if r == 0:
+            assert np.array_equal(s["labels"], o["labels"])   # labels = prob[0] > 0.5
+    assert np.abs(o["prob"][0] + o["prob"][1] - 1.0).max() <= 2e-5
