@@ -31,6 +31,12 @@ resolution, written in the paper's order:
             prunable bricks are not solved; every level's field starts as the trilinear
             upsample of the parent field and solved bricks overwrite their s^3, so sampling
             a pruned region falls back to the nearest solved ancestor (reading R26).
+  dims      volumes need not be cubic nor s 2^k ("bricks at the border of the
+            volume may be smaller than s^3 voxels"; reading R31): level l+1 has dims
+            ceil(d_l / 2) per axis (the pyramid's); the root is the first level whose
+            dims are all <= s; a level has ceil(d_l / s) bricks per axis, the last one per
+            axis smaller; brick B's children are the bricks 2B + (0|1) that exist; a window
+            has side min(s_e, d_l) per axis (a level narrower than s_e is taken whole).
 Solves use rw_oracle.solve_brick (fp64 Jacobi-PCG); the output is the level-0 field.
 """
 from __future__ import annotations
@@ -50,14 +56,27 @@ def seed_bits(seeds):
 
 
 def seed_bit_pyramid(seeds, levels):
-    """Level l bits = OR of the 2^3 children bits of level l-1 (reading R22); level 0 first."""
+    """Level l bits = OR of the bits of the (up to 2^3) present children at level l-1
+    (reading R22); dims ceil(d/2) per axis (R31); level 0 first."""
     out = [seed_bits(seeds)]
     for _ in range(levels - 1):
         b = out[-1]
         nz, ny, nx = b.shape
-        c = b.reshape(nz // 2, 2, ny // 2, 2, nx // 2, 2)
+        oz, oy, ox = (nz + 1) // 2, (ny + 1) // 2, (nx + 1) // 2
+        pad = np.zeros((2 * oz, 2 * oy, 2 * ox), np.uint8)     # absent children: no label
+        pad[:nz, :ny, :nx] = b
+        c = pad.reshape(oz, 2, oy, 2, ox, 2)
         out.append(np.bitwise_or.reduce(np.bitwise_or.reduce(np.bitwise_or.reduce(c, 5), 3), 1))
     return out
+
+
+def level_dims(shape, s):
+    """Per-level dims (level 0 first) down to the root, the first level with every dim <= s
+    (reading R31)."""
+    dims = [tuple(int(a) for a in shape)]
+    while max(dims[-1]) > s:
+        dims.append(tuple((a + 1) // 2 for a in dims[-1]))
+    return dims
 
 
 def seeds_from_bits(bits):
@@ -99,9 +118,11 @@ def upsample(P, shape):
 
 
 def window_origin(brick, s, se, D):
-    """Reading R23: low margin ceil((se - s)/2), shifted inward to fit [0, D)."""
+    """Reading R23: low margin ceil((se - s)/2), shifted inward to fit [0, D); a level
+    narrower than se is taken whole (R31)."""
+    side = min(se, D)
     o = brick * s - int(math.ceil((se - s) / 2))
-    return int(min(max(o, 0), D - se))
+    return int(min(max(o, 0), D - side))
 
 
 def window_system(P_par, fx_l, val_l, brick, s, se, Dl):
@@ -114,21 +135,23 @@ def window_system(P_par, fx_l, val_l, brick, s, se, Dl):
     not a user seed takes the parent field sampled at its centre (reading R25); faces on
     the volume boundary stay Neumann (reading c4).  samp = the parent field sampled at every
     window voxel (the initial guess)."""
-    w0 = [window_origin(c, s, se, Dl) for c in brick]
-    sl = tuple(slice(a, a + se) for a in w0)
-    zs, ys, xs = (np.arange(a, a + se) for a in w0)
+    Dl = (Dl,) * 3 if np.isscalar(Dl) else tuple(Dl)
+    w0 = [window_origin(c, s, se, d) for c, d in zip(brick, Dl)]
+    side = [min(se, d) for d in Dl]
+    sl = tuple(slice(a, a + w) for a, w in zip(w0, side))
+    zs, ys, xs = (np.arange(a, a + w) for a, w in zip(w0, side))
     samp = sample_parent(P_par, zs, ys, xs)
     fixed = fx_l[sl].copy()
     values = np.where(fixed, val_l[sl], 0.0)
-    shell = np.zeros((se, se, se), bool)
+    shell = np.zeros(tuple(side), bool)
     for ax in range(3):
         lo = [slice(None)] * 3
         hi = [slice(None)] * 3
         lo[ax] = 0
-        hi[ax] = se - 1
+        hi[ax] = side[ax] - 1
         if w0[ax] > 0:
             shell[tuple(lo)] = True
-        if w0[ax] + se < Dl:
+        if w0[ax] + side[ax] < Dl[ax]:
             shell[tuple(hi)] = True
     border = shell & ~fixed
     values = np.where(border, samp, values)
@@ -138,7 +161,8 @@ def window_system(P_par, fx_l, val_l, brick, s, se, Dl):
 def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, eps=1e-6,
                  tol=1e-10, max_iter=100000, scale=1.0 / 65535, offset=0.0, prune=True,
                  prev=None, t_inc=0.01):
-    """Oracle of rw_hier_segment.  vol/seeds [D, D, D] (z, y, x), D = s 2^k.
+    """Oracle of rw_hier_segment / rw_hier_segment_ooc.  vol/seeds [nz, ny, nx] (z, y, x), any
+    dims (reading R31); the in-HBM driver takes cubic D = s 2^k.
 
     prev: the dict a previous call returned (same volume and geometry) -> incremental
     labelling H_it (reading R27): every solved brick whose previous node was
@@ -151,10 +175,8 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, ep
     first), computed [level] = set of bricks holding a computed node, bits [level]).
     """
     vol = np.asarray(vol)
-    D = vol.shape[0]
-    assert vol.shape == (D, D, D) and D % s == 0
-    k = int(round(math.log2(D // s)))
-    assert s * 2 ** k == D, "volume side must be s * 2^k"
+    dims = level_dims(vol.shape, s)          # reading R31 (P:109-111); cubic s 2^k: D / 2^l
+    k = len(dims) - 1
     levels = k + 1
     se = int(math.floor(e * s))
     inc = prev is not None
@@ -165,17 +187,17 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, ep
     fields = [None] * levels
     computed = [set() for _ in range(levels)]
 
-    def region(b):
-        return tuple(slice(c * s, (c + 1) * s) for c in b)
+    def region(b, l):
+        return tuple(slice(c * s, min((c + 1) * s, d)) for c, d in zip(b, dims[l]))
 
     def decide(l, b, xb, old):
         """(state, values kept): reuse (R27) before the pruning rule."""
         if inc and b in prev["computed"][l]:
-            cb, ob = bits[l][region(b)], prev["bits"][l][region(b)]
+            cb, ob = bits[l][region(b, l)], prev["bits"][l][region(b, l)]
             dconf = np.any((cb == 3) & (cb != ob))
             if not dconf and np.max(np.abs(xb - old)) < t_inc:
                 return "reused", old
-        return _prune_state(b, xb, bits[l], s, t_hom, t_bin, prune), xb
+        return _prune_state(b, xb, bits[l][region(b, l)], t_hom, t_bin, prune), xb
 
     # ---- root (Eq. 1)
     g = ro.normalise(vols[k], scale, offset)
@@ -193,25 +215,27 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, ep
 
     # ---- levels k-1 .. 0 (Eq. 3 with H_p and H_it)
     for l in range(k - 1, -1, -1):
-        Dl = D >> l
-        nb = Dl // s
+        Dl = dims[l]
+        nb = tuple((d + s - 1) // s for d in Dl)
+
+        def kids(b):
+            return {(2 * b[0] + cz, 2 * b[1] + cy, 2 * b[2] + cx)
+                    for cz in range(2) for cy in range(2) for cx in range(2)
+                    if 2 * b[0] + cz < nb[0] and 2 * b[1] + cy < nb[1] and 2 * b[2] + cx < nb[2]}
         active, keep = set(), set()
         for b, stt in state.items():
-            kids = {(2 * b[0] + cz, 2 * b[1] + cy, 2 * b[2] + cx)
-                    for cz in range(2) for cy in range(2) for cx in range(2)}
             if stt in (None, "cfl"):
-                active |= kids
+                active |= kids(b)
             elif stt == "reused":
-                keep |= kids
+                keep |= kids(b)
         for b in reused_desc:
-            keep |= {(2 * b[0] + cz, 2 * b[1] + cy, 2 * b[2] + cx)
-                     for cz in range(2) for cy in range(2) for cx in range(2)}
+            keep |= kids(b)
         P_par = fields[l + 1]
-        up = upsample(P_par, (Dl, Dl, Dl))
+        up = upsample(P_par, Dl)
         F = prev["fields"][l].copy() if inc else up.copy()
-        for b in ((bz, by, bx) for bz in range(nb) for by in range(nb) for bx in range(nb)):
+        for b in ((bz, by, bx) for bz in range(nb[0]) for by in range(nb[1]) for bx in range(nb[2])):
             if b not in active and b not in keep:
-                F[region(b)] = up[region(b)]           # pruned region: nearest solved ancestor
+                F[region(b, l)] = up[region(b, l)]     # pruned region: nearest solved ancestor
         computed[l] = {b for b in keep if inc and b in prev["computed"][l]}
         gl = ro.normalise(vols[l], scale, offset)
         fx_l, val_l = seeds_from_bits(bits[l])
@@ -219,16 +243,16 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, ep
         new_state = {}
         for (bz, by, bx) in sorted(active):
             w0, fixed, values, samp = window_system(P_par, fx_l, val_l, (bz, by, bx), s, se, Dl)
-            sl = tuple(slice(a, a + se) for a in w0)
+            sl = tuple(slice(a, a + w) for a, w in zip(w0, fixed.shape))
             x0 = prev["fields"][l][sl] if inc else samp
             o = ro.solve_brick(gl[sl], fixed, values, beta, eps, tol, max_iter, x0=x0)
             xw = np.where(fixed, values, np.clip(o["x"], 0.0, 1.0))
-            # contract: the brick's own s^3
-            bo = [bz * s - w0[0], by * s - w0[1], bx * s - w0[2]]
-            xb = xw[bo[0]:bo[0] + s, bo[1]:bo[1] + s, bo[2]:bo[2] + s]
-            old = prev["fields"][l][region((bz, by, bx))] if inc else None
+            # contract: the brick's own s^3 (smaller at the volume border)
+            rg = region((bz, by, bx), l)
+            xb = xw[tuple(slice(r.start - a, r.stop - a) for r, a in zip(rg, w0))]
+            old = prev["fields"][l][rg] if inc else None
             stt, kept = decide(l, (bz, by, bx), xb, old)
-            F[region((bz, by, bx))] = kept
+            F[rg] = kept
             computed[l].add((bz, by, bx))
             stats[l]["solved"] += 1
             stats[l]["iters"] += o["iters"]
@@ -240,11 +264,9 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, beta=100.0, ep
     return dict(prob=fields[0], stats=stats, fields=fields, computed=computed, bits=bits)
 
 
-def _prune_state(b, xb, bits_l, s, t_hom, t_bin, prune):
+def _prune_state(b, xb, cb, t_hom, t_bin, prune):
     """None (keep refining: children are solved) or 'hom' / 'dt'; a seed
-    conflict inside the brick at its level vetoes pruning ('cfl')."""
-    bz, by, bx = b
-    cb = bits_l[bz * s:(bz + 1) * s, by * s:(by + 1) * s, bx * s:(bx + 1) * s]
+    conflict inside the brick (bits cb of its region) vetoes pruning ('cfl')."""
     if not prune or np.any(cb == 3):
         return "cfl" if np.any(cb == 3) else None
     mn, mx = float(xb.min()), float(xb.max())
