@@ -275,11 +275,46 @@ typedef struct {
   int32_t levels;
   int64_t active[16], solved[16], pruned_hom[16], pruned_dt[16], conflict[16], reused[16],
       iters[16];
+  int64_t pool_used;    /* rw_hier_segment_ooc: brick-pool slots used (0 otherwise)        */
 } rw_hier_stats;
 size_t rw_hier_workspace_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg);
 rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d,
                           const uint8_t* seeds, rw_hier_config cfg, void* workspace,
                           size_t ws_bytes, float* prob, rw_hier_stats* stats, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * rw_hier_segment_ooc -- the hierarchical random walker out of core (P:105
+ *   "applicable to arbitrarily large out-of-core datasets ... all computations are local to a
+ *   single brick or its direct neighborhood"; P:109-111 volumes of any size; P:151 nearest
+ *   computed ancestor; P:261 constant memory).  Same method, seeds and pruning as
+ *   rw_hier_segment (H and H_p; readings R22-R26) on volumes of ANY dims (reading R31: level
+ *   dims ceil(d/2), root = first level with every dim <= s, smaller border bricks, windows of
+ *   side min(s_e, d_l) per axis).  On cubic s 2^k volumes the output equals rw_hier_segment's
+ *   bit for bit.
+ *   Memory: the volume, the labels and the output stay in HOST memory.  The level-0 data is
+ *   streamed through the caller's queue (z-slabs once for the pyramid, then one slot per batch
+ *   of leaf windows); the device holds pyramid levels >= 1 of the intensities and seed bits
+ *   (1/7 of the volume), per-level page tables, a pool of pool_bricks s^3 fp32 bricks (solved
+ *   bricks and the unsolved ones a window samples, materialised as the upsample of their
+ *   parent level), one batch of windows and one output slab.  The dense field pyramid of
+ *   rw_hier_segment is never formed.
+ *   vol_h      host [nz][ny][nx] of dtype;  seeds_h  host u8 [nz][ny][nx] (0 / 1 fg / 2 bg).
+ *   cfg        as rw_hier_segment; incremental must be 0 (H_it needs rw_hier_segment).
+ *   pool_bricks  brick-pool capacity (RW_ENOMEM if the run needs more; stats.pool_used).
+ *   q          rw_queue with slot_bytes >= rw_hier_ooc_queue_bytes(d, dtype, cfg), depth >= 2.
+ *   prob_h / labels_h   out host fp32 / u8 [nz][ny][nx], either may be NULL (labels: p > 0.5).
+ *   workspace  device, >= rw_hier_ooc_workspace_bytes(d, dtype, cfg, pool_bricks), 256-B aligned.
+ *   Blocks the host (brick lists are built on the host between levels); work on `stream`.
+ *   Errors: RW_EINVAL for bad arguments (s % 4, floor(e s) % 4, incremental, small queue),
+ *   RW_ENOMEM for a small workspace or a full pool.
+ * ---------------------------------------------------------------------------------- */
+size_t rw_hier_ooc_workspace_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg,
+                                   int64_t pool_bricks);
+size_t rw_hier_ooc_queue_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg);
+rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_dims d,
+                              const uint8_t* seeds_h, rw_hier_config cfg, int64_t pool_bricks,
+                              struct rw_queue* q, void* workspace, size_t ws_bytes, float* prob_h,
+                              uint8_t* labels_h, rw_hier_stats* stats, void* stream);
 
 /* ------------------------------------------------------------------------------------
  * rw_hier_segment_labels -- multi-class hierarchical segmentation (P:107

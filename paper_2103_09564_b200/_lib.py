@@ -37,7 +37,8 @@ class rw_hier_config(C.Structure):
 class rw_hier_stats(C.Structure):
     _fields_ = [("levels", C.c_int32)] + [(f, C.c_int64 * 16) for f in
                                           ("active", "solved", "pruned_hom", "pruned_dt",
-                                           "conflict", "reused", "iters")]
+                                           "conflict", "reused", "iters")] + [
+        ("pool_used", C.c_int64)]
 
 
 P, I32, F32, SZ = C.c_void_p, C.c_int32, C.c_float, C.c_size_t
@@ -73,6 +74,10 @@ SIGNATURES = {
     "rw_hier_labels_workspace_bytes": (SZ, [rw_dims, I32, I32, rw_hier_config]),
     "rw_hier_segment_labels": (I32, [P, I32, rw_norm, rw_dims, P, I32, rw_hier_config, P, SZ,
                                      P, P, P, C.POINTER(rw_hier_stats), P]),
+    "rw_hier_ooc_workspace_bytes": (SZ, [rw_dims, I32, rw_hier_config, C.c_int64]),
+    "rw_hier_ooc_queue_bytes": (SZ, [rw_dims, I32, rw_hier_config]),
+    "rw_hier_segment_ooc": (I32, [P, I32, rw_norm, rw_dims, P, rw_hier_config, C.c_int64, P, P,
+                                  SZ, P, P, C.POINTER(rw_hier_stats), P]),
     "rw_get_option": (C.c_int64, [I32]),
     "rw_resident_available": (I32, [rw_dims, I32]),
 }

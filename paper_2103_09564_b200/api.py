@@ -393,6 +393,61 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True, be
     return prob, stats, {"prob": prob, "workspace": workspace}
 
 
+NP_DTYPES = {"uint8": 0, "uint16": 1, "int16": 2, "float32": 3}
+
+
+def hier_segment_ooc(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True, beta=100.0,
+                     eps=1e-6, tol=1e-6, max_iter=5000, tol_mode=0, norm=None, max_batch=1024,
+                     pool_bricks=None, want_prob=True, want_labels=True, device="cuda",
+                     queue=None, workspace=None, stream=None):
+    """rw_hier_segment_ooc: the hierarchical random walker with the
+    volume, labels and output in HOST memory.  vol: numpy [nz, ny, nx] (u8/u16/i16/f32), any
+    dims; seeds: numpy u8 (0 / 1 fg / 2 bg).  pool_bricks: device brick-pool capacity (default:
+    the level-0 brick count / 8 + 4096).  Returns (prob fp32 numpy or None, labels u8 numpy or
+    None, stats dict)."""
+    import numpy as np
+    vol = np.ascontiguousarray(vol)
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint8)
+    if vol.ndim != 3 or seeds.shape != vol.shape:
+        raise ValueError("hier_segment_ooc: vol and seeds must be 3-D arrays of one shape")
+    dt = NP_DTYPES[str(vol.dtype)]
+    nz, ny, nx = vol.shape
+    d = rw_dims(nx, ny, nz)
+    tdt = {0: torch.uint8, 1: torch.uint16, 2: torch.int16, 3: torch.float32}[dt]
+    sc, of = norm or DEFAULT_NORM[tdt]
+    cfg = rw_hier_config(s, e, t_hom, t_bin, int(prune), beta, eps, tol, max_iter, tol_mode,
+                         max_batch, 0, 0.01)
+    if pool_bricks is None:
+        nb0 = -(-nx // s) * -(-ny // s) * -(-nz // s)
+        pool_bricks = nb0 // 8 + 4096
+    need = lib().rw_hier_ooc_workspace_bytes(d, dt, cfg, int(pool_bricks))
+    qb = lib().rw_hier_ooc_queue_bytes(d, dt, cfg)
+    if need == 0 or qb == 0:
+        raise ValueError("hier_segment_ooc: need s % 4 == 0, e in (1, 2] with floor(e*s) % 4 == 0")
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need, device)
+    own_q = queue is None
+    if own_q:
+        queue = Queue(qb, depth=2)
+    prob = np.empty(vol.shape, np.float32) if want_prob else None
+    lab = np.empty(vol.shape, np.uint8) if want_labels else None
+    st = rw_hier_stats()
+    try:
+        check(lib().rw_hier_segment_ooc(C.c_void_p(vol.ctypes.data), dt, rw_norm(sc, of), d,
+                                        C.c_void_p(seeds.ctypes.data), cfg, int(pool_bricks),
+                                        queue._q, _ptr(workspace), workspace.numel(),
+                                        None if prob is None else C.c_void_p(prob.ctypes.data),
+                                        None if lab is None else C.c_void_p(lab.ctypes.data),
+                                        C.byref(st), _stream(stream, workspace.device)),
+              "rw_hier_segment_ooc")
+    finally:
+        if own_q:
+            queue.close()
+    stats = _stats_dict(st)
+    stats["pool_used"] = int(st.pool_used)
+    return prob, lab, stats
+
+
 def _stats_dict(st):
     L = st.levels
     out = {f: [int(getattr(st, f)[l]) for l in range(L)]

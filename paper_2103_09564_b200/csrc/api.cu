@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <functional>
+#include <thread>
 #include <string>
 #include <utility>
 #include <vector>
@@ -44,6 +46,21 @@ cudaError_t launch_fill(const float*, int, float*, int, int, const int4*, int, u
                         cudaStream_t);
 cudaError_t launch_weights_ex(const void*, int, float, float, int, int, int, int, int, float,
                               float, int, float*, void*, int, cudaStream_t);
+cudaError_t launch_ooc_seedor0(const uint8_t*, int, int, const OocGeo&, uint8_t*, int, cudaStream_t);
+cudaError_t launch_ooc_seedor(const uint8_t*, int, const OocGeo&, uint8_t*, int, cudaStream_t);
+cudaError_t launch_ooc_materialize(const int4*, int, int, const OocGeo&, int*, float*, cudaStream_t);
+cudaError_t launch_ooc_gather(const void*, int, const uint8_t*, const uint8_t*, int, bool,
+                              const OocGeo&, const int*, const float*, int, int, int, int,
+                              const int4*, int, void*, uint8_t*, float*, float*, int, cudaStream_t);
+cudaError_t launch_ooc_wfix(float*, int, int, int, int, int, int, cudaStream_t);
+cudaError_t launch_ooc_contract(const float*, int, int, int, int, const int4*, const int4*, int, int,
+                                const OocGeo&, const uint8_t*, int*, float*, float, float, int, int*,
+                                cudaStream_t);
+size_t queue_slot_bytes(const rw_queue* q);
+rw_status queue_push_fill(rw_queue* q, size_t bytes, void (*fill)(void*, void*), void* ctx,
+                          cudaStream_t copy_s, void** dev_slot, int32_t* slot_id);
+cudaError_t launch_ooc_out(int, const OocGeo&, const int*, const float*, const float*, int, int, int,
+                           float*, uint8_t*, int, cudaStream_t);
 }  // namespace rw
 
 namespace {
@@ -1293,6 +1310,492 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
     if (r != RW_OK) return r;
     RW_TIMED(RW_K_HIER, s, 1, rw::launch_label_max(pk, n, k, best, out_labels, num_sms(), s));
   }
+  return RW_OK;
+}
+
+// ------------------------------------------------------------------ out-of-core driver
+// rw_hier_segment_ooc (include/rw.h): the hierarchical driver with the volume, seeds and
+// output in host memory and the level fields as page tables over a brick pool
+// (csrc/hier_ooc.cu).  Device memory: intensity and seed-bit pyramid levels >= 1 (1/7 of the
+// volume in its dtype + 1/7 byte per voxel), the pool, one batch of windows, one output slab.
+namespace {
+
+struct OocPlan {
+  rw::OocGeo G;
+  int k, s, se, Bc;
+  int wx[17], wy[17], wz[17], wxp[17];   // window dims per level (root: the level), x padded
+  size_t es;
+  long long pt_total, pool_cap, nwmax;
+  int oz[17];                            // output slab planes per level
+};
+
+int ceil4(int v) { return (v + 3) & ~3; }
+
+bool ooc_plan(rw_dims d, rw_dtype dt, const rw_hier_config& c, int64_t pool_bricks, OocPlan* P) {
+  if (d.nx < 1 || d.ny < 1 || d.nz < 1) return false;
+  if (c.s < 4 || c.s % 4 != 0 || !(c.e > 1.f && c.e <= 2.f)) return false;
+  const int se = (int)std::floor((double)c.e * c.s);
+  if (se % 4 != 0 || se <= c.s || pool_bricks < 1) return false;
+  OocPlan& p = *P;
+  p.s = c.s;
+  p.se = se;
+  p.es = dtype_size(dt);
+  p.Bc = c.max_batch > 0 ? c.max_batch : 1024;
+  int l = 0;
+  p.G.nx[0] = d.nx; p.G.ny[0] = d.ny; p.G.nz[0] = d.nz;
+  while (std::max(p.G.nx[l], std::max(p.G.ny[l], p.G.nz[l])) > c.s) {   // reading R31
+    if (l == 16) return false;
+    p.G.nx[l + 1] = (p.G.nx[l] + 1) / 2;
+    p.G.ny[l + 1] = (p.G.ny[l] + 1) / 2;
+    p.G.nz[l + 1] = (p.G.nz[l] + 1) / 2;
+    ++l;
+  }
+  p.k = l;
+  p.G.k = l;
+  p.G.s = c.s;
+  long long o = 0;
+  p.nwmax = 0;
+  for (int m = 0; m <= p.k; ++m) {
+    p.G.bx[m] = (p.G.nx[m] + c.s - 1) / c.s;
+    p.G.by[m] = (p.G.ny[m] + c.s - 1) / c.s;
+    p.G.bz[m] = (p.G.nz[m] + c.s - 1) / c.s;
+    p.G.pt[m] = o;
+    o += (long long)p.G.bx[m] * p.G.by[m] * p.G.bz[m];
+    const bool root = m == p.k;
+    p.wx[m] = root ? p.G.nx[m] : std::min(se, p.G.nx[m]);
+    p.wy[m] = root ? p.G.ny[m] : std::min(se, p.G.ny[m]);
+    p.wz[m] = root ? p.G.nz[m] : std::min(se, p.G.nz[m]);
+    p.wxp[m] = ceil4(p.wx[m]);
+    p.nwmax = std::max(p.nwmax, (long long)p.wxp[m] * p.wy[m] * p.wz[m]);
+  }
+  p.pt_total = o;
+  p.pool_cap = pool_bricks;
+  p.oz[0] = std::min(c.s, p.G.nz[0]);
+  for (int m = 0; m < p.k; ++m) p.oz[m + 1] = std::min(p.G.nz[m + 1], (p.oz[m] + 1) / 2 + 2);
+  return true;
+}
+
+struct OocLayout {
+  size_t lev[17], bits[17], pt, pool, org, brick, state, iters, status, jobs, wvol, wfixed, wval,
+      wx0, wprob, W, solve, out[17], lab, total;
+};
+constexpr int kOocJobs = 4096;   // materialisation jobs per launch
+
+OocLayout ooc_layout(const OocPlan& p) {
+  OocLayout L{};
+  size_t o = 0;
+  for (int m = 1; m <= p.k; ++m) {
+    const size_t n = (size_t)p.G.nx[m] * p.G.ny[m] * p.G.nz[m];
+    L.lev[m] = o; o += up(n * p.es);
+    L.bits[m] = o; o += up(n);
+  }
+  const size_t s3 = (size_t)p.s * p.s * p.s, B = (size_t)p.Bc, nw = (size_t)p.nwmax;
+  L.pt = o; o += up((size_t)p.pt_total * 4);
+  L.pool = o; o += up((size_t)p.pool_cap * s3 * 4);
+  L.org = o; o += up(B * 16);
+  L.brick = o; o += up(B * 16);
+  L.state = o; o += up(B * 4);
+  L.iters = o; o += up(B * 4);
+  L.status = o; o += up(B * 4);
+  L.jobs = o; o += up((size_t)kOocJobs * 16);
+  L.wvol = o; o += up(B * nw * p.es);
+  L.wfixed = o; o += up(B * nw);
+  L.wval = o; o += up(B * nw * 4);
+  L.wx0 = o; o += up(B * nw * 4);
+  L.wprob = o; o += up(B * nw * 4);
+  bool pad = false;
+  size_t sws = 0;
+  for (int m = 0; m <= p.k; ++m) {
+    const bool pm = p.wxp[m] != p.wx[m];
+    pad |= pm;
+    const int nb = m == p.k ? 1 : p.Bc;
+    const rw_dims dw{p.wxp[m], p.wy[m], p.wz[m]};
+    sws = std::max(sws, layout(make_plan(nb, dw, 1), pm, 0).total);
+  }
+  L.W = o; o += pad ? up(3 * B * nw * 4) : 0;
+  L.solve = o; o += up(sws);
+  for (int m = 0; m <= p.k; ++m) {
+    L.out[m] = o; o += up((size_t)p.G.nx[m] * p.G.ny[m] * p.oz[m] * 4);
+  }
+  L.lab = o; o += up((size_t)p.G.nx[0] * p.G.ny[0] * p.oz[0]);
+  L.total = o;
+  return L;
+}
+
+// parent rows of child voxel i (level dims of the parent np): hier.cu's pcoord, exactly
+inline void pc_host(int i, int np, int& i0, int& i1) {
+  float u = std::fmin(std::fmax(0.5f * (float)i - 0.25f, 0.f), (float)(np - 1));
+  i0 = (int)std::floor(u);
+  i1 = std::min(i0 + 1, np - 1);
+}
+
+struct GatherCtx {
+  const char* vol;
+  const uint8_t* seeds;
+  const OocPlan* p;
+  const int4* org;
+  int nb, l;
+  size_t vbytes;        // offset of the seeds part in the slot
+};
+
+// level-0 windows from host memory into the pinned slot: [nb][wz][wy][wxp] intensities,
+// then the labels in the same layout (x padding zeroed)
+void gather_windows(void* dst, void* ctx_) {
+  const GatherCtx& c = *(const GatherCtx*)ctx_;
+  const OocPlan& p = *c.p;
+  const int wx = p.wx[0], wy = p.wy[0], wz = p.wz[0], wxp = p.wxp[0];
+  const size_t es = p.es, nx = p.G.nx[0], ny = p.G.ny[0];
+  char* dv = (char*)dst;
+  uint8_t* ds = (uint8_t*)dst + c.vbytes;
+  unsigned nt = std::thread::hardware_concurrency();
+  nt = std::max(1u, std::min(nt, 32u));
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (int j = (int)t; j < c.nb; j += (int)nt) {
+        const int4 o = c.org[j];
+        for (int lz = 0; lz < wz; ++lz)
+          for (int ly = 0; ly < wy; ++ly) {
+            const size_t src = ((size_t)(o.z + lz) * ny + (o.y + ly)) * nx + o.x;
+            const size_t row = (((size_t)j * wz + lz) * wy + ly) * wxp;
+            std::memcpy(dv + row * es, c.vol + src * es, (size_t)wx * es);
+            std::memcpy(ds + row, c.seeds + src, wx);
+            if (wxp > wx) {
+              std::memset(dv + (row + wx) * es, 0, (size_t)(wxp - wx) * es);
+              std::memset(ds + row + wx, 0, wxp - wx);
+            }
+          }
+      }
+    });
+  for (auto& x : th) x.join();
+}
+
+struct SlabCtx {
+  const char* vol;
+  const uint8_t* seeds;
+  size_t vbytes, sbytes;
+};
+void copy_slab(void* dst, void* ctx_) {
+  const SlabCtx& c = *(const SlabCtx*)ctx_;
+  std::thread a([&] { std::memcpy(dst, c.vol, c.vbytes); });
+  std::memcpy((char*)dst + c.vbytes, c.seeds, c.sbytes);
+  a.join();
+}
+
+}  // namespace
+
+size_t rw_hier_ooc_workspace_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg,
+                                   int64_t pool_bricks) {
+  OocPlan p;
+  if (dtype < RW_U8 || dtype > RW_F32 || !ooc_plan(d, dtype, cfg, pool_bricks, &p)) return 0;
+  return ooc_layout(p).total;
+}
+
+size_t rw_hier_ooc_queue_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg) {
+  OocPlan p;
+  if (dtype < RW_U8 || dtype > RW_F32 || !ooc_plan(d, dtype, cfg, 1, &p)) return 0;
+  const size_t win = (size_t)p.Bc * p.wxp[0] * p.wy[0] * p.wz[0] * (p.es + 1);
+  const size_t plane = (size_t)d.nx * d.ny * (p.es + 1);
+  return std::max(win, std::min((size_t)d.nz, (size_t)16) * plane);
+}
+
+rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_dims d,
+                              const uint8_t* seeds_h, rw_hier_config cfg, int64_t pool_bricks,
+                              struct rw_queue* q, void* workspace, size_t ws_bytes, float* prob_h,
+                              uint8_t* labels_h, rw_hier_stats* stats, void* stream) {
+  if (!vol_h || !seeds_h || !q || !workspace)
+    return fail(RW_EINVAL, "rw_hier_segment_ooc: vol, seeds, queue and workspace must be non-NULL");
+  if (dtype < RW_U8 || dtype > RW_F32) return fail(RW_EINVAL, "rw_hier_segment_ooc: bad dtype");
+  if (cfg.incremental) return fail(RW_EINVAL, "rw_hier_segment_ooc: incremental runs need rw_hier_segment");
+  OocPlan p;
+  if (!ooc_plan(d, dtype, cfg, pool_bricks, &p))
+    return fail(RW_EINVAL, "rw_hier_segment_ooc: need s %% 4 == 0, e in (1, 2] with floor(e s) %% 4 "
+                "== 0, pool_bricks >= 1, <= 17 levels");
+  if (!(cfg.eps > 0.f) || !(cfg.tol > 0.f) || cfg.max_iter < 1)
+    return fail(RW_EINVAL, "rw_hier_segment_ooc: need eps > 0, tol > 0, max_iter >= 1");
+  const OocLayout L = ooc_layout(p);
+  if (ws_bytes < L.total)
+    return fail(RW_ENOMEM, "rw_hier_segment_ooc: workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  if (rw::queue_slot_bytes(q) < rw_hier_ooc_queue_bytes(d, dtype, cfg))
+    return fail(RW_EINVAL, "rw_hier_segment_ooc: queue slots smaller than rw_hier_ooc_queue_bytes");
+  if (((uintptr_t)workspace & 255u) != 0) return fail(RW_EINVAL, "rw_hier_segment_ooc: workspace must be 256-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  auto PTR = [&](size_t off) { return (void*)(ws + off); };
+  const int sms = num_sms();
+  const rw::OocGeo& G = p.G;
+  const int k = p.k, S = p.s;
+  const size_t es = p.es;
+  rw_hier_stats st{};
+  st.levels = k + 1;
+
+  // ---- pyramid levels >= 1 of the intensities and of the seed bits (R22), streamed
+  // from host memory through the queue in z-slabs of an even number of planes
+  const size_t plane = (size_t)d.nx * d.ny;
+  if (k >= 1) {
+    int SL = (int)std::min<size_t>(rw::queue_slot_bytes(q) / (plane * (es + 1)), (size_t)d.nz);
+    SL &= ~1;
+    if (SL < 2) SL = std::min(2, d.nz);
+    void* lev1 = PTR(L.lev[1]);
+    for (int z0 = 0; z0 < d.nz; z0 += SL) {
+      const int nzs = std::min(SL, d.nz - z0);
+      SlabCtx sc{(const char*)vol_h + (size_t)z0 * plane * es, seeds_h + (size_t)z0 * plane,
+                 (size_t)nzs * plane * es, (size_t)nzs * plane};
+      void* dev = nullptr;
+      int32_t sid = 0;
+      rw_status r = rw::queue_push_fill(q, sc.vbytes + sc.sbytes, copy_slab, &sc, s, &dev, &sid);
+      if (r != RW_OK) return r;
+      r = rw_build_pyramid_slab(dev, dtype, d, z0, nzs, 1, &lev1, stream);
+      if (r != RW_OK) return r;
+      RW_TIMED(RW_K_HIER, s, 1, rw::launch_ooc_seedor0((const uint8_t*)dev + sc.vbytes, z0, nzs, G,
+                                                       (uint8_t*)PTR(L.bits[1]), sms, s));
+      r = rw_queue_release(q, sid, stream);
+      if (r != RW_OK) return r;
+    }
+    if (k >= 2) {
+      void* outs[16];
+      for (int m = 2; m <= k; ++m) outs[m - 2] = PTR(L.lev[m]);
+      const rw_dims d1{G.nx[1], G.ny[1], G.nz[1]};
+      rw_status r = rw_build_pyramid(lev1, dtype, d1, k - 1, outs, stream);
+      if (r != RW_OK) return r;
+      for (int m = 1; m < k; ++m)
+        RW_TIMED(RW_K_HIER, s, 1, rw::launch_ooc_seedor((const uint8_t*)PTR(L.bits[m]), m, G,
+                                                        (uint8_t*)PTR(L.bits[m + 1]), sms, s));
+    }
+  }
+
+  int* PT = (int*)PTR(L.pt);
+  float* pool = (float*)PTR(L.pool);
+  RW_CK(cudaMemsetAsync(PT, 0xff, (size_t)p.pt_total * 4, s));      // -1: not materialised
+  std::vector<int> hpt((size_t)p.pt_total, -1);
+  long long next_slot = 0;
+  auto pti = [&](int m, int bx, int by, int bz) {
+    return G.pt[m] + ((long long)bz * G.by[m] + by) * G.bx[m] + bx;
+  };
+  int4* d_org = (int4*)PTR(L.org);
+  int4* d_brick = (int4*)PTR(L.brick);
+  int4* d_jobs = (int4*)PTR(L.jobs);
+  int* d_state = (int*)PTR(L.state);
+  int* d_iters = (int*)PTR(L.iters);
+  int* d_status = (int*)PTR(L.status);
+  uint8_t* wfixed = (uint8_t*)PTR(L.wfixed);
+  float* wval = (float*)PTR(L.wval);
+  float* wx0 = (float*)PTR(L.wx0);
+  float* wprob = (float*)PTR(L.wprob);
+  float* Wb = L.W ? (float*)PTR(L.W) : nullptr;
+  char* sws = ws + L.solve;
+
+  // ---- materialisation (R26): bricks of level m+1 .. k-1 that a window or a finer
+  // materialisation samples, coarsest first
+  std::vector<std::vector<int4>> jobs(k + 1);
+  std::function<rw_status(int, int, int, int)> ensure = [&](int m, int bx, int by, int bz) -> rw_status {
+    if (hpt[pti(m, bx, by, bz)] >= 0) return RW_OK;
+    const int c[3] = {bx, by, bz};
+    const int nd[3] = {G.nx[m], G.ny[m], G.nz[m]}, pd[3] = {G.nx[m + 1], G.ny[m + 1], G.nz[m + 1]};
+    int lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+      int i0, i1, j0, j1;
+      pc_host(c[a] * S, pd[a], i0, i1);
+      pc_host(std::min((c[a] + 1) * S, nd[a]) - 1, pd[a], j0, j1);
+      lo[a] = i0 / S;
+      hi[a] = j1 / S;
+    }
+    for (int z = lo[2]; z <= hi[2]; ++z)
+      for (int y = lo[1]; y <= hi[1]; ++y)
+        for (int x = lo[0]; x <= hi[0]; ++x) {
+          rw_status r = ensure(m + 1, x, y, z);
+          if (r != RW_OK) return r;
+        }
+    if (next_slot >= p.pool_cap)
+      return fail(RW_ENOMEM, "rw_hier_segment_ooc: brick pool full (%lld bricks); pass a larger "
+                  "pool_bricks", (long long)p.pool_cap);
+    const int slot = (int)next_slot++;
+    hpt[pti(m, bx, by, bz)] = slot;
+    jobs[m].push_back(make_int4(bx, by, bz, slot));
+    return RW_OK;
+  };
+  auto run_jobs = [&]() -> rw_status {
+    for (int m = k - 1; m >= 0; --m) {
+      for (size_t f = 0; f < jobs[m].size(); f += kOocJobs) {
+        const int nj = (int)std::min((size_t)kOocJobs, jobs[m].size() - f);
+        RW_CK(cudaMemcpyAsync(d_jobs, jobs[m].data() + f, nj * sizeof(int4), cudaMemcpyHostToDevice, s));
+        RW_TIMED(RW_K_HIER, s, 1, rw::launch_ooc_materialize(d_jobs, nj, m, G, PT, pool, s));
+        RW_CK(cudaStreamSynchronize(s));   // d_jobs is reused
+      }
+      jobs[m].clear();
+    }
+    return RW_OK;
+  };
+
+  // ---- one chunk of windows at level l: gather, solve, contract
+  std::vector<int> h_state, h_iters;
+  auto solve_chunk = [&](int l, const std::vector<int4>& org, const std::vector<int4>& br,
+                         size_t first, int nb) -> rw_status {
+    const bool root = l == k;
+    const int wx = p.wx[l], wy = p.wy[l], wz = p.wz[l], wxp = p.wxp[l];
+    RW_CK(cudaMemcpyAsync(d_org, org.data() + first, nb * sizeof(int4), cudaMemcpyHostToDevice, s));
+    RW_CK(cudaMemcpyAsync(d_brick, br.data() + first, nb * sizeof(int4), cudaMemcpyHostToDevice, s));
+    void* wvol = PTR(L.wvol);
+    int32_t sid = -1;
+    const uint8_t* wseed = nullptr;
+    if (l == 0) {      // leaf windows from host memory through the queue
+      const size_t vb = (size_t)nb * wxp * wy * wz * es;
+      GatherCtx gc{(const char*)vol_h, seeds_h, &p, org.data() + first, nb, l, vb};
+      void* dev = nullptr;
+      rw_status r = rw::queue_push_fill(q, vb + (size_t)nb * wxp * wy * wz, gather_windows, &gc, s,
+                                        &dev, &sid);
+      if (r != RW_OK) return r;
+      wvol = dev;
+      wseed = (const uint8_t*)dev + vb;
+    }
+    RW_TIMED(RW_K_HIER, s, 1,
+             rw::launch_ooc_gather(l == 0 ? nullptr : PTR(L.lev[l]), (int)dtype,
+                                   l == 0 ? nullptr : (const uint8_t*)PTR(L.bits[l]), wseed, l,
+                                   root, G, PT, pool, wx, wy, wz, wxp, d_org, nb, wvol, wfixed,
+                                   wval, wx0, sms, s));
+    const rw_dims dw{wxp, wy, wz};
+    const rw::Plan P = make_plan(nb, dw, 1);
+    const bool pad = wxp != wx;
+    const Layout Lw = layout(P, pad, 0);
+    rw_status r;
+    if (pad) {         // x padding: stored weights with the padding edges cut (k_ooc_wfix)
+      RW_TIMED(RW_K_WEIGHTS, s, 1,
+               rw::launch_weights(wvol, dtype, nm.scale, nm.offset, nb, wxp, wy, wz, cfg.beta,
+                                  cfg.eps, Wb, nullptr, nullptr, sms, s));
+      RW_TIMED(RW_K_HIER, s, 1, rw::launch_ooc_wfix(Wb, nb, wx, wy, wz, wxp, sms, s));
+      r = solve_core(nb, dw, nullptr, dtype, nm, Wb, wfixed, wval, 1, cfg.beta, cfg.eps, cfg.tol,
+                     cfg.max_iter, cfg.tol_mode, root ? nullptr : wx0, sws, Lw, P, wprob, d_iters,
+                     nullptr, d_status, nullptr, s);
+    } else {
+      r = solve_core(nb, dw, wvol, dtype, nm, nullptr, wfixed, wval, 1, cfg.beta, cfg.eps, cfg.tol,
+                     cfg.max_iter, cfg.tol_mode, root ? nullptr : wx0, sws, Lw, P, wprob, d_iters,
+                     nullptr, d_status, nullptr, s);
+    }
+    if (r != RW_OK) return r;
+    if (sid >= 0) {
+      r = rw_queue_release(q, sid, stream);
+      if (r != RW_OK) return r;
+    }
+    RW_TIMED(RW_K_HIER, s, 1,
+             rw::launch_ooc_contract(wprob, wx, wy, wz, wxp, d_org, d_brick, nb, l, G,
+                                     l == 0 ? nullptr : (const uint8_t*)PTR(L.bits[l]), PT, pool,
+                                     cfg.t_hom, cfg.t_bin, cfg.prune, d_state, s));
+    h_state.resize(first + nb);
+    h_iters.resize(first + nb);
+    RW_CK(cudaMemcpyAsync(h_state.data() + first, d_state, nb * sizeof(int), cudaMemcpyDeviceToHost, s));
+    RW_CK(cudaMemcpyAsync(h_iters.data() + first, d_iters, nb * sizeof(int), cudaMemcpyDeviceToHost, s));
+    RW_CK(cudaStreamSynchronize(s));
+    return RW_OK;
+  };
+  auto tally = [&](int l, size_t nb) {
+    st.active[l] = (int64_t)nb;
+    st.solved[l] = (int64_t)nb;
+    for (size_t i = 0; i < nb; ++i) {
+      st.iters[l] += h_iters[i];
+      st.pruned_hom[l] += h_state[i] == 1;
+      st.pruned_dt[l] += h_state[i] == 2;
+      st.conflict[l] += h_state[i] == 3;
+    }
+  };
+
+  // ---- root (Eq. 1): the whole coarsest level, x0 = 0.5
+  std::vector<int4> active{make_int4(0, 0, 0, 0)};
+  {
+    std::vector<int4> org{make_int4(0, 0, 0, 0)}, br{make_int4(0, 0, 0, (int)next_slot++)};
+    hpt[pti(k, 0, 0, 0)] = br[0].w;
+    h_state.clear();
+    rw_status r = solve_chunk(k, org, br, 0, 1);
+    if (r != RW_OK) return r;
+    tally(k, 1);
+  }
+  // ---- levels k-1 .. 0 (Eq. 3, H_p)
+  const int lo = (int)std::ceil((p.se - p.s) / 2.0);
+  for (int l = k - 1; l >= 0; --l) {
+    std::vector<int4> kids;
+    for (size_t i = 0; i < active.size(); ++i) {
+      if (h_state[i] != 0 && h_state[i] != 3) continue;       // 1, 2: pruned
+      const int4 b = active[i];
+      for (int c = 0; c < 8; ++c) {
+        const int x = 2 * b.x + (c & 1), y = 2 * b.y + ((c >> 1) & 1), z = 2 * b.z + (c >> 2);
+        if (x < G.bx[l] && y < G.by[l] && z < G.bz[l]) kids.push_back(make_int4(x, y, z, 0));
+      }
+    }
+    const int dl[3] = {G.nx[l], G.ny[l], G.nz[l]}, wd[3] = {p.wx[l], p.wy[l], p.wz[l]};
+    auto place = [&](int b, int a) { return std::min(std::max(b * S - lo, 0), dl[a] - wd[a]); };
+    std::vector<int4> org(kids.size());
+    for (size_t i = 0; i < kids.size(); ++i) {
+      org[i] = make_int4(place(kids[i].x, 0), place(kids[i].y, 1), place(kids[i].z, 2), 0);
+      // parent-field samples of the window (border seeds, x0): its level-(l+1) bricks
+      const int o3[3] = {org[i].x, org[i].y, org[i].z};
+      const int pd[3] = {G.nx[l + 1], G.ny[l + 1], G.nz[l + 1]};
+      int blo[3], bhi[3];
+      for (int a = 0; a < 3; ++a) {
+        int i0, i1, j0, j1;
+        pc_host(o3[a], pd[a], i0, i1);
+        pc_host(o3[a] + wd[a] - 1, pd[a], j0, j1);
+        blo[a] = i0 / S;
+        bhi[a] = j1 / S;
+      }
+      for (int z = blo[2]; z <= bhi[2]; ++z)
+        for (int y = blo[1]; y <= bhi[1]; ++y)
+          for (int x = blo[0]; x <= bhi[0]; ++x) {
+            rw_status r = ensure(l + 1, x, y, z);
+            if (r != RW_OK) return r;
+          }
+    }
+    rw_status r = run_jobs();
+    if (r != RW_OK) return r;
+    if (next_slot + (long long)kids.size() > p.pool_cap)
+      return fail(RW_ENOMEM, "rw_hier_segment_ooc: brick pool full (%lld bricks); pass a larger "
+                  "pool_bricks", (long long)p.pool_cap);
+    for (auto& b : kids) {
+      b.w = (int)next_slot++;
+      hpt[pti(l, b.x, b.y, b.z)] = b.w;
+    }
+    h_state.clear();
+    h_iters.clear();
+    for (size_t f = 0; f < kids.size(); f += p.Bc) {
+      const int nb = (int)std::min((size_t)p.Bc, kids.size() - f);
+      r = solve_chunk(l, org, kids, f, nb);
+      if (r != RW_OK) return r;
+    }
+    tally(l, kids.size());
+    active.swap(kids);
+  }
+
+  // ---- output: level-0 slabs; per level the planes the slab needs, coarsest first
+  if (prob_h || labels_h) {
+    const size_t pl0 = (size_t)G.nx[0] * G.ny[0];
+    for (int Z0 = 0; Z0 < G.nz[0]; Z0 += p.oz[0]) {
+      int z0[17], zc[17];
+      z0[0] = Z0;
+      zc[0] = std::min(p.oz[0], G.nz[0] - Z0);
+      for (int m = 0; m < k; ++m) {
+        int a0, a1, b0, b1;
+        pc_host(z0[m], G.nz[m + 1], a0, a1);
+        pc_host(z0[m] + zc[m] - 1, G.nz[m + 1], b0, b1);
+        z0[m + 1] = a0;
+        zc[m + 1] = b1 - a0 + 1;
+      }
+      for (int m = k; m >= 0; --m) {
+        const bool last = m == 0;
+        RW_TIMED(RW_K_HIER, s, 1,
+                 rw::launch_ooc_out(m, G, PT, pool, m == k ? nullptr : (const float*)PTR(L.out[m + 1]),
+                                    m == k ? 0 : z0[m + 1], z0[m], zc[m],
+                                    (!last || prob_h) ? (float*)PTR(L.out[m]) : nullptr,
+                                    (last && labels_h) ? (uint8_t*)PTR(L.lab) : nullptr, sms, s));
+      }
+      if (prob_h)
+        RW_CK(cudaMemcpyAsync(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4,
+                              cudaMemcpyDeviceToHost, s));
+      if (labels_h)
+        RW_CK(cudaMemcpyAsync(labels_h + (size_t)Z0 * pl0, PTR(L.lab), (size_t)zc[0] * pl0,
+                              cudaMemcpyDeviceToHost, s));
+    }
+    RW_CK(cudaStreamSynchronize(s));
+  }
+  st.pool_used = next_slot;
+  if (stats) *stats = st;
   return RW_OK;
 }
 

@@ -116,6 +116,35 @@ extern "C" rw_status rw_queue_push(rw_queue* q, const void* host_src, size_t byt
   return RW_OK;
 }
 
+// Library-internal (rw_hier_segment_ooc): push a slot whose pinned buffer is filled by
+// `fill` (e.g. a host-side gather of many small pieces) instead of one contiguous source.
+namespace rw {
+size_t queue_slot_bytes(const rw_queue* q) { return q ? q->slot_bytes : 0; }
+rw_status queue_push_fill(rw_queue* q, size_t bytes, void (*fill)(void* dst, void* ctx),
+                          void* ctx, cudaStream_t copy_s, void** dev_slot, int32_t* slot_id) {
+  if (!q || !fill || !dev_slot || bytes > q->slot_bytes)
+    return qfail(RW_EINVAL, "rw_queue: bad fill push (bytes > slot_bytes?)");
+  const int s = q->next;
+  if (!q->released[s])
+    return qfail(RW_EINVAL, "rw_queue: the next slot has not been released");
+  q->next = (q->next + 1) % q->depth;
+  if (q->used[s] && (cudaEventSynchronize(q->ready[s]) != cudaSuccess ||
+                     cudaEventSynchronize(q->freed[s]) != cudaSuccess))
+    return qfail(RW_ECUDA, "rw_queue: waiting for slot release failed");
+  fill(q->host[s], ctx);
+  if (bytes > 0 && (cudaMemcpyAsync(q->dev[s], q->host[s], bytes, cudaMemcpyHostToDevice,
+                                    copy_s) != cudaSuccess))
+    return qfail(RW_ECUDA, "rw_queue: H2D copy enqueue failed");
+  if (cudaEventRecord(q->ready[s], copy_s) != cudaSuccess)
+    return qfail(RW_ECUDA, "rw_queue: event record failed");
+  q->used[s] = true;
+  q->released[s] = false;
+  *dev_slot = q->dev[s];
+  if (slot_id) *slot_id = s;
+  return RW_OK;
+}
+}  // namespace rw
+
 extern "C" rw_status rw_queue_wait(rw_queue* q, int32_t slot_id, void* compute_stream) {
   if (!q || slot_id < 0 || slot_id >= q->depth) return qfail(RW_EINVAL, "rw_queue_wait: bad slot");
   if (cudaStreamWaitEvent((cudaStream_t)compute_stream, q->ready[slot_id], 0) != cudaSuccess)

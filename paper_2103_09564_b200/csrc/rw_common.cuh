@@ -84,6 +84,15 @@ struct Ctl {
                     // (k+1) % rr == 0 and k < max_iter-1, alpha_k p_k is already in x
 };
 
+// Geometry of the out-of-core hierarchical driver (hier_ooc.cu, reading R31): per level the
+// dims, the bricks per axis and the offset of the level's page table.
+struct OocGeo {
+  int nx[17], ny[17], nz[17];      // level dims
+  int bx[17], by[17], bz[17];      // bricks per axis
+  long long pt[17];                // page-table offset of each level
+  int s, k;                        // brick side, root level
+};
+
 // Outputs of one fused pyramid group (<= 5 levels).
 struct PyrOut {
   void* p[5];

@@ -1,0 +1,89 @@
+"""GPU parity of rw_hier_segment_ooc (SURVEY §8(f) f1 out of core: host volume / labels /
+output, brick pool + page tables instead of dense level fields; P:105, P:109-111, P:151,
+reading R31) against oracle/hier_oracle.py on ragged non-cubic volumes, and bit-for-bit
+agreement with the in-HBM driver rw_hier_segment on cubic s 2^k volumes."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2103_09564_b200 as rwb
+from oracle import hier_oracle as ho
+from paper_2103_09564_b200._lib import RWError
+from gpu_helpers import dev
+from test_hier_oracle import small_volume
+from test_hier_ragged_pins import _ragged_volume
+
+pytestmark = pytest.mark.gpu
+
+P_TOL = 1e-4   # as test_gpu_hier.py: GPU tol 1e-7 vs oracle 1e-10, errors through <= 4 levels
+
+
+def _check_vs_oracle(vol, seeds, **kw):
+    prob, lab, st = rwb.hier_segment_ooc(vol, seeds, tol=1e-7, max_iter=20000, **kw)
+    ref = ho.hier_segment(vol, seeds, tol=1e-10, **kw)
+    assert st["levels"] == len(ref["stats"])
+    for l, rs in enumerate(ref["stats"]):
+        assert st["solved"][l] == rs["solved"], (l, st, ref["stats"])
+        assert st["pruned_hom"][l] == rs["pruned_hom"] and st["pruned_dt"][l] == rs["pruned_dt"]
+        assert st["conflict"][l] == rs["conflict"]
+    d = np.abs(prob.astype(np.float64) - ref["prob"])
+    assert d.max() <= P_TOL, d.max()
+    sure = np.abs(ref["prob"] - 0.5) > 1e-3
+    assert np.array_equal(lab[sure], (ref["prob"] > 0.5)[sure])
+    assert np.array_equal(lab, (prob > 0.5).astype(np.uint8))     # labels = p > 0.5 (R10)
+    return prob, st
+
+
+@pytest.mark.parametrize("shape,prune", [((40, 56, 72), False), ((40, 56, 72), True),
+                                         ((36, 64, 48), True), ((24, 40, 72), False)])
+def test_ooc_ragged_matches_oracle(shape, prune):
+    """Ragged, non-cubic volumes, s = 16, e = 1.25: smaller border bricks on every level,
+    windows narrower than s_e at the coarse levels, x sides padded to a multiple of 4 (root
+    9 -> 12, level 2 18 -> 20)."""
+    vol, seeds = _ragged_volume(shape, 1, 150)
+    _, st = _check_vs_oracle(vol, seeds, s=16, e=1.25, beta=100.0, prune=prune)
+    assert st["pool_used"] >= sum(st["solved"])
+
+
+@pytest.mark.parametrize("D,s,e,prune", [(64, 16, 1.25, True), (64, 16, 1.25, False),
+                                         (32, 8, 1.5, True)])
+def test_ooc_cubic_matches_oracle(D, s, e, prune):
+    vol, seeds = small_volume(D, seed=D + s)
+    _check_vs_oracle(vol, seeds, s=s, e=e, beta=50.0, prune=prune)
+
+
+@pytest.mark.parametrize("D,s,prune", [(128, 16, True), (256, 32, True), (256, 32, False)])
+def test_ooc_bitwise_equals_in_hbm_driver(D, s, prune):
+    """Cubic s 2^k: the page-table field (materialised upsamples, pool) reproduces the dense
+    field pyramid of rw_hier_segment bit for bit (same samples, same solves; the resident
+    solver for s_e = 40)."""
+    vol, seeds = small_volume(D, seed=3)
+    kw = dict(s=s, e=1.25, beta=50.0, tol=1e-6, prune=prune)
+    ref, st_ref, _ = rwb.hier_segment(dev(vol), dev(seeds), **kw)
+    torch.cuda.synchronize()
+    prob, lab, st = rwb.hier_segment_ooc(vol, seeds, **kw)
+    assert st["solved"] == st_ref["solved"] and st["iters"] == st_ref["iters"]
+    assert np.array_equal(prob, ref.cpu().numpy())
+    assert np.array_equal(lab, (prob > 0.5).astype(np.uint8))
+
+
+def test_ooc_labels_only_and_single_brick():
+    """Labels without the fp32 output; a volume that is one brick (root = level 0, windows
+    from host memory) equals rw_solve_bricks on the whole volume."""
+    vol, seeds = _ragged_volume((12, 16, 20), 2, 10)
+    prob, lab, st = rwb.hier_segment_ooc(vol, seeds, s=32, e=1.25, beta=50.0, tol=1e-7)
+    assert st["levels"] == 1 and st["solved"] == [1]
+    fixed, val = ho.seeds_from_bits(ho.seed_bits(seeds))
+    out = rwb.solve_bricks(dev(fixed.astype(np.uint8)), dev(val.astype(np.float32)),
+                           vol=dev(vol), beta=50.0, tol=1e-7)
+    torch.cuda.synchronize()
+    assert np.abs(prob - out["prob"][0, 0].cpu().numpy()).max() <= 1e-5
+    p2, l2, _ = rwb.hier_segment_ooc(vol, seeds, s=32, e=1.25, beta=50.0, tol=1e-7,
+                                     want_prob=False)
+    assert p2 is None and np.array_equal(l2, lab)
+
+
+def test_ooc_pool_full_is_an_error():
+    vol, seeds = small_volume(64, seed=5)
+    with pytest.raises(RWError, match="RW_ENOMEM"):
+        rwb.hier_segment_ooc(vol, seeds, s=16, e=1.25, beta=50.0, prune=False, pool_bricks=4)
