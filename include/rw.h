@@ -276,6 +276,8 @@ typedef struct {
   int64_t active[16], solved[16], pruned_hom[16], pruned_dt[16], conflict[16], reused[16],
       iters[16];
   int64_t pool_used;    /* rw_hier_segment_ooc: brick-pool slots used (0 otherwise)        */
+  double ms_pyramid, ms_levels, ms_output;   /* rw_hier_segment_ooc: host wall time of the    */
+                        /* pyramid streaming, the level loop and the output slabs        */
 } rw_hier_stats;
 size_t rw_hier_workspace_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg);
 rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d,

@@ -38,7 +38,8 @@ class rw_hier_stats(C.Structure):
     _fields_ = [("levels", C.c_int32)] + [(f, C.c_int64 * 16) for f in
                                           ("active", "solved", "pruned_hom", "pruned_dt",
                                            "conflict", "reused", "iters")] + [
-        ("pool_used", C.c_int64)]
+        ("pool_used", C.c_int64), ("ms_pyramid", C.c_double), ("ms_levels", C.c_double),
+        ("ms_output", C.c_double)]
 
 
 P, I32, F32, SZ = C.c_void_p, C.c_int32, C.c_float, C.c_size_t

@@ -419,7 +419,7 @@ def hier_segment_ooc(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True
                          max_batch, 0, 0.01)
     if pool_bricks is None:
         nb0 = -(-nx // s) * -(-ny // s) * -(-nz // s)
-        pool_bricks = nb0 // 8 + 4096
+        pool_bricks = nb0 // 16 + 4096
     need = lib().rw_hier_ooc_workspace_bytes(d, dt, cfg, int(pool_bricks))
     qb = lib().rw_hier_ooc_queue_bytes(d, dt, cfg)
     if need == 0 or qb == 0:
@@ -445,6 +445,7 @@ def hier_segment_ooc(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True
             queue.close()
     stats = _stats_dict(st)
     stats["pool_used"] = int(st.pool_used)
+    stats["ms"] = {"pyramid": st.ms_pyramid, "levels": st.ms_levels, "output": st.ms_output}
     return prob, lab, stats
 
 

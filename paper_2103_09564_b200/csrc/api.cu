@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <chrono>
 #include <functional>
 #include <thread>
 #include <string>
@@ -57,6 +58,9 @@ cudaError_t launch_ooc_contract(const float*, int, int, int, int, const int4*, c
                                 const OocGeo&, const uint8_t*, int*, float*, float, float, int, int*,
                                 cudaStream_t);
 size_t queue_slot_bytes(const rw_queue* q);
+int queue_depth(const rw_queue* q);
+void* queue_host_slot(rw_queue* q, int i);
+void host_parallel_copy(void* dst, const void* src, size_t bytes);
 rw_status queue_push_fill(rw_queue* q, size_t bytes, void (*fill)(void*, void*), void* ctx,
                           cudaStream_t copy_s, void** dev_slot, int32_t* slot_id);
 cudaError_t launch_ooc_out(int, const OocGeo&, const int*, const float*, const float*, int, int, int,
@@ -1370,7 +1374,14 @@ bool ooc_plan(rw_dims d, rw_dtype dt, const rw_hier_config& c, int64_t pool_bric
   }
   p.pt_total = o;
   p.pool_cap = pool_bricks;
-  p.oz[0] = std::min(c.s, p.G.nz[0]);
+  // level-0 output slab: <= s planes and one fp32 slab per queue slot (D2H staging)
+  {
+    const size_t plane = (size_t)d.nx * d.ny, es1 = p.es + 1;
+    const size_t win = (size_t)p.Bc * p.wxp[0] * p.wy[0] * p.wz[0] * es1;
+    const size_t slot = std::max(win, std::min((size_t)d.nz, (size_t)16) * plane * es1);
+    const size_t fit = std::max<size_t>(1, slot / (plane * 4));
+    p.oz[0] = (int)std::min<size_t>(std::min(c.s, p.G.nz[0]), fit);
+  }
   for (int m = 0; m < p.k; ++m) p.oz[m + 1] = std::min(p.G.nz[m + 1], (p.oz[m] + 1) / 2 + 2);
   return true;
 }
@@ -1477,9 +1488,8 @@ struct SlabCtx {
 };
 void copy_slab(void* dst, void* ctx_) {
   const SlabCtx& c = *(const SlabCtx*)ctx_;
-  std::thread a([&] { std::memcpy(dst, c.vol, c.vbytes); });
-  std::memcpy((char*)dst + c.vbytes, c.seeds, c.sbytes);
-  a.join();
+  rw::host_parallel_copy(dst, c.vol, c.vbytes);
+  rw::host_parallel_copy((char*)dst + c.vbytes, c.seeds, c.sbytes);
 }
 
 }  // namespace
@@ -1496,7 +1506,7 @@ size_t rw_hier_ooc_queue_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg) {
   if (dtype < RW_U8 || dtype > RW_F32 || !ooc_plan(d, dtype, cfg, 1, &p)) return 0;
   const size_t win = (size_t)p.Bc * p.wxp[0] * p.wy[0] * p.wz[0] * (p.es + 1);
   const size_t plane = (size_t)d.nx * d.ny * (p.es + 1);
-  return std::max(win, std::min((size_t)d.nz, (size_t)16) * plane);
+  return std::max(win, std::min((size_t)d.nz, (size_t)16) * plane);   // as ooc_plan's oz[0]
 }
 
 rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_dims d,
@@ -1528,6 +1538,9 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
   const size_t es = p.es;
   rw_hier_stats st{};
   st.levels = k + 1;
+  auto wall = [] { return std::chrono::duration<double, std::milli>(
+                       std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double t0 = wall();
 
   // ---- pyramid levels >= 1 of the intensities and of the seed bits (R22), streamed
   // from host memory through the queue in z-slabs of an even number of planes
@@ -1564,6 +1577,9 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
     }
   }
 
+  RW_CK(cudaStreamSynchronize(s));
+  st.ms_pyramid = wall() - t0;
+  t0 = wall();
   int* PT = (int*)PTR(L.pt);
   float* pool = (float*)PTR(L.pool);
   RW_CK(cudaMemsetAsync(PT, 0xff, (size_t)p.pt_total * 4, s));      // -1: not materialised
@@ -1763,9 +1779,38 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
     active.swap(kids);
   }
 
+  st.ms_levels = wall() - t0;
+  t0 = wall();
   // ---- output: level-0 slabs; per level the planes the slab needs, coarsest first
   if (prob_h || labels_h) {
     const size_t pl0 = (size_t)G.nx[0] * G.ny[0];
+    // D2H through the queue's pinned slots (all pushes are complete here), round robin; the
+    // host copies a slot out to the caller's buffer while the next ones are in flight
+    const int nsl = rw::queue_depth(q);
+    std::vector<cudaEvent_t> oev(nsl);
+    for (auto& e : oev) RW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct Pend { int slot; void* dst; size_t bytes; };
+    std::vector<Pend> pend;
+    int nxt = 0;
+    rw_status r = RW_OK;
+    auto drain = [&]() -> rw_status {
+      const Pend c = pend.front();
+      pend.erase(pend.begin());
+      RW_CK(cudaEventSynchronize(oev[c.slot]));
+      rw::host_parallel_copy(c.dst, rw::queue_host_slot(q, c.slot), c.bytes);
+      return RW_OK;
+    };
+    auto stage = [&](void* dst, const void* src, size_t bytes) -> rw_status {
+      if ((int)pend.size() == nsl) {
+        rw_status rr = drain();
+        if (rr != RW_OK) return rr;
+      }
+      const int sl = nxt++ % nsl;
+      RW_CK(cudaMemcpyAsync(rw::queue_host_slot(q, sl), src, bytes, cudaMemcpyDeviceToHost, s));
+      RW_CK(cudaEventRecord(oev[sl], s));
+      pend.push_back({sl, dst, bytes});
+      return RW_OK;
+    };
     for (int Z0 = 0; Z0 < G.nz[0]; Z0 += p.oz[0]) {
       int z0[17], zc[17];
       z0[0] = Z0;
@@ -1785,15 +1830,16 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
                                     (!last || prob_h) ? (float*)PTR(L.out[m]) : nullptr,
                                     (last && labels_h) ? (uint8_t*)PTR(L.lab) : nullptr, sms, s));
       }
-      if (prob_h)
-        RW_CK(cudaMemcpyAsync(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4,
-                              cudaMemcpyDeviceToHost, s));
-      if (labels_h)
-        RW_CK(cudaMemcpyAsync(labels_h + (size_t)Z0 * pl0, PTR(L.lab), (size_t)zc[0] * pl0,
-                              cudaMemcpyDeviceToHost, s));
+      if (prob_h) { r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4); if (r != RW_OK) return r; }
+      if (labels_h) { r = stage(labels_h + (size_t)Z0 * pl0, PTR(L.lab), (size_t)zc[0] * pl0); if (r != RW_OK) return r; }
     }
-    RW_CK(cudaStreamSynchronize(s));
+    while (!pend.empty()) {
+      r = drain();
+      if (r != RW_OK) return r;
+    }
+    for (auto e : oev) cudaEventDestroy(e);
   }
+  st.ms_output = wall() - t0;
   st.pool_used = next_slot;
   if (stats) *stats = st;
   return RW_OK;

@@ -120,6 +120,11 @@ extern "C" rw_status rw_queue_push(rw_queue* q, const void* host_src, size_t byt
 // `fill` (e.g. a host-side gather of many small pieces) instead of one contiguous source.
 namespace rw {
 size_t queue_slot_bytes(const rw_queue* q) { return q ? q->slot_bytes : 0; }
+int queue_depth(const rw_queue* q) { return q ? q->depth : 0; }
+// the pinned host buffer of slot i (rw_hier_segment_ooc stages its D2H output there once
+// every push has completed)
+void* queue_host_slot(rw_queue* q, int i) { return q->host[i]; }
+void host_parallel_copy(void* dst, const void* src, size_t bytes) { parallel_copy(dst, src, bytes); }
 rw_status queue_push_fill(rw_queue* q, size_t bytes, void (*fill)(void* dst, void* ctx),
                           void* ctx, cudaStream_t copy_s, void** dev_slot, int32_t* slot_id) {
   if (!q || !fill || !dev_slot || bytes > q->slot_bytes)
