@@ -336,7 +336,8 @@ def config_lines(dev, workers):
                                 "peak_kind": peak_kind, "unit": "GB/s", "frac": ach / peak,
                                 "alg_bytes_per_voxel_iter": BYTES_1}}
     del p
-    # cfg4: 256^3 K = 4, three RHS on one operator (one-pass streaming, 2 + 1 rhs launches)
+    # cfg4: 256^3 K = 4, three RHS on one operator (one-pass streaming, one launch of three
+    # single-rhs CTA layers)
     lp = wl.cfg4()
     seeds, vol = t2d(lp.labels), t2d(lp.vol)
     ws = api.alloc_workspace(rwb.solve_labels_workspace_bytes(1, lp.dims, lp.K), dev)
@@ -353,16 +354,37 @@ def config_lines(dev, workers):
     api.profile_enable(False)
     it = out["iters"].cpu().numpy().ravel()
     nvox = float(lp.vol[0].size)
-    # per voxel-iteration and rhs: r, q, p, x read + written (32 B); per launch group: dinv
-    # and the f32 intensity (8 B); groups {rhs 1, 2}, {rhs 3}
-    alg = (32.0 * float(it.sum()) + 8.0 * (max(it[0], it[1]) + it[2])) * nvox
+    # per voxel-iteration and rhs: r, q, p, x read + written (32 B) + dinv and the f32
+    # intensity (8 B): each rhs's CTA layer reads its own operator (one CTA layer per rhs)
+    alg = 40.0 * float(it.sum()) * nvox
     ach = alg / (prof["passA"][1] / 1e3) / 1e9
     res["cfg4"] = {"workload": "256^3 f32, K = 4 (3 RHS on one operator), tol 1e-6",
                    "full_solve_ms": ms, "iters_per_rhs": it.tolist(),
                    "voxel_rhs_cg_iter_per_s": float(it.sum()) * nvox / (ms / 1e3),
                    "roofline": {"bound": "hbm", "kernel": "passA (multi-rhs)", "achieved": ach,
                                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                                "frac": ach / peak}}
+                                "frac": ach / peak, "alg_bytes_per_voxel_rhs_iter": 40}}
+    del seeds, vol, ws, out
+    torch.cuda.empty_cache()
+    # multi-label bricks on the resident solver: 128 bricks of 64^3 with the cfg4 recipe
+    # (K = 4 -> 3 rhs as (rhs, brick) pairs on each brick's operator)
+    lp = wl.cfg4(n=64, seeds_per_label=32)
+    B = 128
+    seeds = t2d(np.broadcast_to(lp.labels, (B,) + lp.labels.shape[-3:]))
+    vol = t2d(np.broadcast_to(lp.vol, (B,) + lp.vol.shape[-3:]))
+    ws = api.alloc_workspace(rwb.solve_labels_workspace_bytes(B, (64, 64, 64), lp.K), dev)
+    out = {}
+
+    def runm():
+        out.update(rwb.solve_labels(seeds, lp.K, vol=vol, beta=lp.beta, eps=lp.eps, tol=lp.tol,
+                                    max_iter=lp.max_iter, workspace=ws))
+    runm()
+    ms = _ev_ms(runm, reps=3)
+    it = out["iters"].cpu().numpy()
+    res["multilabel_64"] = {"workload": "128 x 64^3 f32 bricks, K = 4 (cfg4 recipe), tol 1e-6, "
+                                        "resident (rhs, brick) pairs",
+                            "full_solve_ms": ms, "iters_per_rhs": it[:, 0].tolist(),
+                            "voxel_rhs_cg_iter_per_s": float(it.sum()) * 64 ** 3 / (ms / 1e3)}
     del seeds, vol, ws, out
     torch.cuda.empty_cache()
     # cfg5: 2048^3 u16 pyramid (fused 5 levels, resident) and the hierarchical solve on the
@@ -381,7 +403,6 @@ def config_lines(dev, workers):
     seeds2 = wl.cfg5_new_seeds(vol, seeds)
     gen_s = time.time() - t
     vol_d, seeds_d, seeds2_d = t2d(vol), t2d(seeds), t2d(seeds2)
-    del vol
     state = {}
 
     def hier(prev=None, sd=seeds_d):
@@ -394,6 +415,7 @@ def config_lines(dev, workers):
     torch.cuda.synchronize()
     ms_h = _ev_ms(hier, reps=1, warm=0)
     st = state["stats"]
+    lab_hbm = (state["prob"] > 0.5).to(torch.uint8).cpu().numpy()
     ms_i = _ev_ms(lambda: hier(prev=dict(state), sd=seeds2_d), reps=1, warm=0)
     st2 = state["stats"]
     res["cfg5"] = {
@@ -408,6 +430,17 @@ def config_lines(dev, workers):
         "generate_s": gen_s}
     del vol_d, seeds_d, seeds2_d, state
     torch.cuda.empty_cache()
+    # the same H_p run out of core (rw_hier_segment_ooc: host volume / labels / output, brick
+    # pool + page tables), labels only
+    t = time.time()
+    _, lab_ooc, sto = rwb.hier_segment_ooc(vol, seeds, s=32, e=1.25, prune=True, tol=1e-6,
+                                           max_iter=5000, want_prob=False)
+    res["cfg5"]["ooc"] = {"wall_ms": (time.time() - t) * 1e3, "ms_phases": sto["ms"],
+                          "bricks_solved": int(sum(sto["solved"])), "pool_bricks": sto["pool_used"],
+                          "labels_equal_in_hbm_driver": bool(np.array_equal(lab_ooc, lab_hbm)),
+                          "note": "host 16 GiB volume in, u8 labels out; 4096x4096x2048 (64 GiB) "
+                                  "in profiles/r02/r02_ooc_4096x4096x2048.json"}
+    del vol, seeds, seeds2, lab_ooc, lab_hbm
     return res
 
 
