@@ -204,6 +204,37 @@ __device__ __forceinline__ void tm_ld8x3(uint32_t t0, uint32_t t1, uint32_t t2, 
   };
   a0 = F(0); a1 = F(4); b0 = F(8); b1 = F(12); c0 = F(16); c1 = F(20);
 }
+// two 8-column loads, one wait
+__device__ __forceinline__ void tm_ld8x2(uint32_t t0, uint32_t t1, float4& a0, float4& a1,
+                                         float4& b0, float4& b1) {
+  uint32_t a[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%16];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8, %9, %10, %11, %12, %13, %14, %15}, [%17];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+        "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]),
+        "=r"(a[14]), "=r"(a[15])
+      : "r"(t0), "r"(t1));
+  auto F = [&](int i) {
+    return make_float4(__uint_as_float(a[i]), __uint_as_float(a[i + 1]), __uint_as_float(a[i + 2]),
+                       __uint_as_float(a[i + 3]));
+  };
+  a0 = F(0); a1 = F(4); b0 = F(8); b1 = F(12);
+}
+// two / three 4-column loads, one wait
+__device__ __forceinline__ void tm_ld4x2(uint32_t t0, uint32_t t1, float4& u, float4& v) {
+  uint32_t a[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%8];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%9];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+        "=r"(a[7])
+      : "r"(t0), "r"(t1));
+  u = make_float4(__uint_as_float(a[0]), __uint_as_float(a[1]), __uint_as_float(a[2]), __uint_as_float(a[3]));
+  v = make_float4(__uint_as_float(a[4]), __uint_as_float(a[5]), __uint_as_float(a[6]), __uint_as_float(a[7]));
+}
 // DSMEM stores that complete (in bytes) on the receiving CTA's mbarrier
 __device__ __forceinline__ void st_async4(uint32_t a, float4 v, uint32_t bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
@@ -680,8 +711,12 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 #pragma unroll
       for (int zl = 0; zl < ZS; ++zl) {   // one plane (NR items) of dinv and x at a time
         float4 dv[NR], xv[NR];
-        tm_plane(cD, zl, dv);
-        if (k > 0) tm_plane(cV, zl, xv);
+        if (k > 0) {                      // dinv and x of the plane: one TMEM round trip
+          if constexpr (NR == 2) tm_ld8x2(cD + 8u * zl, cV + 8u * zl, dv[0], dv[1], xv[0], xv[1]);
+          else tm_ld4x2(cD + 4u * zl, cV + 4u * zl, dv[0], xv[0]);
+        } else {
+          tm_plane(cD, zl, dv);
+        }
 #pragma unroll
         for (int rr = 0; rr < NR; ++rr) {
           const int it = NR * zl + rr, y = NR * j + rr;
@@ -710,9 +745,16 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         const int so = 2 * j * N + 4 * qx;
         const float4 p0 = ld4(Pz + so), p1 = ld4(Pz + so + N);
         float4 q0, q1;
+        // the plane's +x, +z and (zl > 0) -z weights: one TMEM round trip
+        float4 wx0, wx1, wz0, wz1, wzm0, wzm1;
+        if (zl == 0) {
+          tm_ld8x2(cX, cZ, wx0, wx1, wz0, wz1);
+          wzm0 = ld4(WZM + so);
+          wzm1 = ld4(WZM + so + N);
+        } else {
+          tm_ld8x3(cX + 8u * zl, cZ + 8u * zl, cZ + 8u * (zl - 1), wx0, wx1, wz0, wz1, wzm0, wzm1);
+        }
         {  // x terms (same term order as stencil1: +x, -x, +y, -y, +z, -z)
-          float4 wx0, wx1;
-          tm_ld8(cX + 8u * zl, wx0, wx1);
           const float xr0 = shr(p0.x), xr1 = shr(p1.x);
           const float wl0 = shl(wx0.w), wl1 = shl(wx1.w);
           const float dl0 = shl(xd3(p0, xr0)), dl1 = shl(xd3(p1, xr1));
@@ -730,14 +772,6 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
           q1 = terms2(q1, p1, pyp, p0, wy1, wy0);
         }
         {  // z terms
-          float4 wz0, wz1, wzm0, wzm1;
-          tm_ld8(cZ + 8u * zl, wz0, wz1);
-          if (zl == 0) {
-            wzm0 = ld4(WZM + so);
-            wzm1 = ld4(WZM + so + N);
-          } else {
-            tm_ld8(cZ + 8u * (zl - 1), wzm0, wzm1);
-          }
           q0 = terms2(q0, p0, ld4(Pz + PL + so), ld4(Pz - PL + so), wz0, wzm0);
           q1 = terms2(q1, p1, ld4(Pz + PL + so + N), ld4(Pz - PL + so + N), wz1, wzm1);
         }
@@ -755,9 +789,14 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         const int so = j * N + 4 * qx;
         const float4 p0 = ld4(Pz + so);
         float4 q0;
+        float4 wx0, wz0, wzm0;
+        if (zl == 0) {
+          tm_ld4x2(cX, cZ, wx0, wz0);
+          wzm0 = ld4(WZM + so);
+        } else {
+          tm_ld4x3(cX + 4u * zl, cZ + 4u * zl, cZ + 4u * (zl - 1), wx0, wz0, wzm0);
+        }
         {
-          float4 wx0;
-          tm_ld4x(cX + 4u * zl, wx0);
           const float xr0 = shr(p0.x), wl0 = shl(wx0.w);
           const float dl0 = shl(xd3(p0, xr0));
           float d30;
@@ -772,10 +811,6 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
           q0 = terms2(q0, p0, pyp, pym, wy0, wym0);
         }
         {
-          float4 wz0, wzm0;
-          tm_ld4x(cZ + 4u * zl, wz0);
-          if (zl == 0) wzm0 = ld4(WZM + so);
-          else tm_ld4x(cZ + 4u * (zl - 1), wzm0);
           q0 = terms2(q0, p0, ld4(Pz + PL + so), ld4(Pz - PL + so), wz0, wzm0);
         }
         if (!G::EXACT && !act) q0 = f4(0.f);
