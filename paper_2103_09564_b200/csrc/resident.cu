@@ -522,11 +522,16 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
       for (int i = 0; i < nv; ++i) s_bred[warp][i] = v[i];
     __syncthreads();
     if (t == 0) {
-      double a0 = 0.0, a1 = 0.0;
+      // four interleaved partial sums (w mod 4), then pairwise: a quarter of the dependent
+      // fp64 add chain of a serial sum, in a fixed order (deterministic, batch-invariant)
+      double b0[4] = {0.0, 0.0, 0.0, 0.0}, b1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
       for (int w = 0; w < NW; ++w) {
-        a0 += s_bred[w][0];
-        if (nv > 1) a1 += s_bred[w][1];
+        b0[w & 3] += s_bred[w][0];
+        if (nv > 1) b1[w & 3] += s_bred[w][1];
       }
+      const double a0 = (b0[0] + b0[1]) + (b0[2] + b0[3]);
+      const double a1 = (b1[0] + b1[1]) + (b1[2] + b1[3]);
       mbar_arrive_expect_tx(&s_bar[bi], CL * 8u * nv);
       const uint32_t slot = sptr(&slots[rank]), bar = sptr(&s_bar[bi]);
       for (int c = 0; c < CL; ++c) {
@@ -537,17 +542,18 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     if (warp == 0) {
       mbar_wait(&s_bar[bi], ph);
       if (t == 0) {
-        double a0 = 0.0, a1 = 0.0;
+        double b0[4] = {0.0, 0.0, 0.0, 0.0}, b1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
         for (int c = 0; c < CL; ++c) {
           if (nv == 1) {
-            a0 += reinterpret_cast<const double*>(slots)[c];
+            b0[c & 3] += reinterpret_cast<const double*>(slots)[c];
           } else {
             const double2 e = reinterpret_cast<const double2*>(slots)[c];
-            a0 += e.x;
-            a1 += e.y;
+            b0[c & 3] += e.x;
+            b1[c & 3] += e.y;
           }
         }
-        s_res = make_double2(a0, a1);
+        s_res = make_double2((b0[0] + b0[1]) + (b0[2] + b0[3]), (b1[0] + b1[1]) + (b1[2] + b1[3]));
       }
     }
     ph ^= 1u;
