@@ -392,6 +392,12 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
  * clusters of 4 planes (latency: twice the SMs per brick -- a single 32^3 brick solves in
  * 0.55 instead of 0.74 ms).  Within one setting results are batch-invariant; across the
  * two they agree to the solver tolerance.
+ * RW_OPT_L2_WORKERS: 1 (default) or 0.  64^3 resident solves from u16 / f32 intensities
+ * (nrhs 1, >= 64 bricks): the 16-CTA clusters fit 7 times (112 SMs); 4-CTA "L2 worker"
+ * clusters on the remaining SMs draw bricks from the same counter and run the resident
+ * kernel's arithmetic operation for operation with the CG state in global memory, so every
+ * brick's outputs are bit-identical whichever cluster solved it (batch-invariant).  The
+ * workers use the streaming r region of the workspace (rw_solve_workspace_bytes).
  * RW_OPT_STREAM_ZC: 0 (default, automatic) or the streaming solver's z-chunk (planes per
  * CTA column tile, 4..4096).  The chunk fixes the fp64 partial-sum tree, so results are
  * bitwise reproducible for a given chunk; different chunks agree to the solver tolerance.
@@ -401,7 +407,7 @@ rw_status rw_hier_segment_labels(const void* vol, rw_dtype dtype, rw_norm nm, rw
  * ---------------------------------------------------------------------------------- */
 enum { RW_OPT_SOLVER = 0, RW_OPT_COSCHED = 1, RW_OPT_RESIDUAL_REPLACE = 2,
        RW_OPT_STREAM_PASSES = 3, RW_OPT_RESIDENT_WIDE = 4, RW_OPT_DEVICE_LOOP = 5,
-       RW_OPT_STREAM_ZC = 6 };
+       RW_OPT_STREAM_ZC = 6, RW_OPT_L2_WORKERS = 7 };
 enum { RW_SOLVER_AUTO = 0, RW_SOLVER_STREAMING = 1, RW_SOLVER_RESIDENT = 2 };
 rw_status rw_set_option(int32_t key, int64_t value);
 int64_t rw_get_option(int32_t key);
@@ -439,7 +445,8 @@ void rw_queue_destroy(rw_queue* q);
  *   launches  out host int64[RW_K_COUNT] or NULL;  ms  out host double[RW_K_COUNT] or NULL.
  * ---------------------------------------------------------------------------------- */
 enum { RW_K_WEIGHTS = 0, RW_K_SETUP = 1, RW_K_PASSA = 2, RW_K_PASSB = 3, RW_K_FINALIZE = 4,
-       RW_K_PYRAMID = 5, RW_K_OTHER = 6, RW_K_RESIDENT = 7, RW_K_HIER = 8, RW_K_COUNT = 9 };
+       RW_K_PYRAMID = 5, RW_K_OTHER = 6, RW_K_RESIDENT = 7, RW_K_HIER = 8, RW_K_L2RES = 9,
+       RW_K_COUNT = 10 };
 rw_status rw_profile_enable(int32_t on);
 rw_status rw_profile_read(int64_t* launches, double* ms);
 

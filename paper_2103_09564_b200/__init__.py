@@ -11,4 +11,5 @@ from .api import (  # noqa: F401
     solver, resident_available, hier_segment, hier_segment_labels, hier_segment_ooc, stream_passes,
     set_stream_passes, get_stream_passes, set_resident_wide, get_resident_wide,
     set_device_loop, get_device_loop, device_loop, set_stream_zc, get_stream_zc, stream_zc,
+    set_l2_workers, get_l2_workers, l2_workers,
 )

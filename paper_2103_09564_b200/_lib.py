@@ -84,7 +84,7 @@ SIGNATURES = {
 }
 
 KERNEL_CLASSES = ["weights", "setup", "passA", "passB", "finalize", "pyramid", "other",
-                  "resident", "hier"]
+                  "resident", "hier", "l2res"]
 
 
 def header_symbols(path: str = HEADER):

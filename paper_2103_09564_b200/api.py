@@ -132,6 +132,26 @@ def stream_passes(n):
         set_stream_passes(old)
 
 
+def set_l2_workers(on):
+    """rw_set_option(RW_OPT_L2_WORKERS): bit-identical 4-CTA worker clusters on the SMs the 64^3
+    resident clusters leave free (1, default) or not (0)."""
+    check(lib().rw_set_option(7, int(bool(on))), "rw_set_option")
+
+
+def get_l2_workers():
+    return bool(lib().rw_get_option(7))
+
+
+@contextlib.contextmanager
+def l2_workers(on):
+    old = get_l2_workers()
+    set_l2_workers(on)
+    try:
+        yield
+    finally:
+        set_l2_workers(old)
+
+
 def set_stream_zc(zc):
     """rw_set_option(RW_OPT_STREAM_ZC): 0 (default, automatic) or the streaming solver's
     z-chunk in planes (4..4096)."""

@@ -80,6 +80,7 @@ int g_rr = 0;
 int g_passes = 1;   // RW_OPT_STREAM_PASSES
 int g_res_wide = 0; // RW_OPT_RESIDENT_WIDE
 int g_zc = 0;       // RW_OPT_STREAM_ZC (0 = auto)
+int g_l2w = 1;      // RW_OPT_L2_WORKERS
 int g_dev_loop = 1; // RW_OPT_DEVICE_LOOP
 
 rw_status fail(rw_status st, const char* fmt, ...) {
@@ -135,7 +136,8 @@ rw::Plan make_plan(int B, rw_dims d, int R) {
   // 256 threads for every nrhs: measured on cfg4 (3 RHS, 256^3) 1.31 s with 128-thread
   // tiles vs 0.99 s with 256 (pass A keeps 2 RHS per CTA within the shared-memory budget)
   P.threads = 256;
-  P.tpx = d.nx / 4 < 16 ? d.nx / 4 : 16;
+  const int tpx_max = env_int("RW_TPX", 16);   // A/B knob: threads along x per tile
+  P.tpx = d.nx / 4 < tpx_max ? d.nx / 4 : tpx_max;
   P.TX = 4 * P.tpx;
   P.TY = P.threads / P.tpx < 128 ? P.threads / P.tpx : 128;
   P.hx = P.TX < d.nx ? 4 : 0;
@@ -348,17 +350,23 @@ int cosched_bricks(int B, rw_dims d, int nrhs, bool weights_given, size_t ws_byt
   return ws_bytes >= main_bytes + extra ? Bs : 0;   // a smaller workspace: no co-scheduling
 }
 
+// second stream + fork / join events of the calling thread on the current device (created on
+// first use; a solve that forks joins before returning, so reuse across calls is ordered)
 rw_status cosched_handles(cudaStream_t* s2, cudaEvent_t* fork, cudaEvent_t* join) {
-  static cudaStream_t st = nullptr;
-  static cudaEvent_t ef = nullptr, ej = nullptr;
-  if (!st) {
-    RW_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    RW_CK(cudaEventCreateWithFlags(&ef, cudaEventDisableTiming));
-    RW_CK(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+  struct H { cudaStream_t st = nullptr; cudaEvent_t ef = nullptr, ej = nullptr; };
+  static thread_local H h[64];
+  int dev = 0;
+  RW_CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(RW_EINVAL, "co-scheduling: device index out of range");
+  H& x = h[dev];
+  if (!x.st) {
+    RW_CK(cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking));
+    RW_CK(cudaEventCreateWithFlags(&x.ef, cudaEventDisableTiming));
+    RW_CK(cudaEventCreateWithFlags(&x.ej, cudaEventDisableTiming));
   }
-  *s2 = st;
-  *fork = ef;
-  *join = ej;
+  *s2 = x.st;
+  *fork = x.ef;
+  *join = x.ej;
   return RW_OK;
 }
 
@@ -539,9 +547,23 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
     const int Bs = cosched_bricks(P.B, d, nrhs, W != nullptr, ws_bytes, Lw.total);
     A.nb = P.B - Bs;
     A.nsolve = P.R * A.nb;   // (rhs, brick) pairs: each rhs is its own resident solve
+    // L2 workers (RW_OPT_L2_WORKERS, resident.cu k_l2res): bit-identical 4-CTA clusters on the
+    // SMs the 16-CTA clusters leave free, drawing from the same brick counter; their CG state
+    // goes to the streaming r region of the workspace (unused by the resident solver)
+    int nw = 0;
+    rw::L2Args L2{};
+    if (g_l2w && Bs == 0 && fused && d.nx == 64 && d.ny == 64 && d.nz == 64 && P.R == 1 &&
+        P.B >= 64 && !g_res_wide) {
+      nw = rw::l2res_workers(rw::resident_clusters64(vm_vol));
+      const size_t per = rw::l2res_bytes_per_worker();
+      nw = (int)std::min<size_t>((size_t)nw, (Lw.p - Lw.r) / per);
+      L2.buf = reinterpret_cast<float*>(ws + Lw.r);
+      L2.stride = (long long)(per / sizeof(float));
+      L2.rmin = env_int("RW_L2_RMIN", 48);
+    }
     cudaStream_t s2 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
-    if (Bs > 0) {
+    if (Bs > 0 || nw > 0) {
       rw_status cs = cosched_handles(&s2, &fork, &join);
       if (cs != RW_OK) return cs;
       RW_CK(cudaEventRecord(fork, s));
@@ -557,6 +579,11 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
     }
 #endif
     RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, g_res_wide, s));
+    if (nw > 0) {
+      RW_TIMED(RW_K_L2RES, s2, 1, rw::launch_l2res(A, L2, nw, s2));
+      RW_CK(cudaEventRecord(join, s2));
+      RW_CK(cudaStreamWaitEvent(s, join, 0));
+    }
 #ifdef RW_RES_TIMING
     if (A.dbg) {
       long long h[128];
@@ -684,6 +711,11 @@ rw_status rw_set_option(int32_t key, int64_t value) {
     g_res_wide = (int)value;
     return RW_OK;
   }
+  if (key == RW_OPT_L2_WORKERS) {
+    if (value != 0 && value != 1) return fail(RW_EINVAL, "rw_set_option: L2 workers must be 0 or 1");
+    g_l2w = (int)value;
+    return RW_OK;
+  }
   if (key == RW_OPT_STREAM_ZC) {
     if (value != 0 && (value < 4 || value > 4096)) return fail(RW_EINVAL, "rw_set_option: z chunk must be 0 or 4..4096");
     g_zc = (int)value;
@@ -710,7 +742,7 @@ int64_t rw_get_option(int32_t key) {
   return key == RW_OPT_SOLVER ? g_solver : key == RW_OPT_COSCHED ? g_cosched_pm
          : key == RW_OPT_RESIDUAL_REPLACE ? g_rr : key == RW_OPT_STREAM_PASSES ? g_passes
          : key == RW_OPT_RESIDENT_WIDE ? g_res_wide : key == RW_OPT_DEVICE_LOOP ? g_dev_loop
-         : key == RW_OPT_STREAM_ZC ? g_zc : -1;
+         : key == RW_OPT_STREAM_ZC ? g_zc : key == RW_OPT_L2_WORKERS ? g_l2w : -1;
 }
 
 int32_t rw_resident_available(rw_dims d, int32_t nrhs) {

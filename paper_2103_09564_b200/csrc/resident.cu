@@ -1016,4 +1016,378 @@ cudaError_t launch_resident(int nx, const ResArgs& A, int wide, cudaStream_t s) 
   return launch_shape<VM_STORED>(nx, A, wide, s);
 }
 
+
+// ---------------------------------------------------------------------------------------
+// L2 workers (RW_OPT_L2_WORKERS): the 64^3 16-CTA clusters of k_resident fit 7 times on a
+// B200 (112 SMs); the other 36 SMs would idle.  k_l2res runs on them, drawing bricks from the
+// SAME counter, and reproduces k_resident<64, 16> operation for operation: a 4-CTA cluster
+// plays the 16 cluster ranks (4 virtual ranks per CTA, the same 512-thread map per virtual
+// rank), every per-voxel expression, every per-thread accumulation order, the warp shuffle
+// trees, the four-way interleaved warp and rank sums and the decisions are k_resident's.  The
+// CG state lives in global memory (L2-resident: 7 arrays x 1 MB per worker cluster) instead of
+// shared / tensor memory and registers.  A brick's bits therefore do not depend on which
+// kind of cluster solved it (tested bitwise), so batch invariance holds.
+// Halo planes and -y / -z weights come straight from the neighbours' global arrays (the
+// resident kernel's -z weight of plane 0 and -y weight of row 2j are the +z / +y weights of
+// the plane / row below, the same grady() expression on the same operands).  Step 1 -> 2
+// needs every p update of the brick visible: a cluster barrier (release / acquire).
+namespace l2 {
+constexpr int N = 64, CL = 16, CW = 4, VPC = CL / CW, ZS = 4, QX = 16, NI = 8, T = 512, NW = 16;
+constexpr int PL = N * N;
+}  // namespace l2
+
+template <int VM>
+__global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
+  using namespace res;
+  using namespace l2;
+  __shared__ __align__(8) uint64_t s_bar[4];          // [1] pq, [2] (rz, rr), [3] brick-start
+  __shared__ __align__(16) double s_pq[CL];
+  __shared__ __align__(16) double2 s_rz[CL];
+  __shared__ __align__(16) double2 s_ini[CL];
+  __shared__ double s_bred[VPC][NW][2];
+  __shared__ double2 s_res;
+  __shared__ int s_brick;
+  const int t = threadIdx.x, warp = t >> 5, lane_ = t & 31;
+  const int rank = cl_rank();
+  const int qx = t % QX, j = t / QX;                   // Cfg<64, 16>: EXACT map
+  const int wid = blockIdx.x / CW;                     // worker cluster
+  const long long n = (long long)PL * N;
+  float* const Dv = Wk.buf + (long long)wid * Wk.stride;
+  float* const Wx = Dv + n;
+  float* const Wy = Wx + n;
+  float* const Wz = Wy + n;
+  float* const Rg = Wz + n;
+  float* const Qg = Rg + n;
+  float* const Pp = Qg + n;
+  if (t == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&s_bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  cl_arrive();
+  cl_wait();
+  const uint32_t brk = sptr(&s_brick);
+  uint32_t ph1 = 0, ph2 = 0, ph3 = 0;
+  auto shl = [&](float v) { return __shfl_up_sync(0xffffffffu, v, 1, QX); };
+  auto shr = [&](float v) { return __shfl_down_sync(0xffffffffu, v, 1, QX); };
+  // brick-local index of item `it` of virtual rank vr (plane zl = it / 2, row 2j + it % 2)
+  auto gi = [&](int vr, int it) {
+    return (long long)(vr * ZS + it / 2) * PL + (2 * j + (it & 1)) * N + 4 * qx;
+  };
+  // k_resident's cluster_sum over the 16 (virtual) ranks: per virtual rank a warp xor tree,
+  // the four-way interleaved warp sum -> rank partial, st.async of the VPC partials into slot
+  // (rank * VPC + v) of every CTA, the four-way interleaved sum of the 16 slots in rank order
+  auto cluster_sum = [&](double (*v)[2], int nv, int bi, auto* slots, uint32_t& ph) -> double2 {
+#pragma unroll
+    for (int vv = 0; vv < VPC; ++vv)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        if (i < nv) v[vv][i] = warp_sum(v[vv][i]);
+    if ((t & 31) == 0)
+      for (int vv = 0; vv < VPC; ++vv)
+        for (int i = 0; i < nv; ++i) s_bred[vv][warp][i] = v[vv][i];
+    __syncthreads();
+    if (t == 0) {
+      mbar_arrive_expect_tx(&s_bar[bi], CL * 8u * nv);
+      for (int vv = 0; vv < VPC; ++vv) {
+        double b0[4] = {0.0, 0.0, 0.0, 0.0}, b1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          b0[w & 3] += s_bred[vv][w][0];
+          if (nv > 1) b1[w & 3] += s_bred[vv][w][1];
+        }
+        const double a0 = (b0[0] + b0[1]) + (b0[2] + b0[3]);
+        const double a1 = (b1[0] + b1[1]) + (b1[2] + b1[3]);
+        const uint32_t slot = sptr(&slots[rank * VPC + vv]), bar = sptr(&s_bar[bi]);
+        for (int c = 0; c < CW; ++c) {
+          if (nv == 1) st_async_f64(mapa(slot, c), a0, mapa(bar, c));
+          else st_async_f64x2(mapa(slot, c), a0, a1, mapa(bar, c));
+        }
+      }
+    }
+    if (warp == 0) {
+      mbar_wait(&s_bar[bi], ph);
+      if (t == 0) {
+        double b0[4] = {0.0, 0.0, 0.0, 0.0}, b1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < CL; ++c) {
+          if (nv == 1) {
+            b0[c & 3] += reinterpret_cast<const double*>(slots)[c];
+          } else {
+            const double2 e = reinterpret_cast<const double2*>(slots)[c];
+            b0[c & 3] += e.x;
+            b1[c & 3] += e.y;
+          }
+        }
+        s_res = make_double2((b0[0] + b0[1]) + (b0[2] + b0[3]), (b1[0] + b1[1]) + (b1[2] + b1[3]));
+      }
+    }
+    ph ^= 1u;
+    __syncthreads();
+    return s_res;
+  };
+
+  while (true) {
+    // ---- next brick from the resident kernel's counter; stop while Wk.rmin bricks remain
+    // (those go to the faster resident clusters: a worker brick takes several of theirs)
+    if (rank == 0 && t == 0) {
+      int c = *reinterpret_cast<volatile int*>(A.next);
+      int nb = A.nsolve;
+      while (c < A.nsolve - Wk.rmin) {
+        const int o = atomicCAS(A.next, c, c + 1);
+        if (o == c) { nb = c; break; }
+        c = o;
+      }
+      for (int cc = 0; cc < CW; ++cc) st_cl_u32(mapa(brk, cc), (uint32_t)nb);
+    }
+    cl_arrive();
+    cl_wait();
+    const int b = s_brick;
+    if (b >= A.nsolve) break;
+    float* const X = A.x + (long long)b * n;
+
+    // ---- brick load: k_resident's fused assembly, per virtual rank
+    uint32_t fixm[VPC];
+    double iacc[VPC][5];
+    using TV = typename VolT<VM>::T;
+#pragma unroll
+    for (int vv = 0; vv < VPC; ++vv) {
+      const int vr = rank * VPC + vv;
+      fixm[vv] = 0u;
+      for (int i = 0; i < 5; ++i) iacc[vv][i] = 0.0;
+#pragma unroll
+      for (int it = 0; it < NI; ++it) {
+        const int zl = it / 2, y = 2 * j + (it & 1);
+        const QuadOut o = assemble_quad<TV, N, N>(A, (long long)b * n, 0, vr * ZS + zl, y, 4 * qx, iacc[vv]);
+        fixm[vv] |= o.fm << (4 * it);
+        const long long g = gi(vr, it);
+        st4(Dv + g, o.dv);
+        st4(Wx + g, o.wx);
+        st4(Wy + g, o.wy);
+        st4(Wz + g, o.wz);
+        st4(X + g, o.xv);
+        st4(Rg + g, o.rv);
+        st4(Pp + g, f4(0.f));
+      }
+    }
+    double nu, bb, nf, rz, rrn;
+    {
+      double v0[VPC][2], v1[VPC][2], v2[VPC][2];
+      for (int vv = 0; vv < VPC; ++vv) {
+        v0[vv][0] = iacc[vv][4]; v0[vv][1] = 0.0;
+        v1[vv][0] = iacc[vv][2]; v1[vv][1] = iacc[vv][3];
+        v2[vv][0] = iacc[vv][0]; v2[vv][1] = iacc[vv][1];
+      }
+      nu = cluster_sum(v0, 1, 1, s_pq, ph1).x;
+      const double2 a1 = cluster_sum(v1, 2, 3, s_ini, ph3);
+      bb = a1.x;
+      nf = a1.y;
+      const double2 a2 = cluster_sum(v2, 2, 2, s_rz, ph2);
+      rz = a2.x;
+      rrn = a2.y;
+    }
+
+    int st = ST_ACTIVE, k = 0;
+    double rz_prev = 0.0, pq_prev = 0.0;
+    float al = 0.f;
+    const double t2 = (double)A.C.tol * (double)A.C.tol;
+    while (true) {
+      if (k == 0) {
+        if (nf == 0.0 || nu == 0.0) st = ST_TRIVIAL;
+        else if (bb == 0.0) st = ST_ZERO_B;
+      } else if (!(pq_prev > 0.0) || !isfinite(rz) || !isfinite(pq_prev)) {
+        st = ST_BREAKDOWN;
+      }
+      if (st == ST_ACTIVE) {
+        const bool conv = (A.C.tol_mode == 0) ? (rrn <= t2 * bb) : (rrn <= t2);
+        if (conv) st = ST_CONVERGED;
+        else if (k >= A.C.max_iter) st = ST_MAXITER;
+      }
+      if (st != ST_ACTIVE) break;
+      const float be = k > 0 ? (float)(rz / rz_prev) : 0.f;
+
+      // ---- step 1: x += alpha p (lagged); p = dinv r + beta p
+#pragma unroll
+      for (int vv = 0; vv < VPC; ++vv) {
+        const int vr = rank * VPC + vv;
+#pragma unroll
+        for (int it = 0; it < NI; ++it) {
+          const long long g = gi(vr, it);
+          const float4 dv = ld4(Dv + g), po = ld4(Pp + g), r = ld4(Rg + g);
+          if (k > 0) st4(X + g, fma4p(al, po, ld4(X + g)));
+          st4(Pp + g, pnew4p(be, po, dv, r));
+        }
+      }
+      cl_arrive();        // every p update of the brick visible to the cluster (global memory)
+      cl_wait();
+
+      // ---- step 2: q = L_UU p, per-thread p.q (planes 1, 2, then 0, 3 as k_resident)
+      double v1[VPC][2];
+#pragma unroll
+      for (int vv = 0; vv < VPC; ++vv) {
+        const int vr = rank * VPC + vv;
+        float2 apq0 = make_float2(0.f, 0.f), apq1 = make_float2(0.f, 0.f);
+        auto spmv = [&](int zl) {
+          const int z = vr * ZS + zl;
+          const long long so = 2 * j * N + 4 * qx;
+          const float* Pz = Pp + (long long)z * PL;
+          const float4 p0 = ld4(Pz + so), p1 = ld4(Pz + so + N);
+          const float4 wx0 = ld4(Wx + (long long)z * PL + so), wx1 = ld4(Wx + (long long)z * PL + so + N);
+          const float4 wz0 = ld4(Wz + (long long)z * PL + so), wz1 = ld4(Wz + (long long)z * PL + so + N);
+          const float4 wzm0 = z > 0 ? ld4(Wz + (long long)(z - 1) * PL + so) : f4(0.f);
+          const float4 wzm1 = z > 0 ? ld4(Wz + (long long)(z - 1) * PL + so + N) : f4(0.f);
+          float4 q0, q1;
+          {
+            const float xr0 = shr(p0.x), xr1 = shr(p1.x);
+            const float wl0 = shl(wx0.w), wl1 = shl(wx1.w);
+            const float dl0 = shl(xd3(p0, xr0)), dl1 = shl(xd3(p1, xr1));
+            float d30, d31;
+            q0 = xterms(p0, xr0, dl0, wx0, qx > 0 ? wl0 : 0.f, d30);
+            q1 = xterms(p1, xr1, dl1, wx1, qx > 0 ? wl1 : 0.f, d31);
+          }
+          {
+            const float* Wyz = Wy + (long long)z * PL;
+            const float4 wy0 = ld4(Wyz + so), wy1 = ld4(Wyz + so + N);
+            const float4 pym = j > 0 ? ld4(Pz + so - N) : f4(0.f);
+            const float4 pyp = j < N / 2 - 1 ? ld4(Pz + so + 2 * N) : f4(0.f);
+            const float4 wym0 = j > 0 ? ld4(Wyz + so - N) : f4(0.f);
+            q0 = terms2(q0, p0, p1, pym, wy0, wym0);
+            q1 = terms2(q1, p1, pyp, p0, wy1, wy0);
+          }
+          {
+            const float4 pzp0 = z + 1 < N ? ld4(Pz + PL + so) : f4(0.f);
+            const float4 pzp1 = z + 1 < N ? ld4(Pz + PL + so + N) : f4(0.f);
+            const float4 pzm0 = z > 0 ? ld4(Pz - PL + so) : f4(0.f);
+            const float4 pzm1 = z > 0 ? ld4(Pz - PL + so + N) : f4(0.f);
+            q0 = terms2(q0, p0, pzp0, pzm0, wz0, wzm0);
+            q1 = terms2(q1, p1, pzp1, pzm1, wz1, wzm1);
+          }
+          st4(Qg + (long long)z * PL + so, q0);
+          st4(Qg + (long long)z * PL + so + N, q1);
+          dot4acc(p0, q0, apq0, apq1);
+          dot4acc(p1, q1, apq0, apq1);
+        };
+        spmv(1);
+        spmv(2);
+        spmv(0);
+        spmv(3);
+        v1[vv][0] = (double)hsum(apq0, apq1);
+        v1[vv][1] = 0.0;
+      }
+      const double pq = cluster_sum(v1, 1, 1, s_pq, ph1).x;
+      al = (pq > 0.0 && isfinite(pq)) ? (float)(rz / pq) : 0.f;
+
+      // ---- step 3: r -= alpha q; partials r.(dinv r), r.r
+      double v2[VPC][2];
+#pragma unroll
+      for (int vv = 0; vv < VPC; ++vv) {
+        const int vr = rank * VPC + vv;
+        float2 az0 = make_float2(0.f, 0.f), az1 = az0, ar0 = az0, ar1 = az0;
+#pragma unroll
+        for (int it = 0; it < NI; ++it) {
+          const long long g = gi(vr, it);
+          const float4 dv = ld4(Dv + g);
+          float4 rn = fma4p(-al, ld4(Qg + g), ld4(Rg + g));
+          if (dv.x == 0.f) rn.x = 0.f;
+          if (dv.y == 0.f) rn.y = 0.f;
+          if (dv.z == 0.f) rn.z = 0.f;
+          if (dv.w == 0.f) rn.w = 0.f;
+          st4(Rg + g, rn);
+          const float2 z0 = __fmul2_rn(lo2(dv), lo2(rn)), z1 = __fmul2_rn(hi2(dv), hi2(rn));
+          az0 = __ffma2_rn(lo2(rn), z0, az0);
+          az1 = __ffma2_rn(hi2(rn), z1, az1);
+          dot4acc(rn, rn, ar0, ar1);
+        }
+        v2[vv][0] = (double)hsum(az0, az1);
+        v2[vv][1] = (double)hsum(ar0, ar1);
+      }
+      const double2 srr = cluster_sum(v2, 2, 2, s_rz, ph2);
+      rz_prev = rz;
+      pq_prev = pq;
+      rz = srr.x;
+      rrn = srr.y;
+      ++k;
+    }
+
+    // ---- finalise (row a6), as k_resident
+    const bool upd = (st == ST_CONVERGED || st == ST_MAXITER) && k >= 1;
+#pragma unroll
+    for (int vv = 0; vv < VPC; ++vv) {
+      const int vr = rank * VPC + vv;
+#pragma unroll
+      for (int it = 0; it < NI; ++it) {
+        const long long g = gi(vr, it);
+        float4 xv = ld4(X + g);
+        if (upd && al != 0.f) xv = fma4p(al, ld4(Pp + g), xv);
+        const uint32_t fm = fixm[vv] >> (4 * it);
+        float o[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (fm & (1u << e)) continue;
+          o[e] = st == ST_ZERO_B ? 0.f : fminf(fmaxf(o[e], 0.f), 1.f);
+        }
+        st4(X + g, make_float4(o[0], o[1], o[2], o[3]));
+        if (A.labels)
+          *reinterpret_cast<uchar4*>(A.labels + (long long)b * n + g) =
+              make_uchar4(o[0] > 0.5f, o[1] > 0.5f, o[2] > 0.5f, o[3] > 0.5f);
+      }
+    }
+    if (rank == 0 && t == 0) {
+      A.status[b] = st;
+      A.iters[b] = (st == ST_TRIVIAL || st == ST_ZERO_B) ? 0 : k;
+      if (A.resid) {
+        double res = 0.0;
+        if (st == ST_CONVERGED || st == ST_MAXITER || st == ST_BREAKDOWN) {
+          res = sqrt(rrn);
+          if (A.C.tol_mode == 0) res = bb > 0.0 ? res / sqrt(bb) : 0.0;
+        }
+        A.resid[b] = (float)res;
+      }
+    }
+    // the brick's global arrays are reused by the next brick: everyone done reading them
+    cl_arrive();
+    cl_wait();
+  }
+}
+
+// number of worker clusters that fit the SMs the 64^3 resident clusters leave free
+int l2res_workers(int ncl_res) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int freesm = sms - 16 * ncl_res;
+  return freesm > 0 ? freesm / l2::CW : 0;
+}
+
+size_t l2res_bytes_per_worker() { return (size_t)7 * l2::PL * l2::N * sizeof(float); }
+
+template <int VM>
+static cudaError_t launch_l2res_vm(const ResArgs& A, const L2Args& W, int nw, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nw * l2::CW);
+  cfg.blockDim = dim3(l2::T);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = l2::CW;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_l2res<VM>, A, W);
+}
+
+cudaError_t launch_l2res(const ResArgs& A, const L2Args& W, int nw, cudaStream_t s) {
+  if (nw <= 0) return cudaSuccess;
+  if (A.vdt == VM_U16) return launch_l2res_vm<VM_U16>(A, W, nw, s);
+  if (A.vdt == VM_F32) return launch_l2res_vm<VM_F32>(A, W, nw, s);
+  return cudaErrorNotSupported;
+}
+
+int resident_clusters64(int vdt) {
+  if (vdt == VM_U16) return resident_clusters<64, 16, VM_U16>();
+  if (vdt == VM_F32) return resident_clusters<64, 16, VM_F32>();
+  return 0;
+}
+
 }  // namespace rw

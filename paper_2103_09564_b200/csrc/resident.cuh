@@ -32,6 +32,17 @@ struct ResArgs {
                        // in a caller-provided buffer; null in the library
 };
 
+// L2 workers (resident.cu k_l2res): storage of the worker clusters' CG state in global memory
+struct L2Args {
+  float* buf;          // nw * stride floats
+  long long stride;    // floats per worker cluster (7 arrays of the brick)
+  int rmin;            // a worker takes a brick only while more than rmin remain undrawn
+};
+int l2res_workers(int ncl_res);
+size_t l2res_bytes_per_worker();
+int resident_clusters64(int vdt);
+cudaError_t launch_l2res(const ResArgs& A, const L2Args& W, int nw, cudaStream_t s);
+
 // vdt: the VM_* mode the launch will use (VM_U16 / VM_F32 fused from intensities, else
 // VM_STORED); wide: RW_OPT_RESIDENT_WIDE
 bool resident_supported(int nx, int ny, int nz, int R, int vdt, int wide);

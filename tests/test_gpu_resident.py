@@ -210,3 +210,17 @@ def test_resident_multi_rhs_bitwise_and_linearity():
         if r == 0:
             assert np.array_equal(s["labels"], o["labels"])   # labels = prob[0] > 0.5
     assert np.abs(o["prob"][0] + o["prob"][1] - 1.0).max() <= 2e-5
+
+
+def test_l2_workers_bitwise_batch_invariant():
+    """RW_OPT_L2_WORKERS (default on): 4-CTA worker clusters on the SMs the 64^3 16-CTA
+    clusters leave free reproduce the resident arithmetic from global memory, so the whole
+    batch is bit-identical with and without them, whichever cluster solved a brick."""
+    p = wl.cfg2(bricks=list(range(0, 512, 4)))          # 128 bricks: workers take some
+    on = resident(p)
+    with rwb.l2_workers(False):
+        off = resident(p)
+    for k in ("prob", "iters", "resid", "status", "labels"):
+        assert np.array_equal(on[k], off[k]), k
+    alone = resident(p.subset([77]))
+    assert np.array_equal(alone["prob"][0, 0], on["prob"][0, 77])
