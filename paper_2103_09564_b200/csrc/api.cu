@@ -561,6 +561,13 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       L2.stride = (long long)(per / sizeof(float));
       L2.rmin = env_int("RW_L2_RMIN", 48);
     }
+    // experiment knobs (tools/l2w_ab.py): RW_L2_ONLY=1 runs the worker clusters alone on all
+    // bricks (RW_L2_NW of them) -- measures one worker kind in isolation
+    const bool l2only = nw > 0 && env_int("RW_L2_ONLY", 0) != 0;
+    if (l2only) {
+      nw = std::min<size_t>((size_t)env_int("RW_L2_NW", nw), (Lw.p - Lw.r) / rw::l2res_bytes_per_worker());
+      L2.rmin = 0;
+    }
     cudaStream_t s2 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     if (Bs > 0 || nw > 0) {
@@ -578,7 +585,7 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       A.dbg = dbg;
     }
 #endif
-    RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, g_res_wide, s));
+    if (!l2only) RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, g_res_wide, s));
     if (nw > 0) {
       RW_TIMED(RW_K_L2RES, s2, 1, rw::launch_l2res(A, L2, nw, s2));
       RW_CK(cudaEventRecord(join, s2));
