@@ -591,7 +591,9 @@ def run_b200(args, rank, world, local_rank):
                          "alg_bytes_per_voxel_iter": SMEM_BYTES_RES,
                          "ncu_shared_wavefronts_pct_of_peak": 40.0,
                          "note": "LDS/STS bytes of one iteration counted in the SASS; 112 of 148 "
-                                 "SMs host 16-CTA clusters (DESIGN.md 5b)"}
+                                 "SMs host 16-CTA clusters, the other 36 bit-identical L2 worker "
+                                 "clusters (k_l2res, state in L2, DESIGN.md 5b); achieved = all "
+                                 "voxel-iterations of the step over the resident launch"}
         roofline = {"bound": "alu", "kernel": "resident", "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "TFLOP/s", "frac": achieved / peak,
                     "traffic": ncu_traffic("resident"),

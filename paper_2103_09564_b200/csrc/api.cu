@@ -568,6 +568,16 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       nw = std::min<size_t>((size_t)env_int("RW_L2_NW", nw), (Lw.p - Lw.r) / rw::l2res_bytes_per_worker());
       L2.rmin = 0;
     }
+    const bool l2dbg = nw > 0 && env_int("RW_DEBUG_L2W", 0) != 0;
+    if (l2dbg) {   // debug: count the workers' bricks (ctr[0] is the streaming loop's, unused here)
+      L2.nsolved = Bf.ctr;
+      RW_CK(cudaMemsetAsync(Bf.ctr, 0, sizeof(int), s));
+    }
+    const bool l2hold = l2only && env_int("RW_L2_HOLD", 0) != 0;
+    if (l2hold) {   // experiment: idle clusters on the resident SMs (launched after the fork)
+      L2.done = Bf.ctr + 1;
+      RW_CK(cudaMemsetAsync(Bf.ctr + 1, 0, sizeof(int), s));
+    }
     cudaStream_t s2 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     if (Bs > 0 || nw > 0) {
@@ -585,11 +595,18 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       A.dbg = dbg;
     }
 #endif
+    if (l2hold) RW_CK(rw::launch_hold16(rw::resident_clusters64(vm_vol), Bf.ctr + 1, 4 * nw, s));
     if (!l2only) RW_TIMED(RW_K_RESIDENT, s, 1, rw::launch_resident(d.nx, A, g_res_wide, s));
     if (nw > 0) {
       RW_TIMED(RW_K_L2RES, s2, 1, rw::launch_l2res(A, L2, nw, s2));
       RW_CK(cudaEventRecord(join, s2));
       RW_CK(cudaStreamWaitEvent(s, join, 0));
+    }
+    if (l2dbg) {
+      int h = 0;
+      RW_CK(cudaMemcpyAsync(&h, Bf.ctr, sizeof h, cudaMemcpyDeviceToHost, s));
+      RW_CK(cudaStreamSynchronize(s));
+      fprintf(stderr, "[l2w] workers %d solved %d of %d bricks (rmin %d)\n", nw, h, A.nsolve, L2.rmin);
     }
 #ifdef RW_RES_TIMING
     if (A.dbg) {

@@ -1333,6 +1333,7 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
       }
     }
     if (rank == 0 && t == 0) {
+      if (Wk.nsolved) atomicAdd(Wk.nsolved, 1);
       A.status[b] = st;
       A.iters[b] = (st == ST_TRIVIAL || st == ST_ZERO_B) ? 0 : k;
       if (A.resid) {
@@ -1348,6 +1349,45 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
     cl_arrive();
     cl_wait();
   }
+  if (Wk.done && t == 0) atomicAdd(Wk.done, 1);
+}
+
+// experiment (RW_L2_HOLD): occupy the SMs of the resident clusters without any traffic
+__global__ void __launch_bounds__(512, 1) k_hold16(int* done, int target) {
+  extern __shared__ float hs_[];
+  if (threadIdx.x == 0) {
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (*reinterpret_cast<volatile int*>(done) < target) {
+      __nanosleep(2000);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 5000000000ull) break;
+    }
+    hs_[0] = 0.f;
+  }
+  __syncthreads();
+}
+
+cudaError_t launch_hold16(int ncl, int* done, int target, cudaStream_t s) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_hold16, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024);
+    cudaFuncSetAttribute(k_hold16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    init = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncl * 16);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = 180 * 1024;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 16;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_hold16, done, target);
 }
 
 // number of worker clusters that fit the SMs the 64^3 resident clusters leave free

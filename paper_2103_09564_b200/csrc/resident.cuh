@@ -37,7 +37,12 @@ struct L2Args {
   float* buf;          // nw * stride floats
   long long stride;    // floats per worker cluster (7 arrays of the brick)
   int rmin;            // a worker takes a brick only while more than rmin remain undrawn
+  int* nsolved;        // debug (RW_DEBUG_L2W): bricks solved by the workers, or null
+  int* done;           // experiment (RW_L2_HOLD): worker CTAs count themselves out here, or null
 };
+// experiment (RW_L2_HOLD): idle 16-CTA clusters holding the resident kernel's SMs until
+// `target` worker CTAs have exited (or ~5 s)
+cudaError_t launch_hold16(int ncl, int* done, int target, cudaStream_t s);
 int l2res_workers(int ncl_res);
 size_t l2res_bytes_per_worker();
 int resident_clusters64(int vdt);
