@@ -633,7 +633,7 @@ def run_b200(args, rank, world, local_rank):
                      "gpu_launches": int(sum(v[0] for v in sprof.values()))}
 
     # ---------------- end to end through the API with host buffers ----------------
-    # rw_solve_bricks_host: pinned host inputs -> chunked H2D / solve / D2H pipeline -> host
+    # rw_solve_bricks_host: pinned host inputs -> H2D / solve / D2H pipeline -> host
     # fp32 probabilities + labels + iterations (the copies are inside the timed region,
     # overlapped with the solve).  Measured twice: with the fp32 probabilities copied back
     # (the headline e2e: rw_solve_bricks' output) and with labels only.
@@ -674,10 +674,14 @@ def run_b200(args, rank, world, local_rank):
         return {"value": work_all / (ems / args.steps / 1000.0), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": ems / args.steps,
-                "api": "rw_solve_bricks_host (pinned host buffers, chunked H2D/solve/D2H overlap)",
+                "api": ("rw_solve_bricks_host (pinned host buffers; one persistent resident "
+                        "launch over the batch, chunks streamed H2D / D2H through a device ring "
+                        "with ready / done flags)" if solver_used == "resident" else
+                        "rw_solve_bricks_host (pinned host buffers, chunked H2D/solve/D2H "
+                        "overlap)"),
                 "returns": "fp32 prob + u8 labels + iters/resid/status" if with_prob
                            else "u8 labels + iters/resid/status",
-                "chunk": args.e2e_chunk or -(-BATCH // 32)}
+                "chunk": args.e2e_chunk or -(-BATCH // (64 if solver_used == "resident" else 32))}
 
     e2e = e2e_run(True)
     e2e_labels = e2e_run(False)

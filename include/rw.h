@@ -165,12 +165,17 @@ rw_status rw_solve_bricks(int32_t batch, rw_dims d, const void* vol, rw_dtype dt
  * rw_solve_bricks_host -- rw_solve_bricks (nrhs = 1, weights from vol) on HOST buffers with
  *   the transfers pipelined against the solve ("H2D on a copy stream
  *   overlaps compute on the compute stream (events). Results go D2H"; P:105 brick-wise
- *   loading).  The batch is cut into chunks of `chunk` bricks (0: batch/32 rounded up):
- *   chunk c+2's inputs go host->device on a copy stream while chunk c is solved and chunk
- *   c-1's results go device->host on a second copy stream.  Chunk solves alternate between
- *   two compute streams and two solve workspaces, so chunk c+1's resident clusters start on
- *   the SMs chunk c leaves idle in its tail.  Device memory is O(chunk): three-slot rings of
- *   input and output chunks, two chunk workspaces, per-brick scalars of the batch.
+ *   loading).  The batch is cut into chunks of `chunk` bricks (0: batch/32 rounded up).
+ *   Resident-solver shapes (64^3 / 40^3 / 32^3 bricks, u16 or f32 intensities, solver not
+ *   forced to streaming): ONE persistent resident launch (plus the L2 worker clusters) covers
+ *   the whole batch while the chunks stream through a device ring of min(nchunks, 16) chunk
+ *   slots: the H2D copy stream writes chunk c's inputs and then a 4-byte ready flag, the
+ *   clusters start a brick of chunk c only once that flag is set, the chunk's last finished
+ *   brick sets a host-mapped flag and the calling thread then queues the chunk's D2H copy; a
+ *   slot is refilled once the D2H of its previous chunk has run.  Other shapes: chunk c+2's
+ *   inputs go host->device on a copy stream while chunk c is solved (separate launches on
+ *   two alternating compute streams and workspaces) and chunk c-1's results go
+ *   device->host.  Device memory is O(ring) / O(chunk), plus per-brick scalars of the batch.
  *   vol_h, fixed_h, values_h   host [batch][n] (page-locked for overlap; pageable works).
  *   prob_h / labels_h          out host fp32 / u8 [batch][n], either may be NULL.
  *   iters_h out host int32 [batch];  resid_h, status_h  out host [batch] or NULL.

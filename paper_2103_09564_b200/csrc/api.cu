@@ -911,18 +911,257 @@ HostLayout host_layout(int batch, rw_dims d, rw_dtype dtype, int chunk) {
   return L;
 }
 
-int host_chunk(int batch, int chunk) {
+// ---- host-streamed resident solve (one persistent launch over the whole batch)
+// The resident solver keeps every SM busy for the whole call; the batch's chunks stream
+// through a device ring of `ring_chunks` chunk slots: the H2D stream writes chunk c's inputs
+// into slot c % S and then a 4-byte ready flag (copy-engine ordered); the resident / L2-worker
+// clusters start a brick of chunk c only once its flag is set; the chunk's last finished brick
+// sets a host-mapped flag, and the host then queues the chunk's D2H copy.  A chunk's H2D waits
+// until the D2H of the chunk that used its slot before has completed.
+struct StreamedLayout {
+  size_t vol, fixed, val, prob, lab, iters, resid, status, in_ready, done, ctr, l2w, total;
+  int ring_chunks, ring, nch, nw;
+};
+
+// device ring: at least 16 chunks and 256 bricks (0.8 GB of cfg2 bricks) -- a worker brick
+// (12 ms) holds its chunk's slot while the clusters run ~100 bricks ahead
+constexpr int kRingChunks = 16, kRingBricks = 256;
+
+int streamed_vm(rw_dims d, rw_dtype dtype) {
+  const int vm = dtype == RW_U16 ? rw::VM_U16 : dtype == RW_F32 ? rw::VM_F32 : -1;
+  if (vm < 0 || g_solver == RW_SOLVER_STREAMING) return -1;
+  if (!rw::resident_supported(d.nx, d.ny, d.nz, 1, vm, g_res_wide)) return -1;
+  return vm;
+}
+
+StreamedLayout streamed_layout(int batch, rw_dims d, rw_dtype dtype, int chunk, int vm) {
+  StreamedLayout L{};
+  const size_t n = (size_t)d.nx * d.ny * d.nz;
+  L.nch = (batch + chunk - 1) / chunk;
+  L.ring_chunks = std::min(L.nch, std::max(kRingChunks, (kRingBricks + chunk - 1) / chunk));
+  if (env_int("RW_HOST_RING", 0) > 0)   // test knob: a short ring (slot reuse)
+    L.ring_chunks = std::min(L.nch, env_int("RW_HOST_RING", 0));
+  L.ring = L.ring_chunks * chunk;
+  const size_t M = (size_t)L.ring;
+  L.nw = 0;
+  if (g_l2w && vm >= 0 && d.nx == 64 && batch >= 64 && !g_res_wide)
+    L.nw = rw::l2res_workers(rw::resident_clusters64(vm));
+  size_t o = 0;
+  L.vol = o; o += up(M * n * dtype_size_(dtype));
+  L.fixed = o; o += up(M * n);
+  L.val = o; o += up(M * n * 4);
+  L.prob = o; o += up(M * n * 4);
+  L.lab = o; o += up(M * n);
+  L.iters = o; o += up((size_t)batch * 4);
+  L.resid = o; o += up((size_t)batch * 4);
+  L.status = o; o += up((size_t)batch * 4);
+  L.in_ready = o; o += up((size_t)L.nch * 4);
+  L.done = o; o += up((size_t)L.nch * 4);
+  L.ctr = o; o += up(16);
+  L.l2w = o; o += (size_t)L.nw * rw::l2res_bytes_per_worker();
+  L.total = o;
+  return L;
+}
+
+// per-thread, per-device host-mapped chunk flags and a pinned "1" for the ready-flag copies
+struct MappedFlags {
+  int* h = nullptr;
+  int cap = 0;
+  int* one = nullptr;
+};
+rw_status mapped_flags(int nch, MappedFlags** out) {
+  static thread_local MappedFlags mf[64];
+  int dev = 0;
+  RW_CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(RW_EINVAL, "device index out of range");
+  MappedFlags& m = mf[dev];
+  if (m.cap < nch) {
+    if (m.h) cudaFreeHost(m.h);
+    m.h = nullptr;
+    m.cap = 0;
+    RW_CK(cudaHostAlloc((void**)&m.h, (size_t)nch * sizeof(int), cudaHostAllocMapped));
+    m.cap = nch;
+  }
+  if (!m.one) {
+    RW_CK(cudaHostAlloc((void**)&m.one, sizeof(int), cudaHostAllocDefault));
+    *m.one = 1;
+  }
+  *out = &m;
+  return RW_OK;
+}
+
+int host_chunk(int batch, int chunk, bool streamed = false) {
   if (chunk > 0) return std::min(chunk, batch);
-  return std::max(1, (batch + 31) / 32);   // auto: 32 chunks (measured on 512 cfg2 bricks:
-                                           // e2e 366 / 365 / 363 / 360 G/s at 16 / 24 / 32 / 48)
+  // auto, chunked path: 32 chunks (measured on 512 cfg2 bricks: e2e 366 / 365 / 363 / 360 G/s
+  // at 16 / 24 / 32 / 48); streamed resident path: 64 chunks (58.0 / 58.4 / 59.3 ms at
+  // 8 / 16 / 32, profiles/r02/r02_host1.md)
+  return std::max(1, (batch + (streamed ? 63 : 31)) / (streamed ? 64 : 32));
 }
 
 }  // namespace
 
 size_t rw_solve_host_workspace_bytes(int32_t batch, rw_dims d, rw_dtype dtype, int32_t chunk) {
   if (!dims_ok(d) || batch < 1 || chunk < 0 || dtype < RW_U8 || dtype > RW_F32) return 0;
-  return host_layout(batch, d, dtype, host_chunk(batch, chunk)).total;
+  size_t t = host_layout(batch, d, dtype, host_chunk(batch, chunk)).total;
+  const int vm = streamed_vm(d, dtype);
+  if (vm >= 0)
+    t = std::max(t, streamed_layout(batch, d, dtype, host_chunk(batch, chunk, true), vm).total);
+  return t;
 }
+
+namespace {
+// rw_solve_bricks_host on the resident solver: see StreamedLayout
+rw_status solve_host_streamed(int32_t batch, rw_dims d, const void* vol_h, rw_dtype dtype,
+                              rw_norm nm, const uint8_t* fixed_h, const float* values_h,
+                              float beta, float eps, float tol, int32_t max_iter,
+                              int32_t tol_mode, int C, int vm, char* ws, float* prob_h,
+                              uint8_t* labels_h, int32_t* iters_h, float* resid_h,
+                              int32_t* status_h, cudaStream_t user) {
+  const StreamedLayout L = streamed_layout(batch, d, dtype, C, vm);
+  const size_t n = (size_t)d.nx * d.ny * d.nz, es = dtype_size_(dtype);
+  const int nch = L.nch, S = L.ring_chunks;
+  MappedFlags* mf = nullptr;
+  rw_status fr = mapped_flags(nch, &mf);
+  if (fr != RW_OK) return fr;
+  volatile int* hdone = mf->h;
+  for (int c = 0; c < nch; ++c) hdone[c] = 0;
+  int* in_ready = (int*)(ws + L.in_ready);
+  cudaStream_t h2d = nullptr, d2h = nullptr, cs = nullptr, s2 = nullptr;
+  std::vector<cudaEvent_t> ev_out((size_t)nch, nullptr);
+  cudaEvent_t e_user = nullptr, e_fork = nullptr, e_join = nullptr;
+  auto cleanup = [&]() {
+    for (cudaEvent_t e : ev_out)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {e_user, e_fork, e_join})
+      if (e) cudaEventDestroy(e);
+    for (cudaStream_t t : {h2d, d2h, cs, s2})
+      if (t) cudaStreamDestroy(t);
+  };
+  int next_in = 0;
+  bool launched = false;
+  // chunk c's inputs and then its ready flag (copy-engine ordered on the H2D stream)
+  auto enqueue_in = [&](int c) -> rw_status {
+    const size_t b0 = (size_t)c * C, nb = (size_t)std::min(C, batch - c * C);
+    const size_t k = (size_t)(c % S) * C;
+    RW_CK(cudaMemcpyAsync(ws + L.vol + k * n * es, (const char*)vol_h + b0 * n * es, nb * n * es,
+                          cudaMemcpyHostToDevice, h2d));
+    RW_CK(cudaMemcpyAsync(ws + L.fixed + k * n, fixed_h + b0 * n, nb * n, cudaMemcpyHostToDevice, h2d));
+    RW_CK(cudaMemcpyAsync(ws + L.val + k * n * 4, values_h + b0 * n, nb * n * 4,
+                          cudaMemcpyHostToDevice, h2d));
+    RW_CK(cudaMemcpyAsync(in_ready + c, mf->one, sizeof(int), cudaMemcpyHostToDevice, h2d));
+    return RW_OK;
+  };
+  auto run = [&]() -> rw_status {
+    for (cudaStream_t* t : {&h2d, &d2h, &cs, &s2})
+      RW_CK(cudaStreamCreateWithFlags(t, cudaStreamNonBlocking));
+    for (auto& e : ev_out) RW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (cudaEvent_t* e : {&e_user, &e_fork, &e_join})
+      RW_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    RW_CK(cudaEventRecord(e_user, user));        // work the caller enqueued before this call
+    RW_CK(cudaStreamWaitEvent(cs, e_user, 0));
+    RW_CK(cudaStreamWaitEvent(d2h, e_user, 0));
+    RW_CK(cudaMemsetAsync(ws + L.in_ready, 0, (size_t)nch * 4, cs));
+    RW_CK(cudaMemsetAsync(ws + L.done, 0, (size_t)nch * 4, cs));
+    RW_CK(cudaMemsetAsync(ws + L.ctr, 0, 16, cs));
+    RW_CK(cudaEventRecord(e_fork, cs));          // flags zeroed before any copy or cluster
+    RW_CK(cudaStreamWaitEvent(h2d, e_fork, 0));
+    RW_CK(cudaStreamWaitEvent(s2, e_fork, 0));
+    rw::ResArgs A{};
+    A.B = batch;
+    A.nb = batch;
+    A.nsolve = batch;
+    A.next = (int*)(ws + L.ctr) + 2;
+    A.iters = (int*)(ws + L.iters);
+    A.status = (int*)(ws + L.status);
+    A.resid = (float*)(ws + L.resid);
+    A.x = (float*)(ws + L.prob);
+    A.labels = labels_h ? (uint8_t*)(ws + L.lab) : nullptr;
+    A.C = rw::Ctl{tol, tol_mode, max_iter, nm.scale, nm.offset, rw::nbl2_of(beta), eps, 0, g_rr};
+    A.vol = ws + L.vol;
+    A.vdt = vm;
+    A.fixed = (const uint8_t*)(ws + L.fixed);
+    A.values = (const float*)(ws + L.val);
+    A.x0 = nullptr;
+    A.ring = L.ring;
+    A.chunk = C;
+    A.in_ready = in_ready;
+    A.done = (int*)(ws + L.done);
+    A.host_done = mf->h;
+    A.abort = (int*)(ws + L.ctr) + 3;
+    RW_TIMED(RW_K_RESIDENT, cs, 1, rw::launch_resident(d.nx, A, g_res_wide, cs));
+    launched = true;
+    if (L.nw > 0) {
+      rw::L2Args W{};
+      W.buf = (float*)(ws + L.l2w);
+      W.stride = (long long)(rw::l2res_bytes_per_worker() / sizeof(float));
+      W.rmin = env_int("RW_L2_RMIN", 48);
+      RW_TIMED(RW_K_L2RES, s2, 1, rw::launch_l2res(A, W, L.nw, s2));
+    }
+    RW_CK(cudaEventRecord(e_join, s2));
+    RW_CK(cudaStreamWaitEvent(cs, e_join, 0));
+    // host loop: queue inputs as the ring allows, results as chunks complete
+    int next_out = 0;
+    const bool starve = env_int("RW_HOST_TEST_ABORT", 0) != 0;   // test knob: never feed the launch
+    while (next_out < nch) {
+      bool progress = false;
+      // slot (next_in % S) is free once the D2H of chunk next_in - S was queued AND has run
+      // (an event never recorded would query as complete)
+      while (!starve && next_in < nch && (next_in < S || (next_in - S < next_out &&
+                                              cudaEventQuery(ev_out[next_in - S]) == cudaSuccess))) {
+        rw_status r = enqueue_in(next_in);
+        if (r != RW_OK) return r;
+        ++next_in;
+        progress = true;
+      }
+      if (hdone[next_out]) {
+        const int c = next_out;
+        const size_t b0 = (size_t)c * C, nb = (size_t)std::min(C, batch - c * C);
+        const size_t k = (size_t)(c % S) * C;
+        if (prob_h)
+          RW_CK(cudaMemcpyAsync(prob_h + b0 * n, ws + L.prob + k * n * 4, nb * n * 4,
+                                cudaMemcpyDeviceToHost, d2h));
+        if (labels_h)
+          RW_CK(cudaMemcpyAsync(labels_h + b0 * n, ws + L.lab + k * n, nb * n,
+                                cudaMemcpyDeviceToHost, d2h));
+        RW_CK(cudaEventRecord(ev_out[c], d2h));
+        ++next_out;
+        progress = true;
+      } else if (!progress) {
+        // the launch ended (or failed) without publishing this chunk: never spin forever
+        const cudaError_t q = cudaStreamQuery(cs);
+        if (q != cudaErrorNotReady && !hdone[next_out]) {
+          if (q != cudaSuccess)
+            return fail(RW_ECUDA, "rw_solve_bricks_host: resident launch: %s", cudaGetErrorString(q));
+          // aborted (inputs did not arrive in time): the caller falls back to the chunked path
+          return RW_EUNSUPPORTED;
+        }
+        std::this_thread::yield();
+      }
+    }
+    RW_CK(cudaEventRecord(e_join, cs));
+    RW_CK(cudaStreamWaitEvent(d2h, e_join, 0));
+    RW_CK(cudaMemcpyAsync(iters_h, ws + L.iters, (size_t)batch * 4, cudaMemcpyDeviceToHost, d2h));
+    if (resid_h)
+      RW_CK(cudaMemcpyAsync(resid_h, ws + L.resid, (size_t)batch * 4, cudaMemcpyDeviceToHost, d2h));
+    if (status_h)
+      RW_CK(cudaMemcpyAsync(status_h, ws + L.status, (size_t)batch * 4, cudaMemcpyDeviceToHost, d2h));
+    RW_CK(cudaEventRecord(e_user, d2h));
+    RW_CK(cudaStreamWaitEvent(user, e_user, 0));   // the caller's stream sees the whole call
+    RW_CK(cudaStreamSynchronize(d2h));
+    return RW_OK;
+  };
+  rw_status r = run();
+  if (r != RW_OK && launched) {
+    // release every cluster that may still wait for a chunk, then drain the launch
+    for (int c = next_in; c < nch; ++c)
+      cudaMemcpyAsync(in_ready + c, mf->one, sizeof(int), cudaMemcpyHostToDevice, h2d);
+    cudaStreamSynchronize(h2d);
+    cudaStreamSynchronize(cs);
+  }
+  cleanup();
+  return r;
+}
+}  // namespace
 
 rw_status rw_solve_bricks_host(int32_t batch, rw_dims d, const void* vol_h, rw_dtype dtype,
                                rw_norm nm, const uint8_t* fixed_h, const float* values_h,
@@ -942,6 +1181,23 @@ rw_status rw_solve_bricks_host(int32_t batch, rw_dims d, const void* vol_h, rw_d
     return fail(RW_ENOMEM, "rw_solve_bricks_host: workspace too small: %zu < %zu bytes", ws_bytes,
                 L.total);
   char* ws = (char*)workspace;
+  const int vm_st = streamed_vm(d, dtype);
+  // a tool that serialises launches (ncu, compute-sanitizer: CUDA_INJECTION64_PATH;
+  // CUDA_LAUNCH_BLOCKING) would block the host inside the persistent launch before it can
+  // queue the inputs: use the chunked path there
+  const bool serialised = getenv("CUDA_INJECTION64_PATH") || env_int("CUDA_LAUNCH_BLOCKING", 0);
+  if (vm_st >= 0 && !serialised && env_int("RW_HOST_CHUNKED", 0) == 0) {
+    const int Cs = host_chunk(batch, chunk, true);
+    const StreamedLayout Ls = streamed_layout(batch, d, dtype, Cs, vm_st);
+    if (ws_bytes < Ls.total)
+      return fail(RW_ENOMEM, "rw_solve_bricks_host: workspace too small: %zu < %zu bytes",
+                  ws_bytes, Ls.total);
+    const rw_status r = solve_host_streamed(batch, d, vol_h, dtype, nm, fixed_h, values_h, beta,
+                                            eps, tol, max_iter, tol_mode, Cs, vm_st, ws, prob_h,
+                                            labels_h, iters_h, resid_h, status_h,
+                                            (cudaStream_t)stream);
+    if (r != RW_EUNSUPPORTED) return r;   // else aborted: the chunked path below
+  }
   const size_t n = (size_t)d.nx * d.ny * d.nz, es = dtype_size(dtype);
   const int nch = (batch + C - 1) / C;
   cudaStream_t user = (cudaStream_t)stream;

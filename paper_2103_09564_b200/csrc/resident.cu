@@ -330,6 +330,47 @@ struct QuadOut {
   uint32_t fm;
 };
 
+// ring mode (host-streamed solve): the slot's bytes were rewritten by a copy engine during
+// this launch, so brick inputs are read through L2 only (ld.global.cg: no stale L1 lines of
+// the slot's previous chunk); the kernels' own arrays keep the default caching
+template <typename V>
+__device__ __forceinline__ V ldin(const V* p, bool cg) { return cg ? __ldcg(p) : *p; }
+// wait until chunk c's inputs are on the device (ring mode; one thread).  Returns the brick
+// to solve, or A.nsolve (exit) if the launch was aborted: inputs that never arrive within 2 s
+// (a tool serialising launches blocks the host before it can queue them) must not hang the GPU
+__device__ __forceinline__ int wait_chunk(const ResArgs& A, int b) {
+  if (A.ring && b < A.nsolve) {
+    const volatile int* f = A.in_ready + b / A.chunk;
+    const volatile int* ab = A.abort;
+    if (*f == 0) {
+      unsigned long long t0, t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      while (*f == 0) {
+        __nanosleep(256);
+        if (*ab) return A.nsolve;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 2000000000ull) {
+          atomicExch(A.abort, 1);
+          return A.nsolve;
+        }
+      }
+    }
+    __threadfence();
+  }
+  return b;
+}
+// brick b (ring mode) is complete on every CTA of the cluster: count it; the chunk's last
+// brick publishes the chunk to the host (one thread, after a cluster barrier that follows
+// every thread's __threadfence)
+__device__ __forceinline__ void brick_done(const ResArgs& A, int b) {
+  const int c = b / A.chunk;
+  const int nbc = min(A.chunk, A.nsolve - c * A.chunk);
+  if (atomicAdd(A.done + c, 1) + 1 == nbc) {
+    __threadfence_system();
+    *reinterpret_cast<volatile int*>(A.host_done + c) = 1;
+  }
+}
+
 template <typename T> struct Quad4;
 template <> struct Quad4<uint16_t> { using V = ushort4; };
 template <> struct Quad4<float> { using V = float4; };
@@ -344,10 +385,11 @@ __device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long bas
   // one vector load per neighbour quad (own, +-y, +-z) and scalars for x-1 / x+4 of
   // intensity, Dirichlet mask, Dirichlet value and initial guess
   struct NQ { float g[4], xv[4]; bool f[4]; };
+  const bool cg = A.ring != 0;
   auto quad = [&](long long i, NQ& q) {
-    const typename Quad4<T>::V v = *reinterpret_cast<const typename Quad4<T>::V*>(vol + i);
-    const uchar4 f = *reinterpret_cast<const uchar4*>(A.fixed + i);
-    const float4 val = *reinterpret_cast<const float4*>(A.values + voff + i);
+    const typename Quad4<T>::V v = ldin(reinterpret_cast<const typename Quad4<T>::V*>(vol + i), cg);
+    const uchar4 f = ldin(reinterpret_cast<const uchar4*>(A.fixed + i), cg);
+    const float4 val = ldin(reinterpret_cast<const float4*>(A.values + voff + i), cg);
     const float4 x0 = A.x0 ? *reinterpret_cast<const float4*>(A.x0 + voff + i) : make_float4(0.5f, 0.5f, 0.5f, 0.5f);
     const float gv[4] = {(float)v.x, (float)v.y, (float)v.z, (float)v.w};
     const bool fv[4] = {f.x != 0, f.y != 0, f.z != 0, f.w != 0};
@@ -360,9 +402,9 @@ __device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long bas
     }
   };
   auto one = [&](long long i, float& g, float& xv, bool& f) {
-    g = normv((float)vol[i], sc, of);
-    f = A.fixed[i] != 0;
-    xv = f ? A.values[voff + i] : (A.x0 ? A.x0[voff + i] : 0.5f);
+    g = normv((float)ldin(vol + i, cg), sc, of);
+    f = ldin(A.fixed + i, cg) != 0;
+    xv = f ? ldin(A.values + voff + i, cg) : (A.x0 ? A.x0[voff + i] : 0.5f);
   };
   NQ c0, yp{}, ym{}, zp{}, zm{};
   quad(i0, c0);
@@ -565,7 +607,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   while (true) {
     // ---- next brick (rank 0 draws it, DSMEM broadcast, cluster barrier)
     if (rank == 0 && t == 0) {
-      const int nb = atomicAdd(A.next, 1);
+      const int nb = wait_chunk(A, atomicAdd(A.next, 1));
       for (int c = 0; c < CL; ++c) st_cl_u32(mapa(brk, c), (uint32_t)nb);
     }
     cl_arrive();
@@ -577,6 +619,9 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     const int b = pr % A.nb;
     const long long rb = (long long)(pr / A.nb) * A.B + b;
     const long long xoff = (rb - b) * n;   // rhs offset of the pair's arrays
+    // data slot of the brick (ring mode: b % ring); recomputed after the loop so that it does
+    // not stay live across the iterations
+    auto slot_of = [&]() { return A.ring ? (long long)(b % A.ring) : (long long)b; };
 
     // ---- load the slab: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
     uint32_t fixm = 0;   // bit 4*it+e: voxel is fixed (dinv == 0)
@@ -590,7 +635,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         const int zl = it / NR, rr = it % NR, y = NR * j + rr;
         QuadOut o{};
         if (act) {
-          o = assemble_quad<T, N, G::NZ>(A, (long long)b * n, xoff, z0 + zl, y, 4 * qx, iacc);
+          o = assemble_quad<T, N, G::NZ>(A, slot_of() * n, xoff, z0 + zl, y, 4 * qx, iacc);
           fixm |= o.fm << (4 * it);
           const int so = y * N + 4 * qx;
           st4(WY + zl * PL + so, o.wy);
@@ -871,6 +916,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 
     // ---- finalise (row a6): last lagged x update, clamp, fixed values kept, labels
     const bool upd = (st == ST_CONVERGED || st == ST_MAXITER) && k >= 1;
+    const long long bs = slot_of();
 #pragma unroll
     for (int it = 0; it < NI; ++it) {
       const int zl = it / NR, rr = it % NR, y = NR * j + rr;
@@ -884,7 +930,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         if (fm & (1u << e)) continue;            // fixed: x holds the Dirichlet value
         o[e] = st == ST_ZERO_B ? 0.f : fminf(fmaxf(o[e], 0.f), 1.f);
       }
-      const long long g = (long long)b * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
+      const long long g = bs * n + (long long)(z0 + zl) * PL + y * N + 4 * qx;
       if (!act) continue;
       st4(A.x + xoff + g, make_float4(o[0], o[1], o[2], o[3]));
       if (A.labels && xoff == 0)   // labels = prob[0] > 0.5 (rw.h)
@@ -902,6 +948,12 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         }
         A.resid[rb] = (float)res;
       }
+    }
+    if (A.ring) {   // host-streamed solve: publish the brick (then its chunk) once complete
+      __threadfence();
+      cl_arrive();
+      cl_wait();
+      if (rank == 0 && t == 0) brick_done(A, b);
     }
   }
   // ---- release tensor memory
@@ -1034,6 +1086,8 @@ cudaError_t launch_resident(int nx, const ResArgs& A, int wide, cudaStream_t s) 
 namespace l2 {
 constexpr int N = 64, CL = 16, CW = 4, VPC = CL / CW, ZS = 4, QX = 16, NI = 8, T = 512, NW = 16;
 constexpr int PL = N * N;
+constexpr int DVS = 3;                                        // virtual ranks with dinv in smem
+constexpr int SMEM = DVS * NI * T * 16;                       // 192 KB
 }  // namespace l2
 
 template <int VM>
@@ -1047,7 +1101,11 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
   __shared__ double s_bred[VPC][NW][2];
   __shared__ double2 s_res;
   __shared__ int s_brick;
-  const int t = threadIdx.x, warp = t >> 5, lane_ = t & 31;
+  __shared__ uint32_t s_taddr;
+  // dinv of virtual ranks 0..DVS-1 in shared memory ([vv][it][thread] float4: conflict-free),
+  // the last one's in global memory; r of all four in tensor memory (128 columns per thread)
+  extern __shared__ __align__(16) float4 s_dv[];
+  const int t = threadIdx.x, warp = t >> 5;
   const int rank = cl_rank();
   const int qx = t % QX, j = t / QX;                   // Cfg<64, 16>: EXACT map
   const int wid = blockIdx.x / CW;                     // worker cluster
@@ -1059,11 +1117,23 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
   float* const Rg = Wz + n;
   float* const Qg = Rg + n;
   float* const Pp = Qg + n;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                 :: "r"(sptr(&s_taddr)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
   if (t == 0) {
     for (int i = 0; i < 4; ++i) mbar_init(&s_bar[i], 1);
     fence_mbar_init();
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // r of (vv, it): columns tr + 32 vv + 4 it of this thread's lane
+  const uint32_t tr = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2);
+  auto dv_ld = [&](int vv, int it, long long g) {
+    return vv < DVS ? s_dv[(vv * NI + it) * T + t] : ld4(Dv + g);
+  };
   cl_arrive();
   cl_wait();
   const uint32_t brk = sptr(&s_brick);
@@ -1138,13 +1208,15 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
         if (o == c) { nb = c; break; }
         c = o;
       }
+      nb = wait_chunk(A, nb);
       for (int cc = 0; cc < CW; ++cc) st_cl_u32(mapa(brk, cc), (uint32_t)nb);
     }
     cl_arrive();
     cl_wait();
     const int b = s_brick;
     if (b >= A.nsolve) break;
-    float* const X = A.x + (long long)b * n;
+    const long long bs = A.ring ? (long long)(b % A.ring) : (long long)b;   // data slot
+    float* const X = A.x + bs * n;
 
     // ---- brick load: k_resident's fused assembly, per virtual rank
     uint32_t fixm[VPC];
@@ -1158,18 +1230,20 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
 #pragma unroll
       for (int it = 0; it < NI; ++it) {
         const int zl = it / 2, y = 2 * j + (it & 1);
-        const QuadOut o = assemble_quad<TV, N, N>(A, (long long)b * n, 0, vr * ZS + zl, y, 4 * qx, iacc[vv]);
+        const QuadOut o = assemble_quad<TV, N, N>(A, bs * n, 0, vr * ZS + zl, y, 4 * qx, iacc[vv]);
         fixm[vv] |= o.fm << (4 * it);
         const long long g = gi(vr, it);
-        st4(Dv + g, o.dv);
+        if (vv < DVS) s_dv[(vv * NI + it) * T + t] = o.dv;
+        else st4(Dv + g, o.dv);
         st4(Wx + g, o.wx);
         st4(Wy + g, o.wy);
         st4(Wz + g, o.wz);
         st4(X + g, o.xv);
-        st4(Rg + g, o.rv);
+        tm_st4(tr + 32u * vv + 4u * it, o.rv);
         st4(Pp + g, f4(0.f));
       }
     }
+    tm_wait_st();
     double nu, bb, nf, rz, rrn;
     {
       double v0[VPC][2], v1[VPC][2], v2[VPC][2];
@@ -1210,12 +1284,14 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
 #pragma unroll
       for (int vv = 0; vv < VPC; ++vv) {
         const int vr = rank * VPC + vv;
+        float4 rr[NI];
+        tm_ld32(tr + 32u * vv, rr);
 #pragma unroll
         for (int it = 0; it < NI; ++it) {
           const long long g = gi(vr, it);
-          const float4 dv = ld4(Dv + g), po = ld4(Pp + g), r = ld4(Rg + g);
+          const float4 dv = dv_ld(vv, it, g), po = ld4(Pp + g);
           if (k > 0) st4(X + g, fma4p(al, po, ld4(X + g)));
-          st4(Pp + g, pnew4p(be, po, dv, r));
+          st4(Pp + g, pnew4p(be, po, dv, rr[it]));
         }
       }
       cl_arrive();        // every p update of the brick visible to the cluster (global memory)
@@ -1283,16 +1359,18 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
       for (int vv = 0; vv < VPC; ++vv) {
         const int vr = rank * VPC + vv;
         float2 az0 = make_float2(0.f, 0.f), az1 = az0, ar0 = az0, ar1 = az0;
+        float4 rr[NI];
+        tm_ld32(tr + 32u * vv, rr);
 #pragma unroll
         for (int it = 0; it < NI; ++it) {
           const long long g = gi(vr, it);
-          const float4 dv = ld4(Dv + g);
-          float4 rn = fma4p(-al, ld4(Qg + g), ld4(Rg + g));
+          const float4 dv = dv_ld(vv, it, g);
+          float4 rn = fma4p(-al, ld4(Qg + g), rr[it]);
           if (dv.x == 0.f) rn.x = 0.f;
           if (dv.y == 0.f) rn.y = 0.f;
           if (dv.z == 0.f) rn.z = 0.f;
           if (dv.w == 0.f) rn.w = 0.f;
-          st4(Rg + g, rn);
+          tm_st4(tr + 32u * vv + 4u * it, rn);
           const float2 z0 = __fmul2_rn(lo2(dv), lo2(rn)), z1 = __fmul2_rn(hi2(dv), hi2(rn));
           az0 = __ffma2_rn(lo2(rn), z0, az0);
           az1 = __ffma2_rn(hi2(rn), z1, az1);
@@ -1301,6 +1379,7 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
         v2[vv][0] = (double)hsum(az0, az1);
         v2[vv][1] = (double)hsum(ar0, ar1);
       }
+      tm_wait_st();
       const double2 srr = cluster_sum(v2, 2, 2, s_rz, ph2);
       rz_prev = rz;
       pq_prev = pq;
@@ -1328,7 +1407,7 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
         }
         st4(X + g, make_float4(o[0], o[1], o[2], o[3]));
         if (A.labels)
-          *reinterpret_cast<uchar4*>(A.labels + (long long)b * n + g) =
+          *reinterpret_cast<uchar4*>(A.labels + bs * n + g) =
               make_uchar4(o[0] > 0.5f, o[1] > 0.5f, o[2] > 0.5f, o[3] > 0.5f);
       }
     }
@@ -1346,10 +1425,16 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
       }
     }
     // the brick's global arrays are reused by the next brick: everyone done reading them
+    if (A.ring) __threadfence();
     cl_arrive();
     cl_wait();
+    if (A.ring && rank == 0 && t == 0) brick_done(A, b);
   }
   if (Wk.done && t == 0) atomicAdd(Wk.done, 1);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(s_taddr) : "memory");
 }
 
 // experiment (RW_L2_HOLD): occupy the SMs of the resident clusters without any traffic
@@ -1402,10 +1487,18 @@ size_t l2res_bytes_per_worker() { return (size_t)7 * l2::PL * l2::N * sizeof(flo
 
 template <int VM>
 static cudaError_t launch_l2res_vm(const ResArgs& A, const L2Args& W, int nw, cudaStream_t s) {
+  static bool init[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!init[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_l2res<VM>, cudaFuncAttributeMaxDynamicSharedMemorySize, l2::SMEM);
+    if (e != cudaSuccess) return e;
+    init[dev] = true;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nw * l2::CW);
   cfg.blockDim = dim3(l2::T);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = l2::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;

@@ -30,6 +30,19 @@ struct ResArgs {
   const float* x0;       // [R][B][n] or null (0.5)
   long long* dbg;      // debug builds only (-DRW_RES_TIMING): per-(rank, phase) clock64 sums
                        // in a caller-provided buffer; null in the library
+  // host-streamed solve (rw_solve_bricks_host, ring > 0): brick b's vol / fixed / values /
+  // x / labels live in device slot b % ring (its iters / status / resid at [b]); a brick of
+  // chunk c = b / chunk is started only once in_ready[c] != 0 (written by the H2D copy
+  // stream after the chunk's inputs); the last finished brick of chunk c sets host_done[c]
+  // (host-mapped) so the host can start the chunk's D2H copy while the launch goes on
+  int ring;
+  int chunk;
+  const int* in_ready;   // [nchunks] device
+  int* done;             // [nchunks] device, zeroed before the launch
+  int* host_done;        // [nchunks] host-mapped, zeroed before the launch
+  int* abort;            // device, zeroed: set when a chunk's inputs did not arrive within 2 s
+                         // (e.g. a profiler serialising the launch): every cluster then exits
+                         // and the host falls back to the chunked pipeline
 };
 
 // L2 workers (resident.cu k_l2res): storage of the worker clusters' CG state in global memory

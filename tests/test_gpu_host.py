@@ -71,3 +71,29 @@ def test_host_pipeline_prob_only_and_labels_only():
     assert torch.equal(a["prob"], ref["prob"].cpu())
     assert torch.equal(b["labels"], ref["labels"].cpu())
     assert torch.equal(a["iters"], b["iters"])
+
+
+@pytest.mark.parametrize("ring,chunk", [(2, 5), (4, 3)])
+def test_host_streamed_ring_reuse_with_workers(ring, chunk, monkeypatch):
+    """The streamed resident path with a ring of only `ring` chunk slots on a batch that
+    wraps it many times, with the L2 worker clusters on (batch >= 64): every slot is refilled
+    only after its previous chunk's D2H has run, so the outputs still equal the device solve."""
+    monkeypatch.setenv("RW_HOST_RING", str(ring))
+    p = wl.cfg2(batch=70)
+    _compare(p, chunk, True)
+
+
+def test_host_chunked_path_still_equal(monkeypatch):
+    """The chunked path (separate launches per chunk; RW_HOST_CHUNKED=1) on a resident shape."""
+    monkeypatch.setenv("RW_HOST_CHUNKED", "1")
+    p = wl.cfg2(batch=20)
+    _compare(p, 6, True)
+
+
+def test_host_streamed_abort_falls_back(monkeypatch):
+    """If a chunk's inputs never reach the persistent launch (RW_HOST_TEST_ABORT starves it,
+    as a tool serialising launches would), every cluster leaves after its 2 s wait and the
+    call falls back to the chunked pipeline: the results still equal the device solve."""
+    monkeypatch.setenv("RW_HOST_TEST_ABORT", "1")
+    p = wl.cfg2(batch=6)
+    _compare(p, 2, True)
