@@ -134,6 +134,30 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       tma_load_3d(st + L.oW, &M.v, bj, t.x0 - P.hxv, yb, pd);
     }
   };
+  // the same boxes of plane j pulled into L2 ahead of the ring (Plan.pf planes beyond it)
+  auto pref = [&](int j) {
+    if (j >= np) return;
+    const int zz = zs + j;
+    const int xb = t.x0 - hx, yb = t.y0 - 1;
+#pragma unroll
+    for (int c = 0; c < RC; ++c) {
+      if (!act[c]) continue;
+      const int pr = ((rbase + c) * P.B + b) * nz + zz;
+      const int pp = ((par * P.R + rbase + c) * P.B + b) * nz + zz;
+      tma_prefetch_3d(&M.r, xb, yb, ONE ? pp : pr);
+      tma_prefetch_3d(&M.p, xb, yb, pp);
+      if (qin) tma_prefetch_3d(&M.q, xb, yb, pp);
+    }
+    const int pd = b * nz + zz;
+    tma_prefetch_3d(&M.d, xb, yb, pd);
+    if (VM == VM_STORED) {
+      tma_prefetch_3d(&M.wx, xb, t.y0, pd);
+      tma_prefetch_3d(&M.wy, t.x0, yb, (P.B + b) * nz + zz);
+      tma_prefetch_3d(&M.wz, t.x0, t.y0, (2 * P.B + b) * nz + zz);
+    } else {
+      tma_prefetch_3d(&M.v, t.x0 - P.hxv, yb, pd);
+    }
+  };
   auto wait = [&](int j) { mbar_wait(bar + (j % NS), (uint32_t)((j / NS) & 1)); };
   auto stg = [&](int j) -> const unsigned char* { return smem + (j % NS) * L.stage; };
   auto F = [](const unsigned char* st, int off) { return reinterpret_cast<const float*>(st + off); };
@@ -179,6 +203,8 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
     prefetch_tmap(VM == VM_STORED ? &M.wx : &M.v);
     // planes 0 .. jz0 + NS - 2 now; step z issues plane (z - zs) + NS - 1
     for (int j = 0; j <= (t.z0 - zs) + NS - 2; ++j) issue(j);
+    if (P.pf > 0)
+      for (int j = (t.z0 - zs) + NS - 1; j <= (t.z0 - zs) + NS - 2 + P.pf; ++j) pref(j);
   }
   // out-of-tile halo columns of the p_new planes stay zero when the tile spans the brick
   if (hx == 0) {
@@ -323,7 +349,10 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       }
     }
     __syncthreads();                          // p_new plane + Wys of plane z complete
-    if (tid == 0) issue(jz + NS - 1);    // refill the slot of plane z-1 (all done with it)
+    if (tid == 0) {
+      issue(jz + NS - 1);                // refill the slot of plane z-1 (all done with it)
+      if (P.pf > 0) pref(jz + NS - 1 + P.pf);
+    }
     if (in) {
       if (VM == VM_STORED) {
         const float* Wxb = F(s0, L.oW);

@@ -333,8 +333,11 @@ struct QuadOut {
 // ring mode (host-streamed solve): the slot's bytes were rewritten by a copy engine during
 // this launch, so brick inputs are read through L2 only (ld.global.cg: no stale L1 lines of
 // the slot's previous chunk); the kernels' own arrays keep the default caching
-template <typename V>
-__device__ __forceinline__ V ldin(const V* p, bool cg) { return cg ? __ldcg(p) : *p; }
+template <bool CG, typename V>
+__device__ __forceinline__ V ldin(const V* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return *p;
+}
 // wait until chunk c's inputs are on the device (ring mode; one thread).  Returns the brick
 // to solve, or A.nsolve (exit) if the launch was aborted: inputs that never arrive within 2 s
 // (a tool serialising launches blocks the host before it can queue them) must not hang the GPU
@@ -375,7 +378,7 @@ template <typename T> struct Quad4;
 template <> struct Quad4<uint16_t> { using V = ushort4; };
 template <> struct Quad4<float> { using V = float4; };
 
-template <typename T, int N, int NZ>
+template <typename T, int N, int NZ, bool CG = false>
 __device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long base, long long voff,
                                                  int z, int y, int x, double (&acc)[5]) {
   const T* vol = reinterpret_cast<const T*>(A.vol);
@@ -385,11 +388,10 @@ __device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long bas
   // one vector load per neighbour quad (own, +-y, +-z) and scalars for x-1 / x+4 of
   // intensity, Dirichlet mask, Dirichlet value and initial guess
   struct NQ { float g[4], xv[4]; bool f[4]; };
-  const bool cg = A.ring != 0;
   auto quad = [&](long long i, NQ& q) {
-    const typename Quad4<T>::V v = ldin(reinterpret_cast<const typename Quad4<T>::V*>(vol + i), cg);
-    const uchar4 f = ldin(reinterpret_cast<const uchar4*>(A.fixed + i), cg);
-    const float4 val = ldin(reinterpret_cast<const float4*>(A.values + voff + i), cg);
+    const typename Quad4<T>::V v = ldin<CG>(reinterpret_cast<const typename Quad4<T>::V*>(vol + i));
+    const uchar4 f = ldin<CG>(reinterpret_cast<const uchar4*>(A.fixed + i));
+    const float4 val = ldin<CG>(reinterpret_cast<const float4*>(A.values + voff + i));
     const float4 x0 = A.x0 ? *reinterpret_cast<const float4*>(A.x0 + voff + i) : make_float4(0.5f, 0.5f, 0.5f, 0.5f);
     const float gv[4] = {(float)v.x, (float)v.y, (float)v.z, (float)v.w};
     const bool fv[4] = {f.x != 0, f.y != 0, f.z != 0, f.w != 0};
@@ -402,9 +404,9 @@ __device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long bas
     }
   };
   auto one = [&](long long i, float& g, float& xv, bool& f) {
-    g = normv((float)ldin(vol + i, cg), sc, of);
-    f = ldin(A.fixed + i, cg) != 0;
-    xv = f ? ldin(A.values + voff + i, cg) : (A.x0 ? A.x0[voff + i] : 0.5f);
+    g = normv((float)ldin<CG>(vol + i), sc, of);
+    f = ldin<CG>(A.fixed + i) != 0;
+    xv = f ? ldin<CG>(A.values + voff + i) : (A.x0 ? A.x0[voff + i] : 0.5f);
   };
   NQ c0, yp{}, ym{}, zp{}, zm{};
   quad(i0, c0);
@@ -468,7 +470,9 @@ __device__ __forceinline__ QuadOut assemble_quad(const ResArgs& A, long long bas
   return o;
 }
 
-template <int N, int CL, int VM>
+// RING: host-streamed solve (ResArgs ring mode); a separate instantiation so that the ring
+// bookkeeping costs the ordinary launch nothing
+template <int N, int CL, int VM, bool RING = false>
 __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   using G = res::Cfg<N, CL>;
   using namespace res;
@@ -607,7 +611,8 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
   while (true) {
     // ---- next brick (rank 0 draws it, DSMEM broadcast, cluster barrier)
     if (rank == 0 && t == 0) {
-      const int nb = wait_chunk(A, atomicAdd(A.next, 1));
+      int nb = atomicAdd(A.next, 1);
+      if constexpr (RING) nb = wait_chunk(A, nb);
       for (int c = 0; c < CL; ++c) st_cl_u32(mapa(brk, c), (uint32_t)nb);
     }
     cl_arrive();
@@ -621,7 +626,10 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
     const long long xoff = (rb - b) * n;   // rhs offset of the pair's arrays
     // data slot of the brick (ring mode: b % ring); recomputed after the loop so that it does
     // not stay live across the iterations
-    auto slot_of = [&]() { return A.ring ? (long long)(b % A.ring) : (long long)b; };
+    auto slot_of = [&]() {
+      if constexpr (RING) return (long long)(b % A.ring);
+      else return (long long)b;
+    };
 
     // ---- load the slab: W, dinv -> TMEM; r -> registers; x, -y/-z weights -> smem
     uint32_t fixm = 0;   // bit 4*it+e: voxel is fixed (dinv == 0)
@@ -635,7 +643,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         const int zl = it / NR, rr = it % NR, y = NR * j + rr;
         QuadOut o{};
         if (act) {
-          o = assemble_quad<T, N, G::NZ>(A, slot_of() * n, xoff, z0 + zl, y, 4 * qx, iacc);
+          o = assemble_quad<T, N, G::NZ, RING>(A, slot_of() * n, xoff, z0 + zl, y, 4 * qx, iacc);
           fixm |= o.fm << (4 * it);
           const int so = y * N + 4 * qx;
           st4(WY + zl * PL + so, o.wy);
@@ -949,7 +957,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
         A.resid[rb] = (float)res;
       }
     }
-    if (A.ring) {   // host-streamed solve: publish the brick (then its chunk) once complete
+    if constexpr (RING) {   // host-streamed solve: publish the brick (then its chunk) once complete
       __threadfence();
       cl_arrive();
       cl_wait();
@@ -967,7 +975,7 @@ __global__ void __launch_bounds__(res::Cfg<N, CL>::T, 1) k_resident(ResArgs A) {
 // ------------------------------------------------------------------------- launcher
 // Supported shapes: N^3 bricks with (N, CL) in {(64, 16), (40, 5), (32, 4)} (CL40 / CL32 below);
 // 40^3 is the paper's expanded brick (s = 32, e = 1.25).
-template <int N, int CL, int VM>
+template <int N, int CL, int VM, bool RING = false>
 static int resident_clusters() {
   // per device: the shared-memory / cluster-size attributes are set on the current device
   // and the co-resident cluster count is a property of that device
@@ -981,9 +989,9 @@ static int resident_clusters() {
   if (cached[dev] > 0) return cached[dev] - 1;
   using G = res::Cfg<N, CL>;
   int nc = 0;
-  if (cudaFuncSetAttribute(k_resident<N, CL, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(k_resident<N, CL, VM, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            G::SMEM) != cudaSuccess ||
-      (CL > 8 && cudaFuncSetAttribute(k_resident<N, CL, VM>,
+      (CL > 8 && cudaFuncSetAttribute(k_resident<N, CL, VM, RING>,
                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
     cudaGetLastError();
     cached[dev] = 1;
@@ -1000,7 +1008,7 @@ static int resident_clusters() {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (cudaOccupancyMaxActiveClusters(&nc, k_resident<N, CL, VM>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&nc, k_resident<N, CL, VM, RING>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     nc = 0;
   }
@@ -1011,10 +1019,10 @@ static int resident_clusters() {
   return nc;
 }
 
-template <int N, int CL, int VM>
-static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
+template <int N, int CL, int VM, bool RING>
+static cudaError_t launch_res_t(const ResArgs& A, cudaStream_t s) {
   using G = res::Cfg<N, CL>;
-  const int nc = resident_clusters<N, CL, VM>();
+  const int nc = resident_clusters<N, CL, VM, RING>();
   if (nc < 1) return cudaErrorNotSupported;
   const int ncl = nc < A.nsolve ? nc : A.nsolve;
   cudaLaunchConfig_t cfg = {};
@@ -1029,7 +1037,15 @@ static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_resident<N, CL, VM>, A);
+  return cudaLaunchKernelEx(&cfg, k_resident<N, CL, VM, RING>, A);
+}
+
+template <int N, int CL, int VM>
+static cudaError_t launch_res(const ResArgs& A, cudaStream_t s) {
+  if constexpr (VM == VM_U16 || VM == VM_F32)
+    if (A.ring) return launch_res_t<N, CL, VM, true>(A, s);
+  if (A.ring) return cudaErrorNotSupported;   // ring mode needs the fused assembly
+  return launch_res_t<N, CL, VM, false>(A, s);
 }
 
 // 40^3 / 32^3 bricks: throughput shape (default) = 8 planes per CTA, one row per thread,
@@ -1090,7 +1106,7 @@ constexpr int DVS = 3;                                        // virtual ranks w
 constexpr int SMEM = DVS * NI * T * 16;                       // 192 KB
 }  // namespace l2
 
-template <int VM>
+template <int VM, bool RING = false>
 __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
   using namespace res;
   using namespace l2;
@@ -1208,14 +1224,14 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
         if (o == c) { nb = c; break; }
         c = o;
       }
-      nb = wait_chunk(A, nb);
+      if constexpr (RING) nb = wait_chunk(A, nb);
       for (int cc = 0; cc < CW; ++cc) st_cl_u32(mapa(brk, cc), (uint32_t)nb);
     }
     cl_arrive();
     cl_wait();
     const int b = s_brick;
     if (b >= A.nsolve) break;
-    const long long bs = A.ring ? (long long)(b % A.ring) : (long long)b;   // data slot
+    const long long bs = RING ? (long long)(b % A.ring) : (long long)b;   // data slot
     float* const X = A.x + bs * n;
 
     // ---- brick load: k_resident's fused assembly, per virtual rank
@@ -1230,7 +1246,7 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
 #pragma unroll
       for (int it = 0; it < NI; ++it) {
         const int zl = it / 2, y = 2 * j + (it & 1);
-        const QuadOut o = assemble_quad<TV, N, N>(A, bs * n, 0, vr * ZS + zl, y, 4 * qx, iacc[vv]);
+        const QuadOut o = assemble_quad<TV, N, N, RING>(A, bs * n, 0, vr * ZS + zl, y, 4 * qx, iacc[vv]);
         fixm[vv] |= o.fm << (4 * it);
         const long long g = gi(vr, it);
         if (vv < DVS) s_dv[(vv * NI + it) * T + t] = o.dv;
@@ -1425,10 +1441,11 @@ __global__ void __launch_bounds__(l2::T, 1) k_l2res(ResArgs A, L2Args Wk) {
       }
     }
     // the brick's global arrays are reused by the next brick: everyone done reading them
-    if (A.ring) __threadfence();
+    if constexpr (RING) __threadfence();
     cl_arrive();
     cl_wait();
-    if (A.ring && rank == 0 && t == 0) brick_done(A, b);
+    if constexpr (RING)
+      if (rank == 0 && t == 0) brick_done(A, b);
   }
   if (Wk.done && t == 0) atomicAdd(Wk.done, 1);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1485,13 +1502,13 @@ int l2res_workers(int ncl_res) {
 
 size_t l2res_bytes_per_worker() { return (size_t)7 * l2::PL * l2::N * sizeof(float); }
 
-template <int VM>
+template <int VM, bool RING>
 static cudaError_t launch_l2res_vm(const ResArgs& A, const L2Args& W, int nw, cudaStream_t s) {
   static bool init[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   if (!init[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_l2res<VM>, cudaFuncAttributeMaxDynamicSharedMemorySize, l2::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_l2res<VM, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, l2::SMEM);
     if (e != cudaSuccess) return e;
     init[dev] = true;
   }
@@ -1507,13 +1524,15 @@ static cudaError_t launch_l2res_vm(const ResArgs& A, const L2Args& W, int nw, cu
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_l2res<VM>, A, W);
+  return cudaLaunchKernelEx(&cfg, k_l2res<VM, RING>, A, W);
 }
 
 cudaError_t launch_l2res(const ResArgs& A, const L2Args& W, int nw, cudaStream_t s) {
   if (nw <= 0) return cudaSuccess;
-  if (A.vdt == VM_U16) return launch_l2res_vm<VM_U16>(A, W, nw, s);
-  if (A.vdt == VM_F32) return launch_l2res_vm<VM_F32>(A, W, nw, s);
+  if (A.vdt == VM_U16)
+    return A.ring ? launch_l2res_vm<VM_U16, true>(A, W, nw, s) : launch_l2res_vm<VM_U16, false>(A, W, nw, s);
+  if (A.vdt == VM_F32)
+    return A.ring ? launch_l2res_vm<VM_F32, true>(A, W, nw, s) : launch_l2res_vm<VM_F32, false>(A, W, nw, s);
   return cudaErrorNotSupported;
 }
 

@@ -35,6 +35,7 @@ struct Plan {
   int one;              // 1: one-pass CG (pass A only, see passA.cu), 0: passes A + B
   int rc;               // right-hand sides per pass-A CTA (0: automatic, passA_rc)
   int ns;               // pass-A TMA ring depth (0: kStages; passA_stages)
+  int pf;               // pass-A L2 prefetch distance in planes beyond the ring (0: off)
   int lastdec;          // one-pass mode, large bricks (U >= kLastDecMinU): the last CTA of a
                         // (rhs, brick) to finish pass k sums the U partials once and stores the
                         // decision of pass k+1 (Bufs.SD) instead of every CTA of pass k+1
