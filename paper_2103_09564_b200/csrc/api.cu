@@ -155,7 +155,7 @@ rw::Plan make_plan(int B, rw_dims d, int R) {
   P.one = 0;
   P.lastdec = 0;
   P.rc = env_int("RW_PASSA_RC", 0);   // A/B knob: right-hand sides per pass-A CTA
-  P.pf = env_int("RW_PASSA_PF", 0);   // A/B knob: L2 prefetch distance (planes beyond the ring)
+  P.pf = env_int("RW_PASSA_PF", -1);  // L2 prefetch distance (planes beyond the ring; -1: auto)
   P.ns = 0;
   P.hxv = P.hx;
   P.TXhv = P.TXh;

@@ -491,8 +491,11 @@ int passA_rc(const Plan& P) {
 // at 12 % warp occupancy with 4 stages, ncu gpurun_out/c4)
 void passA_stages(Plan& P) {
   P.ns = kStages;
-  if (!P.one) return;
-  if (a_layout(P, passA_rc(P), P.vm).total > 112 * 1024) P.ns = kStages - 1;
+  if (P.one && a_layout(P, passA_rc(P), P.vm).total > 112 * 1024) P.ns = kStages - 1;
+  // L2 prefetch of the boxes 2 planes beyond the ring where the ring is one stage short
+  // (measured, tools/gpu_pf.sh: cfg4 822 -> 757 ms at 3 stages; with 4 stages it costs --
+  // cfg3 1577 -> 1707 ms, cfg2 streaming 148 -> 144 G); RW_PASSA_PF overrides
+  if (P.pf < 0) P.pf = P.ns < kStages ? 2 : 0;
 }
 
 size_t passA_smem(const Plan& P, int rc) { return (size_t)a_layout(P, rc, P.vm).total; }
