@@ -25,4 +25,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_re
 SCMD="python bench.py --solver streaming --host-loop --steps 1 --warmup 3 --no-cpu-baseline --no-rows --no-configs"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_passA -s 60 -c 1 -o $O/passA $SCMD > $O/ncu3.log 2>&1; echo "ncu3 rc=$?"
 fi
+# summaries on the box (gpurun copies back at most 64 MiB): the .ncu-rep files are dropped
+# unless KEEP_REP=1
+if [ "${SKIP_FULL:-0}" = "0" ]; then
+python tools/ncu_summary.py --launches $O/launches.csv --rep $O/resident.ncu-rep $O/passA.ncu-rep --bench $O/bench.json --out $O/summary > /dev/null 2>&1; echo "summary rc=$?"
+timeout 300 python tools/ncu_hot.py $O/resident.ncu-rep 40 > $O/resident_hot.txt 2>&1
+timeout 300 python tools/ncu_hot.py $O/passA.ncu-rep 40 > $O/passA_hot.txt 2>&1
+[ "${KEEP_REP:-0}" = "1" ] || rm -f $O/*.ncu-rep
+fi
 ls -la $O
