@@ -176,6 +176,11 @@ rw_status rw_solve_bricks(int32_t batch, rw_dims d, const void* vol, rw_dtype dt
  *   inputs go host->device on a copy stream while chunk c is solved (separate launches on
  *   two alternating compute streams and workspaces) and chunk c-1's results go
  *   device->host.  Device memory is O(ring) / O(chunk), plus per-brick scalars of the batch.
+ *   Library-owned host memory: a per-thread, per-device host-mapped array of chunk-done
+ *   flags (4 B per chunk, grown as needed, kept across calls) and one pinned int.  A tool
+ *   that serialises launches (CUDA_INJECTION64_PATH set, CUDA_LAUNCH_BLOCKING=1) gets the
+ *   chunked pipeline; a persistent launch whose inputs do not arrive within 2 s leaves and
+ *   the call redoes the batch on the chunked pipeline (same results).
  *   vol_h, fixed_h, values_h   host [batch][n] (page-locked for overlap; pageable works).
  *   prob_h / labels_h          out host fp32 / u8 [batch][n], either may be NULL.
  *   iters_h out host int32 [batch];  resid_h, status_h  out host [batch] or NULL.
