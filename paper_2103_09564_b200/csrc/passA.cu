@@ -41,8 +41,12 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   if (Bf.kdev) k = *reinterpret_cast<const volatile int*>(Bf.kdev);   // device-driven loop
   __shared__ float s_beta[RC], s_alpha[RC];
   __shared__ int s_act[RC];
-  const int u = blockIdx.x, b = blockIdx.y;
-  const int rbase = r_first + blockIdx.z * RC;
+  // grid.x = U units x nl rhs layers, the layer fastest: the CTAs of the nl layers of one unit
+  // are launched together and stream the same tile's operator boxes (intensities, dinv) at
+  // about the same planes, so all but the first read them from L2
+  const int nl = gridDim.x / P.U;
+  const int u = blockIdx.x / nl, b = blockIdx.y;
+  const int rbase = r_first + (blockIdx.x % nl) * RC;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const ALayout L = a_layout(P, RC, VM);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -451,7 +455,7 @@ static cudaError_t launch_one(const Plan& P, const Bufs& Bf, const Ctl& C, int k
     if (e != cudaSuccess) return e;
     attr = L.total;
   }
-  k_passA<RC, VM, ONE, NS><<<dim3(P.U, P.B, nz), P.threads, L.total, s>>>(P, Bf, C, k, r0, M);
+  k_passA<RC, VM, ONE, NS><<<dim3(P.U * nz, P.B, 1), P.threads, L.total, s>>>(P, Bf, C, k, r0, M);
   return cudaGetLastError();
 }
 
