@@ -332,10 +332,10 @@ Prof g_prof;
 size_t dtype_size_(rw_dtype t) { return t == RW_U8 ? 1 : (t == RW_F32 ? 4 : 2); }
 
 // share of a batch given to the streaming passes next to the resident clusters (per mille,
-// RW_OPT_COSCHED).  Off by default: measured on B200 (tools/cosched_sweep.py), any
-// concurrent streaming traffic slows the latency-bound clusters by ~30 % (their DSMEM /
-// mbarrier round trips share the memory fabric) -- 512 cfg2 bricks: 70 ms alone, 91-106 ms
-// co-scheduled at 4-26 % streaming share.
+// RW_OPT_COSCHED).  Off by default: measured on B200 (tools/cosched_sweep.py, fork before the
+// resident launch), concurrent streaming traffic slows the latency-bound clusters -- 512 cfg2
+// bricks: 55.4 ms with the L2 workers, 76-92 ms co-scheduled at a 4-20 % streaming share
+// (profiles/r02/r02_h_cosched.jsonl).
 int g_cosched_pm = 0;
 
 int cosched_candidate(int B, rw_dims d, int nrhs, bool weights_given) {
@@ -588,10 +588,10 @@ rw_status solve_core(int32_t batch, rw_dims d, const void* vol, rw_dtype dtype, 
       RW_CK(cudaStreamWaitEvent(s2, fork, 0));
     }
 #ifdef RW_RES_TIMING
-    // debug builds only (tools/ab_res.sh): phase cycle sums of the resident kernel
-    static long long* dbg = nullptr;
+    // debug builds only (tools/ab_res.sh): phase cycle sums of the resident kernel, in the
+    // streaming q region of the workspace (unused by the resident solver; >= 2 n floats)
+    long long* const dbg = reinterpret_cast<long long*>(ws + Lw.q);
     if (getenv("RW_DEBUG_RES_TIMING")) {
-      if (!dbg) RW_CK(cudaMalloc(&dbg, 16 * 8 * sizeof(long long)));
       RW_CK(cudaMemsetAsync(dbg, 0, 16 * 8 * sizeof(long long), s));
       A.dbg = dbg;
     }
