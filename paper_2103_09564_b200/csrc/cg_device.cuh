@@ -126,6 +126,64 @@ __device__ __forceinline__ float stencil1(float p, float xp, float xm, float yp,
   return dv == 0.f ? 0.f : q;
 }
 
+// ---- packed fp32 pairs for pass A (sm_100a FFMA2 / FADD2 / FMUL2): every lane computes
+// exactly the IEEE round-to-nearest result of the scalar op it replaces (negation is exact,
+// so a - b == a + (-b)), so the packed forms are bit-identical to pnew4 / fma4 / mul4 /
+// stencil1 / grady and only take fewer issue slots.  A float4 quad is the register pairs
+// (x, y) and (z, w).
+__device__ __forceinline__ float2 pa_lo(float4 v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 pa_hi(float4 v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float4 pa_cat(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
+__device__ __forceinline__ float2 pa_sub(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float4 pa_fma4(float a, float4 x, float4 y) {     // = fma4
+  const float2 aa = make_float2(a, a);
+  return pa_cat(__ffma2_rn(aa, pa_lo(x), pa_lo(y)), __ffma2_rn(aa, pa_hi(x), pa_hi(y)));
+}
+__device__ __forceinline__ float4 pa_mul4(float4 a, float4 b) {             // = mul4
+  return pa_cat(__fmul2_rn(pa_lo(a), pa_lo(b)), __fmul2_rn(pa_hi(a), pa_hi(b)));
+}
+__device__ __forceinline__ float4 pa_pnew4(float be, float4 po, float4 d, float4 r) {   // = pnew4
+  return pa_fma4(be, po, pa_mul4(d, r));
+}
+// grady(a_e - b_e) of 4 lanes (= four grady(__fsub_rn(a, b)) calls)
+__device__ __forceinline__ float4 pa_grady4(float4 a, float4 b, float nbl2, float eps) {
+  const float2 n2 = make_float2(nbl2, nbl2), e2 = make_float2(eps, eps);
+  const float2 d0 = pa_sub(pa_lo(a), pa_lo(b)), d1 = pa_sub(pa_hi(a), pa_hi(b));
+  float2 t0 = __fmul2_rn(__fmul2_rn(d0, d0), n2), t1 = __fmul2_rn(__fmul2_rn(d1, d1), n2);
+  t0 = make_float2(ex2_approx(t0.x), ex2_approx(t0.y));
+  t1 = make_float2(ex2_approx(t1.x), ex2_approx(t1.y));
+  return pa_cat(__fadd2_rn(t0, e2), __fadd2_rn(t1, e2));
+}
+// q += wp (p - pp) then q += wm (p - pm), per lane (the +a / -a term pair of stencil1)
+__device__ __forceinline__ float4 pa_terms2(float4 q, float4 p, float4 pp, float4 pm, float4 wp,
+                                            float4 wm) {
+  float2 a = __ffma2_rn(pa_lo(wp), pa_sub(pa_lo(p), pa_lo(pp)), pa_lo(q));
+  float2 b = __ffma2_rn(pa_hi(wp), pa_sub(pa_hi(p), pa_hi(pp)), pa_hi(q));
+  a = __ffma2_rn(pa_lo(wm), pa_sub(pa_lo(p), pa_lo(pm)), a);
+  b = __ffma2_rn(pa_hi(wm), pa_sub(pa_hi(p), pa_hi(pm)), b);
+  return pa_cat(a, b);
+}
+// stencil1 of the quad p (x-neighbours xl / xr across it), same term order:
+// q = wx (p - p[+x]); q += wxm (p - p[-x]); +y, -y, +z, -z; q = 0 where dv == 0.
+// The x differences: p_i - p_{i+1} = d_i, and p_i - p_{i-1} = -d_{i-1} exactly.
+__device__ __forceinline__ float4 pa_stencil4(float4 p, float xl, float xr, float4 yp, float4 ym,
+                                              float4 zp, float4 zm, float4 wx, float4 wxm,
+                                              float4 wy, float4 wym, float4 wz, float4 wzm,
+                                              float4 dv) {
+  const float d0 = __fsub_rn(p.x, p.y), d1 = __fsub_rn(p.y, p.z), d2 = __fsub_rn(p.z, p.w);
+  const float d3 = __fsub_rn(p.w, xr), dm = __fsub_rn(p.x, xl);
+  float2 a = __fmul2_rn(pa_lo(wx), make_float2(d0, d1));
+  float2 b = __fmul2_rn(pa_hi(wx), make_float2(d2, d3));
+  a = __ffma2_rn(pa_lo(wxm), make_float2(dm, -d0), a);
+  b = __ffma2_rn(pa_hi(wxm), make_float2(-d1, -d2), b);
+  float4 q = pa_terms2(pa_cat(a, b), p, yp, ym, wy, wym);
+  q = pa_terms2(q, p, zp, zm, wz, wzm);
+  return make_float4(dv.x == 0.f ? 0.f : q.x, dv.y == 0.f ? 0.f : q.y,
+                     dv.z == 0.f ? 0.f : q.z, dv.w == 0.f ? 0.f : q.w);
+}
+
 // --------------------------------------------------------------------------- scalars
 // Decision of pass A(k) for one (rhs, brick), computed redundantly by every CTA of the
 // brick from the same partials in the same order (so every CTA agrees).

@@ -168,14 +168,14 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
   // r of this iteration at box offset `off` (one-pass: r_{k-1} - alpha_{k-1} q_{k-1})
   auto rk4 = [&](const unsigned char* st, int c, int off) -> float4 {
     const float4 r = ld4(F(st, L.oR + c * L.bRP) + off);
-    return qin ? fma4(-al[c], ld4(F(st, L.oQ + c * L.bRP) + off), r) : r;
+    return qin ? pa_fma4(-al[c], ld4(F(st, L.oQ + c * L.bRP) + off), r) : r;
   };
   auto rk1 = [&](const unsigned char* st, int c, int off) -> float {
     const float r = F(st, L.oR + c * L.bRP)[off];
     return qin ? __fmaf_rn(-al[c], F(st, L.oQ + c * L.bRP)[off], r) : r;
   };
   auto centre_pnew = [&](const unsigned char* st, int c) -> float4 {
-    return pnew4(be[c], ld4(F(st, L.oP + c * L.bRP) + crow), ld4(F(st, L.oD) + crow),
+    return pa_pnew4(be[c], ld4(F(st, L.oP + c * L.bRP) + crow), ld4(F(st, L.oD) + crow),
                  rk4(st, c, crow));
   };
   // normalised intensities of 4 consecutive intensity-box elements (one vector smem load)
@@ -196,6 +196,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
 #pragma unroll
     for (int e = 0; e < 4; ++e) g[e] = normv(g[e], gsc, gof);
   };
+  auto g4 = [](const float g[4]) { return make_float4(g[0], g[1], g[2], g[3]); };
   auto gvol1 = [&](const unsigned char* st, int off) -> float {
     return normv((float)reinterpret_cast<const T*>(st + L.oW)[off], gsc, gof);
   };
@@ -243,10 +244,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       if (t.z0 > 0) {
         float gm[4];
         gvol4(stg(0), vrow, gm);
-        wzm = make_float4(grady(__fsub_rn(gcur[0], gm[0]), nbl2, eps),
-                          grady(__fsub_rn(gcur[1], gm[1]), nbl2, eps),
-                          grady(__fsub_rn(gcur[2], gm[2]), nbl2, eps),
-                          grady(__fsub_rn(gcur[3], gm[3]), nbl2, eps));
+        wzm = pa_grady4(g4(gcur), g4(gm), nbl2, eps);
       }
     }
   }
@@ -295,7 +293,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
         for (int c = 0; c < RC; ++c) {
           float4 v = f4(0.f);
           if (act[c])
-            v = pnew4(be[c], ld4(F(s0, L.oP + c * L.bRP) + off), ld4(F(s0, L.oD) + off),
+            v = pa_pnew4(be[c], ld4(F(s0, L.oP + c * L.bRP) + off), ld4(F(s0, L.oD) + off),
                       rk4(s0, c, off));
           st4(spz + c * spc + brow * TXP + 4 + 4 * g, v);
         }
@@ -324,32 +322,19 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
       const float gl = hasl ? gvol1(s0, vrow - 1) : 0.f;
       const float gr = hasr ? gvol1(s0, vrow + 4) : 0.f;
       const bool hz = z + 1 < nz;
-      const float a0 = grady(__fsub_rn(gcur[1], gcur[0]), nbl2, eps);
-      const float a1 = grady(__fsub_rn(gcur[2], gcur[1]), nbl2, eps);
-      const float a2 = grady(__fsub_rn(gcur[3], gcur[2]), nbl2, eps);
-      const float a3 = hasr ? grady(__fsub_rn(gr, gcur[3]), nbl2, eps) : 0.f;
+      const float4 gc4 = g4(gcur);
+      wx = pa_grady4(make_float4(gcur[1], gcur[2], gcur[3], gr), gc4, nbl2, eps);
+      if (!hasr) wx.w = 0.f;
       const float am0 = hasl ? grady(__fsub_rn(gcur[0], gl), nbl2, eps) : 0.f;
-      wx = make_float4(a0, a1, a2, a3);
-      wxm = make_float4(am0, a0, a1, a2);
-      wy = hasu ? make_float4(grady(__fsub_rn(gu[0], gcur[0]), nbl2, eps),
-                              grady(__fsub_rn(gu[1], gcur[1]), nbl2, eps),
-                              grady(__fsub_rn(gu[2], gcur[2]), nbl2, eps),
-                              grady(__fsub_rn(gu[3], gcur[3]), nbl2, eps))
-                : f4(0.f);
-      wz = hz ? make_float4(grady(__fsub_rn(gz[0], gcur[0]), nbl2, eps),
-                            grady(__fsub_rn(gz[1], gcur[1]), nbl2, eps),
-                            grady(__fsub_rn(gz[2], gcur[2]), nbl2, eps),
-                            grady(__fsub_rn(gz[3], gcur[3]), nbl2, eps))
-              : f4(0.f);
+      wxm = make_float4(am0, wx.x, wx.y, wx.z);
+      wy = hasu ? pa_grady4(g4(gu), gc4, nbl2, eps) : f4(0.f);
+      wz = hz ? pa_grady4(g4(gz), gc4, nbl2, eps) : f4(0.f);
       st4(Wys + buf * TY * TX + xrow, wy);
       wym = f4(0.f);
       if (t.ly == 0 && hasd) {               // first tile row: -y weights from the halo row
         float gd[4];
         gvol4(s0, vrow - TXhv, gd);
-        wym = make_float4(grady(__fsub_rn(gcur[0], gd[0]), nbl2, eps),
-                          grady(__fsub_rn(gcur[1], gd[1]), nbl2, eps),
-                          grady(__fsub_rn(gcur[2], gd[2]), nbl2, eps),
-                          grady(__fsub_rn(gcur[3], gd[3]), nbl2, eps));
+        wym = pa_grady4(g4(gcur), g4(gd), nbl2, eps);
       }
     }
     __syncthreads();                          // p_new plane + Wys of plane z complete
@@ -380,16 +365,12 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
         const float xl = s[spo - 1];
         const float xr = s[spo + 4];
         const float4 p = pc[c];
-        float4 q;
-        q.x = stencil1(p.x, p.y, xl, yp.x, ym.x, pn[c].x, pm[c].x, wx.x, wxm.x, wy.x, wym.x, wz.x, wzm.x, dvc.x);
-        q.y = stencil1(p.y, p.z, p.x, yp.y, ym.y, pn[c].y, pm[c].y, wx.y, wxm.y, wy.y, wym.y, wz.y, wzm.y, dvc.y);
-        q.z = stencil1(p.z, p.w, p.y, yp.z, ym.z, pn[c].z, pm[c].z, wx.z, wxm.z, wy.z, wym.z, wz.z, wzm.z, dvc.z);
-        q.w = stencil1(p.w, xr, p.z, yp.w, ym.w, pn[c].w, pm[c].w, wx.w, wxm.w, wy.w, wym.w, wz.w, wzm.w, dvc.w);
+        const float4 q = pa_stencil4(p, xl, xr, yp, ym, pn[c], pm[c], wx, wxm, wy, wym, wz, wzm, dvc);
         const long long ov = (long long)(rbase + c) * BN + o;
         if (xup) {
           const float4 po = ld4(F(s0, L.oP + c * L.bRP) + crow);
           const float4 xo = ONE ? xz[c] : ld4(F(s0, L.oX + c * L.bX) + xrow);
-          st4(Bf.x + ov, fma4(al[c], po, xo));
+          st4(Bf.x + ov, pa_fma4(al[c], po, xo));
         }
         st4(Pnew + ov, p);
         st4(Qout + ov, q);
@@ -397,7 +378,7 @@ k_passA(Plan P, Bufs Bf, Ctl C, int k, int r_first, const __grid_constant__ Maps
         if (ONE) {
           const float4 rk = rk4(s0, c, crow);
           st4(Rout + ov, rk);
-          const float4 dr = mul4(dvc, rk), dq = mul4(dvc, q);
+          const float4 dr = pa_mul4(dvc, rk), dq = pa_mul4(dvc, q);
           acc1[c][0] += (double)dot4f(rk, dr);
           acc1[c][1] += (double)dot4f(rk, rk);
           acc1[c][2] += (double)dot4f(q, dr);
