@@ -329,6 +329,31 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
                               uint8_t* labels_h, rw_hier_stats* stats, void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * rw_hier_segment_labels_ooc -- multi-class hierarchical segmentation out of core (SURVEY
+ *   8(f) f1; P:107 one run per class, the class with the largest foreground probability wins;
+ *   P:319 homogeneity pruning only; P:105 / P:261 constant device memory).  K complete
+ *   rw_hier_segment_ooc runs in one workspace, class k = 1..K as the foreground: the host
+ *   class seeds travel through the queue unchanged and become class k's 0 / 1 / 2 seeds on
+ *   the device right after each H2D copy; the output slabs of run k are merged on the host
+ *   into the running maximum best_h and its class labels_h (strict >, so ties go to the
+ *   lowest class id, reading R11).  dt pruning is disabled whatever cfg.t_bin says.  On cubic
+ *   s 2^k volumes best_h / labels_h equal rw_hier_segment_labels' best / out_labels bit for
+ *   bit.  The intensity pyramid is rebuilt by every class run (K passes over the host volume).
+ *   class_seeds_h  host u8 [nz][ny][nx]: 0 unseeded, 1..K class seeds (any other nonzero
+ *               value acts as a background seed for every class).
+ *   best_h      out host fp32 [nz][ny][nx]: the winning class's probability (non-NULL).
+ *   labels_h    out host u8 [nz][ny][nx]: argmax class 1..K (non-NULL).
+ *   stats       out host (nullable): K entries, one per class run.
+ *   Other arguments, blocking behaviour and errors as rw_hier_segment_ooc; RW_EINVAL for K
+ *   outside 2..255 or a NULL output.
+ * ---------------------------------------------------------------------------------- */
+rw_status rw_hier_segment_labels_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_dims d,
+                                     const uint8_t* class_seeds_h, int32_t K, rw_hier_config cfg,
+                                     int64_t pool_bricks, struct rw_queue* q, void* workspace,
+                                     size_t ws_bytes, float* best_h, uint8_t* labels_h,
+                                     rw_hier_stats* stats, void* stream);
+
+/* ------------------------------------------------------------------------------------
  * rw_hier_segment_labels -- multi-class hierarchical segmentation (P:107
  *   "The method is run once for each class, where only seeds for the current class are
  *   considered foreground and all other seeds as background ... the class of a voxel is

@@ -79,6 +79,8 @@ SIGNATURES = {
     "rw_hier_ooc_queue_bytes": (SZ, [rw_dims, I32, rw_hier_config]),
     "rw_hier_segment_ooc": (I32, [P, I32, rw_norm, rw_dims, P, rw_hier_config, C.c_int64, P, P,
                                   SZ, P, P, C.POINTER(rw_hier_stats), P]),
+    "rw_hier_segment_labels_ooc": (I32, [P, I32, rw_norm, rw_dims, P, I32, rw_hier_config,
+                                         C.c_int64, P, P, SZ, P, P, C.POINTER(rw_hier_stats), P]),
     "rw_get_option": (C.c_int64, [I32]),
     "rw_resident_available": (I32, [rw_dims, I32]),
 }

@@ -469,6 +469,62 @@ def hier_segment_ooc(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True
     return prob, lab, stats
 
 
+def hier_segment_labels_ooc(vol, labels, K, s=32, e=1.25, t_hom=0.3, prune=True, beta=100.0,
+                            eps=1e-6, tol=1e-6, max_iter=5000, tol_mode=0, norm=None,
+                            max_batch=1024, pool_bricks=None, device="cuda", queue=None,
+                            workspace=None, stream=None):
+    """rw_hier_segment_labels_ooc: K one-vs-rest out-of-core runs and the
+    argmax class, volume / class seeds / outputs in HOST memory.  vol: numpy [nz, ny, nx], any
+    dims; labels: numpy u8 in 0..K.  Returns (best fp32 numpy, labels u8 numpy in 1..K, list of
+    K stats dicts)."""
+    import numpy as np
+    vol = np.ascontiguousarray(vol)
+    labels = np.ascontiguousarray(labels, dtype=np.uint8)
+    if vol.ndim != 3 or labels.shape != vol.shape:
+        raise ValueError("hier_segment_labels_ooc: vol and labels must be 3-D arrays of one shape")
+    dt = NP_DTYPES[str(vol.dtype)]
+    nz, ny, nx = vol.shape
+    d = rw_dims(nx, ny, nz)
+    tdt = {0: torch.uint8, 1: torch.uint16, 2: torch.int16, 3: torch.float32}[dt]
+    sc, of = norm or DEFAULT_NORM[tdt]
+    cfg = rw_hier_config(s, e, t_hom, -1.0, int(prune), beta, eps, tol, max_iter, tol_mode,
+                         max_batch, 0, 0.01)
+    if pool_bricks is None:
+        nb0 = -(-nx // s) * -(-ny // s) * -(-nz // s)
+        pool_bricks = nb0 // 16 + 4096
+    need = lib().rw_hier_ooc_workspace_bytes(d, dt, cfg, int(pool_bricks))
+    qb = lib().rw_hier_ooc_queue_bytes(d, dt, cfg)
+    if need == 0 or qb == 0:
+        raise ValueError("hier_segment_labels_ooc: need s % 4 == 0, e in (1, 2] with "
+                         "floor(e*s) % 4 == 0")
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need, device)
+    own_q = queue is None
+    if own_q:
+        queue = Queue(qb, depth=2)
+    best = np.empty(vol.shape, np.float32)
+    lab = np.empty(vol.shape, np.uint8)
+    st = (rw_hier_stats * int(K))()
+    try:
+        check(lib().rw_hier_segment_labels_ooc(C.c_void_p(vol.ctypes.data), dt, rw_norm(sc, of), d,
+                                               C.c_void_p(labels.ctypes.data), int(K), cfg,
+                                               int(pool_bricks), queue._q, _ptr(workspace),
+                                               workspace.numel(), C.c_void_p(best.ctypes.data),
+                                               C.c_void_p(lab.ctypes.data), st,
+                                               _stream(stream, workspace.device)),
+              "rw_hier_segment_labels_ooc")
+    finally:
+        if own_q:
+            queue.close()
+    stats = []
+    for x in st:
+        sd = _stats_dict(x)
+        sd["pool_used"] = int(x.pool_used)
+        sd["ms"] = {"pyramid": x.ms_pyramid, "levels": x.ms_levels, "output": x.ms_output}
+        stats.append(sd)
+    return best, lab, stats
+
+
 def _stats_dict(st):
     L = st.levels
     out = {f: [int(getattr(st, f)[l]) for l in range(L)]

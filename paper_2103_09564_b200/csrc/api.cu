@@ -49,6 +49,7 @@ cudaError_t launch_weights_ex(const void*, int, float, float, int, int, int, int
                               float, int, float*, void*, int, cudaStream_t);
 cudaError_t launch_ooc_seedor0(const uint8_t*, int, int, const OocGeo&, uint8_t*, int, cudaStream_t);
 cudaError_t launch_ooc_seedor(const uint8_t*, int, const OocGeo&, uint8_t*, int, cudaStream_t);
+cudaError_t launch_ooc_remap(uint8_t*, long long, int, int, cudaStream_t);
 cudaError_t launch_ooc_materialize(const int4*, int, int, const OocGeo&, int*, float*, cudaStream_t);
 cudaError_t launch_ooc_gather(const void*, int, const uint8_t*, const uint8_t*, int, bool,
                               const OocGeo&, const int*, const float*, int, int, int, int,
@@ -1805,6 +1806,37 @@ void copy_slab(void* dst, void* ctx_) {
   rw::host_parallel_copy((char*)dst + c.vbytes, c.seeds, c.sbytes);
 }
 
+// Multi-class merge of one staged output slab ("the class of a voxel is the one that
+// maximizes the foreground probability"; ties to the lowest class id, reading R11): class
+// `cls`'s probabilities `src` against the running maximum `best` / its class `lab`.  Class 1
+// initialises both.  Split over host threads like parallel_copy.
+void merge_best(float* best, uint8_t* lab, const float* src, size_t n, int cls) {
+  unsigned nt = std::thread::hardware_concurrency();
+  nt = std::max(1u, std::min(nt, 16u));
+  if ((size_t)nt * (1u << 18) > n) nt = (unsigned)std::max<size_t>(1, n >> 18);
+  const size_t per = (n + nt - 1) / nt;
+  auto work = [=](size_t a, size_t b) {
+    if (cls == 1) {
+      std::memcpy(best + a, src + a, (b - a) * sizeof(float));
+      std::memset(lab + a, 1, b - a);
+    } else {
+      for (size_t i = a; i < b; ++i)
+        if (src[i] > best[i]) {
+          best[i] = src[i];
+          lab[i] = (uint8_t)cls;
+        }
+    }
+  };
+  if (nt < 2) { work(0, n); return; }
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t) {
+    const size_t a = (size_t)t * per, b = std::min(n, a + per);
+    if (a >= b) break;
+    th.emplace_back(work, a, b);
+  }
+  for (auto& x : th) x.join();
+}
+
 }  // namespace
 
 size_t rw_hier_ooc_workspace_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg,
@@ -1822,10 +1854,15 @@ size_t rw_hier_ooc_queue_bytes(rw_dims d, rw_dtype dtype, rw_hier_config cfg) {
   return std::max(win, std::min((size_t)d.nz, (size_t)16) * plane);   // as ooc_plan's oz[0]
 }
 
-rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_dims d,
+// One out-of-core hierarchical run.  cls = 0: rw_hier_segment_ooc as documented (seeds_h is
+// 0 / 1 fg / 2 bg; prob_h / labels_h the binary outputs).  cls >= 1 (one class of
+// rw_hier_segment_labels_ooc): seeds_h holds class labels 0..K, turned into class cls's
+// one-vs-rest seeds on the device right after each H2D copy (k_ooc_remap); prob_h is the
+// running maximum and labels_h its class, merged on the host as the output slabs arrive.
+static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_dims d,
                               const uint8_t* seeds_h, rw_hier_config cfg, int64_t pool_bricks,
                               struct rw_queue* q, void* workspace, size_t ws_bytes, float* prob_h,
-                              uint8_t* labels_h, rw_hier_stats* stats, void* stream) {
+                              uint8_t* labels_h, rw_hier_stats* stats, void* stream, int cls) {
   if (!vol_h || !seeds_h || !q || !workspace)
     return fail(RW_EINVAL, "rw_hier_segment_ooc: vol, seeds, queue and workspace must be non-NULL");
   if (dtype < RW_U8 || dtype > RW_F32) return fail(RW_EINVAL, "rw_hier_segment_ooc: bad dtype");
@@ -1873,6 +1910,9 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
       if (r != RW_OK) return r;
       r = rw_build_pyramid_slab(dev, dtype, d, z0, nzs, 1, &lev1, stream);
       if (r != RW_OK) return r;
+      if (cls > 0)
+        RW_TIMED(RW_K_HIER, s, 1, rw::launch_ooc_remap((uint8_t*)dev + sc.vbytes,
+                                                       (long long)sc.sbytes, cls, sms, s));
       RW_TIMED(RW_K_HIER, s, 1, rw::launch_ooc_seedor0((const uint8_t*)dev + sc.vbytes, z0, nzs, G,
                                                        (uint8_t*)PTR(L.bits[1]), sms, s));
       r = rw_queue_release(q, sid, stream);
@@ -1976,6 +2016,9 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
       if (r != RW_OK) return r;
       wvol = dev;
       wseed = (const uint8_t*)dev + vb;
+      if (cls > 0)
+        RW_TIMED(RW_K_HIER, s, 1, rw::launch_ooc_remap((uint8_t*)dev + vb,
+                                                       (long long)nb * wxp * wy * wz, cls, sms, s));
     }
     RW_TIMED(RW_K_HIER, s, 1,
              rw::launch_ooc_gather(l == 0 ? nullptr : PTR(L.lev[l]), (int)dtype,
@@ -2102,7 +2145,7 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
     const int nsl = rw::queue_depth(q);
     std::vector<cudaEvent_t> oev(nsl);
     for (auto& e : oev) RW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    struct Pend { int slot; void* dst; size_t bytes; };
+    struct Pend { int slot; void* dst; size_t bytes; uint8_t* lab; };
     std::vector<Pend> pend;
     int nxt = 0;
     rw_status r = RW_OK;
@@ -2110,10 +2153,13 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
       const Pend c = pend.front();
       pend.erase(pend.begin());
       RW_CK(cudaEventSynchronize(oev[c.slot]));
-      rw::host_parallel_copy(c.dst, rw::queue_host_slot(q, c.slot), c.bytes);
+      if (c.lab)
+        merge_best((float*)c.dst, c.lab, (const float*)rw::queue_host_slot(q, c.slot), c.bytes / 4, cls);
+      else
+        rw::host_parallel_copy(c.dst, rw::queue_host_slot(q, c.slot), c.bytes);
       return RW_OK;
     };
-    auto stage = [&](void* dst, const void* src, size_t bytes) -> rw_status {
+    auto stage = [&](void* dst, const void* src, size_t bytes, uint8_t* lab) -> rw_status {
       if ((int)pend.size() == nsl) {
         rw_status rr = drain();
         if (rr != RW_OK) return rr;
@@ -2121,7 +2167,7 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
       const int sl = nxt++ % nsl;
       RW_CK(cudaMemcpyAsync(rw::queue_host_slot(q, sl), src, bytes, cudaMemcpyDeviceToHost, s));
       RW_CK(cudaEventRecord(oev[sl], s));
-      pend.push_back({sl, dst, bytes});
+      pend.push_back({sl, dst, bytes, lab});
       return RW_OK;
     };
     for (int Z0 = 0; Z0 < G.nz[0]; Z0 += p.oz[0]) {
@@ -2141,10 +2187,15 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
                  rw::launch_ooc_out(m, G, PT, pool, m == k ? nullptr : (const float*)PTR(L.out[m + 1]),
                                     m == k ? 0 : z0[m + 1], z0[m], zc[m],
                                     (!last || prob_h) ? (float*)PTR(L.out[m]) : nullptr,
-                                    (last && labels_h) ? (uint8_t*)PTR(L.lab) : nullptr, sms, s));
+                                    (last && labels_h && cls == 0) ? (uint8_t*)PTR(L.lab) : nullptr, sms, s));
       }
-      if (prob_h) { r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4); if (r != RW_OK) return r; }
-      if (labels_h) { r = stage(labels_h + (size_t)Z0 * pl0, PTR(L.lab), (size_t)zc[0] * pl0); if (r != RW_OK) return r; }
+      if (cls > 0) {   // class cls's probabilities merged into the running maximum / class
+        r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4, labels_h + (size_t)Z0 * pl0);
+        if (r != RW_OK) return r;
+        continue;
+      }
+      if (prob_h) { r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4, nullptr); if (r != RW_OK) return r; }
+      if (labels_h) { r = stage(labels_h + (size_t)Z0 * pl0, PTR(L.lab), (size_t)zc[0] * pl0, nullptr); if (r != RW_OK) return r; }
     }
     while (!pend.empty()) {
       r = drain();
@@ -2155,6 +2206,34 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
   st.ms_output = wall() - t0;
   st.pool_used = next_slot;
   if (stats) *stats = st;
+  return RW_OK;
+}
+
+rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_dims d,
+                              const uint8_t* seeds_h, rw_hier_config cfg, int64_t pool_bricks,
+                              struct rw_queue* q, void* workspace, size_t ws_bytes, float* prob_h,
+                              uint8_t* labels_h, rw_hier_stats* stats, void* stream) {
+  return hier_ooc_run(vol_h, dtype, nm, d, seeds_h, cfg, pool_bricks, q, workspace, ws_bytes,
+                      prob_h, labels_h, stats, stream, 0);
+}
+
+rw_status rw_hier_segment_labels_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_dims d,
+                                     const uint8_t* class_seeds_h, int32_t K, rw_hier_config cfg,
+                                     int64_t pool_bricks, struct rw_queue* q, void* workspace,
+                                     size_t ws_bytes, float* best_h, uint8_t* labels_h,
+                                     rw_hier_stats* stats, void* stream) {
+  if (K < 2 || K > 255) return fail(RW_EINVAL, "rw_hier_segment_labels_ooc: K must be in 2..255");
+  if (!best_h || !labels_h)
+    return fail(RW_EINVAL, "rw_hier_segment_labels_ooc: best and labels must be non-NULL");
+  // K one-vs-rest runs, each a complete out-of-core run in the same workspace; the
+  // host keeps only the running maximum and its class
+  cfg.t_bin = -1.f;      // the dt assumption does not hold for non-binary segmentation
+  for (int c = 1; c <= K; ++c) {
+    rw_status r = hier_ooc_run(vol_h, dtype, nm, d, class_seeds_h, cfg, pool_bricks, q, workspace,
+                               ws_bytes, best_h, labels_h, stats ? stats + (c - 1) : nullptr,
+                               stream, c);
+    if (r != RW_OK) return r;
+  }
   return RW_OK;
 }
 

@@ -95,6 +95,31 @@ __global__ void k_ooc_seedor0(const uint8_t* __restrict__ seeds, int z0, int nzs
   }
 }
 
+// one-vs-rest seeds of class `cls` ("only seeds for the current class are considered
+// foreground and all other seeds as background"), in place on a freshly copied slot:
+// class label (0 unseeded, 1..K) -> 0 / 1 (fg: label == cls) / 2 (bg: any other class)
+__global__ void k_ooc_remap(uint8_t* __restrict__ seeds, long long n, int cls) {
+  // words when the slot's seed part is 4-byte aligned, bytes otherwise (odd u8 volumes)
+  const long long n4 = (reinterpret_cast<uintptr_t>(seeds) & 3u) == 0 ? n / 4 : 0;
+  uint32_t* s4 = reinterpret_cast<uint32_t*>(seeds);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t v = s4[i];
+    uint32_t o = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t c = (v >> (8 * b)) & 0xffu;
+      o |= (c == 0u ? 0u : (c == (uint32_t)cls ? 1u : 2u)) << (8 * b);
+    }
+    s4[i] = o;
+  }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint8_t c = seeds[i];
+    seeds[i] = c == 0 ? 0 : (c == cls ? 1 : 2);
+  }
+}
+
 // bits of level m -> level m+1 (any dims)
 __global__ void k_ooc_seedor(const uint8_t* __restrict__ in, int m, OocGeo G,
                              uint8_t* __restrict__ out) {
@@ -308,6 +333,12 @@ cudaError_t launch_ooc_seedor0(const uint8_t* seeds, int z0, int nzs, const OocG
                                uint8_t* out, int sms, cudaStream_t s) {
   const long long n = (long long)((z0 + nzs + 1) / 2 - z0 / 2) * G.ny[1] * G.nx[1];
   k_ooc_seedor0<<<grid_n(n, sms), 256, 0, s>>>(seeds, z0, nzs, G, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ooc_remap(uint8_t* seeds, long long n, int cls, int sms, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_ooc_remap<<<grid_n((n + 3) / 4, sms), 256, 0, s>>>(seeds, n, cls);
   return cudaGetLastError();
 }
 

@@ -87,3 +87,70 @@ def test_ooc_pool_full_is_an_error():
     vol, seeds = small_volume(64, seed=5)
     with pytest.raises(RWError, match="RW_ENOMEM"):
         rwb.hier_segment_ooc(vol, seeds, s=16, e=1.25, beta=50.0, prune=False, pool_bricks=4)
+
+
+def _ragged_classes(shape, seed, nseed):
+    """Three-class seeds on a ragged volume: the blob seeds are class 1, the outside seeds
+    class 2 (lower z half) or 3 (upper z half)."""
+    vol, seeds = _ragged_volume(shape, seed, nseed)
+    lab = seeds.copy()
+    z = np.arange(shape[0])[:, None, None]
+    lab[(seeds == 2) & (z >= shape[0] // 2)] = 3
+    return vol, lab
+
+
+@pytest.mark.parametrize("shape,prune", [((40, 56, 72), True), ((36, 64, 48), False)])
+def test_ooc_labels_ragged_match_oracle(shape, prune):
+    """rw_hier_segment_labels_ooc on ragged non-cubic volumes: K = 3 one-vs-rest
+    out-of-core runs (class seeds remapped on the device after the H2D copy, running maximum
+    merged on the host) against the oracle's K explicit runs: pruning decisions identical,
+    best = the winning class's probability within P_TOL, labels equal wherever the oracle's
+    top two classes differ by more than 1e-3 (reading R18)."""
+    vol, lab = _ragged_classes(shape, 2, 120)
+    best, got, st = rwb.hier_segment_labels_ooc(vol, lab, 3, s=16, e=1.25, beta=100.0, tol=1e-7,
+                                                max_iter=20000, prune=prune)
+    ref = ho.hier_segment_labels(vol, lab, 3, s=16, e=1.25, beta=100.0, tol=1e-10, prune=prune)
+    for k in range(3):
+        for l, rs in enumerate(ref["stats"][k]):
+            g = st[k]
+            assert g["solved"][l] == rs["solved"] and g["pruned_hom"][l] == rs["pruned_hom"]
+            assert g["pruned_dt"][l] == 0 and g["conflict"][l] == rs["conflict"]
+    assert got.min() >= 1 and got.max() <= 3
+    assert np.abs(best.astype(np.float64) - ref["prob"].max(0)).max() <= P_TOL
+    srt = np.sort(ref["prob"], axis=0)
+    sure = srt[-1] - srt[-2] > 1e-3
+    assert sure.mean() > 0.9
+    assert np.array_equal(got[sure], ref["labels"][sure])
+
+
+@pytest.mark.parametrize("D,s,prune", [(128, 16, True), (64, 16, False)])
+def test_ooc_labels_bitwise_equal_in_hbm_driver(D, s, prune):
+    """Cubic s 2^k: best / labels equal rw_hier_segment_labels' bit for bit, and the merged
+    best is the maximum over the K binary out-of-core runs on the one-vs-rest seeds."""
+    from test_hier_oracle import multi_volume
+    vol, lab = multi_volume(D, seed=7)
+    kw = dict(s=s, e=1.25, beta=50.0, tol=1e-6, prune=prune)
+    ref = rwb.hier_segment_labels(dev(vol), dev(lab), 3, **kw)
+    torch.cuda.synchronize()
+    best, got, st = rwb.hier_segment_labels_ooc(vol, lab, 3, **kw)
+    assert np.array_equal(best, ref["best"].cpu().numpy())
+    assert np.array_equal(got, ref["labels"].cpu().numpy())
+    for k in range(3):
+        assert st[k]["solved"] == ref["stats"][k]["solved"]
+    fields = []
+    for k in range(1, 4):
+        seeds = np.where(lab == k, 1, np.where(lab > 0, 2, 0)).astype(np.uint8)
+        p, _, _ = rwb.hier_segment_ooc(vol, seeds, t_bin=-1.0, **kw)
+        fields.append(p)
+    fields = np.asarray(fields)
+    assert np.array_equal(best, fields.max(0))
+    assert np.array_equal(got, (np.argmax(fields, 0) + 1).astype(np.uint8))   # ties -> lowest id
+
+
+def test_ooc_labels_rejects_bad_arguments():
+    from test_hier_oracle import multi_volume
+    vol, lab = multi_volume(32, seed=1)
+    with pytest.raises(RWError, match="K must be in 2..255"):
+        rwb.hier_segment_labels_ooc(vol, lab, 1, s=8, e=1.5)
+    with pytest.raises(ValueError):
+        rwb.hier_segment_labels_ooc(vol, lab[:-1], 3, s=8, e=1.5)
