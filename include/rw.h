@@ -338,7 +338,8 @@ rw_status rw_hier_segment_ooc(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
  *   into the running maximum best_h and its class labels_h (strict >, so ties go to the
  *   lowest class id, reading R11).  dt pruning is disabled whatever cfg.t_bin says.  On cubic
  *   s 2^k volumes best_h / labels_h equal rw_hier_segment_labels' best / out_labels bit for
- *   bit.  The intensity pyramid is rebuilt by every class run (K passes over the host volume).
+ *   bit.  Class 1's run builds the intensity pyramid; classes 2..K reuse it and stream only
+ *   the class seeds for their seed-bit pyramids (the workspace must not be touched in between).
  *   class_seeds_h  host u8 [nz][ny][nx]: 0 unseeded, 1..K class seeds (any other nonzero
  *               value acts as a background seed for every class).
  *   best_h      out host fp32 [nz][ny][nx]: the winning class's probability (non-NULL).

@@ -1896,20 +1896,26 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
   // from host memory through the queue in z-slabs of an even number of planes
   const size_t plane = (size_t)d.nx * d.ny;
   if (k >= 1) {
-    int SL = (int)std::min<size_t>(rw::queue_slot_bytes(q) / (plane * (es + 1)), (size_t)d.nz);
+    // classes 2..K of a multi-class run reuse class 1's intensity pyramid (same volume, same
+    // workspace; nothing else writes L.lev): their slabs carry the class seeds only
+    const bool with_vol = cls <= 1;
+    const size_t ves = with_vol ? es : 0;
+    int SL = (int)std::min<size_t>(rw::queue_slot_bytes(q) / (plane * (ves + 1)), (size_t)d.nz);
     SL &= ~1;
     if (SL < 2) SL = std::min(2, d.nz);
     void* lev1 = PTR(L.lev[1]);
     for (int z0 = 0; z0 < d.nz; z0 += SL) {
       const int nzs = std::min(SL, d.nz - z0);
       SlabCtx sc{(const char*)vol_h + (size_t)z0 * plane * es, seeds_h + (size_t)z0 * plane,
-                 (size_t)nzs * plane * es, (size_t)nzs * plane};
+                 (size_t)nzs * plane * ves, (size_t)nzs * plane};
       void* dev = nullptr;
       int32_t sid = 0;
       rw_status r = rw::queue_push_fill(q, sc.vbytes + sc.sbytes, copy_slab, &sc, s, &dev, &sid);
       if (r != RW_OK) return r;
-      r = rw_build_pyramid_slab(dev, dtype, d, z0, nzs, 1, &lev1, stream);
-      if (r != RW_OK) return r;
+      if (with_vol) {
+        r = rw_build_pyramid_slab(dev, dtype, d, z0, nzs, 1, &lev1, stream);
+        if (r != RW_OK) return r;
+      }
       if (cls > 0)
         RW_TIMED(RW_K_HIER, s, 1, rw::launch_ooc_remap((uint8_t*)dev + sc.vbytes,
                                                        (long long)sc.sbytes, cls, sms, s));
@@ -1919,11 +1925,13 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
       if (r != RW_OK) return r;
     }
     if (k >= 2) {
-      void* outs[16];
-      for (int m = 2; m <= k; ++m) outs[m - 2] = PTR(L.lev[m]);
-      const rw_dims d1{G.nx[1], G.ny[1], G.nz[1]};
-      rw_status r = rw_build_pyramid(lev1, dtype, d1, k - 1, outs, stream);
-      if (r != RW_OK) return r;
+      if (with_vol) {
+        void* outs[16];
+        for (int m = 2; m <= k; ++m) outs[m - 2] = PTR(L.lev[m]);
+        const rw_dims d1{G.nx[1], G.ny[1], G.nz[1]};
+        rw_status r = rw_build_pyramid(lev1, dtype, d1, k - 1, outs, stream);
+        if (r != RW_OK) return r;
+      }
       for (int m = 1; m < k; ++m)
         RW_TIMED(RW_K_HIER, s, 1, rw::launch_ooc_seedor((const uint8_t*)PTR(L.bits[m]), m, G,
                                                         (uint8_t*)PTR(L.bits[m + 1]), sms, s));
