@@ -113,7 +113,12 @@ def test_cfg3_full_size_residual_and_maximum_principle():
     rel = residual_fp64(g, p.fixed[0], p.values[0, 0], x, p.beta, p.eps)
     assert rel <= 1e-3, rel
     assert x.min() >= 0.0 and x.max() <= 1.0
-    for (z0, y0, x0) in [(100, 200, 200), (40, 300, 120), (200, 60, 400)]:
+    # five fixed sub-blocks (two in opposite volume corners) + seven seeded random ones
+    rng = np.random.default_rng(31)
+    blocks = [(100, 200, 200), (40, 300, 120), (200, 60, 400), (0, 0, 0), (232, 488, 488)]
+    blocks += [(int(rng.integers(0, 233)), int(rng.integers(0, 489)), int(rng.integers(0, 489)))
+               for _ in range(7)]
+    for (z0, y0, x0) in blocks:
         d = local_parity(g, p.fixed[0], p.values[0, 0], x, p.beta, p.eps, z0, y0, x0, 24)
         assert d <= 1e-4, ((z0, y0, x0), d)
 
@@ -148,7 +153,8 @@ def test_cfg4_full_size_multilabel_properties():
     fields = [prob[k].astype(np.float64) for k in range(lp.K - 1)] + [pK]
     for k, xk in enumerate(fields):
         vk = (seeds == k + 1).astype(np.float64)
-        for (z0, y0, x0) in [(100, 110, 90), (60, 128, 150), (150, 40, 120)]:
+        for (z0, y0, x0) in [(100, 110, 90), (60, 128, 150), (150, 40, 120), (0, 0, 0),
+                             (232, 232, 232), (20, 200, 60)]:
             d = local_parity(g, fixed, vk, xk, lp.beta, lp.eps, z0, y0, x0, 24)
             assert d <= 1e-4, (k, (z0, y0, x0), d)
 
