@@ -12,6 +12,8 @@
 //                             initial guess = parent field
 //   k_contract                N^-1: the brick's s^3 of the window solution into the level
 //                             field + min / max / conflict -> prunable
+#include <cstdlib>
+
 #include "rw_common.cuh"
 
 namespace rw {
@@ -172,6 +174,100 @@ __global__ void k_upsample(const float* __restrict__ P, int np, float* __restric
       // streaming (evict-first) store: the 34 GB output of a 2048^3 level would otherwise push
       // the parent rows out of L2 (ncu: 23 GB of parent re-reads, 30 % L2 hit rate)
       __stcs(reinterpret_cast<float4*>(out + row * D) + g, make_float4(o[0], o[1], o[2], o[3]));
+    }
+  }
+}
+
+// k_upsample with the quad's parent rows shared inside the thread: the 2 x 2 output rows
+// (2Z..2Z+1) x (2Y..2Y+1) read parent rows {Z-1, Z, Z+1} x {Y-1, Y, Y+1}; a thread x-interpolates
+// its 4 columns of those 9 rows once (27 8-byte loads instead of 48), then y, then z -- the
+// same fma per output as hier::sample, in the same order (x, y, z), so the values are
+// bit-identical.  Quads on the volume faces (clamped parent coordinates) take the row-by-row
+// form of k_upsample.
+__global__ void __launch_bounds__(256) k_upsample9(const float* __restrict__ P, int np,
+                                                   float* __restrict__ out, int D) {
+  const long long pl = (long long)np * np;
+  const int h = D / 2;
+  for (long long quad = blockIdx.x; quad < (long long)h * h; quad += gridDim.x) {
+    const int Z = (int)(quad / h), Y = (int)(quad % h);
+    int pz[2][2], py[2][2];
+    float fz[2], fy[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      hier::pcoord(2 * Z + a, np, pz[a][0], pz[a][1], fz[a]);
+      hier::pcoord(2 * Y + a, np, py[a][0], py[a][1], fy[a]);
+    }
+    const bool inner = pz[0][1] == pz[1][0] && py[0][1] == py[1][0] && pz[0][0] + 1 == pz[0][1] &&
+                       pz[1][0] + 1 == pz[1][1] && py[0][0] + 1 == py[0][1] && py[1][0] + 1 == py[1][1];
+    if (inner) {
+      const float* base = P + (long long)pz[0][0] * pl + (long long)py[0][0] * np;
+      for (int g = threadIdx.x; g < D / 4; g += blockDim.x) {
+        float c[3][3][4];                       // [parent z][parent y][x]
+        const bool xin = g > 0 && 2 * g + 2 <= np - 1;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const float* r = base + (long long)a * pl + (long long)b * np;
+            if (xin) {
+              const float2 u = *reinterpret_cast<const float2*>(r + 2 * g - 2);
+              const float2 v = *reinterpret_cast<const float2*>(r + 2 * g);
+              const float2 w = *reinterpret_cast<const float2*>(r + 2 * g + 2);
+              c[a][b][0] = __fmaf_rn(0.75f, v.x, (1.f - 0.75f) * u.y);
+              c[a][b][1] = __fmaf_rn(0.25f, v.y, (1.f - 0.25f) * v.x);
+              c[a][b][2] = __fmaf_rn(0.75f, v.y, (1.f - 0.75f) * v.x);
+              c[a][b][3] = __fmaf_rn(0.25f, w.x, (1.f - 0.25f) * v.y);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                int x0, x1;
+                float fx;
+                hier::pcoord(4 * g + e, np, x0, x1, fx);
+                c[a][b][e] = __fmaf_rn(fx, r[x1], (1.f - fx) * r[x0]);
+              }
+            }
+          }
+#pragma unroll
+        for (int zs = 0; zs < 2; ++zs)
+#pragma unroll
+          for (int ys = 0; ys < 2; ++ys) {
+            float o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float c0 = __fmaf_rn(fy[ys], c[zs][ys + 1][e], (1.f - fy[ys]) * c[zs][ys][e]);
+              const float c1 = __fmaf_rn(fy[ys], c[zs + 1][ys + 1][e], (1.f - fy[ys]) * c[zs + 1][ys][e]);
+              o[e] = __fmaf_rn(fz[zs], c1, (1.f - fz[zs]) * c0);
+            }
+            const long long row = (long long)(2 * Z + zs) * D + (2 * Y + ys);
+            __stcs(reinterpret_cast<float4*>(out + row * D) + g, make_float4(o[0], o[1], o[2], o[3]));
+          }
+      }
+    } else {
+      for (int sub = 0; sub < 4; ++sub) {
+        const int zs = sub >> 1, ys = sub & 1;
+        const long long row = (long long)(2 * Z + zs) * D + (2 * Y + ys);
+        const float* r00 = P + (long long)pz[zs][0] * pl + (long long)py[ys][0] * np;
+        const float* r01 = P + (long long)pz[zs][0] * pl + (long long)py[ys][1] * np;
+        const float* r10 = P + (long long)pz[zs][1] * pl + (long long)py[ys][0] * np;
+        const float* r11 = P + (long long)pz[zs][1] * pl + (long long)py[ys][1] * np;
+        for (int g = threadIdx.x; g < D / 4; g += blockDim.x) {
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            int x0, x1;
+            float fx;
+            hier::pcoord(4 * g + e, np, x0, x1, fx);
+            const float c00 = __fmaf_rn(fx, r00[x1], (1.f - fx) * r00[x0]);
+            const float c01 = __fmaf_rn(fx, r01[x1], (1.f - fx) * r01[x0]);
+            const float c10 = __fmaf_rn(fx, r10[x1], (1.f - fx) * r10[x0]);
+            const float c11 = __fmaf_rn(fx, r11[x1], (1.f - fx) * r11[x0]);
+            const float c0 = __fmaf_rn(fy[ys], c01, (1.f - fy[ys]) * c00);
+            const float c1 = __fmaf_rn(fy[ys], c11, (1.f - fy[ys]) * c10);
+            o[e] = __fmaf_rn(fz[zs], c1, (1.f - fz[zs]) * c0);
+          }
+          __stcs(reinterpret_cast<float4*>(out + row * D) + g, make_float4(o[0], o[1], o[2], o[3]));
+        }
+      }
     }
   }
 }
@@ -345,7 +441,9 @@ cudaError_t launch_seed_or(const uint8_t* in, int D, uint8_t* out, int sms, cuda
 
 cudaError_t launch_upsample(const float* P, int np, float* out, int D, int sms, cudaStream_t s) {
   const int th = D / 4 < 256 ? (D / 4 + 31) / 32 * 32 : 256;
-  k_upsample<<<grid_rows((long long)D * D / 4, sms), th, 0, s>>>(P, np, out, D);
+  static const int v = [] { const char* e = getenv("RW_UPSAMPLE_V"); return e ? atoi(e) : 9; }();
+  if (v == 9) k_upsample9<<<grid_rows((long long)D * D / 4, sms), th, 0, s>>>(P, np, out, D);
+  else k_upsample<<<grid_rows((long long)D * D / 4, sms), th, 0, s>>>(P, np, out, D);
   return cudaGetLastError();
 }
 

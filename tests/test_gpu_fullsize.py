@@ -63,8 +63,11 @@ def local_parity(g, fixed, values, x, beta, eps, z0, y0, x0, m):
 
 
 def _oracle_brick(sub):
-    """One cfg2 brick through the fp64 oracle (run in a worker process)."""
-    return ro.solve_problem(sub, tol=1e-10)["prob"]
+    """One cfg2 brick through the fp64 oracle (run in a worker process, one core each: the
+    BLAS dots of 16 workers would otherwise each try to use every core)."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        return ro.solve_problem(sub, tol=1e-10)["prob"]
 
 
 def test_cfg2_full_batch_in_bench_configuration():
