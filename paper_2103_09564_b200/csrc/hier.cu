@@ -178,97 +178,128 @@ __global__ void k_upsample(const float* __restrict__ P, int np, float* __restric
   }
 }
 
-// k_upsample with the quad's parent rows shared inside the thread: the 2 x 2 output rows
-// (2Z..2Z+1) x (2Y..2Y+1) read parent rows {Z-1, Z, Z+1} x {Y-1, Y, Y+1}; a thread x-interpolates
-// its 4 columns of those 9 rows once (27 8-byte loads instead of 48), then y, then z -- the
-// same fma per output as hier::sample, in the same order (x, y, z), so the values are
-// bit-identical.  Quads on the volume faces (clamped parent coordinates) take the row-by-row
-// form of k_upsample.
-__global__ void __launch_bounds__(256) k_upsample9(const float* __restrict__ P, int np,
-                                                   float* __restrict__ out, int D) {
+// Dense trilinear upsample of a large level as a z walk (same values as k_upsample /
+// hier::sample, bit for bit: per output the same three fma in the order x, y, z).
+// A work item is (z chunk, quad column Y, x segment): its threads own 4 consecutive output x
+// each and walk the parent planes p of the chunk.  A plane costs 3 parent-row reads (4 in the
+// clamped first / last column), one x-interpolation per row and one y-interpolation per output
+// row pair; with the previous plane's result carried in registers every step then emits the
+// output rows z = 2p-1 (f = .25) and z = 2p (f = .75), which both blend planes p-1 and p.
+// Against k_upsample (every output row re-reads and re-interpolates its 4 parent rows:
+// 44 instructions per output, 21 GB of DRAM reads for a 4.3 GB parent level, 18.1 ms for a
+// 2048^3 level, profiles/r02/r02_j_upsample.md) this is 15 instructions per output, 5.5 GB of
+// DRAM reads and 7.8 ms (5.1 TB/s) with the next plane's loads in flight during a step.
+// the 4 parent values a thread's 4 outputs can touch in one parent row: x = 2g-1 .. 2g+2,
+// clamped into the row (x = a, y, z, w = d)
+__device__ __forceinline__ float4 up_raw(const float* __restrict__ r, int g, int np) {
+  const float2 bc = *reinterpret_cast<const float2*>(r + 2 * g);
+  return make_float4(r[max(2 * g - 1, 0)], bc.x, bc.y, r[min(2 * g + 2, np - 1)]);
+}
+__device__ __forceinline__ void up_xrow(const float4 v, int g, int np, bool xin, float (&c)[4]) {
+  if (xin) {
+    c[0] = __fmaf_rn(0.75f, v.y, (1.f - 0.75f) * v.x);
+    c[1] = __fmaf_rn(0.25f, v.z, (1.f - 0.25f) * v.y);
+    c[2] = __fmaf_rn(0.75f, v.z, (1.f - 0.75f) * v.y);
+    c[3] = __fmaf_rn(0.25f, v.w, (1.f - 0.25f) * v.z);
+  } else {   // first / last group of the row: clamped parent coordinates, as hier::sample
+    auto pick = [&](int x) {
+      const int k = x - (2 * g - 1);
+      return k <= 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+    };
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int x0, x1;
+      float fx;
+      hier::pcoord(4 * g + e, np, x0, x1, fx);
+      // g = 0: x0 = 0 is v.y (k = 1); v.x holds the clamped duplicate of the same value
+      c[e] = __fmaf_rn(fx, pick(x1), (1.f - fx) * pick(x0));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 3)
+k_upsample_walk(const float* __restrict__ P, int np, float* __restrict__ out, int D, int zsplit) {
   const long long pl = (long long)np * np;
-  const int h = D / 2;
-  for (long long quad = blockIdx.x; quad < (long long)h * h; quad += gridDim.x) {
-    const int Z = (int)(quad / h), Y = (int)(quad % h);
-    int pz[2][2], py[2][2];
-    float fz[2], fy[2];
+  const int h = D / 2, G = D / 4;
+  const int nxs = (G + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int pzc = (np + zsplit - 1) / zsplit;          // parent planes per z chunk
+  const long long items = (long long)zsplit * h * nxs;
+  for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+    const int xs = (int)(it % nxs), Yq = (int)((it / nxs) % h), zc = (int)(it / ((long long)nxs * h));
+    const int g = xs * (int)blockDim.x + (int)threadIdx.x;
+    const int pa = zc * pzc, pb = min(np, pa + pzc);
+    if (g >= G || pa >= pb) continue;
+    int y0[2], y1[2];
+    float fy[2];
+    hier::pcoord(2 * Yq, np, y0[0], y1[0], fy[0]);
+    hier::pcoord(2 * Yq + 1, np, y0[1], y1[1], fy[1]);
+    const bool ydup = y1[0] == y0[1];                  // interior column: 3 distinct parent rows
+    const bool xin = g > 0 && 2 * g + 2 <= np - 1;
+    const float* r0 = P + (long long)y0[0] * np;
+    const float* r1 = P + (long long)y1[0] * np;
+    const float* r2 = P + (long long)y0[1] * np;
+    const float* r3 = P + (long long)y1[1] * np;
+    // raw parent values of plane p (the loads of plane p+1 are issued before plane p is
+    // interpolated, so a thread always has one plane in flight)
+    auto load = [&](int p, float4 (&R)[4]) {
+      const long long o = (long long)p * pl;
+      R[0] = up_raw(r0 + o, g, np);
+      R[1] = up_raw(r1 + o, g, np);
+      if (!ydup) R[2] = up_raw(r2 + o, g, np);
+      R[3] = up_raw(r3 + o, g, np);
+    };
+    // y-interpolated x-interpolations of a parent plane for the two output rows 2Yq, 2Yq+1
+    auto plane = [&](const float4 (&R)[4], float (&cy)[2][4]) {
+      float c0[4], c1[4], c2[4], c3[4];
+      up_xrow(R[0], g, np, xin, c0);
+      up_xrow(R[1], g, np, xin, c1);
+      if (ydup) {
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      hier::pcoord(2 * Z + a, np, pz[a][0], pz[a][1], fz[a]);
-      hier::pcoord(2 * Y + a, np, py[a][0], py[a][1], fy[a]);
-    }
-    const bool inner = pz[0][1] == pz[1][0] && py[0][1] == py[1][0] && pz[0][0] + 1 == pz[0][1] &&
-                       pz[1][0] + 1 == pz[1][1] && py[0][0] + 1 == py[0][1] && py[1][0] + 1 == py[1][1];
-    if (inner) {
-      const float* base = P + (long long)pz[0][0] * pl + (long long)py[0][0] * np;
-      for (int g = threadIdx.x; g < D / 4; g += blockDim.x) {
-        float c[3][3][4];                       // [parent z][parent y][x]
-        const bool xin = g > 0 && 2 * g + 2 <= np - 1;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            const float* r = base + (long long)a * pl + (long long)b * np;
-            if (xin) {
-              const float2 u = *reinterpret_cast<const float2*>(r + 2 * g - 2);
-              const float2 v = *reinterpret_cast<const float2*>(r + 2 * g);
-              const float2 w = *reinterpret_cast<const float2*>(r + 2 * g + 2);
-              c[a][b][0] = __fmaf_rn(0.75f, v.x, (1.f - 0.75f) * u.y);
-              c[a][b][1] = __fmaf_rn(0.25f, v.y, (1.f - 0.25f) * v.x);
-              c[a][b][2] = __fmaf_rn(0.75f, v.y, (1.f - 0.75f) * v.x);
-              c[a][b][3] = __fmaf_rn(0.25f, w.x, (1.f - 0.25f) * v.y);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                int x0, x1;
-                float fx;
-                hier::pcoord(4 * g + e, np, x0, x1, fx);
-                c[a][b][e] = __fmaf_rn(fx, r[x1], (1.f - fx) * r[x0]);
-              }
-            }
-          }
-#pragma unroll
-        for (int zs = 0; zs < 2; ++zs)
-#pragma unroll
-          for (int ys = 0; ys < 2; ++ys) {
-            float o[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float c0 = __fmaf_rn(fy[ys], c[zs][ys + 1][e], (1.f - fy[ys]) * c[zs][ys][e]);
-              const float c1 = __fmaf_rn(fy[ys], c[zs + 1][ys + 1][e], (1.f - fy[ys]) * c[zs + 1][ys][e]);
-              o[e] = __fmaf_rn(fz[zs], c1, (1.f - fz[zs]) * c0);
-            }
-            const long long row = (long long)(2 * Z + zs) * D + (2 * Y + ys);
-            __stcs(reinterpret_cast<float4*>(out + row * D) + g, make_float4(o[0], o[1], o[2], o[3]));
-          }
+        for (int e = 0; e < 4; ++e) c2[e] = c1[e];
+      } else {
+        up_xrow(R[2], g, np, xin, c2);
       }
-    } else {
-      for (int sub = 0; sub < 4; ++sub) {
-        const int zs = sub >> 1, ys = sub & 1;
-        const long long row = (long long)(2 * Z + zs) * D + (2 * Y + ys);
-        const float* r00 = P + (long long)pz[zs][0] * pl + (long long)py[ys][0] * np;
-        const float* r01 = P + (long long)pz[zs][0] * pl + (long long)py[ys][1] * np;
-        const float* r10 = P + (long long)pz[zs][1] * pl + (long long)py[ys][0] * np;
-        const float* r11 = P + (long long)pz[zs][1] * pl + (long long)py[ys][1] * np;
-        for (int g = threadIdx.x; g < D / 4; g += blockDim.x) {
-          float o[4];
+      up_xrow(R[3], g, np, xin, c3);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            int x0, x1;
-            float fx;
-            hier::pcoord(4 * g + e, np, x0, x1, fx);
-            const float c00 = __fmaf_rn(fx, r00[x1], (1.f - fx) * r00[x0]);
-            const float c01 = __fmaf_rn(fx, r01[x1], (1.f - fx) * r01[x0]);
-            const float c10 = __fmaf_rn(fx, r10[x1], (1.f - fx) * r10[x0]);
-            const float c11 = __fmaf_rn(fx, r11[x1], (1.f - fx) * r11[x0]);
-            const float c0 = __fmaf_rn(fy[ys], c01, (1.f - fy[ys]) * c00);
-            const float c1 = __fmaf_rn(fy[ys], c11, (1.f - fy[ys]) * c10);
-            o[e] = __fmaf_rn(fz[zs], c1, (1.f - fz[zs]) * c0);
-          }
-          __stcs(reinterpret_cast<float4*>(out + row * D) + g, make_float4(o[0], o[1], o[2], o[3]));
-        }
+      for (int e = 0; e < 4; ++e) {
+        cy[0][e] = __fmaf_rn(fy[0], c1[e], (1.f - fy[0]) * c0[e]);
+        cy[1][e] = __fmaf_rn(fy[1], c3[e], (1.f - fy[1]) * c2[e]);
       }
+    };
+    // output plane z from the planes lo = pcoord(z).i0 and hi = pcoord(z).i1
+    auto emit = [&](int z, const float (&lo)[2][4], const float (&hi)[2][4]) {
+      int z0, z1;
+      float fz;
+      hier::pcoord(z, np, z0, z1, fz);
+#pragma unroll
+      for (int ys = 0; ys < 2; ++ys) {
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[e] = __fmaf_rn(fz, hi[ys][e], (1.f - fz) * lo[ys][e]);
+        const long long row = (long long)z * D + (2 * Yq + ys);
+        __stcs(reinterpret_cast<float4*>(out + row * D) + g, make_float4(o[0], o[1], o[2], o[3]));
+      }
+    };
+    float prev[2][4], cur[2][4];
+    float4 Rc[4], Rn[4];
+    const int p0 = max(pa, 1) - 1;
+    load(p0, Rc);
+    if (p0 + 1 < pb) load(p0 + 1, Rn);
+    plane(Rc, prev);
+    for (int p = p0 + 1; p < pb; ++p) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) Rc[i] = Rn[i];
+      if (p + 1 < pb) load(p + 1, Rn);
+      plane(Rc, cur);
+      if (p == 1) emit(0, prev, cur);                  // z = 0: planes (0, 1), f = 0
+      emit(2 * p - 1, prev, cur);                      // planes (p-1, p), f = .25
+      emit(2 * p, prev, cur);                          // planes (p-1, p), f = .75
+#pragma unroll
+      for (int ys = 0; ys < 2; ++ys)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) prev[ys][e] = cur[ys][e];
     }
+    if (pb == np) emit(D - 1, prev, prev);             // z = D-1: plane np-1 twice, f = 0
   }
 }
 
@@ -441,9 +472,20 @@ cudaError_t launch_seed_or(const uint8_t* in, int D, uint8_t* out, int sms, cuda
 
 cudaError_t launch_upsample(const float* P, int np, float* out, int D, int sms, cudaStream_t s) {
   const int th = D / 4 < 256 ? (D / 4 + 31) / 32 * 32 : 256;
-  static const int v = [] { const char* e = getenv("RW_UPSAMPLE_V"); return e ? atoi(e) : 9; }();
-  if (v == 9) k_upsample9<<<grid_rows((long long)D * D / 4, sms), th, 0, s>>>(P, np, out, D);
-  else k_upsample<<<grid_rows((long long)D * D / 4, sms), th, 0, s>>>(P, np, out, D);
+  // levels of side >= 512: the z walk (RW_UPSAMPLE_V=0 forces the row-quad kernel, for A/B runs)
+  static const int v = [] { const char* e = getenv("RW_UPSAMPLE_V"); return e ? atoi(e) : 1; }();
+  const int h = D / 2;
+  if (v != 0 && h >= 256) {
+    // ~8 waves of work items over the 3 blocks per SM that 80 registers allow
+    const int mb = 3;
+    const long long cols = (long long)h * ((D / 4 + 255) / 256);
+    int zsplit = (int)((8LL * sms * mb + cols - 1) / cols);
+    zsplit = zsplit < 1 ? 1 : (zsplit > np / 16 ? (np / 16 < 1 ? 1 : np / 16) : zsplit);
+    const long long items = cols * zsplit;
+    k_upsample_walk<<<(int)(items < sms * mb ? items : sms * mb), 256, 0, s>>>(P, np, out, D, zsplit);
+  } else {
+    k_upsample<<<grid_rows((long long)D * D / 4, sms), th, 0, s>>>(P, np, out, D);
+  }
   return cudaGetLastError();
 }
 

@@ -90,3 +90,19 @@ def test_pyramid_and_queue_validation(lib):
     assert lib.rw_build_pyramid(C.c_void_p(4096), 1, _lib.rw_dims(64, 64, 64), 0, arr, None) == 1
     q = C.c_void_p()
     assert lib.rw_queue_create(1024, 1, C.byref(q)) == 1
+
+
+def test_hier_labels_ooc_validation(lib):
+    """rw_hier_segment_labels_ooc rejects K outside 2..255 and NULL outputs before any work
+    (no CUDA call is reached)."""
+    cfg = _lib.rw_hier_config(32, 1.25, 0.3, -1.0, 1, 100.0, 1e-6, 1e-6, 100, 0, 64, 0, 0.01)
+    d = _lib.rw_dims(64, 64, 64)
+    nm = _lib.rw_norm(1.0 / 65535, 0.0)
+    p = C.c_void_p(4096)
+    args = lambda K, best, lab: (p, 1, nm, d, p, K, cfg, 16, p, p, 1 << 20, best, lab, None, None)  # noqa: E731
+    assert lib.rw_hier_segment_labels_ooc(*args(1, p, p)) == 1
+    assert b"K must be in 2..255" in lib.rw_last_error()
+    assert lib.rw_hier_segment_labels_ooc(*args(256, p, p)) == 1
+    assert lib.rw_hier_segment_labels_ooc(*args(3, None, p)) == 1
+    assert b"non-NULL" in lib.rw_last_error()
+    assert lib.rw_hier_segment_labels_ooc(*args(3, p, None)) == 1

@@ -52,11 +52,14 @@ def test_ooc_cubic_matches_oracle(D, s, e, prune):
     _check_vs_oracle(vol, seeds, s=s, e=e, beta=50.0, prune=prune)
 
 
-@pytest.mark.parametrize("D,s,prune", [(128, 16, True), (256, 32, True), (256, 32, False)])
+@pytest.mark.parametrize("D,s,prune", [(128, 16, True), (256, 32, True), (256, 32, False),
+                                       (512, 32, True)])
 def test_ooc_bitwise_equals_in_hbm_driver(D, s, prune):
     """Cubic s 2^k: the page-table field (materialised upsamples, pool) reproduces the dense
     field pyramid of rw_hier_segment bit for bit (same samples, same solves; the resident
-    solver for s_e = 40)."""
+    solver for s_e = 40).  D = 512: the level-0 upsample of the in-HBM driver is the z-walk
+    kernel (k_upsample_walk, levels of side >= 512), checked here against the per-sample
+    form (hier::sample in k_ooc_materialize / k_ooc_out)."""
     vol, seeds = small_volume(D, seed=3)
     kw = dict(s=s, e=1.25, beta=50.0, tol=1e-6, prune=prune)
     ref, st_ref, _ = rwb.hier_segment(dev(vol), dev(seeds), **kw)
