@@ -416,20 +416,79 @@ def hier_segment(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True, be
 NP_DTYPES = {"uint8": 0, "uint16": 1, "int16": 2, "float32": 3}
 
 
+def pinned_empty(shape, dtype):
+    """A page-locked host numpy array (a view of a pinned torch tensor, which it keeps alive)."""
+    import numpy as np
+    n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    t = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    return t.numpy().view(dtype).reshape(shape)
+
+
+class host_register:
+    """Page-locks an existing C-contiguous numpy array in place (cudaHostRegister) for the
+    lifetime of the object / with-block, so rw_queue_push and the out-of-core drivers copy it
+    without staging.  Registration costs about as much as one pass over the array."""
+
+    def __init__(self, arr):
+        if not arr.flags.c_contiguous:
+            raise ValueError("host_register: array must be C-contiguous")
+        self.arr, self.ptr = arr, arr.ctypes.data
+        r = torch.cuda.cudart().cudaHostRegister(self.ptr, arr.nbytes, 0)
+        if int(r) != 0:
+            self.ptr = None
+            raise RuntimeError(f"cudaHostRegister failed ({int(r)})")
+
+    def close(self):
+        if self.ptr is not None:
+            torch.cuda.cudart().cudaHostUnregister(self.ptr)
+            self.ptr = None
+
+    def __enter__(self):
+        return self.arr
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def hier_ooc_alloc(shape, dtype, s=32, e=1.25, pool_bricks=None, max_batch=1024, depth=2,
+                   device="cuda"):
+    """The reusable resources of hier_segment_ooc for [nz, ny, nx] volumes of numpy `dtype`:
+    (Queue, workspace tensor, pool_bricks).  Pass them as queue= / workspace= / pool_bricks= so
+    repeated runs allocate nothing."""
+    import numpy as np
+    dt = NP_DTYPES[str(np.dtype(dtype))]
+    nz, ny, nx = shape
+    d = rw_dims(nx, ny, nz)
+    cfg = rw_hier_config(s, e, 0.3, 0.01, 1, 100.0, 1e-6, 1e-6, 5000, 0, max_batch, 0, 0.01)
+    if pool_bricks is None:
+        pool_bricks = (-(-nx // s) * -(-ny // s) * -(-nz // s)) // 16 + 4096
+    need = lib().rw_hier_ooc_workspace_bytes(d, dt, cfg, int(pool_bricks))
+    qb = lib().rw_hier_ooc_queue_bytes(d, dt, cfg)
+    if need == 0 or qb == 0:
+        raise ValueError("hier_ooc_alloc: need s % 4 == 0, e in (1, 2] with floor(e*s) % 4 == 0")
+    return Queue(qb, depth=depth), alloc_workspace(need, device), int(pool_bricks)
+
+
 def hier_segment_ooc(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True, beta=100.0,
                      eps=1e-6, tol=1e-6, max_iter=5000, tol_mode=0, norm=None, max_batch=1024,
                      pool_bricks=None, want_prob=True, want_labels=True, device="cuda",
-                     queue=None, workspace=None, stream=None):
+                     queue=None, workspace=None, stream=None, out_prob=None, out_labels=None):
     """rw_hier_segment_ooc: the hierarchical random walker with the
     volume, labels and output in HOST memory.  vol: numpy [nz, ny, nx] (u8/u16/i16/f32), any
     dims; seeds: numpy u8 (0 / 1 fg / 2 bg).  pool_bricks: device brick-pool capacity (default:
     the level-0 brick count / 8 + 4096).  Returns (prob fp32 numpy or None, labels u8 numpy or
-    None, stats dict)."""
+    None, stats dict).  out_prob / out_labels: caller-owned C-contiguous numpy outputs of vol's
+    shape (fp32 / u8).  Page-locked buffers (pinned_empty, host_register) skip the library's
+    host staging copies: the copy engine reads vol / seeds and writes the outputs directly."""
     import numpy as np
     vol = np.ascontiguousarray(vol)
     seeds = np.ascontiguousarray(seeds, dtype=np.uint8)
     if vol.ndim != 3 or seeds.shape != vol.shape:
         raise ValueError("hier_segment_ooc: vol and seeds must be 3-D arrays of one shape")
+    for o, t in ((out_prob, np.float32), (out_labels, np.uint8)):
+        if o is not None and (o.dtype != t or o.shape != vol.shape or not o.flags.c_contiguous):
+            raise ValueError("hier_segment_ooc: out_prob / out_labels must be C-contiguous fp32 / u8 "
+                             "arrays of vol's shape")
     dt = NP_DTYPES[str(vol.dtype)]
     nz, ny, nx = vol.shape
     d = rw_dims(nx, ny, nz)
@@ -449,8 +508,8 @@ def hier_segment_ooc(vol, seeds, s=32, e=1.25, t_hom=0.3, t_bin=0.01, prune=True
     own_q = queue is None
     if own_q:
         queue = Queue(qb, depth=2)
-    prob = np.empty(vol.shape, np.float32) if want_prob else None
-    lab = np.empty(vol.shape, np.uint8) if want_labels else None
+    prob = out_prob if out_prob is not None else (np.empty(vol.shape, np.float32) if want_prob else None)
+    lab = out_labels if out_labels is not None else (np.empty(vol.shape, np.uint8) if want_labels else None)
     st = rw_hier_stats()
     try:
         check(lib().rw_hier_segment_ooc(C.c_void_p(vol.ctypes.data), dt, rw_norm(sc, of), d,

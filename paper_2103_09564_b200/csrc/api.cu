@@ -62,6 +62,9 @@ size_t queue_slot_bytes(const rw_queue* q);
 int queue_depth(const rw_queue* q);
 void* queue_host_slot(rw_queue* q, int i);
 void host_parallel_copy(void* dst, const void* src, size_t bytes);
+bool host_is_pinned(const void* p);
+rw_status queue_push_pinned2(rw_queue* q, const void* src0, size_t bytes0, const void* src1, size_t bytes1,
+                             cudaStream_t copy_s, void** dev_slot, int32_t* slot_id);
 rw_status queue_push_fill(rw_queue* q, size_t bytes, void (*fill)(void*, void*), void* ctx,
                           cudaStream_t copy_s, void** dev_slot, int32_t* slot_id);
 cudaError_t launch_ooc_out(int, const OocGeo&, const int*, const float*, const float*, int, int, int,
@@ -1904,13 +1907,17 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
     SL &= ~1;
     if (SL < 2) SL = std::min(2, d.nz);
     void* lev1 = PTR(L.lev[1]);
+    // page-locked caller buffers go to the device directly (no staging copy on the host)
+    const bool in_pinned = rw::host_is_pinned(seeds_h) && (!with_vol || rw::host_is_pinned(vol_h));
     for (int z0 = 0; z0 < d.nz; z0 += SL) {
       const int nzs = std::min(SL, d.nz - z0);
       SlabCtx sc{(const char*)vol_h + (size_t)z0 * plane * es, seeds_h + (size_t)z0 * plane,
                  (size_t)nzs * plane * ves, (size_t)nzs * plane};
       void* dev = nullptr;
       int32_t sid = 0;
-      rw_status r = rw::queue_push_fill(q, sc.vbytes + sc.sbytes, copy_slab, &sc, s, &dev, &sid);
+      rw_status r = in_pinned
+          ? rw::queue_push_pinned2(q, sc.vol, sc.vbytes, sc.seeds, sc.sbytes, s, &dev, &sid)
+          : rw::queue_push_fill(q, sc.vbytes + sc.sbytes, copy_slab, &sc, s, &dev, &sid);
       if (r != RW_OK) return r;
       if (with_vol) {
         r = rw_build_pyramid_slab(dev, dtype, d, z0, nzs, 1, &lev1, stream);
@@ -2167,7 +2174,15 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
         rw::host_parallel_copy(c.dst, rw::queue_host_slot(q, c.slot), c.bytes);
       return RW_OK;
     };
-    auto stage = [&](void* dst, const void* src, size_t bytes, uint8_t* lab) -> rw_status {
+    const bool prob_pinned = rw::host_is_pinned(prob_h), lab_pinned = rw::host_is_pinned(labels_h);
+    bool direct = false;
+    auto stage = [&](void* dst, const void* src, size_t bytes, uint8_t* lab, bool dst_pinned) -> rw_status {
+      // a page-locked destination that needs no host-side merge is written by the copy engine
+      if (!lab && dst_pinned) {
+        RW_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        direct = true;
+        return RW_OK;
+      }
       if ((int)pend.size() == nsl) {
         rw_status rr = drain();
         if (rr != RW_OK) return rr;
@@ -2198,18 +2213,19 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
                                     (last && labels_h && cls == 0) ? (uint8_t*)PTR(L.lab) : nullptr, sms, s));
       }
       if (cls > 0) {   // class cls's probabilities merged into the running maximum / class
-        r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4, labels_h + (size_t)Z0 * pl0);
+        r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4, labels_h + (size_t)Z0 * pl0, false);
         if (r != RW_OK) return r;
         continue;
       }
-      if (prob_h) { r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4, nullptr); if (r != RW_OK) return r; }
-      if (labels_h) { r = stage(labels_h + (size_t)Z0 * pl0, PTR(L.lab), (size_t)zc[0] * pl0, nullptr); if (r != RW_OK) return r; }
+      if (prob_h) { r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4, nullptr, prob_pinned); if (r != RW_OK) return r; }
+      if (labels_h) { r = stage(labels_h + (size_t)Z0 * pl0, PTR(L.lab), (size_t)zc[0] * pl0, nullptr, lab_pinned); if (r != RW_OK) return r; }
     }
     while (!pend.empty()) {
       r = drain();
       if (r != RW_OK) return r;
     }
     for (auto e : oev) cudaEventDestroy(e);
+    if (direct) RW_CK(cudaStreamSynchronize(s));   // the caller's buffers are complete on return
   }
   st.ms_output = wall() - t0;
   st.pool_used = next_slot;

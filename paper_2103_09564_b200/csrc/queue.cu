@@ -125,6 +125,39 @@ int queue_depth(const rw_queue* q) { return q ? q->depth : 0; }
 // every push has completed)
 void* queue_host_slot(rw_queue* q, int i) { return q->host[i]; }
 void host_parallel_copy(void* dst, const void* src, size_t bytes) { parallel_copy(dst, src, bytes); }
+// true when p is page-locked host memory (cudaMallocHost / cudaHostAlloc / cudaHostRegister)
+bool host_is_pinned(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();   // pageable pointers may report an error on some drivers
+  return pinned;
+}
+// Two pinned host pieces copied straight into the next slot's device buffer, back to back
+// (no staging copy through the slot's host buffer); otherwise as rw_queue_push.
+rw_status queue_push_pinned2(rw_queue* q, const void* src0, size_t bytes0, const void* src1,
+                             size_t bytes1, cudaStream_t copy_s, void** dev_slot, int32_t* slot_id) {
+  if (!q || !dev_slot || bytes0 + bytes1 > q->slot_bytes)
+    return qfail(RW_EINVAL, "rw_queue: bad pinned push (bytes > slot_bytes?)");
+  const int s = q->next;
+  if (!q->released[s])
+    return qfail(RW_EINVAL, "rw_queue: the next slot has not been released");
+  q->next = (q->next + 1) % q->depth;
+  if (q->used[s] && (cudaEventSynchronize(q->ready[s]) != cudaSuccess ||
+                     cudaEventSynchronize(q->freed[s]) != cudaSuccess))
+    return qfail(RW_ECUDA, "rw_queue: waiting for slot release failed");
+  if ((bytes0 > 0 && cudaMemcpyAsync(q->dev[s], src0, bytes0, cudaMemcpyHostToDevice, copy_s) != cudaSuccess) ||
+      (bytes1 > 0 && cudaMemcpyAsync((char*)q->dev[s] + bytes0, src1, bytes1, cudaMemcpyHostToDevice,
+                                     copy_s) != cudaSuccess))
+    return qfail(RW_ECUDA, "rw_queue: H2D copy enqueue failed");
+  if (cudaEventRecord(q->ready[s], copy_s) != cudaSuccess)
+    return qfail(RW_ECUDA, "rw_queue: event record failed");
+  q->used[s] = true;
+  q->released[s] = false;
+  *dev_slot = q->dev[s];
+  if (slot_id) *slot_id = s;
+  return RW_OK;
+}
 rw_status queue_push_fill(rw_queue* q, size_t bytes, void (*fill)(void* dst, void* ctx),
                           void* ctx, cudaStream_t copy_s, void** dev_slot, int32_t* slot_id) {
   if (!q || !fill || !dev_slot || bytes > q->slot_bytes)

@@ -86,6 +86,34 @@ def test_ooc_labels_only_and_single_brick():
     assert p2 is None and np.array_equal(l2, lab)
 
 
+def test_ooc_page_locked_buffers_are_bitwise_the_pageable_run():
+    """Page-locked volume / seeds (cudaHostRegister) and pinned outputs take the direct copy-engine
+    path (no staging through the queue's host slots), with a reused queue + workspace: the same
+    bits as the pageable call, twice in a row (slot reuse), with and without the fp32 field."""
+    vol, seeds = _ragged_volume((72, 88, 104), 2, 21)
+    kw = dict(s=16, e=1.25, beta=50.0, tol=1e-6)
+    prob, lab, st = rwb.hier_segment_ooc(vol, seeds, **kw)
+    q, ws, pool = rwb.hier_ooc_alloc(vol.shape, vol.dtype, s=16)
+    op, ol = rwb.pinned_empty(vol.shape, np.float32), rwb.pinned_empty(vol.shape, np.uint8)
+    try:
+        with rwb.host_register(vol), rwb.host_register(seeds):
+            for rep in range(2):
+                op.fill(-1.0), ol.fill(255)
+                p2, l2, st2 = rwb.hier_segment_ooc(vol, seeds, queue=q, workspace=ws, pool_bricks=pool,
+                                                   out_prob=op, out_labels=ol, **kw)
+                assert p2 is op and l2 is ol
+                assert st2["solved"] == st["solved"] and st2["iters"] == st["iters"]
+                assert np.array_equal(op, prob) and np.array_equal(ol, lab)
+            ol.fill(255)
+            p3, l3, _ = rwb.hier_segment_ooc(vol, seeds, queue=q, workspace=ws, pool_bricks=pool,
+                                             want_prob=False, out_labels=ol, **kw)
+            assert p3 is None and np.array_equal(ol, lab)
+        with pytest.raises(ValueError):
+            rwb.hier_segment_ooc(vol, seeds, out_labels=np.empty(vol.shape, np.float32), **kw)
+    finally:
+        q.close()
+
+
 def test_ooc_pool_full_is_an_error():
     vol, seeds = small_volume(64, seed=5)
     with pytest.raises(RWError, match="RW_ENOMEM"):
