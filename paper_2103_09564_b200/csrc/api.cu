@@ -1705,7 +1705,7 @@ bool ooc_plan(rw_dims d, rw_dtype dt, const rw_hier_config& c, int64_t pool_bric
 
 struct OocLayout {
   size_t lev[17], bits[17], pt, pool, org, brick, state, iters, status, jobs, wvol, wfixed, wval,
-      wx0, wprob, W, solve, out[17], lab, total;
+      wx0, wprob, W, solve, out[17], lab, out0b, labb, total;
 };
 constexpr int kOocJobs = 4096;   // materialisation jobs per launch
 
@@ -1746,6 +1746,9 @@ OocLayout ooc_layout(const OocPlan& p) {
     L.out[m] = o; o += up((size_t)p.G.nx[m] * p.G.ny[m] * p.oz[m] * 4);
   }
   L.lab = o; o += up((size_t)p.G.nx[0] * p.G.ny[0] * p.oz[0]);
+  // second level-0 slab buffers: slab i+1 is produced while slab i's D2H copy is in flight
+  L.out0b = o; o += up((size_t)p.G.nx[0] * p.G.ny[0] * p.oz[0] * 4);
+  L.labb = o; o += up((size_t)p.G.nx[0] * p.G.ny[0] * p.oz[0]);
   L.total = o;
   return L;
 }
@@ -2156,10 +2159,28 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
   if (prob_h || labels_h) {
     const size_t pl0 = (size_t)G.nx[0] * G.ny[0];
     // D2H through the queue's pinned slots (all pushes are complete here), round robin; the
-    // host copies a slot out to the caller's buffer while the next ones are in flight
+    // host copies a slot out to the caller's buffer while the next ones are in flight.
+    // The copies run on their own stream: slab i+1's kernels (stream s, the other level-0
+    // buffer) overlap slab i's D2H; a level-0 buffer is rewritten only after its copy ran.
     const int nsl = rw::queue_depth(q);
     std::vector<cudaEvent_t> oev(nsl);
     for (auto& e : oev) RW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaStream_t cs = nullptr;
+    RW_CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t kdone[2] = {nullptr, nullptr}, bdone[2] = {nullptr, nullptr};
+    struct Cleanup {
+      cudaStream_t& cs; std::vector<cudaEvent_t>& oev; cudaEvent_t* a; cudaEvent_t* b;
+      ~Cleanup() {
+        cudaStreamSynchronize(cs);
+        cudaStreamDestroy(cs);
+        for (auto e : oev) cudaEventDestroy(e);
+        for (int i = 0; i < 2; ++i) { if (a[i]) cudaEventDestroy(a[i]); if (b[i]) cudaEventDestroy(b[i]); }
+      }
+    } cleanup{cs, oev, kdone, bdone};
+    for (int i = 0; i < 2; ++i) {
+      RW_CK(cudaEventCreateWithFlags(&kdone[i], cudaEventDisableTiming));
+      RW_CK(cudaEventCreateWithFlags(&bdone[i], cudaEventDisableTiming));
+    }
     struct Pend { int slot; void* dst; size_t bytes; uint8_t* lab; };
     std::vector<Pend> pend;
     int nxt = 0;
@@ -2179,7 +2200,7 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
     auto stage = [&](void* dst, const void* src, size_t bytes, uint8_t* lab, bool dst_pinned) -> rw_status {
       // a page-locked destination that needs no host-side merge is written by the copy engine
       if (!lab && dst_pinned) {
-        RW_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        RW_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs));
         direct = true;
         return RW_OK;
       }
@@ -2188,12 +2209,16 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
         if (rr != RW_OK) return rr;
       }
       const int sl = nxt++ % nsl;
-      RW_CK(cudaMemcpyAsync(rw::queue_host_slot(q, sl), src, bytes, cudaMemcpyDeviceToHost, s));
-      RW_CK(cudaEventRecord(oev[sl], s));
+      RW_CK(cudaMemcpyAsync(rw::queue_host_slot(q, sl), src, bytes, cudaMemcpyDeviceToHost, cs));
+      RW_CK(cudaEventRecord(oev[sl], cs));
       pend.push_back({sl, dst, bytes, lab});
       return RW_OK;
     };
-    for (int Z0 = 0; Z0 < G.nz[0]; Z0 += p.oz[0]) {
+    int slab = 0;
+    for (int Z0 = 0; Z0 < G.nz[0]; Z0 += p.oz[0], ++slab) {
+      const int par = slab & 1;
+      float* out0 = (float*)PTR(par ? L.out0b : L.out[0]);
+      uint8_t* lab0 = (uint8_t*)PTR(par ? L.labb : L.lab);
       int z0[17], zc[17];
       z0[0] = Z0;
       zc[0] = std::min(p.oz[0], G.nz[0] - Z0);
@@ -2206,26 +2231,29 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
       }
       for (int m = k; m >= 0; --m) {
         const bool last = m == 0;
+        if (last && slab >= 2) RW_CK(cudaStreamWaitEvent(s, bdone[par], 0));   // buffer copied out
         RW_TIMED(RW_K_HIER, s, 1,
                  rw::launch_ooc_out(m, G, PT, pool, m == k ? nullptr : (const float*)PTR(L.out[m + 1]),
                                     m == k ? 0 : z0[m + 1], z0[m], zc[m],
-                                    (!last || prob_h) ? (float*)PTR(L.out[m]) : nullptr,
-                                    (last && labels_h && cls == 0) ? (uint8_t*)PTR(L.lab) : nullptr, sms, s));
+                                    last ? (prob_h ? out0 : nullptr) : (float*)PTR(L.out[m]),
+                                    (last && labels_h && cls == 0) ? lab0 : nullptr, sms, s));
       }
+      RW_CK(cudaEventRecord(kdone[par], s));
+      RW_CK(cudaStreamWaitEvent(cs, kdone[par], 0));
       if (cls > 0) {   // class cls's probabilities merged into the running maximum / class
-        r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4, labels_h + (size_t)Z0 * pl0, false);
+        r = stage(prob_h + (size_t)Z0 * pl0, out0, (size_t)zc[0] * pl0 * 4, labels_h + (size_t)Z0 * pl0, false);
         if (r != RW_OK) return r;
-        continue;
+      } else {
+        if (prob_h) { r = stage(prob_h + (size_t)Z0 * pl0, out0, (size_t)zc[0] * pl0 * 4, nullptr, prob_pinned); if (r != RW_OK) return r; }
+        if (labels_h) { r = stage(labels_h + (size_t)Z0 * pl0, lab0, (size_t)zc[0] * pl0, nullptr, lab_pinned); if (r != RW_OK) return r; }
       }
-      if (prob_h) { r = stage(prob_h + (size_t)Z0 * pl0, PTR(L.out[0]), (size_t)zc[0] * pl0 * 4, nullptr, prob_pinned); if (r != RW_OK) return r; }
-      if (labels_h) { r = stage(labels_h + (size_t)Z0 * pl0, PTR(L.lab), (size_t)zc[0] * pl0, nullptr, lab_pinned); if (r != RW_OK) return r; }
+      RW_CK(cudaEventRecord(bdone[par], cs));
     }
     while (!pend.empty()) {
       r = drain();
       if (r != RW_OK) return r;
     }
-    for (auto e : oev) cudaEventDestroy(e);
-    if (direct) RW_CK(cudaStreamSynchronize(s));   // the caller's buffers are complete on return
+    if (direct) RW_CK(cudaStreamSynchronize(cs));   // the caller's buffers are complete on return
   }
   st.ms_output = wall() - t0;
   st.pool_used = next_slot;
