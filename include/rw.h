@@ -316,6 +316,10 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
  *   q          rw_queue with slot_bytes >= rw_hier_ooc_queue_bytes(d, dtype, cfg), depth >= 2.
  *   prob_h / labels_h   out host fp32 / u8 [nz][ny][nx], either may be NULL (labels: p > 0.5).
  *   workspace  device, >= rw_hier_ooc_workspace_bytes(d, dtype, cfg, pool_bricks), 256-B aligned.
+ *   Host buffers may be pageable or page-locked (cudaMallocHost / cudaHostRegister), detected
+ *   per pointer: page-locked vol_h + seeds_h are copied to the device without the staging
+ *   copy through the queue's host slots, and a page-locked prob_h / labels_h is written by
+ *   the copy engine directly (both then run at the PCIe rate).  Results are the same bits.
  *   Blocks the host (brick lists are built on the host between levels); work on `stream`.
  *   Errors: RW_EINVAL for bad arguments (s % 4, floor(e s) % 4, incremental, small queue),
  *   RW_ENOMEM for a small workspace or a full pool.
