@@ -320,6 +320,7 @@ rw_status rw_hier_segment(const void* vol, rw_dtype dtype, rw_norm nm, rw_dims d
  *   per pointer: page-locked vol_h + seeds_h are copied to the device without the staging
  *   copy through the queue's host slots, and a page-locked prob_h / labels_h is written by
  *   the copy engine directly (both then run at the PCIe rate).  Results are the same bits.
+ *   Seed slabs are uploaded sparsely (non-zero 4 KiB segments only, the rest a device memset).
  *   Blocks the host (brick lists are built on the host between levels); work on `stream`.
  *   Errors: RW_EINVAL for bad arguments (s % 4, floor(e s) % 4, incremental, small queue),
  *   RW_ENOMEM for a small workspace or a full pool.

@@ -67,6 +67,12 @@ rw_status queue_push_pinned2(rw_queue* q, const void* src0, size_t bytes0, const
                              cudaStream_t copy_s, void** dev_slot, int32_t* slot_id);
 rw_status queue_push_fill(rw_queue* q, size_t bytes, void (*fill)(void*, void*), void* ctx,
                           cudaStream_t copy_s, void** dev_slot, int32_t* slot_id);
+bool host_nonzero_segments(const uint8_t* p, size_t n, size_t seg, size_t max_segs,
+                           std::vector<std::pair<size_t, size_t>>& segs);
+rw_status queue_push_sparse(rw_queue* q, const void* src0, size_t bytes0, bool pinned0,
+                            const uint8_t* src1, size_t bytes1, bool pinned1,
+                            const std::vector<std::pair<size_t, size_t>>& segs,
+                            cudaStream_t copy_s, void** dev_slot, int32_t* slot_id);
 cudaError_t launch_ooc_out(int, const OocGeo&, const int*, const float*, const float*, int, int, int,
                            float*, uint8_t*, int, cudaStream_t);
 }  // namespace rw
@@ -1911,14 +1917,26 @@ static rw_status hier_ooc_run(const void* vol_h, rw_dtype dtype, rw_norm nm, rw_
     if (SL < 2) SL = std::min(2, d.nz);
     void* lev1 = PTR(L.lev[1]);
     // page-locked caller buffers go to the device directly (no staging copy on the host)
-    const bool in_pinned = rw::host_is_pinned(seeds_h) && (!with_vol || rw::host_is_pinned(vol_h));
+    const bool vol_pinned = with_vol && rw::host_is_pinned(vol_h), seeds_pinned = rw::host_is_pinned(seeds_h);
+    const bool in_pinned = seeds_pinned && (!with_vol || vol_pinned);
+    // Seeds are user scribbles, i.e. almost all zero: host threads scan each slab's
+    // seed bytes (while the previous slab's DMA runs) and only the non-zero 4 KiB segments
+    // cross the link, the rest of the slot's seed part is a device memset.  A slab with more
+    // than 2048 such segments takes the dense copy (RW_OOC_SEED_SEGS: the limit, 0 = always
+    // dense; both paths leave the same bytes in the slot).
+    std::vector<std::pair<size_t, size_t>> segs;
+    const size_t max_segs = (size_t)std::max(0, env_int("RW_OOC_SEED_SEGS", 2048));
     for (int z0 = 0; z0 < d.nz; z0 += SL) {
       const int nzs = std::min(SL, d.nz - z0);
       SlabCtx sc{(const char*)vol_h + (size_t)z0 * plane * es, seeds_h + (size_t)z0 * plane,
                  (size_t)nzs * plane * ves, (size_t)nzs * plane};
       void* dev = nullptr;
       int32_t sid = 0;
-      rw_status r = in_pinned
+      const bool sparse = max_segs > 0 && rw::host_nonzero_segments(sc.seeds, sc.sbytes, 4096, max_segs, segs);
+      rw_status r = sparse
+          ? rw::queue_push_sparse(q, sc.vol, sc.vbytes, vol_pinned, sc.seeds, sc.sbytes, seeds_pinned,
+                                  segs, s, &dev, &sid)
+          : in_pinned
           ? rw::queue_push_pinned2(q, sc.vol, sc.vbytes, sc.seeds, sc.sbytes, s, &dev, &sid)
           : rw::queue_push_fill(q, sc.vbytes + sc.sbytes, copy_slab, &sc, s, &dev, &sid);
       if (r != RW_OK) return r;

@@ -6,9 +6,12 @@
 // `freed` (its consumers done, recorded on the compute stream).  With depth >= 2 the H2D
 // copy of slot k+1 overlaps the kernels consuming slot k; the host-side staging copy of
 // slot k+2 overlaps both.
+#include <algorithm>
+#include <cstdint>
 #include <cstring>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/rw.h"
@@ -150,6 +153,90 @@ rw_status queue_push_pinned2(rw_queue* q, const void* src0, size_t bytes0, const
       (bytes1 > 0 && cudaMemcpyAsync((char*)q->dev[s] + bytes0, src1, bytes1, cudaMemcpyHostToDevice,
                                      copy_s) != cudaSuccess))
     return qfail(RW_ECUDA, "rw_queue: H2D copy enqueue failed");
+  if (cudaEventRecord(q->ready[s], copy_s) != cudaSuccess)
+    return qfail(RW_ECUDA, "rw_queue: event record failed");
+  q->used[s] = true;
+  q->released[s] = false;
+  *dev_slot = q->dev[s];
+  if (slot_id) *slot_id = s;
+  return RW_OK;
+}
+// The non-zero `seg`-byte segments of p[0, n), found on host threads; adjacent segments are
+// merged.  Returns false (segs unspecified) when more than max_segs segments are non-zero.
+bool host_nonzero_segments(const uint8_t* p, size_t n, size_t seg, size_t max_segs,
+                           std::vector<std::pair<size_t, size_t>>& segs) {
+  segs.clear();
+  const size_t nseg = (n + seg - 1) / seg;
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt > 16) nt = 16;
+  if (nt < 1) nt = 1;
+  if (nseg < (size_t)nt * 64) nt = 1;
+  std::vector<std::vector<size_t>> hit(nt);
+  auto scan = [&](unsigned t) {
+    const size_t a = nseg * t / nt, b = nseg * (t + 1) / nt;
+    for (size_t i = a; i < b && hit[t].size() <= max_segs; ++i) {
+      const uint8_t* q = p + i * seg;
+      const size_t len = std::min(seg, n - i * seg);
+      uint64_t acc = 0;
+      size_t j = 0;
+      for (; j + 64 <= len; j += 64) {
+        uint64_t v[8];
+        std::memcpy(v, q + j, 64);
+        acc |= v[0] | v[1] | v[2] | v[3] | v[4] | v[5] | v[6] | v[7];
+      }
+      for (; j < len; ++j) acc |= q[j];
+      if (acc) hit[t].push_back(i);
+    }
+  };
+  if (nt == 1) scan(0);
+  else {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) th.emplace_back(scan, t);
+    for (auto& x : th) x.join();
+  }
+  size_t total = 0;
+  for (auto& h : hit) total += h.size();
+  if (total > max_segs) return false;
+  for (auto& h : hit)
+    for (size_t i : h) {
+      const size_t off = i * seg, len = std::min(seg, n - off);
+      if (!segs.empty() && segs.back().first + segs.back().second == off) segs.back().second += len;
+      else segs.emplace_back(off, len);
+    }
+  return true;
+}
+// One slot = [piece 0 | sparse piece 1]: piece 0 (bytes0, may be 0) is copied whole (directly
+// when page-locked, else staged through the slot's host buffer); piece 1 (bytes1) is zeroed on
+// the device and only its listed non-zero segments are copied.  Otherwise as rw_queue_push.
+rw_status queue_push_sparse(rw_queue* q, const void* src0, size_t bytes0, bool pinned0,
+                            const uint8_t* src1, size_t bytes1, bool pinned1,
+                            const std::vector<std::pair<size_t, size_t>>& segs,
+                            cudaStream_t copy_s, void** dev_slot, int32_t* slot_id) {
+  if (!q || !dev_slot || bytes0 + bytes1 > q->slot_bytes)
+    return qfail(RW_EINVAL, "rw_queue: bad sparse push (bytes > slot_bytes?)");
+  const int s = q->next;
+  if (!q->released[s])
+    return qfail(RW_EINVAL, "rw_queue: the next slot has not been released");
+  q->next = (q->next + 1) % q->depth;
+  if (q->used[s] && (cudaEventSynchronize(q->ready[s]) != cudaSuccess ||
+                     cudaEventSynchronize(q->freed[s]) != cudaSuccess))
+    return qfail(RW_ECUDA, "rw_queue: waiting for slot release failed");
+  char* hs = (char*)q->host[s];
+  char* ds = (char*)q->dev[s];
+  bool ok = true;
+  if (bytes0 > 0) {
+    const void* src = src0;
+    if (!pinned0) { parallel_copy(hs, src0, bytes0); src = hs; }
+    ok = cudaMemcpyAsync(ds, src, bytes0, cudaMemcpyHostToDevice, copy_s) == cudaSuccess;
+  }
+  if (ok && bytes1 > 0) ok = cudaMemsetAsync(ds + bytes0, 0, bytes1, copy_s) == cudaSuccess;
+  for (size_t i = 0; ok && i < segs.size(); ++i) {
+    const size_t off = segs[i].first, len = segs[i].second;
+    const void* src = src1 + off;
+    if (!pinned1) { std::memcpy(hs + bytes0 + off, src1 + off, len); src = hs + bytes0 + off; }
+    ok = cudaMemcpyAsync(ds + bytes0 + off, src, len, cudaMemcpyHostToDevice, copy_s) == cudaSuccess;
+  }
+  if (!ok) return qfail(RW_ECUDA, "rw_queue: H2D copy enqueue failed");
   if (cudaEventRecord(q->ready[s], copy_s) != cudaSuccess)
     return qfail(RW_ECUDA, "rw_queue: event record failed");
   q->used[s] = true;

@@ -114,6 +114,24 @@ def test_ooc_page_locked_buffers_are_bitwise_the_pageable_run():
         q.close()
 
 
+@pytest.mark.parametrize("limit", ["0", "3"])
+def test_ooc_sparse_seed_upload_equals_dense(limit, monkeypatch):
+    """The pyramid phase uploads only the non-zero 4 KiB segments of each slab's seed bytes
+    (the rest is a device memset); with the segment limit at 0 (always dense) or 3 (slabs with
+    more seeded segments fall back to the dense copy) the run gives the same bits, for
+    pageable and page-locked seeds."""
+    vol, seeds = _ragged_volume((72, 88, 104), 4, 40)
+    kw = dict(s=16, e=1.25, beta=50.0, tol=1e-6)
+    prob, lab, st = rwb.hier_segment_ooc(vol, seeds, **kw)
+    monkeypatch.setenv("RW_OOC_SEED_SEGS", limit)
+    p2, l2, st2 = rwb.hier_segment_ooc(vol, seeds, **kw)
+    assert st2["solved"] == st["solved"] and st2["iters"] == st["iters"]
+    assert np.array_equal(p2, prob) and np.array_equal(l2, lab)
+    with rwb.host_register(vol), rwb.host_register(seeds):
+        p3, l3, _ = rwb.hier_segment_ooc(vol, seeds, **kw)
+    assert np.array_equal(p3, prob) and np.array_equal(l3, lab)
+
+
 def test_ooc_pool_full_is_an_error():
     vol, seeds = small_volume(64, seed=5)
     with pytest.raises(RWError, match="RW_ENOMEM"):
