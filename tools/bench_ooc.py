@@ -71,6 +71,9 @@ def main():
     ap.add_argument("--pinned", action="store_true",
                     help="page-locked volume / seeds / outputs (no host staging copies) and a "
                          "queue + workspace allocated once, outside the timed call")
+    ap.add_argument("--no-pin-seeds", action="store_true",
+                    help="with --pinned: leave the seed volume pageable (it is only scanned on "
+                         "the host; its non-zero segments are staged)")
     a = ap.parse_args()
     import torch
     import paper_2103_09564_b200 as rwb
@@ -84,7 +87,7 @@ def main():
     pin_s = None
     if a.pinned:
         t = time.time()
-        regs = [rwb.host_register(vol), rwb.host_register(seeds)]
+        regs = [rwb.host_register(vol)] + ([] if a.no_pin_seeds else [rwb.host_register(seeds)])
         kw["out_labels"] = rwb.pinned_empty(vol.shape, np.uint8)
         if a.prob:
             kw["out_prob"] = rwb.pinned_empty(vol.shape, np.float32)
@@ -111,7 +114,8 @@ def main():
             "iters": st["iters"], "fg_voxels": int(lab.sum(dtype=np.int64)),
             "output": "fp32 prob + u8 labels" if a.prob else "u8 labels"}
     if a.pinned:
-        line["host_buffers"] = "page-locked (registered volume / seeds, pinned outputs); queue and workspace reused"
+        line["host_buffers"] = ("page-locked (registered volume" + ("" if a.no_pin_seeds else " / seeds") +
+                                ", pinned outputs); queue and workspace reused")
         line["pin_and_alloc_s"] = pin_s
     try:
         free, total = torch.cuda.mem_get_info()
